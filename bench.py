@@ -1,0 +1,371 @@
+#!/usr/bin/env python
+"""bench.py -- spin updates/s of the TAPT verifier (PT + TAPT sweeps) on 1..8 B200s.
+
+Workload (BASELINE.json configs[4], the scaling run the metric is quoted on): 3D
+Edwards-Anderson +-1 spin glass, L=32 periodic (32768 spins), 64 slots with beta linear in
+[0.2, 3.0], 4096 disorder instances sharded over the ranks (contiguous blocks of global
+instance ids; RNG streams keyed by global id, so results do not depend on N), multi-replica
+bit-packed spins.  One step = one TAPT round (synthetic i.i.d. +-1 proposals into the 56
+hottest slots + 5 refinement sweeps at the target beta + Metropolis, Eq. 2) followed by 1000
+checkerboard sweeps with a swap pass after every sweep and energy/|m| accumulation plus
+per-beta energy histograms every 10 sweeps.  Per-beta histograms are reduced with NCCL at the
+end of the timed region.
+
+A spin update = one heat-bath decision for one free spin of one replica (refinement sweeps
+count, i.i.d. proposal generation does not) -- BASELINE.md.
+
+  python bench.py [--gpus N --steps K --warmup W]              # this framework (one JSON line)
+  python bench.py --impl reference [--steps K --warmup W]      # the reference's CPU path
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L, R = 32, 64
+N_SPINS = L ** 3
+BETA_MIN, BETA_MAX = 0.2, 3.0
+N_TARGETS, REFINE = 56, 5
+SEED, DISORDER_SEED = 20250923, 43
+METRIC = "spin updates/sec for PT+TAPT sweeps at 1/2/4/8 B200; % of HBM/ALU roofline"
+UNIT = "spin updates/s"
+
+
+def betas():
+    return np.linspace(BETA_MIN, BETA_MAX, R)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--instances", type=int, default=4096)
+    ap.add_argument("--sweeps-per-step", type=int, default=1000)
+    ap.add_argument("--measure-every", type=int, default=10)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-instances", type=int, default=16)
+    ap.add_argument("--cpu-sample-sweeps", type=int, default=100)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- clocks ----
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, dev):
+        self.dev, self.rows, self.proc = dev, [], None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if "Active" in r[3 + k]})
+        pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "power_w_max": max(pw) if pw else None, "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------ CPU baseline ---
+
+def ea_couplings_numpy(seed, gid):
+    """EA +-1 bonds of DESIGN.md 3.4 (coin per (+x,+y,+z) bond in site order from
+    derive(seed, {0x88, gid})), vectorised restatement for building reference graphs."""
+    from oracle import oracle as O
+    s0 = np.uint64(O.derive(seed, [0x88, gid]))
+    k = np.arange(1, 3 * N_SPINS + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        z = s0 + k * np.uint64(O.PHI)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+    J = np.where((z >> np.uint64(63)) != 0, 1.0, -1.0)
+    i = np.arange(N_SPINS)
+    x, y, zz = i % L, (i // L) % L, i // (L * L)
+    nb = np.stack([((x + 1) % L) + L * (y + L * zz), x + L * (((y + 1) % L) + L * zz),
+                   x + L * (y + L * ((zz + 1) % L))], axis=1)
+    ci = np.repeat(i, 3).astype(np.uint32)
+    cj = nb.reshape(-1).astype(np.uint32)
+    return ci, cj, J
+
+
+def cpu_reference_rate(n_inst, n_sweeps, threads, prop_every):
+    """Reference gibbs_sweep (oracle/_ref, unmodified sources) inside the restated PT/TAPT
+    schedule, parallel_for over instances.  Falls back to the oracle C port (1 thread)."""
+    import ctypes as C
+
+    from oracle import oracle as O
+    b = np.ascontiguousarray(betas())
+    mb = np.zeros(R)
+    if O.have_ref():
+        Rf = O.ref()
+        hs = []
+        for k in range(n_inst):
+            ci, cj, J = ea_couplings_numpy(DISORDER_SEED, k)
+            hs.append(Rf.ref_graph_build(N_SPINS, len(ci), ci.ctypes.data_as(O._u32p), cj.ctypes.data_as(O._u32p),
+                                         J.ctypes.data_as(O._f64p), None, None))
+        arr = (C.c_void_p * n_inst)(*hs)
+        t0 = time.perf_counter()
+        Rf.ref_pt_run(arr, n_inst, 0, R, b.ctypes.data_as(O._f64p), SEED, n_sweeps, 1, prop_every, N_TARGETS,
+                      mb.ctypes.data_as(O._f64p), REFINE, threads, None, None, None, None)
+        dt = time.perf_counter() - t0
+        for h in hs:
+            Rf.ref_graph_free(h)
+        kind, cores = "reference", threads
+    else:
+        g = O.Graph.from_couplings(N_SPINS, *ea_couplings_numpy(DISORDER_SEED, 0))
+        t0 = time.perf_counter()
+        for k in range(n_inst):
+            pt = O.PT(g, b, SEED, k, g.index_order())
+            pt.run(n_sweeps, 1, prop_every, N_TARGETS, mb, REFINE)
+        dt = time.perf_counter() - t0
+        kind, cores = "port", 1
+    rounds = n_sweeps // prop_every if prop_every else 0
+    updates = n_inst * (R * N_SPINS * n_sweeps + rounds * N_TARGETS * N_SPINS * REFINE)
+    return updates / dt, dt, kind, cores, updates
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_inst = max(args.cpu_sample_instances, threads)
+    sweeps, every = args.cpu_sample_sweeps, args.cpu_sample_sweeps // 2
+    for _ in range(args.warmup):
+        cpu_reference_rate(n_inst, sweeps, threads, every)
+    tot_u, tot_t, kind, cores = 0, 0.0, "reference", threads
+    for _ in range(args.steps):
+        rate, dt, kind, cores, u = cpu_reference_rate(n_inst, sweeps, threads, every)
+        tot_u += u
+        tot_t += dt
+    v = tot_u / tot_t
+    sample = (f"{n_inst} instances x {sweeps} sweeps of the config-5 geometry (EA L=32, 64 slots), TAPT round "
+              f"every {every} sweeps, per step; {cores} threads on '{cpu_model()}' (nproc={threads})")
+    print(json.dumps({
+        "metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * tot_t / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u64 RNG / f64 exp (reference CPU)", "data": "synthetic",
+        "config": {"workload": "BASELINE configs[4]: 3D EA +-J L=32, 64 slots, beta linear [0.2,3.0], TAPT",
+                   "sample": sample},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ------------------------------------------------------------------ B200 arm --
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    import torch
+    import torch.distributed as dist
+
+    import paper_2509_23043_b200 as T
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if args.instances % world:
+        raise SystemExit("instances must divide evenly over the ranks")
+    I = args.instances // world
+    off = rank * I
+    S = args.sweeps_per_step
+
+    model = T.Model.lattice((L,))
+    ens = T.Ensemble(model, betas(), n_instances=I, seed=SEED, instance_offset=off)
+    stream = torch.cuda.Stream()
+    ens.set_stream(stream.cuda_stream)
+    ens.generate_ea_disorder(DISORDER_SEED)
+    ens.init_random()
+    nb = 2 * 3 * N_SPINS // 64
+    ens.set_histogram(-3 * N_SPINS, 64, nb)
+    targets = np.arange(N_TARGETS, dtype=np.uint32)
+    hist_t = torch.zeros((R, nb), dtype=torch.int64, device="cuda")
+
+    k_ev = []
+
+    def step(timed):
+        ens.generate_proposals(targets, None, REFINE)
+        if timed:
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+        ens.run(S, swap_every=1, measure_every=args.measure_every)
+        if timed:
+            b.record(stream)
+            k_ev.append((a, b))
+
+    for _ in range(args.warmup):
+        step(False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = T.launch_count()
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        t_start.record(stream)
+        for _ in range(args.steps):
+            step(True)
+        ens.histogram(device_ptr=hist_t.data_ptr())
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(hist_t)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = T.launch_count() - l0
+    ms = t_start.elapsed_time(t_end)
+    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
+    ms = float(ms_t.item())
+    upd_step_local = I * (R * N_SPINS * S + N_TARGETS * N_SPINS * REFINE)
+    upd_step = upd_step_local * world
+    value = upd_step * args.steps / (ms * 1e-3)
+
+    # roofline of the dominant kernel (K1, one launch per step, measured on its stream)
+    k_ms = float(np.mean([a.elapsed_time(b) for a, b in k_ev]))
+    k_upd = I * R * N_SPINS * S
+    achieved = k_upd / (k_ms * 1e-3)
+    peak, _ = T.probe_decision_rate(1, 512, 20000)
+    g_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs") if os.path.exists(
+        os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
+    hbm_bytes = I * (2 * 4 * N_SPINS * 2 + N_SPINS)  # spins in+out (2 groups) + bond bytes, per launch
+    roofline = {
+        "bound": "alu", "unit": "Gupdates/s", "achieved": achieved / 1e9, "peak": peak / 1e9,
+        "frac": achieved / peak, "traffic": None,
+        "peak_source": "measured on this GPU: k_decision_probe (one splitmix64 draw + threshold lookup + compare "
+                       "+ bit insert per update, no stencil, no memory traffic); BASELINE.md 4 binds the ALU roofline",
+        "kernel": "k1_lattice_pt<3,true,true>", "kernel_ms_per_launch": k_ms, "updates_per_launch": k_upd,
+        "hbm": {"achieved_gbs": hbm_bytes / (k_ms * 1e-3) / 1e9, "peak_gbs": g_hbm,
+                "frac": hbm_bytes / (k_ms * 1e-3) / 1e9 / g_hbm,
+                "note": "spins stay in shared memory for the whole 1000-sweep launch"},
+    }
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32 multi-spin words / u64 splitmix64", "data": "synthetic",
+        "config": {"workload": "BASELINE configs[4]: 3D EA +-J L=32 periodic, 64 slots beta linear [0.2,3.0], "
+                               "4096 instances sharded, TAPT round (56 targets, 5 refine sweeps) + 1000 sweeps "
+                               "(swap every sweep, measure every 10) per step",
+                   "instances_total": args.instances, "instances_per_gpu": I, "sweeps_per_step": S,
+                   "updates_per_step": upd_step, "parallelism": f"instances sharded over {world} GPU(s)",
+                   "l2": "state 1 GiB/GPU at N=1 > 126 MB L2; spins are shared-memory resident within a launch"},
+        "roofline": roofline, "gpu_launches": launches,
+    }
+    if not args.no_e2e:
+        out["e2e"] = e2e_leg(args, T, torch, ens, stream, I, S, world)
+    out["clocks"] = clk.summary()
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        n_inst = max(args.cpu_sample_instances, threads)
+        rate, dt, kind, cores, _ = cpu_reference_rate(n_inst, args.cpu_sample_sweeps, threads,
+                                                      args.cpu_sample_sweeps // 2)
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+                               "sample": f"{n_inst} instances x {args.cpu_sample_sweeps} sweeps of the config-5 "
+                                         f"geometry with a TAPT round every {args.cpu_sample_sweeps // 2} sweeps "
+                                         f"({dt:.1f} s, '{cpu_model()}')"}
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def e2e_leg(args, T, torch, ens, stream, I, S, world):
+    """Same metric through the public C-ABI call with HOST buffers: per step the externally
+    supplied proposals (bit-packed, pinned host memory) are copied H2D inside the timed
+    region, injected (energy + Eq. 2 on the device), 1000 PT sweeps run, and the per-slot
+    energies are read back D2H."""
+    nbytes = (N_SPINS + 7) // 8
+    rs = np.random.default_rng(7)
+    host = torch.from_numpy(rs.integers(0, 256, size=(I, N_TARGETS, nbytes), dtype=np.uint8)).pin_memory()
+    dev = torch.empty_like(host, device="cuda")
+    energies = torch.empty((I, R), dtype=torch.int64).pin_memory()
+    targets = np.arange(N_TARGETS, dtype=np.uint32)
+
+    def step():
+        with torch.cuda.stream(stream):
+            dev.copy_(host, non_blocking=True)
+        ens.inject_proposals_packed(None, targets, device_ptr=dev.data_ptr())
+        ens.run(S, swap_every=1, measure_every=args.measure_every)
+        energies.copy_(torch.from_numpy(ens.energies()))
+
+    for _ in range(1):
+        step()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    dt_t = torch.tensor([dt], dtype=torch.float64, device="cuda")
+    if world > 1:
+        import torch.distributed as dist
+        dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
+    dt = float(dt_t.item())
+    upd = I * R * N_SPINS * S * world * args.steps
+    return {"value": upd / dt, "unit": UNIT, "h2d_bytes_per_step": int(host.numel()),
+            "d2h_bytes_per_step": int(I * R * 8),
+            "path": "tapt_inject_proposals_packed (host-supplied proposals) + tapt_run + tapt_ensemble_get_energies"}
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,211 @@
+/*
+ * tapt_gpu.h -- C ABI of the B200-native TAPT verifier (parallel-tempering engine).
+ *
+ * The reference (/root/reference) is a C++20 library whose parallel-tempering
+ * layer exists only as a specification; this header is the flat, exception-free
+ * boundary a reference-side binding (C++ wrapper, ctypes, cgo, JNI ...) calls.
+ * Every entry point below names the reference interface it replaces:
+ *
+ *   tapt_model_create_lattice   LatticeSpec::grid2d / grid3d + graph()      proj/include/tapt/lattice.hpp:25-35, proj/src/lattice.cpp:5-24,55-87
+ *   tapt_model_create_graph     CouplingGraph::Builder(...).build()          proj/include/tapt/spin_model.hpp:32-48, proj/src/spin_model.cpp:15-77
+ *   tapt_gibbs_sweep            gibbs_sweep(g, s, beta, rng)                 proj/include/tapt/mcmc.hpp:43-45, proj/src/mcmc.cpp:30-45
+ *   tapt_ensemble_create        BetaLadder / TAPTConfig / replica state
+ *   tapt_ensemble_init_random   random_configuration per replica             proj/src/spin_model.cpp:116-121, PAPER.md:89-90 (Alg. 1 l.1-2)
+ *   tapt_sweep                  M x gibbs_sweep of every replica             PAPER.md:107-111 (Alg. 1)
+ *   tapt_swap_pass              swap_pass(replicas, ladder, parity, rng)     SPEC.md:400-408, PAPER.md:131 (Eq. 1)
+ *   tapt_run                    run_pt / run_tapt inner loop (fused)
+ *   tapt_inject_proposals       generator_move / mh_corrected_move           SPEC.md:409-425, PAPER.md:137 (Eq. 2)
+ *   tapt_generate_proposals     stand-in for IsingFormer.sample (synthetic)  BASELINE.json configs[1], configs[4]
+ *   tapt_get_energies/_spins    energy(g, s) / magnetization(s) readout      proj/src/spin_model.cpp:79-89,109-114
+ *   tapt_get_observables        RunTrace accumulators
+ *   tapt_last_error / status    tapt::*Error exceptions                      proj/include/tapt/errors.hpp:11-41
+ *
+ * Conventions
+ *   - Every function returns a tapt_status (0 = OK); no C++ exception crosses this
+ *     boundary.  The message of the last failure on the calling thread is
+ *     returned by tapt_last_error().  Status codes map 1:1 onto the reference's
+ *     eight exception types (errors.hpp) plus CUDA / NCCL / internal failures.
+ *   - Host buffers are caller-owned and copied synchronously.  Handles own all
+ *     device memory; destroy them explicitly.  Calls on one handle are stream-ordered
+ *     on the handle's CUDA stream (tapt_ensemble_set_stream).
+ *   - Slots are ladder positions (index 0 = hottest); a swap moves the
+ *     configuration, beta and dynamics stream stay with the slot.
+ *     All per-replica inputs/outputs are ordered BY SLOT.
+ *   - Spin arrays are int8 +-1, [instance][slot][site], row-major.
+ *   - Results depend only on (seed, global instance id, slot), never on the number
+ *     of GPUs, the grid shape or the kernel choice.
+ */
+#ifndef TAPT_GPU_H
+#define TAPT_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TAPT_OK = 0,
+    TAPT_ERR_CONFIG = 1,            /* ConfigError          errors.hpp:13 */
+    TAPT_ERR_DIMENSION = 2,         /* DimensionError       errors.hpp:17 */
+    TAPT_ERR_CLAMPED_SITE = 3,      /* ClampedSiteError     errors.hpp:21 */
+    TAPT_ERR_SIZE = 4,              /* SizeError            errors.hpp:25 */
+    TAPT_ERR_GEOMETRY = 5,          /* GeometryError        errors.hpp:29 */
+    TAPT_ERR_NUMERIC = 6,           /* NumericError         errors.hpp:33 */
+    TAPT_ERR_FORMAT = 7,            /* FormatError          errors.hpp:37 */
+    TAPT_ERR_TRAINING_DIVERGED = 8, /* TrainingDivergedError errors.hpp:41 */
+    TAPT_ERR_CUDA = 9,
+    TAPT_ERR_NCCL = 10,
+    TAPT_ERR_INTERNAL = 11
+} tapt_status;
+
+typedef struct tapt_model_s* tapt_model_t;
+typedef struct tapt_ensemble_s* tapt_ensemble_t;
+
+/* Sweep orders. */
+enum {
+    TAPT_ORDER_COLOUR = 0,    /* colour classes (checkerboard / greedy colouring): the parallel chain */
+    TAPT_ORDER_REFERENCE = 1  /* index-ascending, bit-exact with the reference gibbs_sweep (mcmc.cpp:34) */
+};
+
+enum { TAPT_BOUNDARY_OPEN = 0, TAPT_BOUNDARY_PERIODIC = 1 };
+
+const char* tapt_last_error(void);
+const char* tapt_version(void);
+/* Number of CUDA devices visible (0 without a GPU); never fails. */
+int tapt_device_count(void);
+/* Kernels this library has launched so far (benchmark evidence); never fails. */
+unsigned long long tapt_launch_count(void);
+/* Measured ceiling of the per-update ALU work (one splitmix64 draw + threshold lookup +
+ * compare + bit insert, no stencil, no memory traffic), in decisions per second. */
+tapt_status tapt_probe_decision_rate(int blocks_per_sm, int threads, uint32_t iters, double* decisions_per_s,
+                                     double* seconds);
+
+/* ----------------------------------------------------------------- models -- */
+
+/* LatticeSpec::grid2d(ly, lx, J, boundary) for dim == 2 (lz ignored),
+ * LatticeSpec::grid3d(l = lx, J, boundary) for dim == 3.  J must be integer-valued. */
+tapt_status tapt_model_create_lattice(int dim, int ly, int lx, int lz, double J, int boundary, tapt_model_t* out);
+
+/* CouplingGraph::Builder: n spins, n_couplings (i, j, J) triples (duplicates summed,
+ * i != j), per-spin fields h (nullable), clamp values (nullable; 0 free, +-1 clamped).
+ * Couplings and fields must be integer-valued (device thresholds are exact tables). */
+tapt_status tapt_model_create_graph(uint32_t n, uint32_t n_couplings, const uint32_t* ci, const uint32_t* cj,
+                                    const double* J, const double* h, const int8_t* clamp, tapt_model_t* out);
+tapt_status tapt_model_destroy(tapt_model_t m);
+tapt_status tapt_model_info(tapt_model_t m, uint32_t* n_spins, uint32_t* n_free, uint32_t* n_couplings,
+                            int32_t* lmin, int32_t* lmax, uint32_t* n_colours, uint32_t* n_levels);
+/* Couplings after merging/sorting (CouplingGraph::couplings(), spin_model.hpp:57). */
+tapt_status tapt_model_couplings(tapt_model_t m, uint32_t* ci, uint32_t* cj, double* J);
+/* Greedy colour of each site (clamped: -1) and dependency level (index-order schedule). */
+tapt_status tapt_model_schedule(tapt_model_t m, int32_t* colour, int32_t* level);
+/* FNV-1a content digest identical to CouplingGraph::digest() (spin_model.cpp:68-75). */
+tapt_status tapt_model_digest(tapt_model_t m, uint64_t* digest);
+
+/* Host-side energy of one configuration (spin_model.cpp:79-89), for API parity. */
+tapt_status tapt_model_energy(tapt_model_t m, const int8_t* s, size_t len, double* out);
+
+/* -------------------------------------------------------- drop-in sweeps -- */
+
+/* gibbs_sweep(g, s, beta, rng) on the device: updates s (host, n_spins entries) in
+ * place with n_sweeps consecutive index-ascending heat-bath sweeps starting at
+ * stream state *rng_state, advances *rng_state by n_sweeps*n_free draws and
+ * writes each sweep's energy change to dE (nullable).  Bit-exact with the
+ * reference for integer couplings. */
+tapt_status tapt_gibbs_sweep(tapt_model_t m, int8_t* s, size_t len, double beta, uint64_t* rng_state,
+                             uint32_t n_sweeps, double* dE);
+
+/* ------------------------------------------------------------- ensembles -- */
+
+typedef struct {
+    uint32_t n_instances;     /* instances on this device                              */
+    uint64_t instance_offset; /* global id of the first local instance (sharding)      */
+    uint32_t n_slots;         /* R: ladder length (1..256)                              */
+    const double* betas;      /* R values, strictly increasing, >= 0      */
+    uint64_t seed;            /* root seed of every stream        */
+    int order;                /* TAPT_ORDER_COLOUR or TAPT_ORDER_REFERENCE              */
+} tapt_ensemble_desc;
+
+tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, tapt_ensemble_t* out);
+tapt_status tapt_ensemble_destroy(tapt_ensemble_t e);
+/* cudaStream_t to enqueue on (NULL: the handle's own non-blocking stream). */
+tapt_status tapt_ensemble_set_stream(tapt_ensemble_t e, void* cuda_stream);
+tapt_status tapt_ensemble_synchronize(tapt_ensemble_t e);
+/* Kernel that serves sweeps of this ensemble: "lattice" (K1) or "csr" (K2). */
+const char* tapt_ensemble_kernel(tapt_ensemble_t e);
+
+/* Edwards-Anderson +-J disorder for lattice models, one sign per bond:
+ * signs [n_instances][n_bonds] (+-1, bond order of LatticeSpec::graph), or generate
+ * them on the device from (seed, global instance id). */
+tapt_status tapt_ensemble_set_bond_signs(tapt_ensemble_t e, const int8_t* signs, size_t n_bonds);
+tapt_status tapt_ensemble_generate_ea_disorder(tapt_ensemble_t e, uint64_t disorder_seed);
+tapt_status tapt_ensemble_get_bond_signs(tapt_ensemble_t e, int8_t* signs, size_t n_bonds);
+/* Per-instance clamp values [n_instances][n_spins] (only sites clamped in the model
+ * may be non-zero; they override the model's clamp values). */
+tapt_status tapt_ensemble_set_clamps(tapt_ensemble_t e, const int8_t* clamps);
+
+/* random_configuration(g, derive(seed, {kInit, gid, slot})) for every slot. */
+tapt_status tapt_ensemble_init_random(tapt_ensemble_t e);
+tapt_status tapt_ensemble_set_spins(tapt_ensemble_t e, const int8_t* spins);
+tapt_status tapt_ensemble_get_spins(tapt_ensemble_t e, int8_t* spins);
+/* Same, bit-packed: [instance][slot][ceil(n/8)] bytes, LSB-first, +1 -> 1 (ISFD1 order, mcmc.cpp:86-90). */
+tapt_status tapt_ensemble_get_spins_packed(tapt_ensemble_t e, uint8_t* packed);
+tapt_status tapt_ensemble_get_energies(tapt_ensemble_t e, int64_t* E);      /* [I][R] by slot  */
+tapt_status tapt_ensemble_get_permutation(tapt_ensemble_t e, uint8_t* buffer_of_slot); /* [I][R] */
+tapt_status tapt_ensemble_counters(tapt_ensemble_t e, uint64_t* sweeps, uint64_t* passes, uint64_t* rounds);
+/* [I][R-1] swap attempts / accepts by pair; [I][R] proposal attempts / accepts by slot (nullable). */
+tapt_status tapt_get_acceptance(tapt_ensemble_t e, uint64_t* swap_att, uint64_t* swap_acc, uint64_t* prop_att,
+                                uint64_t* prop_acc);
+
+/* Observables: per (instance, slot): count, sum E, sum E^2, sum |M|, sum M^2 (M = sum of
+ * all spins), accumulated at measurement points of tapt_run. */
+tapt_status tapt_get_observables(tapt_ensemble_t e, int64_t* obs /* [I][R][5] */);
+/* Energy histograms per slot summed over local instances: bins of `width` from e_lo. */
+tapt_status tapt_set_histogram(tapt_ensemble_t e, int64_t e_lo, int64_t width, uint32_t nbins);
+/* dst: [R][nbins] uint64, host (dst_on_device = 0) or device pointer. */
+tapt_status tapt_get_histogram(tapt_ensemble_t e, uint64_t* dst, int dst_on_device);
+tapt_status tapt_get_best(tapt_ensemble_t e, int64_t* best /* [I] */);
+tapt_status tapt_reset_observables(tapt_ensemble_t e);
+
+/* n_sweeps sweeps of every slot, no swaps (Alg. 1 lines 21-25). */
+tapt_status tapt_sweep(tapt_ensemble_t e, uint32_t n_sweeps);
+/* One swap pass over pairs (r, r+1), r = parity, parity+2, ... (Eq. 1). */
+tapt_status tapt_swap_pass(tapt_ensemble_t e, int parity);
+
+typedef struct {
+    uint32_t n_sweeps;      /* sweeps to run                                           */
+    uint32_t swap_every;    /* swap pass after every k-th global sweep (0: none);
+                               parity alternates with the global pass counter        */
+    uint32_t measure_every; /* accumulate observables every k-th global sweep (0: none) */
+    uint64_t measure_from;  /* ... only once the global sweep count exceeds this       */
+} tapt_schedule;
+
+/* Fused PT loop (run_pt inner loop): per global sweep T: sweep all slots; swap pass
+ * if swap_every | T; measure if due.  Runs device-resident with no host round trips. */
+tapt_status tapt_run(tapt_ensemble_t e, const tapt_schedule* s);
+
+/* Proposal injection (generator_move, Eq. 2).  proposals: [I][n_targets][n_spins] int8
+ * for slots targets[0..n_targets) (host pointer, or device pointer if on_device).
+ * Clamped sites are forced to their clamp values.  Round q uses accept draw slot+1 of
+ * derive(seed, {kCoordinator, gid, q+1}).  log_q_cur / log_q_prop ([I][n_targets],
+ * nullable): MH-corrected acceptance.  accepted: [I][n_targets]
+ * (nullable). */
+tapt_status tapt_inject_proposals(tapt_ensemble_t e, const int8_t* proposals, int on_device, const uint32_t* targets,
+                                  uint32_t n_targets, const double* log_q_cur, const double* log_q_prop,
+                                  uint8_t* accepted);
+/* Same, bit-packed proposals [I][n_targets][ceil(n/8)] (ISFD1 bit order). */
+tapt_status tapt_inject_proposals_packed(tapt_ensemble_t e, const uint8_t* proposals, int on_device,
+                                         const uint32_t* targets, uint32_t n_targets, uint8_t* accepted);
+
+/* Synthetic stand-in generator + Eq. 2 in one call (BASELINE configs 2 and 5): for each
+ * target slot r, i.i.d. spins with P(+1) = (1 + sign*m_bias[r])/2 (sign: coin), clamps,
+ * then `refine` sweeps at beta_r, then Metropolis acceptance.  m_bias: [n_targets]
+ * (nullable = fair coin). */
+tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, uint32_t n_targets,
+                                    const double* m_bias, uint32_t refine, uint8_t* accepted);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TAPT_GPU_H */

@@ -1,0 +1,425 @@
+"""paper_2509_23043_b200 -- B200-native TAPT verifier (parallel-tempering engine).
+
+Python mirror of the C ABI in include/tapt_gpu.h (libtapt_b200.so, built for sm_100a by
+paper_2509_23043_b200/csrc/Makefile).  The names follow the reference's C++ API
+(CouplingGraph / LatticeSpec / gibbs_sweep, /root/reference/proj/include/tapt) and the
+specified tempering layer (BetaLadder, swap_pass, generator_move, run_pt).
+
+There is no CPU fallback: importing works without a GPU, but every call that sweeps,
+swaps or accepts runs on the device and raises CudaError when none is present.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libtapt_b200.so")
+
+ORDER_COLOUR, ORDER_REFERENCE = 0, 1
+BOUNDARY_OPEN, BOUNDARY_PERIODIC = 0, 1
+
+
+class TaptError(RuntimeError):
+    status = 11
+
+
+class ConfigError(TaptError):
+    status = 1
+
+
+class DimensionError(TaptError):
+    status = 2
+
+
+class ClampedSiteError(TaptError):
+    status = 3
+
+
+class SizeError(TaptError):
+    status = 4
+
+
+class GeometryError(TaptError):
+    status = 5
+
+
+class NumericError(TaptError):
+    status = 6
+
+
+class FormatError(TaptError):
+    status = 7
+
+
+class TrainingDivergedError(TaptError):
+    status = 8
+
+
+class CudaError(TaptError):
+    status = 9
+
+
+class NcclError(TaptError):
+    status = 10
+
+
+_BY_STATUS = {c.status: c for c in (ConfigError, DimensionError, ClampedSiteError, SizeError, GeometryError,
+                                    NumericError, FormatError, TrainingDivergedError, CudaError, NcclError)}
+
+_u64p = C.POINTER(C.c_uint64)
+_u32p = C.POINTER(C.c_uint32)
+_i32p = C.POINTER(C.c_int32)
+_i64p = C.POINTER(C.c_int64)
+_i8p = C.POINTER(C.c_int8)
+_u8p = C.POINTER(C.c_uint8)
+_f64p = C.POINTER(C.c_double)
+_vp = C.c_void_p
+
+
+class EnsembleDesc(C.Structure):
+    _fields_ = [("n_instances", C.c_uint32), ("instance_offset", C.c_uint64), ("n_slots", C.c_uint32),
+                ("betas", _f64p), ("seed", C.c_uint64), ("order", C.c_int)]
+
+
+class Schedule(C.Structure):
+    _fields_ = [("n_sweeps", C.c_uint32), ("swap_every", C.c_uint32), ("measure_every", C.c_uint32),
+                ("measure_from", C.c_uint64)]
+
+
+_SIGS = {
+    "tapt_last_error": (C.c_char_p, []),
+    "tapt_version": (C.c_char_p, []),
+    "tapt_device_count": (C.c_int, []),
+    "tapt_launch_count": (C.c_ulonglong, []),
+    "tapt_probe_decision_rate": (C.c_int, [C.c_int, C.c_int, C.c_uint32, _f64p, _f64p]),
+    "tapt_model_create_lattice": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(_vp)]),
+    "tapt_model_create_graph": (C.c_int, [C.c_uint32, C.c_uint32, _u32p, _u32p, _f64p, _f64p, _i8p, C.POINTER(_vp)]),
+    "tapt_model_destroy": (C.c_int, [_vp]),
+    "tapt_model_info": (C.c_int, [_vp, _u32p, _u32p, _u32p, _i32p, _i32p, _u32p, _u32p]),
+    "tapt_model_couplings": (C.c_int, [_vp, _u32p, _u32p, _f64p]),
+    "tapt_model_schedule": (C.c_int, [_vp, _i32p, _i32p]),
+    "tapt_model_digest": (C.c_int, [_vp, _u64p]),
+    "tapt_model_energy": (C.c_int, [_vp, _i8p, C.c_size_t, _f64p]),
+    "tapt_gibbs_sweep": (C.c_int, [_vp, _i8p, C.c_size_t, C.c_double, _u64p, C.c_uint32, _f64p]),
+    "tapt_ensemble_create": (C.c_int, [_vp, C.POINTER(EnsembleDesc), C.POINTER(_vp)]),
+    "tapt_ensemble_destroy": (C.c_int, [_vp]),
+    "tapt_ensemble_set_stream": (C.c_int, [_vp, _vp]),
+    "tapt_ensemble_synchronize": (C.c_int, [_vp]),
+    "tapt_ensemble_kernel": (C.c_char_p, [_vp]),
+    "tapt_ensemble_set_bond_signs": (C.c_int, [_vp, _i8p, C.c_size_t]),
+    "tapt_ensemble_generate_ea_disorder": (C.c_int, [_vp, C.c_uint64]),
+    "tapt_ensemble_get_bond_signs": (C.c_int, [_vp, _i8p, C.c_size_t]),
+    "tapt_ensemble_set_clamps": (C.c_int, [_vp, _i8p]),
+    "tapt_ensemble_init_random": (C.c_int, [_vp]),
+    "tapt_ensemble_set_spins": (C.c_int, [_vp, _i8p]),
+    "tapt_ensemble_get_spins": (C.c_int, [_vp, _i8p]),
+    "tapt_ensemble_get_spins_packed": (C.c_int, [_vp, _u8p]),
+    "tapt_ensemble_get_energies": (C.c_int, [_vp, _i64p]),
+    "tapt_ensemble_get_permutation": (C.c_int, [_vp, _u8p]),
+    "tapt_ensemble_counters": (C.c_int, [_vp, _u64p, _u64p, _u64p]),
+    "tapt_get_acceptance": (C.c_int, [_vp, _u64p, _u64p, _u64p, _u64p]),
+    "tapt_get_observables": (C.c_int, [_vp, _i64p]),
+    "tapt_set_histogram": (C.c_int, [_vp, C.c_int64, C.c_int64, C.c_uint32]),
+    "tapt_get_histogram": (C.c_int, [_vp, _vp, C.c_int]),
+    "tapt_get_best": (C.c_int, [_vp, _i64p]),
+    "tapt_reset_observables": (C.c_int, [_vp]),
+    "tapt_sweep": (C.c_int, [_vp, C.c_uint32]),
+    "tapt_swap_pass": (C.c_int, [_vp, C.c_int]),
+    "tapt_run": (C.c_int, [_vp, C.POINTER(Schedule)]),
+    "tapt_inject_proposals": (C.c_int, [_vp, _vp, C.c_int, _u32p, C.c_uint32, _f64p, _f64p, _u8p]),
+    "tapt_inject_proposals_packed": (C.c_int, [_vp, _vp, C.c_int, _u32p, C.c_uint32, _u8p]),
+    "tapt_generate_proposals": (C.c_int, [_vp, _u32p, C.c_uint32, _f64p, C.c_uint32, _u8p]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libtapt_b200.so (raises if it was not built -- there is no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: build it with `make -C paper_2509_23043_b200/csrc` "
+                              "(or __graft_entry__.build()); the TAPT engine has no CPU fallback")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _SIGS.items():
+            f = getattr(L, name)
+            f.restype = res
+            f.argtypes = args
+        _lib = L
+    return _lib
+
+
+def exported_symbols():
+    return list(_SIGS)
+
+
+def _check(status):
+    if status != 0:
+        msg = lib().tapt_last_error().decode(errors="replace")
+        raise _BY_STATUS.get(status, TaptError)(msg)
+
+
+def _p(a, t):
+    return None if a is None else a.ctypes.data_as(t)
+
+
+def device_count() -> int:
+    return int(lib().tapt_device_count())
+
+
+def launch_count() -> int:
+    """Kernels launched by libtapt_b200.so in this process."""
+    return int(lib().tapt_launch_count())
+
+
+def probe_decision_rate(blocks_per_sm=1, threads=512, iters=2000):
+    """Measured decisions/s of the bare per-update ALU work (roofline denominator)."""
+    r, sec = C.c_double(), C.c_double()
+    _check(lib().tapt_probe_decision_rate(blocks_per_sm, threads, iters, C.byref(r), C.byref(sec)))
+    return r.value, sec.value
+
+
+# ------------------------------------------------------------------- models --
+
+class Model:
+    """A device-resident Ising problem (CouplingGraph, spin_model.hpp:30-113)."""
+
+    def __init__(self, handle, kind):
+        self._h = handle
+        self.kind = kind
+        n, nf, nc = C.c_uint32(), C.c_uint32(), C.c_uint32()
+        lo, hi, nco, nlv = C.c_int32(), C.c_int32(), C.c_uint32(), C.c_uint32()
+        _check(lib().tapt_model_info(self._h, C.byref(n), C.byref(nf), C.byref(nc), C.byref(lo), C.byref(hi),
+                                     C.byref(nco), C.byref(nlv)))
+        self.n_spins, self.n_free, self.n_couplings = n.value, nf.value, nc.value
+        self.lmin, self.lmax, self.n_colours, self.n_levels = lo.value, hi.value, nco.value, nlv.value
+
+    @classmethod
+    def lattice(cls, dims, J=1.0, periodic=True):
+        """LatticeSpec::grid2d(ly, lx) for dims=(ly, lx); grid3d(l) for dims=(l,)."""
+        dims = tuple(int(x) for x in dims)
+        h = _vp()
+        if len(dims) == 2:
+            _check(lib().tapt_model_create_lattice(2, dims[0], dims[1], 1, float(J), int(bool(periodic)), C.byref(h)))
+        elif len(dims) == 1:
+            _check(lib().tapt_model_create_lattice(3, dims[0], dims[0], dims[0], float(J), int(bool(periodic)),
+                                                   C.byref(h)))
+        else:
+            raise ConfigError("dims must be (ly, lx) or (l,)")
+        m = cls(h, "lattice")
+        m.dims = dims
+        return m
+
+    @classmethod
+    def graph(cls, n, ci, cj, J, h=None, clamp=None):
+        """CouplingGraph::Builder(n).add_coupling(...).add_field(...).set_clamp(...).build()."""
+        ci = np.ascontiguousarray(ci, np.uint32)
+        cj = np.ascontiguousarray(cj, np.uint32)
+        J = np.ascontiguousarray(J, np.float64)
+        hh = None if h is None else np.ascontiguousarray(h, np.float64)
+        cl = None if clamp is None else np.ascontiguousarray(clamp, np.int8)
+        hdl = _vp()
+        _check(lib().tapt_model_create_graph(int(n), len(ci), _p(ci, _u32p), _p(cj, _u32p), _p(J, _f64p),
+                                             _p(hh, _f64p), _p(cl, _i8p), C.byref(hdl)))
+        return cls(hdl, "graph")
+
+    def couplings(self):
+        m = self.n_couplings
+        ci, cj, J = np.zeros(m, np.uint32), np.zeros(m, np.uint32), np.zeros(m)
+        _check(lib().tapt_model_couplings(self._h, _p(ci, _u32p), _p(cj, _u32p), _p(J, _f64p)))
+        return ci, cj, J
+
+    def schedule(self):
+        col, lev = np.zeros(self.n_spins, np.int32), np.zeros(self.n_spins, np.int32)
+        _check(lib().tapt_model_schedule(self._h, _p(col, _i32p), _p(lev, _i32p)))
+        return col, lev
+
+    def digest(self) -> int:
+        d = C.c_uint64()
+        _check(lib().tapt_model_digest(self._h, C.byref(d)))
+        return d.value
+
+    def energy(self, s) -> float:
+        s = np.ascontiguousarray(s, np.int8)
+        out = C.c_double()
+        _check(lib().tapt_model_energy(self._h, _p(s, _i8p), len(s), C.byref(out)))
+        return out.value
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tapt_model_destroy(self._h)
+            self._h = None
+
+
+def gibbs_sweep(model: Model, s: np.ndarray, beta: float, rng_state: int, n_sweeps: int = 1):
+    """Drop-in for tapt::gibbs_sweep (mcmc.cpp:30-45), on the device, index-ascending.
+    Updates s in place; returns (new rng_state, per-sweep dE array)."""
+    if s.dtype != np.int8 or not s.flags.c_contiguous:
+        raise DimensionError("spins must be a contiguous int8 array")
+    st = C.c_uint64(rng_state)
+    dE = np.zeros(max(n_sweeps, 1))
+    _check(lib().tapt_gibbs_sweep(model._h, _p(s, _i8p), len(s), float(beta), C.byref(st), int(n_sweeps),
+                                  _p(dE, _f64p)))
+    return st.value, dE[:n_sweeps]
+
+
+# ---------------------------------------------------------------- ensembles --
+
+class Ensemble:
+    """I instances x R ladder slots of replicas, device-resident."""
+
+    def __init__(self, model: Model, betas, n_instances=1, seed=0, instance_offset=0, order="colour"):
+        self.model = model
+        self.betas = np.ascontiguousarray(betas, np.float64)
+        self.R = len(self.betas)
+        self.I = int(n_instances)
+        self.n = model.n_spins
+        o = {"colour": ORDER_COLOUR, "color": ORDER_COLOUR, "checkerboard": ORDER_COLOUR,
+             "reference": ORDER_REFERENCE, "index": ORDER_REFERENCE}[order] if isinstance(order, str) else int(order)
+        d = EnsembleDesc(self.I, int(instance_offset), self.R, _p(self.betas, _f64p), int(seed) & (2**64 - 1), o)
+        self._h = _vp()
+        _check(lib().tapt_ensemble_create(model._h, C.byref(d), C.byref(self._h)))
+        self.kernel = lib().tapt_ensemble_kernel(self._h).decode()
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tapt_ensemble_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    # -- setup
+    def set_stream(self, cuda_stream_ptr):
+        _check(lib().tapt_ensemble_set_stream(self._h, cuda_stream_ptr))
+
+    def synchronize(self):
+        _check(lib().tapt_ensemble_synchronize(self._h))
+
+    def set_bond_signs(self, signs):
+        signs = np.ascontiguousarray(signs, np.int8).reshape(self.I, -1)
+        _check(lib().tapt_ensemble_set_bond_signs(self._h, _p(signs, _i8p), signs.shape[1]))
+
+    def generate_ea_disorder(self, seed):
+        _check(lib().tapt_ensemble_generate_ea_disorder(self._h, int(seed)))
+
+    def bond_signs(self, n_bonds):
+        out = np.zeros((self.I, n_bonds), np.int8)
+        _check(lib().tapt_ensemble_get_bond_signs(self._h, _p(out, _i8p), n_bonds))
+        return out
+
+    def set_clamps(self, clamps):
+        clamps = np.ascontiguousarray(clamps, np.int8).reshape(self.I, self.n)
+        _check(lib().tapt_ensemble_set_clamps(self._h, _p(clamps, _i8p)))
+
+    def init_random(self):
+        _check(lib().tapt_ensemble_init_random(self._h))
+
+    def set_spins(self, spins):
+        spins = np.ascontiguousarray(spins, np.int8).reshape(self.I, self.R, self.n)
+        _check(lib().tapt_ensemble_set_spins(self._h, _p(spins, _i8p)))
+
+    # -- readout
+    def spins(self):
+        out = np.zeros((self.I, self.R, self.n), np.int8)
+        _check(lib().tapt_ensemble_get_spins(self._h, _p(out, _i8p)))
+        return out
+
+    def spins_packed(self):
+        out = np.zeros((self.I, self.R, (self.n + 7) // 8), np.uint8)
+        _check(lib().tapt_ensemble_get_spins_packed(self._h, _p(out, _u8p)))
+        return out
+
+    def energies(self):
+        out = np.zeros((self.I, self.R), np.int64)
+        _check(lib().tapt_ensemble_get_energies(self._h, _p(out, _i64p)))
+        return out
+
+    def permutation(self):
+        out = np.zeros((self.I, self.R), np.uint8)
+        _check(lib().tapt_ensemble_get_permutation(self._h, _p(out, _u8p)))
+        return out
+
+    def counters(self):
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        _check(lib().tapt_ensemble_counters(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    def acceptance(self):
+        np_ = max(self.R - 1, 1)
+        sa, sc = np.zeros((self.I, np_), np.uint64), np.zeros((self.I, np_), np.uint64)
+        pa, pc = np.zeros((self.I, self.R), np.uint64), np.zeros((self.I, self.R), np.uint64)
+        _check(lib().tapt_get_acceptance(self._h, _p(sa, _u64p), _p(sc, _u64p), _p(pa, _u64p), _p(pc, _u64p)))
+        return sa[:, : self.R - 1], sc[:, : self.R - 1], pa, pc
+
+    def observables(self):
+        out = np.zeros((self.I, self.R, 5), np.int64)
+        _check(lib().tapt_get_observables(self._h, _p(out, _i64p)))
+        return out
+
+    def set_histogram(self, e_lo, width, nbins):
+        self._nbins = int(nbins)
+        _check(lib().tapt_set_histogram(self._h, int(e_lo), int(width), int(nbins)))
+
+    def histogram(self, device_ptr=None):
+        if device_ptr is not None:
+            _check(lib().tapt_get_histogram(self._h, device_ptr, 1))
+            return None
+        out = np.zeros((self.R, self._nbins), np.uint64)
+        _check(lib().tapt_get_histogram(self._h, out.ctypes.data, 0))
+        return out
+
+    def best(self):
+        out = np.zeros(self.I, np.int64)
+        _check(lib().tapt_get_best(self._h, _p(out, _i64p)))
+        return out
+
+    def reset_observables(self):
+        _check(lib().tapt_reset_observables(self._h))
+
+    # -- dynamics
+    def sweep(self, n_sweeps=1):
+        _check(lib().tapt_sweep(self._h, int(n_sweeps)))
+
+    def swap_pass(self, parity):
+        _check(lib().tapt_swap_pass(self._h, int(parity)))
+
+    def run(self, n_sweeps, swap_every=1, measure_every=0, measure_from=0):
+        s = Schedule(int(n_sweeps), int(swap_every), int(measure_every), int(measure_from))
+        _check(lib().tapt_run(self._h, C.byref(s)))
+
+    def inject_proposals(self, proposals, targets, log_q_cur=None, log_q_prop=None, device_ptr=None):
+        t = np.ascontiguousarray(targets, np.uint32)
+        acc = np.zeros((self.I, len(t)), np.uint8)
+        lqc = None if log_q_cur is None else np.ascontiguousarray(log_q_cur, np.float64)
+        lqp = None if log_q_prop is None else np.ascontiguousarray(log_q_prop, np.float64)
+        if device_ptr is not None:
+            _check(lib().tapt_inject_proposals(self._h, device_ptr, 1, _p(t, _u32p), len(t), _p(lqc, _f64p),
+                                               _p(lqp, _f64p), _p(acc, _u8p)))
+        else:
+            p = np.ascontiguousarray(proposals, np.int8).reshape(self.I, len(t), self.n)
+            _check(lib().tapt_inject_proposals(self._h, p.ctypes.data, 0, _p(t, _u32p), len(t), _p(lqc, _f64p),
+                                               _p(lqp, _f64p), _p(acc, _u8p)))
+        return acc
+
+    def inject_proposals_packed(self, packed, targets, device_ptr=None):
+        t = np.ascontiguousarray(targets, np.uint32)
+        acc = np.zeros((self.I, len(t)), np.uint8)
+        if device_ptr is not None:
+            _check(lib().tapt_inject_proposals_packed(self._h, device_ptr, 1, _p(t, _u32p), len(t), _p(acc, _u8p)))
+        else:
+            p = np.ascontiguousarray(packed, np.uint8)
+            _check(lib().tapt_inject_proposals_packed(self._h, p.ctypes.data, 0, _p(t, _u32p), len(t), _p(acc, _u8p)))
+        return acc
+
+    def generate_proposals(self, targets, m_bias=None, refine=5):
+        t = np.ascontiguousarray(targets, np.uint32)
+        mb = None if m_bias is None else np.ascontiguousarray(m_bias, np.float64)
+        acc = np.zeros((self.I, len(t)), np.uint8)
+        _check(lib().tapt_generate_proposals(self._h, _p(t, _u32p), len(t), _p(mb, _f64p), int(refine),
+                                             _p(acc, _u8p)))
+        return acc

@@ -1,0 +1,154 @@
+// common.cuh -- device-side building blocks shared by every TAPT kernel.
+//
+// RNG: the reference's counter-based splitmix64 (proj/include/tapt/rng.hpp:21-32,58-65).
+// Draw k (1-based) of a stream whose state is s0 is  mix_final(s0 + k*phi), so any
+// draw can be computed from (stream state, counter) with no sequential state.
+//
+// Heat-bath decision (proj/src/mcmc.cpp:13-15,38):  uniform() < p  with
+// uniform = (x>>11)*2^-53.  The host turns p into the integer threshold
+// T = ceil(p*2^53), so the device decides with integers only:  (x>>11) < T.
+// Fast path: only the high 32 bits of x are produced; they decide unless they
+// equal the high word of T*2^11-1 (probability 2^-32), in which case the exact
+// 64-bit test is redone.
+#pragma once
+#include <cstdint>
+
+namespace tapt_dev {
+
+constexpr uint64_t kPhi = 0x9E3779B97F4A7C15ull;
+constexpr uint64_t kM1 = 0xBF58476D1CE4E5B9ull;
+constexpr uint64_t kM2 = 0x94D049BB133111EBull;
+
+__host__ __device__ __forceinline__ uint64_t mix_final(uint64_t z) {
+    z = (z ^ (z >> 30)) * kM1;
+    z = (z ^ (z >> 27)) * kM2;
+    return z ^ (z >> 31);
+}
+
+__host__ __device__ __forceinline__ uint64_t draw(uint64_t s0, uint64_t k) { return mix_final(s0 + k * kPhi); }
+
+// High word of mix_final(z): the last xor-shift only needs z_hi for the top word.
+__device__ __forceinline__ uint32_t mix_final_hi(uint64_t z) {
+    z = (z ^ (z >> 30)) * kM1;
+    z = (z ^ (z >> 27)) * kM2;
+    const uint32_t h = static_cast<uint32_t>(z >> 32);
+    return h ^ (h >> 31);
+}
+
+// High word of T*2^11 - 1 (T in [0, 2^53]); T = 0 maps to 0 and is resolved by the tie path.
+__host__ __device__ __forceinline__ uint32_t thr_hi(uint64_t T) {
+    return T == 0 ? 0u : static_cast<uint32_t>(((T << 11) - 1ull) >> 32);
+}
+
+// Exact decision on a full draw.
+__host__ __device__ __forceinline__ bool below(uint64_t x, uint64_t T) { return (x >> 11) < T; }
+
+// Metropolis decision with a tabulated threshold over integer energy differences
+// (swap Eq. 1 / proposal Eq. 2):  accept iff uniform < exp(c * dE).
+//   dE >= 0          -> always (exp >= 1 > uniform)
+//   0 < -dE < K      -> tab[-dE]
+//   K <= -dE <= kz   -> threshold 1 (exp(c*dE)*2^53 in (0,1])
+//   -dE > kz         -> threshold 0 (exp underflows to 0)
+struct MetroTable {
+    const uint64_t* tab;  // per row: K entries, tab[0] = 2^53
+    const uint32_t* off;  // row offset into tab
+    const uint32_t* K;    // row length
+    const int64_t* kz;    // largest -dE with nonzero probability (-1: none beyond table)
+    const uint8_t* always;  // row accepts everything (c == 0)
+};
+
+__device__ __forceinline__ bool metro_accept(const MetroTable& t, int row, int64_t dE, uint64_t x) {
+    if (dE >= 0 || t.always[row]) return true;
+    const int64_t k = -dE;
+    uint64_t T;
+    if (k < static_cast<int64_t>(t.K[row]))
+        T = t.tab[t.off[row] + k];
+    else
+        T = (k <= t.kz[row]) ? 1ull : 0ull;
+    return below(x, T);
+}
+
+// ------------------------------------------------------------ bit slicing --
+
+__device__ __forceinline__ uint32_t maj3(uint32_t a, uint32_t b, uint32_t c) { return (a & b) | (c & (a | b)); }
+
+// Add a 3-plane sliced value (u0 + 2u1 + 4u2) into a K-plane sliced counter.
+template <int K>
+__device__ __forceinline__ void sliced_add3(uint32_t (&C)[K], uint32_t u0, uint32_t u1, uint32_t u2) {
+    uint32_t carry = C[0] & u0;
+    C[0] ^= u0;
+    uint32_t s = C[1] ^ u1 ^ carry;
+    carry = maj3(C[1], u1, carry);
+    C[1] = s;
+    s = C[2] ^ u2 ^ carry;
+    carry = maj3(C[2], u2, carry);
+    C[2] = s;
+#pragma unroll
+    for (int k = 3; k < K; ++k) {
+        const uint32_t c = C[k] & carry;
+        C[k] ^= carry;
+        carry = c;
+    }
+}
+
+// Add a 1-plane value into a K-plane sliced counter.
+template <int K>
+__device__ __forceinline__ void sliced_add1(uint32_t (&C)[K], uint32_t u) {
+    uint32_t carry = u;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        const uint32_t c = C[k] & carry;
+        C[k] ^= carry;
+        carry = c;
+    }
+}
+
+// 32x32 bit transpose across a warp: afterwards lane b holds, in bit l, bit b of
+// lane l's input word.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t w) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int j = 16 >> s;
+        const uint32_t m = masks[s];
+        const uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, w, j);
+        w = (lane & j) ? ((w & ~m) | ((o & ~m) >> j)) : ((w & m) | ((o & m) << j));
+    }
+    return w;
+}
+
+// Per-replica totals of a K-plane sliced counter summed over the warp: lane b
+// returns sum over lanes of the value held for replica (bit) b.
+template <int K>
+__device__ __forceinline__ uint32_t warp_sliced_total(const uint32_t (&C)[K]) {
+    uint32_t tot = 0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) tot += static_cast<uint32_t>(__popc(warp_transpose32(C[k]))) << k;
+    return tot;
+}
+
+// Lane b receives sum over lanes of v[b] (butterfly reduce-scatter, 31 shuffles).
+__device__ __forceinline__ int32_t warp_reduce_scatter32(int32_t (&v)[32]) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int j = 16 >> s;  // partner distance; keep half of the entries each stage
+#pragma unroll
+        for (int e = 0; e < j; ++e) {
+            // entries e and e+j: lanes with bit j clear keep e, others keep e+j
+            const bool hi = (lane & j) != 0;
+            const int32_t send = hi ? v[e] : v[e + j];
+            const int32_t recv = __shfl_xor_sync(0xFFFFFFFFu, send, j);
+            if (hi)
+                v[e + j] += recv;
+            else
+                v[e] += recv;
+            // compact: the kept entry goes to position e
+            v[e] = hi ? v[e + j] : v[e];
+        }
+    }
+    return v[0];
+}
+
+}  // namespace tapt_dev

@@ -1,0 +1,1455 @@
+// engine.cu -- host driver of the B200 TAPT verifier and the C ABI of include/tapt_gpu.h.
+//
+// Responsibilities: build the device model (the reference's CouplingGraph semantics,
+// spin_model.cpp:15-77, and LatticeSpec, lattice.cpp:55-87), turn every probability
+// the reference evaluates with libm exp into an exact integer threshold table on the
+// host (heat-bath: mcmc.cpp:13-15; swaps: Eq. 1; proposals: Eq. 2), derive the RNG
+// stream states (rng.hpp:21-27), choose the kernel (K1 lattice / K2 CSR), and keep the
+// global sweep / pass / round counters that address every random draw.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "tapt/errors.hpp"
+#include "tapt/rng.hpp"
+#include "tapt_gpu.h"
+
+namespace tapt_dev {
+cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st);
+cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st);
+size_t k1_smem_bytes(int n, bool dis);
+size_t k2_smem_bytes(int n, int R, int nidx);
+cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st);
+__global__ void k_init_random(uint32_t*, int, int, int, int, const uint64_t*, const int8_t*, int);
+__global__ void k_energy_csr(const uint32_t*, int, int, int, int, const uint32_t*, const uint32_t*, const int8_t*, int,
+                             int, const int32_t*, int32_t*);
+__global__ void k_get_spins(const uint32_t*, int, int, int, int, const uint8_t*, int, int8_t*);
+__global__ void k_get_packed(const uint32_t*, int, int, int, const uint8_t*, int, uint8_t*);
+__global__ void k_set_spins(uint32_t*, int, int, int, int, const uint8_t*, const int8_t*, int, const int8_t*, int);
+__global__ void k_set_packed(uint32_t*, int, int, int, int, const uint8_t*, int, const int8_t*, int);
+__global__ void k_swap_pass(const int32_t*, uint8_t*, uint8_t*, int, const uint64_t*, uint64_t, int, MetroTable,
+                            uint64_t*, uint64_t*);
+__global__ void k_accept_proposals(int32_t*, const uint8_t*, int, const int32_t*, int, const uint32_t*,
+                                   const uint64_t*, MetroTable, const uint8_t*, uint8_t*, uint64_t*, uint64_t*);
+__global__ void k_apply_proposals(uint32_t*, int, int, int, const uint8_t*, int, const uint32_t*, int, int,
+                                  const uint32_t*, int, const uint8_t*);
+__global__ void k_gen_proposals(uint32_t*, int, int, int, int, const uint64_t*, const uint64_t*, const int8_t*, int);
+__global__ void k_ea_signs(int8_t*, int, int, const uint64_t*);
+__global__ void k_bond_bytes(const int8_t*, uint8_t*, LatDims, int);
+__global__ void k_csr_from_signs(const int8_t*, int, const uint32_t*, int, int, int8_t*);
+}  // namespace tapt_dev
+
+using namespace tapt_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_launches{0};  // kernels launched by this library (bench evidence)
+
+#define CUDA_OK(expr)                                                                                    \
+    do {                                                                                                 \
+        cudaError_t e_ = (expr);                                                                         \
+        if (e_ != cudaSuccess) throw tapt::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class F>
+tapt_status guard(F&& f) {
+    try {
+        f();
+        return TAPT_OK;
+    } catch (const tapt::ConfigError& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_CONFIG;
+    } catch (const tapt::DimensionError& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_DIMENSION;
+    } catch (const tapt::ClampedSiteError& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_CLAMPED_SITE;
+    } catch (const tapt::SizeError& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_SIZE;
+    } catch (const tapt::GeometryError& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_GEOMETRY;
+    } catch (const tapt::NumericError& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_NUMERIC;
+    } catch (const tapt::FormatError& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_FORMAT;
+    } catch (const tapt::CudaError& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_CUDA;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return TAPT_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_INTERNAL;
+    }
+}
+
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+    void alloc(size_t count) {
+        if (count == n && p) return;
+        release();
+        if (count == 0) return;
+        CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+        n = count;
+    }
+    void zero(cudaStream_t st) {
+        if (p) CUDA_OK(cudaMemsetAsync(p, 0, n * sizeof(T), st));
+    }
+    void upload(const std::vector<T>& h, cudaStream_t st) {
+        alloc(h.size());
+        if (n) CUDA_OK(cudaMemcpyAsync(p, h.data(), n * sizeof(T), cudaMemcpyHostToDevice, st));
+    }
+    void upload(const T* h, size_t count, cudaStream_t st) {
+        alloc(count);
+        if (n) CUDA_OK(cudaMemcpyAsync(p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+    }
+    std::vector<T> download(cudaStream_t st) const {
+        std::vector<T> h(n);
+        if (n) {
+            CUDA_OK(cudaMemcpyAsync(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, st));
+            CUDA_OK(cudaStreamSynchronize(st));
+        }
+        return h;
+    }
+};
+
+bool is_integer(double v) { return std::isfinite(v) && std::nearbyint(v) == v && std::fabs(v) < 1e9; }
+
+int ilog2_exact(int v) {
+    if (v <= 0 || (v & (v - 1))) return -1;
+    int k = 0;
+    while ((1 << k) < v) ++k;
+    return k;
+}
+
+// ceil(p * 2^53): uniform() < p  <=>  (x >> 11) < threshold  (uniform = (x>>11) 2^-53, rng.hpp:35)
+uint64_t threshold_of(double p) {
+    if (!(p > 0.0)) return 0;
+    if (p >= 1.0) return 1ull << 53;
+    return static_cast<uint64_t>(std::ceil(p * 9007199254740992.0));
+}
+
+// The reference heat-bath conditional, evaluated exactly as mcmc.cpp:13-15 does.
+double conditional_up(double beta, double local) { return 1.0 / (1.0 + std::exp(-2.0 * beta * local)); }
+
+uint64_t fnv1a(const void* data, size_t n, uint64_t h) {
+    const unsigned char* c = static_cast<const unsigned char*>(data);
+    for (size_t k = 0; k < n; ++k) {
+        h ^= c[k];
+        h *= 0x100000001B3ull;
+    }
+    return h;
+}
+
+// Host table for the Metropolis rule  accept iff uniform < exp(c * dE)  (dE integer <= 0).
+struct HostMetro {
+    std::vector<uint64_t> tab;
+    std::vector<uint32_t> off, K;
+    std::vector<int64_t> kz;
+    std::vector<uint8_t> always;
+    void add_row(double c) {
+        off.push_back(static_cast<uint32_t>(tab.size()));
+        if (!(c > 0.0)) {  // c == 0: exp(0) = 1 > uniform always
+            always.push_back(1);
+            K.push_back(1);
+            kz.push_back(-1);
+            tab.push_back(1ull << 53);
+            return;
+        }
+        always.push_back(0);
+        uint32_t k = 0;
+        for (;; ++k) {
+            const double e = std::exp(c * -static_cast<double>(k));
+            const uint64_t T = threshold_of(e);
+            tab.push_back(T);
+            if (T <= 1) break;
+            if (tab.size() > (64u << 20)) throw tapt::ConfigError("beta spacing too fine for exact Metropolis tables");
+        }
+        K.push_back(k + 1);
+        // largest k with exp(-c k) > 0 (threshold 1 between K and kz, 0 beyond)
+        int64_t lo = k, hi = int64_t(1) << 40;
+        if (std::exp(c * -static_cast<double>(lo)) == 0.0) {
+            kz.push_back(lo - 1);
+            return;
+        }
+        while (hi - lo > 1) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            if (std::exp(c * -static_cast<double>(mid)) > 0.0)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        kz.push_back(lo);
+    }
+};
+
+struct DevMetro {
+    DevBuf<uint64_t> tab;
+    DevBuf<uint32_t> off, K;
+    DevBuf<int64_t> kz;
+    DevBuf<uint8_t> always;
+    void upload(const HostMetro& h, cudaStream_t st) {
+        tab.upload(h.tab, st);
+        off.upload(h.off, st);
+        K.upload(h.K, st);
+        kz.upload(h.kz, st);
+        always.upload(h.always, st);
+    }
+    MetroTable view() const { return MetroTable{tab.p, off.p, K.p, kz.p, always.p}; }
+};
+
+}  // namespace
+
+// =================================================================== model ===
+
+struct tapt_model_s {
+    uint32_t n = 0;
+    std::vector<uint32_t> ci, cj;  // merged, sorted (i<j)
+    std::vector<double> J;
+    std::vector<uint32_t> bond_of;  // per merged coupling: index in the add order (lattices)
+    std::vector<double> h;
+    std::vector<int8_t> clamp;
+    std::vector<uint32_t> rowptr, col, adj_bond;
+    std::vector<int8_t> adjJ;
+    std::vector<int32_t> hi;
+    std::vector<uint32_t> free_sites, rank;
+    std::vector<int32_t> colour, level;
+    std::vector<uint32_t> col_ptr, col_sites, lev_ptr, lev_sites;
+    int lmin = 0, lmax = 0, max_sumabs = 0;
+    uint64_t digest = 0;
+    // lattice
+    bool lattice = false, k1 = false;
+    int dim = 0, ly = 0, lx = 0, lz = 0, boundary = 0, J0 = 0, Jsign = 1;
+    uint32_t nbonds = 0;
+    LatDims ld{};
+    // device copies
+    bool on_device = false;
+    DevBuf<uint32_t> d_rowptr, d_col, d_rank, d_colptr, d_colsites, d_levptr, d_levsites, d_adjbond;
+    DevBuf<int8_t> d_J, d_clamp;
+    DevBuf<int32_t> d_h;
+
+    void ensure_device(cudaStream_t st) {
+        if (on_device) return;
+        d_rowptr.upload(rowptr, st);
+        d_col.upload(col, st);
+        d_rank.upload(rank, st);
+        d_colptr.upload(col_ptr, st);
+        d_colsites.upload(col_sites, st);
+        d_levptr.upload(lev_ptr, st);
+        d_levsites.upload(lev_sites, st);
+        d_adjbond.upload(adj_bond, st);
+        d_J.upload(adjJ, st);
+        d_clamp.upload(clamp, st);
+        d_h.upload(hi, st);
+        CUDA_OK(cudaStreamSynchronize(st));
+        on_device = true;
+    }
+};
+
+namespace {
+
+// CouplingGraph::Builder::build semantics (spin_model.cpp:15-77) plus the schedules.
+void build_model(tapt_model_s& m, uint32_t n, const std::vector<uint32_t>& ai, const std::vector<uint32_t>& aj,
+                 const std::vector<double>& aJ, const double* h, const int8_t* clamp) {
+    m.n = n;
+    std::map<std::pair<uint32_t, uint32_t>, std::pair<double, uint32_t>> merged;
+    for (size_t k = 0; k < ai.size(); ++k) {
+        uint32_t i = ai[k], j = aj[k];
+        if (i == j) throw tapt::ConfigError("self-coupling on spin " + std::to_string(i));
+        if (i >= n || j >= n) throw tapt::ConfigError("coupling index out of range");
+        if (i > j) std::swap(i, j);
+        auto it = merged.find({i, j});
+        if (it == merged.end())
+            merged.emplace(std::make_pair(i, j), std::make_pair(aJ[k], static_cast<uint32_t>(k)));
+        else
+            it->second.first += aJ[k];
+    }
+    m.h.assign(n, 0.0);
+    m.clamp.assign(n, 0);
+    for (uint32_t i = 0; i < n; ++i) {
+        if (h) m.h[i] = h[i];
+        if (clamp && clamp[i]) {
+            if (clamp[i] != 1 && clamp[i] != -1) throw tapt::ConfigError("clamp value must be ±1");
+            m.clamp[i] = clamp[i];
+        }
+    }
+    for (const auto& [key, v] : merged) {
+        m.ci.push_back(key.first);
+        m.cj.push_back(key.second);
+        m.J.push_back(v.first);
+        m.bond_of.push_back(v.second);
+    }
+    // digest: FNV-1a over (n, couplings {u32,u32,f64}, fields, clamps) as spin_model.cpp:68-75
+    {
+        uint64_t d = fnv1a(&m.n, 0, 0xCBF29CE484222325ull);
+        const uint64_t n64 = n;
+        d = fnv1a(&n64, sizeof(n64), 0xCBF29CE484222325ull);
+        struct Rec {
+            uint32_t i, j;
+            double v;
+        };
+        static_assert(sizeof(Rec) == 16, "layout");
+        for (size_t k = 0; k < m.ci.size(); ++k) {
+            Rec r{m.ci[k], m.cj[k], m.J[k]};
+            d = fnv1a(&r, sizeof(r), d);
+        }
+        if (n) d = fnv1a(m.h.data(), n * sizeof(double), d);
+        if (n) d = fnv1a(m.clamp.data(), n, d);
+        m.digest = d;
+    }
+    // CSR, neighbours ascending (spin_model.cpp:52-63 yields this order)
+    std::vector<std::vector<std::pair<uint32_t, size_t>>> adj(n);
+    for (size_t k = 0; k < m.ci.size(); ++k) {
+        adj[m.ci[k]].push_back({m.cj[k], k});
+        adj[m.cj[k]].push_back({m.ci[k], k});
+    }
+    m.rowptr.assign(n + 1, 0);
+    m.hi.assign(n, 0);
+    bool integral = true;
+    for (uint32_t i = 0; i < n; ++i) {
+        std::sort(adj[i].begin(), adj[i].end());
+        m.rowptr[i + 1] = m.rowptr[i] + static_cast<uint32_t>(adj[i].size());
+        for (auto& [j, k] : adj[i]) {
+            m.col.push_back(j);
+            const double v = m.J[k];
+            if (!is_integer(v) || std::fabs(v) > 127) integral = false;
+            m.adjJ.push_back(static_cast<int8_t>(integral ? v : 0));
+            m.adj_bond.push_back(m.bond_of[k]);
+        }
+        if (!is_integer(m.h[i])) integral = false;
+        m.hi[i] = integral ? static_cast<int32_t>(m.h[i]) : 0;
+    }
+    if (!integral)
+        throw tapt::NumericError(
+            "the device path needs integer-valued couplings (|J| <= 127) and fields: thresholds are exact tables");
+    for (uint32_t i = 0; i < n; ++i)
+        if (!m.clamp[i]) m.free_sites.push_back(i);
+    m.rank.assign(n, 0);
+    for (uint32_t q = 0; q < m.free_sites.size(); ++q) m.rank[m.free_sites[q]] = q;
+    // local-field range over free sites; byte-SWAR capacity check is done when K2 is chosen
+    m.lmin = 0;
+    m.lmax = 0;
+    bool first = true;
+    for (uint32_t i : m.free_sites) {
+        int sa = 0;
+        for (uint32_t k = m.rowptr[i]; k < m.rowptr[i + 1]; ++k) sa += std::abs((int)m.adjJ[k]);
+        m.max_sumabs = std::max(m.max_sumabs, sa);
+        const int lo = m.hi[i] - sa, hi = m.hi[i] + sa;
+        if (first || lo < m.lmin) m.lmin = lo;
+        if (first || hi > m.lmax) m.lmax = hi;
+        first = false;
+    }
+    // greedy colouring (ascending order) and dependency levels of the index order
+    m.colour.assign(n, -1);
+    m.level.assign(n, -1);
+    int ncol = 0, nlev = 0;
+    std::vector<int> mark;
+    for (uint32_t i : m.free_sites) {
+        mark.assign(ncol + 2, 0);
+        int lv = 0;
+        for (uint32_t k = m.rowptr[i]; k < m.rowptr[i + 1]; ++k) {
+            const uint32_t j = m.col[k];
+            if (m.colour[j] >= 0) mark[m.colour[j]] = 1;
+            if (j < i && m.level[j] >= 0) lv = std::max(lv, m.level[j] + 1);
+        }
+        int c = 0;
+        while (mark[c]) ++c;
+        m.colour[i] = c;
+        m.level[i] = lv;
+        ncol = std::max(ncol, c + 1);
+        nlev = std::max(nlev, lv + 1);
+    }
+    auto classes = [&](const std::vector<int32_t>& cls, int nc, std::vector<uint32_t>& ptr,
+                       std::vector<uint32_t>& sites) {
+        ptr.assign(nc + 1, 0);
+        for (uint32_t i : m.free_sites) ++ptr[cls[i] + 1];
+        for (int c = 0; c < nc; ++c) ptr[c + 1] += ptr[c];
+        sites.assign(m.free_sites.size(), 0);
+        std::vector<uint32_t> cur(ptr.begin(), ptr.end() - 1);
+        for (uint32_t i : m.free_sites) sites[cur[cls[i]]++] = i;
+    };
+    classes(m.colour, ncol, m.col_ptr, m.col_sites);
+    classes(m.level, nlev, m.lev_ptr, m.lev_sites);
+}
+
+}  // namespace
+
+// ================================================================ ensemble ===
+
+struct tapt_ensemble_s {
+    tapt_model_s* m = nullptr;
+    uint32_t I = 0;
+    uint64_t gid0 = 0;
+    int R = 0, W = 0, G = 0, order = 0;
+    std::vector<double> betas;
+    uint64_t seed = 0;
+    bool use_k1 = false;
+    int k1_threads = 0, k2_threads = 256;
+    int nidx = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t T = 0, P = 0, Q = 0;  // sweeps, swap passes, proposal rounds (global)
+    int clamp_sets = 1;
+    bool have_disorder = false;
+    uint32_t launch_chunk = 2000;
+
+    DevBuf<uint32_t> words;
+    DevBuf<int32_t> E;
+    DevBuf<uint8_t> slot_of, buf_of;
+    DevBuf<uint64_t> streams, coord, thr;
+    DevMetro swap_tab, prop_tab;
+    DevBuf<uint64_t> swap_att, swap_acc, prop_att, prop_acc;
+    DevBuf<long long> obs;
+    DevBuf<unsigned long long> hist;
+    long long e_lo = 0, width = 1;
+    int nbins = 0;
+    DevBuf<int> best;
+    DevBuf<int8_t> signs, csrJ, clampval;
+    DevBuf<uint8_t> bonds;
+    // proposal scratch
+    DevBuf<uint32_t> pwords;
+    DevBuf<int32_t> pE;
+    DevBuf<uint8_t> pslot, pacc, pforced, pbytes;
+    DevBuf<int8_t> pint8;
+    DevBuf<uint64_t> pstreams, paccs, ptup;
+    DevBuf<uint32_t> ptargets;
+
+    int n() const { return (int)m->n; }
+    int group_words() const { return G; }
+
+    const int8_t* clamp_ptr() const { return clampval.p ? clampval.p : m->d_clamp.p; }
+    int clamp_count() const { return clampval.p ? (int)I : 1; }
+    bool has_clamps() const { return m->free_sites.size() != m->n; }
+
+    CsrArgs csr_args(bool level_order) const {
+        CsrArgs g{};
+        g.rowptr = m->d_rowptr.p;
+        g.col = m->d_col.p;
+        g.J = csrJ.p ? csrJ.p : m->d_J.p;
+        g.nJ = csrJ.p ? (int)I : 1;
+        g.nnz = (int)m->col.size();
+        g.h = m->d_h.p;
+        g.rank = m->d_rank.p;
+        g.class_ptr = level_order ? m->d_levptr.p : m->d_colptr.p;
+        g.class_sites = level_order ? m->d_levsites.p : m->d_colsites.p;
+        g.n_classes = (int)((level_order ? m->lev_ptr.size() : m->col_ptr.size()) - 1);
+        g.lmin = m->lmin;
+        return g;
+    }
+
+    PTArgs base_args() {
+        PTArgs a{};
+        a.words = words.p;
+        a.I = (int)I;
+        a.G = G;
+        a.W = W;
+        a.B = R;
+        a.n = n();
+        a.bonds = bonds.p;
+        a.n_free = (uint32_t)m->free_sites.size();
+        a.R = R;
+        a.streams = streams.p;
+        a.slot_of = slot_of.p;
+        a.buf_of = buf_of.p;
+        a.thr = thr.p;
+        a.nidx = nidx;
+        a.E = E.p;
+        a.coord = coord.p;
+        a.swap_tab = swap_tab.view();
+        a.swap_att = swap_att.p;
+        a.swap_acc = swap_acc.p;
+        a.obs = obs.p;
+        a.hist = nbins ? hist.p : nullptr;
+        a.e_lo = e_lo;
+        a.width = width;
+        a.nbins = nbins;
+        a.best = best.p;
+        return a;
+    }
+
+    void launch(const PTArgs& a, bool cluster) {
+        ++g_launches;
+        cudaError_t e;
+        if (use_k1)
+            e = launch_k1(a, m->ld, k1_threads, cluster, stream);
+        else
+            e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_threads, cluster, stream);
+        if (e != cudaSuccess) throw tapt::CudaError(std::string("sweep kernel launch: ") + cudaGetErrorString(e));
+        CUDA_OK(cudaGetLastError());
+    }
+
+    // Exact energies of every buffer from the spins.
+    void recompute_energies() {
+        if (use_k1) {
+            PTArgs a = base_args();
+            a.energy_only = 1;
+            a.n_sweeps = 0;
+            a.swap_every = 0;
+            a.measure_every = 0;
+            a.best = nullptr;
+            launch(a, false);
+        } else {
+            CsrArgs g = csr_args(false);
+            ++g_launches;
+            k_energy_csr<<<dim3(G, I), 256, 0, stream>>>(words.p, n(), G, W, R, g.rowptr, g.col, g.J, g.nJ, g.nnz,
+                                                          g.h, E.p);
+            CUDA_OK(cudaGetLastError());
+        }
+    }
+
+    void update_best_from_E() {
+        // best = min(best, min over buffers) -- done on the host side of small arrays
+        auto e = E.download(stream);
+        auto b = best.download(stream);
+        for (uint32_t i = 0; i < I; ++i)
+            for (int r = 0; r < R; ++r) b[i] = std::min(b[i], e[(size_t)i * R + r]);
+        best.upload(b, stream);
+    }
+
+    void run(uint32_t n_sweeps, uint32_t swap_every, uint32_t measure_every, uint64_t measure_from) {
+        if (n_sweeps == 0) return;
+        if (swap_every && R < 2) swap_every = 0;
+        const bool cluster = G > 1;
+        uint32_t done = 0;
+        while (done < n_sweeps) {
+            const uint32_t chunk = std::min(launch_chunk, n_sweeps - done);
+            PTArgs a = base_args();
+            a.t0 = T;
+            a.n_sweeps = (int)chunk;
+            a.swap_every = (int)swap_every;
+            a.p0 = P;
+            a.measure_every = (int)measure_every;
+            a.measure_from = measure_from;
+            launch(a, cluster);
+            if (swap_every) P += (T + chunk) / swap_every - T / swap_every;
+            T += chunk;
+            done += chunk;
+        }
+    }
+};
+
+namespace {
+
+void check_model(const tapt_model_s* m) {
+    if (!m) throw tapt::ConfigError("null model handle");
+}
+void check_ens(const tapt_ensemble_s* e) {
+    if (!e) throw tapt::ConfigError("null ensemble handle");
+}
+
+// LatticeSpec::graph_clamped bond list (lattice.cpp:55-87): per site, +x then +y (then +z);
+// wrap bonds only when periodic and the extent is > 2.
+void lattice_bonds(int dim, int ly, int lx, int l, bool periodic, std::vector<uint32_t>& ci,
+                   std::vector<uint32_t>& cj) {
+    if (dim == 2) {
+        for (int r = 0; r < ly; ++r)
+            for (int c = 0; c < lx; ++c) {
+                const uint32_t i = (uint32_t)(r * lx + c);
+                if (c + 1 < lx) {
+                    ci.push_back(i);
+                    cj.push_back((uint32_t)(r * lx + c + 1));
+                } else if (periodic && lx > 2) {
+                    ci.push_back(i);
+                    cj.push_back((uint32_t)(r * lx));
+                }
+                if (r + 1 < ly) {
+                    ci.push_back(i);
+                    cj.push_back((uint32_t)((r + 1) * lx + c));
+                } else if (periodic && ly > 2) {
+                    ci.push_back(i);
+                    cj.push_back((uint32_t)c);
+                }
+            }
+        return;
+    }
+    auto idx = [l](int x, int y, int z) { return (uint32_t)(x + l * (y + (long)l * z)); };
+    for (int z = 0; z < l; ++z)
+        for (int y = 0; y < l; ++y)
+            for (int x = 0; x < l; ++x) {
+                const uint32_t i = idx(x, y, z);
+                if (x + 1 < l) {
+                    ci.push_back(i);
+                    cj.push_back(idx(x + 1, y, z));
+                } else if (periodic && l > 2) {
+                    ci.push_back(i);
+                    cj.push_back(idx(0, y, z));
+                }
+                if (y + 1 < l) {
+                    ci.push_back(i);
+                    cj.push_back(idx(x, y + 1, z));
+                } else if (periodic && l > 2) {
+                    ci.push_back(i);
+                    cj.push_back(idx(x, 0, z));
+                }
+                if (z + 1 < l) {
+                    ci.push_back(i);
+                    cj.push_back(idx(x, y, z + 1));
+                } else if (periodic && l > 2) {
+                    ci.push_back(i);
+                    cj.push_back(idx(x, y, 0));
+                }
+            }
+}
+
+void sync_if(cudaStream_t st) { CUDA_OK(cudaStreamSynchronize(st)); }
+
+}  // namespace
+
+// ==================================================================== C ABI ===
+
+extern "C" {
+
+const char* tapt_last_error(void) { return g_last_error.c_str(); }
+const char* tapt_version(void) { return "tapt-b200 0.1 (sm_100a)"; }
+unsigned long long tapt_launch_count(void) { return g_launches.load(); }
+
+tapt_status tapt_probe_decision_rate(int blocks_per_sm, int threads, uint32_t iters, double* decisions_per_s,
+                                     double* seconds) {
+    return guard([&] {
+        if (tapt_device_count() == 0) throw tapt::CudaError("no CUDA device");
+        cudaStream_t st;
+        CUDA_OK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        int dev = 0, nsm = 0;
+        CUDA_OK(cudaGetDevice(&dev));
+        CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        const int blocks = nsm * std::max(1, blocks_per_sm);
+        DevBuf<uint32_t> sink;
+        sink.alloc((size_t)blocks * threads);
+        cudaEvent_t a, b;
+        CUDA_OK(cudaEventCreate(&a));
+        CUDA_OK(cudaEventCreate(&b));
+        ++g_launches;
+        CUDA_OK(launch_decision_probe(blocks, threads, iters, sink.p, st));  // warm-up
+        CUDA_OK(cudaEventRecord(a, st));
+        ++g_launches;
+        CUDA_OK(launch_decision_probe(blocks, threads, iters, sink.p, st));
+        CUDA_OK(cudaEventRecord(b, st));
+        CUDA_OK(cudaEventSynchronize(b));
+        float ms = 0;
+        CUDA_OK(cudaEventElapsedTime(&ms, a, b));
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaStreamDestroy(st);
+        const double n = (double)blocks * threads * iters * 64.0;
+        if (seconds) *seconds = ms * 1e-3;
+        if (decisions_per_s) *decisions_per_s = n / (ms * 1e-3);
+    });
+}
+int tapt_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+tapt_status tapt_model_create_lattice(int dim, int ly, int lx, int lz, double J, int boundary, tapt_model_t* out) {
+    return guard([&] {
+        if (!out) throw tapt::ConfigError("null output handle");
+        if (dim != 2 && dim != 3) throw tapt::ConfigError("lattice dim must be 2 or 3");
+        if (dim == 2 && (ly < 1 || lx < 1)) throw tapt::ConfigError("grid2d dimensions must be >= 1");
+        if (dim == 3 && lx < 1) throw tapt::ConfigError("grid3d size must be >= 1");
+        (void)lz;
+        if (!is_integer(J)) throw tapt::NumericError("lattice coupling must be integer-valued on the device path");
+        auto m = std::make_unique<tapt_model_s>();
+        std::vector<uint32_t> ci, cj;
+        const bool per = boundary == TAPT_BOUNDARY_PERIODIC;
+        const int l = lx;
+        lattice_bonds(dim, ly, lx, l, per, ci, cj);
+        const uint32_t n = dim == 2 ? (uint32_t)(ly * lx) : (uint32_t)(l * l * l);
+        std::vector<double> Jv(ci.size(), J);
+        build_model(*m, n, ci, cj, Jv, nullptr, nullptr);
+        m->lattice = true;
+        m->dim = dim;
+        m->ly = dim == 2 ? ly : l;
+        m->lx = lx;
+        m->lz = dim == 2 ? 1 : l;
+        m->boundary = boundary;
+        m->J0 = (int)std::fabs(J);
+        m->Jsign = J < 0 ? -1 : 1;
+        m->nbonds = (uint32_t)ci.size();
+        const int a = ilog2_exact(lx), b = ilog2_exact(m->ly);
+        m->k1 = per && a >= 2 && b >= 2 && (dim == 2 || a == b) && n <= 40000 && m->J0 <= 127;
+        m->ld.dim = dim;
+        m->ld.log2Lx = a;
+        m->ld.log2Ly = b;
+        m->ld.log2hx = a - 1;
+        m->ld.J0 = m->J0;
+        *out = m.release();
+    });
+}
+
+tapt_status tapt_model_create_graph(uint32_t n, uint32_t nc, const uint32_t* ci, const uint32_t* cj, const double* J,
+                                    const double* h, const int8_t* clamp, tapt_model_t* out) {
+    return guard([&] {
+        if (!out) throw tapt::ConfigError("null output handle");
+        if (nc && (!ci || !cj || !J)) throw tapt::ConfigError("null coupling arrays");
+        auto m = std::make_unique<tapt_model_s>();
+        std::vector<uint32_t> a(ci, ci + nc), b(cj, cj + nc);
+        std::vector<double> v(J, J + nc);
+        build_model(*m, n, a, b, v, h, clamp);
+        *out = m.release();
+    });
+}
+
+tapt_status tapt_model_destroy(tapt_model_t m) {
+    return guard([&] { delete m; });
+}
+
+tapt_status tapt_model_info(tapt_model_t m, uint32_t* n_spins, uint32_t* n_free, uint32_t* n_couplings, int32_t* lmin,
+                            int32_t* lmax, uint32_t* n_colours, uint32_t* n_levels) {
+    return guard([&] {
+        check_model(m);
+        if (n_spins) *n_spins = m->n;
+        if (n_free) *n_free = (uint32_t)m->free_sites.size();
+        if (n_couplings) *n_couplings = (uint32_t)m->ci.size();
+        if (lmin) *lmin = m->lmin;
+        if (lmax) *lmax = m->lmax;
+        if (n_colours) *n_colours = (uint32_t)(m->col_ptr.size() - 1);
+        if (n_levels) *n_levels = (uint32_t)(m->lev_ptr.size() - 1);
+    });
+}
+
+tapt_status tapt_model_couplings(tapt_model_t m, uint32_t* ci, uint32_t* cj, double* J) {
+    return guard([&] {
+        check_model(m);
+        for (size_t k = 0; k < m->ci.size(); ++k) {
+            if (ci) ci[k] = m->ci[k];
+            if (cj) cj[k] = m->cj[k];
+            if (J) J[k] = m->J[k];
+        }
+    });
+}
+
+tapt_status tapt_model_schedule(tapt_model_t m, int32_t* colour, int32_t* level) {
+    return guard([&] {
+        check_model(m);
+        if (colour) std::copy(m->colour.begin(), m->colour.end(), colour);
+        if (level) std::copy(m->level.begin(), m->level.end(), level);
+    });
+}
+
+tapt_status tapt_model_digest(tapt_model_t m, uint64_t* digest) {
+    return guard([&] {
+        check_model(m);
+        *digest = m->digest;
+    });
+}
+
+tapt_status tapt_model_energy(tapt_model_t m, const int8_t* s, size_t len, double* out) {
+    return guard([&] {
+        check_model(m);
+        if (len != m->n)
+            throw tapt::DimensionError("configuration length " + std::to_string(len) + " != n_spins " +
+                                       std::to_string(m->n));
+        double e = 0.0;
+        for (size_t k = 0; k < m->ci.size(); ++k) e -= m->J[k] * (double)(s[m->ci[k]] * s[m->cj[k]]);
+        for (uint32_t i = 0; i < m->n; ++i) e -= m->h[i] * (double)s[i];
+        *out = e;
+    });
+}
+
+// ---------------------------------------------------------------- ensembles
+
+tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, tapt_ensemble_t* out) {
+    return guard([&] {
+        check_model(m);
+        if (!d || !out) throw tapt::ConfigError("null descriptor / output");
+        if (d->n_instances == 0) throw tapt::ConfigError("n_instances must be >= 1");
+        if (d->n_slots < 1 || d->n_slots > (uint32_t)kMaxR) throw tapt::ConfigError("n_slots must be in [1, 256]");
+        if (!d->betas) throw tapt::ConfigError("null beta ladder");
+        for (uint32_t r = 0; r < d->n_slots; ++r) {
+            if (!(d->betas[r] >= 0.0) || !std::isfinite(d->betas[r])) throw tapt::ConfigError("beta must be >= 0");
+            if (r && !(d->betas[r] > d->betas[r - 1]))
+                throw tapt::ConfigError("beta ladder must be strictly increasing (SPEC.md:388)");
+        }
+        if (d->order != TAPT_ORDER_COLOUR && d->order != TAPT_ORDER_REFERENCE)
+            throw tapt::ConfigError("unknown sweep order");
+        if (tapt_device_count() == 0) throw tapt::CudaError("no CUDA device: the TAPT engine has no CPU fallback");
+        auto e = std::make_unique<tapt_ensemble_s>();
+        e->m = m;
+        e->I = d->n_instances;
+        e->gid0 = d->instance_offset;
+        e->R = (int)d->n_slots;
+        e->betas.assign(d->betas, d->betas + d->n_slots);
+        e->seed = d->seed;
+        e->order = d->order;
+        e->W = std::min(e->R, kW);
+        e->G = (e->R + kW - 1) / kW;
+        CUDA_OK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+        e->own_stream = true;
+        m->ensure_device(e->stream);
+        const int n = (int)m->n;
+        e->use_k1 = m->k1 && d->order == TAPT_ORDER_COLOUR && !e->has_clamps();
+        if (e->use_k1) {
+            e->nidx = 2 * m->dim + 1;
+            int nt = std::max(32, std::min(512, n / 4));
+            nt = (nt / 32) * 32;
+            e->k1_threads = nt;
+            if (k1_smem_bytes(n, true) > 227 * 1024) throw tapt::SizeError("lattice too large for shared memory");
+        } else {
+            if (m->max_sumabs > 255) throw tapt::SizeError("sum of |J| at a site exceeds 255 (byte-SWAR fields)");
+            e->nidx = m->lmax - m->lmin + 1;
+            if (k2_smem_bytes(n, e->R, e->nidx) > 227 * 1024) throw tapt::SizeError("graph too large for shared memory");
+        }
+        if (e->G > 8) throw tapt::ConfigError("at most 256 slots");
+        // heat-bath thresholds [R][nidx]
+        std::vector<uint64_t> thr((size_t)e->R * e->nidx);
+        for (int r = 0; r < e->R; ++r)
+            for (int k = 0; k < e->nidx; ++k) {
+                double l;
+                if (e->use_k1)
+                    l = (double)(m->Jsign * 0 + m->J0 * (2 * k - 2 * m->dim));
+                else
+                    l = (double)(m->lmin + k);
+                thr[(size_t)r * e->nidx + k] = threshold_of(conditional_up(e->betas[r], l));
+            }
+        e->thr.upload(thr, e->stream);
+        // swap (rows = pairs) and proposal (rows = slots) Metropolis tables
+        HostMetro sw, pr;
+        for (int r = 0; r + 1 < e->R; ++r) sw.add_row(e->betas[r + 1] - e->betas[r]);
+        if (e->R < 2) sw.add_row(0.0);
+        for (int r = 0; r < e->R; ++r) pr.add_row(e->betas[r]);
+        e->swap_tab.upload(sw, e->stream);
+        e->prop_tab.upload(pr, e->stream);
+        // streams
+        std::vector<uint64_t> st((size_t)e->I * e->R), co(e->I);
+        for (uint32_t i = 0; i < e->I; ++i) {
+            const uint64_t gid = e->gid0 + i;
+            for (int r = 0; r < e->R; ++r)
+                st[(size_t)i * e->R + r] = tapt::RngStream::derive(e->seed, {tapt::stream::kReplica, gid, (uint64_t)r}).state();
+            co[i] = tapt::RngStream::derive(e->seed, {tapt::stream::kCoordinator, gid}).state();
+        }
+        e->streams.upload(st, e->stream);
+        e->coord.upload(co, e->stream);
+        // state
+        e->words.alloc((size_t)e->I * e->G * n);
+        e->words.zero(e->stream);
+        e->E.alloc((size_t)e->I * e->R);
+        e->E.zero(e->stream);
+        std::vector<uint8_t> perm((size_t)e->I * e->R);
+        for (uint32_t i = 0; i < e->I; ++i)
+            for (int r = 0; r < e->R; ++r) perm[(size_t)i * e->R + r] = (uint8_t)r;
+        e->slot_of.upload(perm, e->stream);
+        e->buf_of.upload(perm, e->stream);
+        const size_t np = (size_t)e->I * std::max(e->R - 1, 1);
+        e->swap_att.alloc(np);
+        e->swap_acc.alloc(np);
+        e->prop_att.alloc((size_t)e->I * e->R);
+        e->prop_acc.alloc((size_t)e->I * e->R);
+        e->swap_att.zero(e->stream);
+        e->swap_acc.zero(e->stream);
+        e->prop_att.zero(e->stream);
+        e->prop_acc.zero(e->stream);
+        e->obs.alloc((size_t)e->I * e->R * 5);
+        e->obs.zero(e->stream);
+        std::vector<int> b(e->I, 0x7FFFFFFF);
+        e->best.upload(b, e->stream);
+        sync_if(e->stream);
+        *out = e.release();
+        if (m->lattice && m->Jsign < 0 && m->J0 != 0) {  // antiferromagnet: every bond negative
+            std::vector<int8_t> sg((size_t)(*out)->I * m->nbonds, -1);
+            if (tapt_ensemble_set_bond_signs(*out, sg.data(), m->nbonds) != TAPT_OK) {
+                const std::string msg = g_last_error;
+                tapt_ensemble_destroy(*out);
+                *out = nullptr;
+                throw tapt::CudaError(msg);
+            }
+        }
+    });
+}
+
+tapt_status tapt_ensemble_destroy(tapt_ensemble_t e) {
+    return guard([&] {
+        if (!e) return;
+        cudaStreamSynchronize(e->stream);
+        if (e->own_stream) cudaStreamDestroy(e->stream);
+        delete e;
+    });
+}
+
+tapt_status tapt_ensemble_set_stream(tapt_ensemble_t e, void* s) {
+    return guard([&] {
+        check_ens(e);
+        CUDA_OK(cudaStreamSynchronize(e->stream));
+        if (e->own_stream) cudaStreamDestroy(e->stream);
+        if (s) {
+            e->stream = static_cast<cudaStream_t>(s);
+            e->own_stream = false;
+        } else {
+            CUDA_OK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
+            e->own_stream = true;
+        }
+    });
+}
+
+tapt_status tapt_ensemble_synchronize(tapt_ensemble_t e) {
+    return guard([&] {
+        check_ens(e);
+        CUDA_OK(cudaStreamSynchronize(e->stream));
+    });
+}
+
+const char* tapt_ensemble_kernel(tapt_ensemble_t e) { return e && e->use_k1 ? "lattice" : "csr"; }
+
+tapt_status tapt_ensemble_set_bond_signs(tapt_ensemble_t e, const int8_t* signs, size_t n_bonds) {
+    return guard([&] {
+        check_ens(e);
+        tapt_model_s* m = e->m;
+        if (!m->lattice) throw tapt::ConfigError("bond signs apply to lattice models only");
+        if (n_bonds != m->nbonds) throw tapt::DimensionError("bond count mismatch");
+        for (size_t k = 0; k < (size_t)e->I * n_bonds; ++k)
+            if (signs[k] != 1 && signs[k] != -1) throw tapt::ConfigError("bond signs must be +-1");
+        e->signs.upload(signs, (size_t)e->I * n_bonds, e->stream);
+        e->have_disorder = true;
+        const int n = (int)m->n;
+        if (e->use_k1) {
+            e->bonds.alloc((size_t)e->I * n);
+            ++g_launches;
+            k_bond_bytes<<<dim3((n + 255) / 256, e->I), 256, 0, e->stream>>>(e->signs.p, e->bonds.p, m->ld, n);
+            CUDA_OK(cudaGetLastError());
+        } else {
+            const int nnz = (int)m->col.size();
+            e->csrJ.alloc((size_t)e->I * nnz);
+            ++g_launches;
+            k_csr_from_signs<<<dim3((nnz + 255) / 256, e->I), 256, 0, e->stream>>>(
+                e->signs.p, (int)n_bonds, m->d_adjbond.p, nnz, m->J0, e->csrJ.p);
+            CUDA_OK(cudaGetLastError());
+        }
+        e->recompute_energies();
+        sync_if(e->stream);
+    });
+}
+
+tapt_status tapt_ensemble_generate_ea_disorder(tapt_ensemble_t e, uint64_t disorder_seed) {
+    return guard([&] {
+        check_ens(e);
+        tapt_model_s* m = e->m;
+        if (!m->lattice || m->boundary != TAPT_BOUNDARY_PERIODIC || m->lx <= 2 || m->ly <= 2)
+            throw tapt::ConfigError("EA disorder generation needs a periodic lattice with L > 2");
+        if (m->nbonds != (uint32_t)m->dim * m->n) throw tapt::GeometryError("unexpected bond count");
+        std::vector<uint64_t> st(e->I);
+        for (uint32_t i = 0; i < e->I; ++i)
+            st[i] = tapt::RngStream::derive(disorder_seed, {tapt::stream::kDisorder, e->gid0 + i}).state();
+        DevBuf<uint64_t> ds;
+        ds.upload(st, e->stream);
+        DevBuf<int8_t> sg;
+        sg.alloc((size_t)e->I * m->nbonds);
+        const int n = (int)m->n;
+        ++g_launches;
+        k_ea_signs<<<dim3((n + 255) / 256, e->I), 256, 0, e->stream>>>(sg.p, n, m->dim, ds.p);
+        CUDA_OK(cudaGetLastError());
+        std::vector<int8_t> h = sg.download(e->stream);
+        if (m->J0 != 0 && m->Jsign < 0)
+            for (auto& v : h) v = (int8_t)-v;
+        tapt_status s = tapt_ensemble_set_bond_signs(e, h.data(), m->nbonds);
+        if (s != TAPT_OK) throw tapt::CudaError(g_last_error);
+    });
+}
+
+tapt_status tapt_ensemble_get_bond_signs(tapt_ensemble_t e, int8_t* signs, size_t n_bonds) {
+    return guard([&] {
+        check_ens(e);
+        if (n_bonds != e->m->nbonds) throw tapt::DimensionError("bond count mismatch");
+        if (!e->signs.p) {
+            std::fill(signs, signs + (size_t)e->I * n_bonds, (int8_t)1);
+            return;
+        }
+        auto h = e->signs.download(e->stream);
+        std::copy(h.begin(), h.end(), signs);
+    });
+}
+
+tapt_status tapt_ensemble_set_clamps(tapt_ensemble_t e, const int8_t* clamps) {
+    return guard([&] {
+        check_ens(e);
+        const uint32_t n = e->m->n;
+        for (uint32_t i = 0; i < e->I; ++i)
+            for (uint32_t s = 0; s < n; ++s) {
+                const int8_t v = clamps[(size_t)i * n + s];
+                if (v != 0 && v != 1 && v != -1) throw tapt::ConfigError("clamp value must be ±1");
+                if ((v != 0) != (e->m->clamp[s] != 0))
+                    throw tapt::ClampedSiteError("per-instance clamps must cover exactly the model's clamped sites");
+            }
+        e->clampval.upload(clamps, (size_t)e->I * n, e->stream);
+        sync_if(e->stream);
+    });
+}
+
+tapt_status tapt_ensemble_init_random(tapt_ensemble_t e) {
+    return guard([&] {
+        check_ens(e);
+        std::vector<uint64_t> st((size_t)e->I * e->R);
+        for (uint32_t i = 0; i < e->I; ++i)
+            for (int r = 0; r < e->R; ++r)
+                st[(size_t)i * e->R + r] =
+                    tapt::RngStream::derive(e->seed, {tapt::stream::kInit, e->gid0 + i, (uint64_t)r}).state();
+        DevBuf<uint64_t> ds;
+        ds.upload(st, e->stream);
+        std::vector<uint8_t> perm((size_t)e->I * e->R);
+        for (uint32_t i = 0; i < e->I; ++i)
+            for (int r = 0; r < e->R; ++r) perm[(size_t)i * e->R + r] = (uint8_t)r;
+        e->slot_of.upload(perm, e->stream);
+        e->buf_of.upload(perm, e->stream);
+        const int n = e->n();
+        ++g_launches;
+        k_init_random<<<dim3((n + 255) / 256, e->G, e->I), 256, 0, e->stream>>>(e->words.p, n, e->G, e->W, e->R, ds.p,
+                                                                                e->clamp_ptr(), e->clamp_count());
+        CUDA_OK(cudaGetLastError());
+        e->recompute_energies();
+        e->update_best_from_E();
+        sync_if(e->stream);
+    });
+}
+
+static void set_spins_impl(tapt_ensemble_t e, const int8_t* spins, bool force_clamps) {
+    const int n = e->n();
+    DevBuf<int8_t> d;
+    d.upload(spins, (size_t)e->I * e->R * n, e->stream);
+    ++g_launches;
+    k_set_spins<<<dim3((n + 255) / 256, e->G, e->I), 256, 0, e->stream>>>(
+        e->words.p, n, e->G, e->W, e->R, e->slot_of.p, d.p, e->R, force_clamps ? e->clamp_ptr() : nullptr,
+        e->clamp_count());
+    CUDA_OK(cudaGetLastError());
+    e->recompute_energies();
+    e->update_best_from_E();
+    sync_if(e->stream);
+}
+
+tapt_status tapt_ensemble_set_spins(tapt_ensemble_t e, const int8_t* spins) {
+    return guard([&] {
+        check_ens(e);
+        set_spins_impl(e, spins, true);
+    });
+}
+
+tapt_status tapt_ensemble_get_spins(tapt_ensemble_t e, int8_t* spins) {
+    return guard([&] {
+        check_ens(e);
+        const int n = e->n();
+        DevBuf<int8_t> d;
+        d.alloc((size_t)e->I * e->R * n);
+        ++g_launches;
+        k_get_spins<<<dim3((n + 255) / 256, e->R, e->I), 256, 0, e->stream>>>(e->words.p, n, e->G, e->W, e->R,
+                                                                             e->buf_of.p, e->R, d.p);
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaMemcpyAsync(spins, d.p, d.n, cudaMemcpyDeviceToHost, e->stream));
+        sync_if(e->stream);
+    });
+}
+
+tapt_status tapt_ensemble_get_spins_packed(tapt_ensemble_t e, uint8_t* packed) {
+    return guard([&] {
+        check_ens(e);
+        const int n = e->n(), nb = (n + 7) / 8;
+        DevBuf<uint8_t> d;
+        d.alloc((size_t)e->I * e->R * nb);
+        ++g_launches;
+        k_get_packed<<<dim3((nb + 255) / 256, e->R, e->I), 256, 0, e->stream>>>(e->words.p, n, e->G, e->W,
+                                                                               e->buf_of.p, e->R, d.p);
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaMemcpyAsync(packed, d.p, d.n, cudaMemcpyDeviceToHost, e->stream));
+        sync_if(e->stream);
+    });
+}
+
+tapt_status tapt_ensemble_get_energies(tapt_ensemble_t e, int64_t* out) {
+    return guard([&] {
+        check_ens(e);
+        auto E = e->E.download(e->stream);
+        auto bo = e->buf_of.download(e->stream);
+        for (uint32_t i = 0; i < e->I; ++i)
+            for (int r = 0; r < e->R; ++r)
+                out[(size_t)i * e->R + r] = E[(size_t)i * e->R + bo[(size_t)i * e->R + r]];
+    });
+}
+
+tapt_status tapt_ensemble_get_permutation(tapt_ensemble_t e, uint8_t* out) {
+    return guard([&] {
+        check_ens(e);
+        auto bo = e->buf_of.download(e->stream);
+        std::copy(bo.begin(), bo.end(), out);
+    });
+}
+
+tapt_status tapt_ensemble_counters(tapt_ensemble_t e, uint64_t* sweeps, uint64_t* passes, uint64_t* rounds) {
+    return guard([&] {
+        check_ens(e);
+        if (sweeps) *sweeps = e->T;
+        if (passes) *passes = e->P;
+        if (rounds) *rounds = e->Q;
+    });
+}
+
+tapt_status tapt_get_acceptance(tapt_ensemble_t e, uint64_t* sa, uint64_t* sc, uint64_t* pa, uint64_t* pc) {
+    return guard([&] {
+        check_ens(e);
+        const size_t np = (size_t)e->I * (e->R - 1);
+        if (sa && np) std::copy_n(e->swap_att.download(e->stream).begin(), np, sa);
+        if (sc && np) std::copy_n(e->swap_acc.download(e->stream).begin(), np, sc);
+        if (pa) {
+            auto v = e->prop_att.download(e->stream);
+            std::copy(v.begin(), v.end(), pa);
+        }
+        if (pc) {
+            auto v = e->prop_acc.download(e->stream);
+            std::copy(v.begin(), v.end(), pc);
+        }
+    });
+}
+
+tapt_status tapt_get_observables(tapt_ensemble_t e, int64_t* obs) {
+    return guard([&] {
+        check_ens(e);
+        auto v = e->obs.download(e->stream);
+        std::copy(v.begin(), v.end(), obs);
+    });
+}
+
+tapt_status tapt_set_histogram(tapt_ensemble_t e, int64_t e_lo, int64_t width, uint32_t nbins) {
+    return guard([&] {
+        check_ens(e);
+        if (width < 1) throw tapt::ConfigError("histogram bin width must be >= 1");
+        e->e_lo = e_lo;
+        e->width = width;
+        e->nbins = (int)nbins;
+        e->hist.alloc((size_t)e->R * nbins);
+        e->hist.zero(e->stream);
+        sync_if(e->stream);
+    });
+}
+
+tapt_status tapt_get_histogram(tapt_ensemble_t e, uint64_t* dst, int on_device) {
+    return guard([&] {
+        check_ens(e);
+        if (!e->nbins) throw tapt::ConfigError("no histogram configured");
+        CUDA_OK(cudaMemcpyAsync(dst, e->hist.p, e->hist.n * sizeof(uint64_t),
+                                on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, e->stream));
+        sync_if(e->stream);
+    });
+}
+
+tapt_status tapt_get_best(tapt_ensemble_t e, int64_t* best) {
+    return guard([&] {
+        check_ens(e);
+        auto v = e->best.download(e->stream);
+        for (uint32_t i = 0; i < e->I; ++i) best[i] = v[i];
+    });
+}
+
+tapt_status tapt_reset_observables(tapt_ensemble_t e) {
+    return guard([&] {
+        check_ens(e);
+        e->obs.zero(e->stream);
+        e->hist.zero(e->stream);
+        sync_if(e->stream);
+    });
+}
+
+tapt_status tapt_sweep(tapt_ensemble_t e, uint32_t n_sweeps) {
+    return guard([&] {
+        check_ens(e);
+        e->run(n_sweeps, 0, 0, 0);
+    });
+}
+
+tapt_status tapt_swap_pass(tapt_ensemble_t e, int parity) {
+    return guard([&] {
+        check_ens(e);
+        if (parity != 0 && parity != 1) throw tapt::ConfigError("parity must be 0 or 1");
+        if (e->R >= 2) {
+            ++g_launches;
+            k_swap_pass<<<e->I, std::max(32, (e->R / 2 + 31) / 32 * 32), 0, e->stream>>>(
+                e->E.p, e->slot_of.p, e->buf_of.p, e->R, e->coord.p, e->P, parity, e->swap_tab.view(), e->swap_att.p,
+                e->swap_acc.p);
+            CUDA_OK(cudaGetLastError());
+        }
+        e->P += 1;
+    });
+}
+
+tapt_status tapt_run(tapt_ensemble_t e, const tapt_schedule* s) {
+    return guard([&] {
+        check_ens(e);
+        if (!s) throw tapt::ConfigError("null schedule");
+        if (s->measure_every && !e->obs.p) throw tapt::ConfigError("observables not allocated");
+        e->run(s->n_sweeps, s->swap_every, s->measure_every, s->measure_from);
+    });
+}
+
+}  // extern "C"
+
+// ------------------------------------------------------------- proposals ---
+
+namespace {
+
+// Energies of the proposal set (buffers t = 0..T-1 at slots targets[t]), then
+// Metropolis (Eq. 2) and application.  pwords holds the proposals.
+void finish_proposals(tapt_ensemble_s* e, const uint32_t* targets, uint32_t T, bool have_energies,
+                      const double* lqc, const double* lqp, uint8_t* accepted) {
+    const int n = e->n();
+    const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
+    // proposal energies
+    if (!have_energies) {
+        if (e->use_k1) {
+            PTArgs a = e->base_args();
+            a.words = e->pwords.p;
+            a.G = GT;
+            a.W = WT;
+            a.B = (int)T;
+            a.slot_of = e->pslot.p;
+            a.buf_of = nullptr;
+            a.E = e->pE.p;
+            a.energy_only = 1;
+            a.n_sweeps = 0;
+            a.swap_every = 0;
+            a.measure_every = 0;
+            a.best = nullptr;
+            ++g_launches;
+            cudaError_t err = launch_k1(a, e->m->ld, e->k1_threads, false, e->stream);
+            if (err != cudaSuccess) throw tapt::CudaError(cudaGetErrorString(err));
+        } else {
+            CsrArgs g = e->csr_args(false);
+            ++g_launches;
+            k_energy_csr<<<dim3(GT, e->I), 256, 0, e->stream>>>(e->pwords.p, n, GT, WT, (int)T, g.rowptr, g.col, g.J,
+                                                                 g.nJ, g.nnz, g.h, e->pE.p);
+        }
+        CUDA_OK(cudaGetLastError());
+    }
+    // accept streams for this round
+    std::vector<uint64_t> as(e->I);
+    for (uint32_t i = 0; i < e->I; ++i)
+        as[i] = tapt::RngStream::derive(e->seed, {tapt::stream::kCoordinator, e->gid0 + i, e->Q + 1}).state();
+    e->paccs.upload(as, e->stream);
+    e->pacc.alloc((size_t)e->I * T);
+    const uint8_t* forced = nullptr;
+    if (lqc) {  // MH correction: decide on the host with libm exp (bit-exact with the oracle)
+        std::vector<int32_t> Ep = e->pE.download(e->stream);
+        std::vector<int32_t> Eb = e->E.download(e->stream);
+        std::vector<uint8_t> bo = e->buf_of.download(e->stream);
+        std::vector<uint8_t> f((size_t)e->I * T);
+        for (uint32_t i = 0; i < e->I; ++i)
+            for (uint32_t t = 0; t < T; ++t) {
+                const uint32_t r = targets[t];
+                const double ec = Eb[(size_t)i * e->R + bo[(size_t)i * e->R + r]];
+                const double ep = Ep[(size_t)i * T + t];
+                const double a = std::exp(e->betas[r] * (ec - ep)) *
+                                 std::exp(lqc[(size_t)i * T + t] - lqp[(size_t)i * T + t]);
+                const uint64_t x = tapt::RngStream::from_state(as[i]).at(r + 1);
+                const double u = (double)(x >> 11) * 0x1.0p-53;
+                f[(size_t)i * T + t] = u < a ? 1 : 0;
+            }
+        e->pforced.upload(f, e->stream);
+        forced = e->pforced.p;
+    }
+    ++g_launches;
+    k_accept_proposals<<<e->I, std::max(32, ((int)T + 31) / 32 * 32), 0, e->stream>>>(
+        e->E.p, e->buf_of.p, e->R, e->pE.p, (int)T, e->ptargets.p, e->paccs.p, e->prop_tab.view(), forced, e->pacc.p,
+        e->prop_att.p, e->prop_acc.p);
+    CUDA_OK(cudaGetLastError());
+    ++g_launches;
+    k_apply_proposals<<<dim3((n + 255) / 256, e->G, e->I), 256, 0, e->stream>>>(
+        e->words.p, n, e->G, e->W, e->buf_of.p, e->R, e->pwords.p, GT, WT, e->ptargets.p, (int)T, e->pacc.p);
+    CUDA_OK(cudaGetLastError());
+    e->update_best_from_E();
+    if (accepted) {
+        auto a = e->pacc.download(e->stream);
+        std::copy(a.begin(), a.end(), accepted);
+    }
+    e->Q += 1;
+    sync_if(e->stream);
+}
+
+void prepare_targets(tapt_ensemble_s* e, const uint32_t* targets, uint32_t T) {
+    if (T == 0 || T > (uint32_t)e->R) throw tapt::ConfigError("n_targets must be in [1, n_slots]");
+    std::vector<uint8_t> seen(e->R, 0);
+    for (uint32_t t = 0; t < T; ++t) {
+        if (targets[t] >= (uint32_t)e->R) throw tapt::ConfigError("target slot out of range");
+        if (seen[targets[t]]++) throw tapt::ConfigError("duplicate target slot");
+    }
+    const int n = e->n();
+    const int GT = ((int)T + kW - 1) / kW;
+    e->pwords.alloc((size_t)e->I * GT * n);
+    e->pE.alloc((size_t)e->I * T);
+    std::vector<uint32_t> tg(targets, targets + T);
+    e->ptargets.upload(tg, e->stream);
+    std::vector<uint8_t> ps((size_t)e->I * T);
+    for (uint32_t i = 0; i < e->I; ++i)
+        for (uint32_t t = 0; t < T; ++t) ps[(size_t)i * T + t] = (uint8_t)targets[t];
+    e->pslot.upload(ps, e->stream);
+}
+
+}  // namespace
+
+extern "C" {
+
+tapt_status tapt_inject_proposals(tapt_ensemble_t e, const int8_t* proposals, int on_device, const uint32_t* targets,
+                                  uint32_t T, const double* lqc, const double* lqp, uint8_t* accepted) {
+    return guard([&] {
+        check_ens(e);
+        if ((lqc == nullptr) != (lqp == nullptr)) throw tapt::ConfigError("log_q_cur and log_q_prop go together");
+        prepare_targets(e, targets, T);
+        const int n = e->n();
+        const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
+        const int8_t* src = proposals;
+        if (!on_device) {
+            e->pint8.upload(proposals, (size_t)e->I * T * n, e->stream);
+            src = e->pint8.p;
+        }
+        ++g_launches;
+        k_set_spins<<<dim3((n + 255) / 256, GT, e->I), 256, 0, e->stream>>>(e->pwords.p, n, GT, WT, (int)T, nullptr, src,
+                                                                            (int)T, e->clamp_ptr(), e->clamp_count());
+        CUDA_OK(cudaGetLastError());
+        finish_proposals(e, targets, T, false, lqc, lqp, accepted);
+    });
+}
+
+tapt_status tapt_inject_proposals_packed(tapt_ensemble_t e, const uint8_t* proposals, int on_device,
+                                         const uint32_t* targets, uint32_t T, uint8_t* accepted) {
+    return guard([&] {
+        check_ens(e);
+        prepare_targets(e, targets, T);
+        const int n = e->n(), nb = (n + 7) / 8;
+        const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
+        const uint8_t* src = proposals;
+        if (!on_device) {
+            e->pbytes.upload(proposals, (size_t)e->I * T * nb, e->stream);
+            src = e->pbytes.p;
+        }
+        ++g_launches;
+        k_set_packed<<<dim3((n + 255) / 256, GT, e->I), 256, 0, e->stream>>>(e->pwords.p, n, GT, WT, (int)T, src, (int)T,
+                                                                             e->clamp_ptr(), e->clamp_count());
+        CUDA_OK(cudaGetLastError());
+        finish_proposals(e, targets, T, false, nullptr, nullptr, accepted);
+    });
+}
+
+tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, uint32_t T, const double* m_bias,
+                                    uint32_t refine, uint8_t* accepted) {
+    return guard([&] {
+        check_ens(e);
+        prepare_targets(e, targets, T);
+        const int n = e->n();
+        const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
+        // per (instance, target) proposal streams, per (target, sign) bias thresholds
+        std::vector<uint64_t> qs((size_t)e->I * T), full((size_t)e->I * e->R, 0), tup(2 * T);
+        for (uint32_t i = 0; i < e->I; ++i)
+            for (uint32_t t = 0; t < T; ++t) {
+                const uint64_t q = tapt::RngStream::derive(
+                                       e->seed, {tapt::stream::kReplica, e->gid0 + i, (uint64_t)targets[t], e->Q + 1})
+                                       .state();
+                qs[(size_t)i * T + t] = q;
+                full[(size_t)i * e->R + targets[t]] = q;
+            }
+        for (uint32_t t = 0; t < T; ++t) {
+            const double mb = m_bias ? m_bias[t] : 0.0;
+            tup[2 * t + 0] = threshold_of((1.0 + -1.0 * mb) / 2.0);
+            tup[2 * t + 1] = threshold_of((1.0 + 1.0 * mb) / 2.0);
+        }
+        e->pstreams.upload(qs, e->stream);
+        e->ptup.upload(tup, e->stream);
+        ++g_launches;
+        k_gen_proposals<<<dim3((n + 255) / 256, GT, e->I), 256, 0, e->stream>>>(
+            e->pwords.p, n, GT, WT, (int)T, e->pstreams.p, e->ptup.p, e->clamp_ptr(), e->clamp_count());
+        CUDA_OK(cudaGetLastError());
+        bool have_E = false;
+        if (refine) {
+            DevBuf<uint64_t> fs;
+            fs.upload(full, e->stream);
+            PTArgs a = e->base_args();
+            a.words = e->pwords.p;
+            a.G = GT;
+            a.W = WT;
+            a.B = (int)T;
+            a.streams = fs.p;
+            a.slot_of = e->pslot.p;
+            a.buf_of = nullptr;
+            a.E = e->pE.p;
+            a.draw_base = (uint64_t)n + 1;
+            a.t0 = 0;
+            a.n_sweeps = (int)refine;
+            a.swap_every = 0;
+            a.measure_every = 0;
+            a.best = nullptr;
+            if (!e->use_k1) {  // K2 tracks energies incrementally: seed them
+                CsrArgs g = e->csr_args(false);
+                ++g_launches;
+                k_energy_csr<<<dim3(GT, e->I), 256, 0, e->stream>>>(e->pwords.p, n, GT, WT, (int)T, g.rowptr, g.col,
+                                                                     g.J, g.nJ, g.nnz, g.h, e->pE.p);
+                CUDA_OK(cudaGetLastError());
+            }
+            e->launch(a, false);
+            have_E = true;
+            sync_if(e->stream);
+        }
+        finish_proposals(e, targets, T, have_E, nullptr, nullptr, accepted);
+    });
+}
+
+// ------------------------------------------------------------ drop-in sweep
+
+tapt_status tapt_gibbs_sweep(tapt_model_t m, int8_t* s, size_t len, double beta, uint64_t* rng_state,
+                             uint32_t n_sweeps, double* dE) {
+    return guard([&] {
+        check_model(m);
+        if (len != m->n) throw tapt::DimensionError("configuration length mismatch");
+        if (!(beta >= 0.0)) throw tapt::ConfigError("beta must be >= 0");
+        if (!rng_state) throw tapt::ConfigError("null rng state");
+        if (n_sweeps == 0) return;
+        tapt_ensemble_desc d{};
+        d.n_instances = 1;
+        d.n_slots = 1;
+        d.betas = &beta;
+        d.seed = 0;
+        d.order = TAPT_ORDER_REFERENCE;
+        tapt_ensemble_t e = nullptr;
+        if (tapt_ensemble_create(m, &d, &e) != TAPT_OK) throw tapt::CudaError(g_last_error);
+        std::unique_ptr<tapt_ensemble_s, tapt_status (*)(tapt_ensemble_t)> hold(e, tapt_ensemble_destroy);
+        const uint64_t st = *rng_state;
+        e->streams.upload(&st, 1, e->stream);
+        // gibbs_sweep never writes clamped sites and reads whatever they hold (mcmc.cpp:34-37)
+        set_spins_impl(e, s, false);
+        int64_t e0 = 0;
+        tapt_ensemble_get_energies(e, &e0);
+        for (uint32_t k = 0; k < n_sweeps; ++k) {
+            e->run(1, 0, 0, 0);
+            int64_t e1 = 0;
+            if (tapt_ensemble_get_energies(e, &e1) != TAPT_OK) throw tapt::CudaError(g_last_error);
+            if (dE) dE[k] = (double)(e1 - e0);
+            e0 = e1;
+        }
+        if (tapt_ensemble_get_spins(e, s) != TAPT_OK) throw tapt::CudaError(g_last_error);
+        *rng_state = st + (uint64_t)n_sweeps * (uint64_t)m->free_sites.size() * tapt_dev::kPhi;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,353 @@
+// k1_lattice.cu -- K1: fused parallel-tempering kernel for periodic 2D/3D lattices
+// with +-J0 nearest-neighbour bonds (BASELINE configs 1, 2, 3, 5).
+//
+// One CTA owns one group of W <= 32 replicas of one instance; its spins live in
+// shared memory for the whole launch in multi-replica coding (word = site, bit =
+// replica).  An instance with R > 32 slots is a thread-block cluster of R/32 CTAs
+// that exchange per-replica energies through DSMEM once per sweep, so the
+// replica-exchange pass runs in-kernel with no host round trip.
+//
+// Per sweep: colour 0 then colour 1 of the checkerboard.  For a site word, the
+// 2*dim neighbour words give, bit-sliced over the 32 replicas, the count q of
+// neighbours with J*s_j = +1 (so l = J0*(2q - z)); q is spread into 4-bit
+// nibbles so each replica's threshold-table index is one shift+mask.  Every
+// replica then needs one counter-addressed splitmix64 draw:
+//     draw index  k = draw_base + t*n + i + 1     (site rank i: no clamps)
+// which is the reference's per-site stream position (mcmc.cpp:30-45 advances the
+// stream once per free site in ascending order), so the result is bit-exact with
+// the colour-order restatement in oracle/tapt_oracle.c.
+// Energies are recomputed exactly during the colour-1 half: in a bipartite
+// lattice every bond has exactly one colour-1 end, so summing unsatisfied bonds
+// of colour-1 sites counts each bond once:  E = J0 * (2*U - n*dim).
+#include <cuda_runtime.h>
+
+#include "pt_common.cuh"
+
+namespace tapt_dev {
+
+template <int DIM>
+__device__ __forceinline__ int colour_site(int j, int c, const LatDims& d, int& x, int& y, int& z) {
+    // j's low bit picks one of two consecutive rows (opposite colour parity), so a
+    // warp's loads alternate between even and odd words: no shared-memory bank
+    // conflicts for rows of >= 32 sites.
+    const int rb = j & 1, q = j >> 1;
+    const int m = q & ((1 << d.log2hx) - 1);
+    const int row = ((q >> d.log2hx) << 1) | rb;
+    y = row & ((1 << d.log2Ly) - 1);
+    z = (DIM == 3) ? (row >> d.log2Ly) : 0;
+    x = (m << 1) | ((y + z + c) & 1);
+    return x + (row << d.log2Lx);
+}
+
+// Bit-sliced count of neighbours with J*s_j = +1: returns planes q0 (1), q1 (2), q2 (4).
+template <int DIM, bool DIS>
+__device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const uint8_t* __restrict__ bonds, int i,
+                                           int x, int y, int z, const LatDims& d, uint32_t& q0, uint32_t& q1,
+                                           uint32_t& q2) {
+    const int Lx = 1 << d.log2Lx, Ly = 1 << d.log2Ly;
+    const int rowb = i - x;
+    uint32_t p0 = w[rowb + ((x + 1) & (Lx - 1))];
+    uint32_t p1 = w[rowb + ((x - 1) & (Lx - 1))];
+    const int ip = i + ((y == Ly - 1) ? -(Ly - 1) * Lx : Lx);
+    const int im = i + ((y == 0) ? (Ly - 1) * Lx : -Lx);
+    uint32_t p2 = w[ip], p3 = w[im];
+    uint32_t p4 = 0, p5 = 0;
+    if constexpr (DIM == 3) {
+        const int P = Lx * Ly;
+        const int Lz = Ly;
+        const int kp = i + ((z == Lz - 1) ? -(Lz - 1) * P : P);
+        const int km = i + ((z == 0) ? (Lz - 1) * P : -P);
+        p4 = w[kp];
+        p5 = w[km];
+    }
+    if constexpr (DIS) {
+        const uint32_t bb = bonds[i];  // bit d set: bond in direction d has J = -J0
+        p0 ^= 0u - (bb & 1u);
+        p1 ^= 0u - ((bb >> 1) & 1u);
+        p2 ^= 0u - ((bb >> 2) & 1u);
+        p3 ^= 0u - ((bb >> 3) & 1u);
+        if constexpr (DIM == 3) {
+            p4 ^= 0u - ((bb >> 4) & 1u);
+            p5 ^= 0u - ((bb >> 5) & 1u);
+        }
+    }
+    if constexpr (DIM == 3) {
+        const uint32_t sa = p0 ^ p1 ^ p2, ca = maj3(p0, p1, p2);
+        const uint32_t sb = p3 ^ p4 ^ p5, cb = maj3(p3, p4, p5);
+        q0 = sa ^ sb;
+        const uint32_t c0 = sa & sb;
+        q1 = ca ^ cb ^ c0;
+        q2 = maj3(ca, cb, c0);
+    } else {
+        const uint32_t sa = p0 ^ p1 ^ p2, ca = maj3(p0, p1, p2);
+        q0 = sa ^ p3;
+        const uint32_t c0 = sa & p3;
+        q1 = ca ^ c0;
+        q2 = ca & c0;
+    }
+}
+
+// Planes of the number of unsatisfied bonds at a site whose new word is s:
+// bond d is satisfied iff s == p_d, so #unsat = s ? z - q : q.
+template <int DIM>
+__device__ __forceinline__ void unsat_planes(uint32_t s, uint32_t q0, uint32_t q1, uint32_t q2, uint32_t& u0,
+                                             uint32_t& u1, uint32_t& u2) {
+    uint32_t r0, r1, r2;  // z - q
+    if constexpr (DIM == 3) {
+        r0 = q0;
+        r1 = ~q1 ^ q0;
+        r2 = ~q2 ^ (q1 & q0);
+    } else {
+        r0 = q0;
+        r1 = q1 ^ q0;
+        r2 = ~(q0 | q1 | q2);
+    }
+    u0 = (s & r0) | (~s & q0);
+    u1 = (s & r1) | (~s & q1);
+    u2 = (s & r2) | (~s & q2);
+}
+
+// Nibble spread: nibble k of N[m] = q of replica 4k+m.
+__device__ __forceinline__ void nibbles(uint32_t q0, uint32_t q1, uint32_t q2, uint32_t (&N)[4]) {
+    constexpr uint32_t K1 = 0x11111111u;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const uint32_t a = (q0 >> m) & K1;
+        const uint32_t b = (m >= 1 ? (q1 >> (m - 1)) : (q1 << 1)) & (K1 << 1);
+        const uint32_t c = (m >= 2 ? (q2 >> (m - 2)) : (q2 << (2 - m))) & (K1 << 2);
+        N[m] = a | b | c;
+    }
+}
+
+struct K1Smem {
+    PTShared S;
+    uint32_t Uhi[kW][8];   // per own buffer: high words of T*2^11-1 for its current slot
+    uint64_t T64[kW][8];   // per own buffer: exact thresholds (tie path)
+};
+
+// Heat-bath decisions for one site word over the W replicas of this CTA.
+__device__ __forceinline__ uint32_t k1_decide_exact(const K1Smem& sm, int W, uint64_t phi_i, const uint32_t (&N)[4]) {
+    uint32_t nw = 0;
+    for (int b = 0; b < W; ++b) {
+        const uint32_t idx = (N[b & 3] >> (4 * (b >> 2))) & 7u;
+        const uint64_t x = mix_final(sm.S.sb[b] + phi_i);
+        if (below(x, sm.T64[b][idx])) nw |= 1u << b;
+    }
+    return nw;
+}
+
+template <int DIM, bool DIS, bool CLU>
+__global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDims d) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
+    uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K1Smem));
+    uint8_t* bonds = reinterpret_cast<uint8_t*>(words + a.n);
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const int inst = blockIdx.x / a.G, grp = blockIdx.x % a.G;
+    const int n = a.n, W = a.W;
+    const int half = n >> 1, nsub = half >> 1;
+
+    // ---- load this CTA's spins (and the instance's bond signs) into shared memory
+    {
+        const uint4* src = reinterpret_cast<const uint4*>(a.words + ((size_t)inst * a.G + grp) * n);
+        uint4* dst = reinterpret_cast<uint4*>(words);
+        for (int k = tid; k < (n >> 2); k += nt) dst[k] = src[k];
+        if constexpr (DIS) {
+            const uint4* bs = reinterpret_cast<const uint4*>(a.bonds + (size_t)inst * n);
+            uint4* bd = reinterpret_cast<uint4*>(bonds);
+            for (int k = tid; k < (n >> 4); k += nt) bd[k] = bs[k];
+        }
+    }
+    pt_load_perm(a, sm.S, inst);
+    __syncthreads();
+
+    uint64_t pass = a.p0;
+    int par = 0;
+    const int nsw = a.energy_only ? 1 : a.n_sweeps;
+    for (int s = 0; s < nsw; ++s) {
+        const uint64_t t = a.t0 + (uint64_t)s;
+        par = (int)(t & 1);
+        // per-buffer tables and stream bases for the slots the buffers occupy now
+        for (int e = tid; e < W * 8; e += nt) {
+            const int b = e >> 3, k = e & 7;
+            const int slot = sm.S.slot_of[grp * W + b];
+            const uint64_t T = k < a.nidx ? a.thr[(size_t)slot * a.nidx + k] : 0ull;
+            sm.Uhi[b][k] = thr_hi(T);
+            sm.T64[b][k] = T;
+        }
+        pt_stream_bases(a, sm.S, inst, grp, t);
+        __syncthreads();
+
+        uint32_t C[kCnt];
+#pragma unroll
+        for (int k = 0; k < kCnt; ++k) C[k] = 0;
+
+        for (int c = (a.energy_only ? 1 : 0); c < 2; ++c) {
+            for (int j = tid; j < nsub; j += nt) {
+                int xs[2], ys[2], zs[2], is[2];
+                is[0] = colour_site<DIM>(j, c, d, xs[0], ys[0], zs[0]);
+                is[1] = colour_site<DIM>(j + nsub, c, d, xs[1], ys[1], zs[1]);
+                uint32_t q[2][3], N[2][4];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    k1_stencil<DIM, DIS>(words, bonds, is[u], xs[u], ys[u], zs[u], d, q[u][0], q[u][1], q[u][2]);
+                    nibbles(q[u][0], q[u][1], q[u][2], N[u]);
+                }
+                uint32_t nw[2];
+                if (a.energy_only) {
+                    nw[0] = words[is[0]];
+                    nw[1] = words[is[1]];
+                } else {
+                    const uint64_t ph0 = (uint64_t)(uint32_t)is[0] * kPhi;
+                    const uint64_t ph1 = (uint64_t)(uint32_t)is[1] * kPhi;
+                    uint32_t w0 = 0, w1 = 0;
+                    bool tie = false;
+#pragma unroll
+                    for (int b = 0; b < kW; ++b) {
+                        if (b < W) {
+                            const uint64_t base = sm.S.sb[b];
+                            const int m = b & 3, sh = 4 * (b >> 2);
+                            const uint32_t i0 = (N[0][m] >> sh) & 7u;
+                            const uint32_t i1 = (N[1][m] >> sh) & 7u;
+                            const uint32_t u0 = sm.Uhi[b][i0];
+                            const uint32_t u1 = sm.Uhi[b][i1];
+                            const uint32_t x0 = mix_final_hi(base + ph0);
+                            const uint32_t x1 = mix_final_hi(base + ph1);
+                            w0 |= (x0 < u0) ? (1u << b) : 0u;
+                            w1 |= (x1 < u1) ? (1u << b) : 0u;
+                            tie |= (x0 == u0) | (x1 == u1);
+                        }
+                    }
+                    if (tie) {  // probability ~ 2^-32 per decision: redo both words exactly
+                        w0 = k1_decide_exact(sm, W, ph0, N[0]);
+                        w1 = k1_decide_exact(sm, W, ph1, N[1]);
+                    }
+                    nw[0] = w0;
+                    nw[1] = w1;
+                    words[is[0]] = w0;
+                    words[is[1]] = w1;
+                }
+                if (c == 1) {
+#pragma unroll
+                    for (int u = 0; u < 2; ++u) {
+                        uint32_t v0, v1, v2;
+                        unsat_planes<DIM>(nw[u], q[u][0], q[u][1], q[u][2], v0, v1, v2);
+                        sliced_add3<kCnt>(C, v0, v1, v2);
+                    }
+                }
+            }
+            __syncthreads();
+        }
+        // exact energies: E = J0 * (2*U - n*dim)
+        {
+            const uint32_t tot = warp_sliced_total<kCnt>(C);
+            if (lane < W) atomicAdd(&sm.S.Ucnt[lane], tot);
+            __syncthreads();
+            if (tid < W) {
+                sm.S.Eown[par][tid] = d.J0 * (2 * (int)sm.S.Ucnt[tid] - n * DIM);
+                sm.S.Ucnt[tid] = 0;
+            }
+        }
+        if (a.energy_only) break;
+        pt_epilogue<CLU>(a, sm.S, words, inst, grp, t, pass);
+    }
+    if (a.energy_only) {
+        __syncthreads();
+        for (int b = tid; b < W; b += nt) a.E[(size_t)inst * a.B + grp * W + b] = sm.S.Eown[par][b];
+        return;
+    }
+    // ---- write back
+    {
+        uint4* dst = reinterpret_cast<uint4*>(a.words + ((size_t)inst * a.G + grp) * n);
+        const uint4* src = reinterpret_cast<const uint4*>(words);
+        for (int k = tid; k < (n >> 2); k += nt) dst[k] = src[k];
+    }
+    pt_finish<CLU>(a, sm.S, inst, grp, par);
+}
+
+size_t k1_smem_bytes(int n, bool dis) {
+    return sizeof(K1Smem) + (size_t)n * 4 + (dis ? (size_t)n : 0);
+}
+
+template <int DIM, bool DIS, bool CLU>
+static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st) {
+    const size_t smem = k1_smem_bytes(a.n, DIS);
+    auto fn = k1_lattice_pt<DIM, DIS, CLU>;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(a.I * a.G));
+    cfg.blockDim = dim3((unsigned)threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    if (CLU) {
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)a.G;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+    }
+    return cudaLaunchKernelEx(&cfg, fn, a, d);
+}
+
+cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st) {
+    const bool dis = a.bonds != nullptr;
+    if (d.dim == 2) {
+        if (dis) return cluster ? launch_k1_t<2, true, true>(a, d, threads, st) : launch_k1_t<2, true, false>(a, d, threads, st);
+        return cluster ? launch_k1_t<2, false, true>(a, d, threads, st) : launch_k1_t<2, false, false>(a, d, threads, st);
+    }
+    if (dis) return cluster ? launch_k1_t<3, true, true>(a, d, threads, st) : launch_k1_t<3, true, false>(a, d, threads, st);
+    return cluster ? launch_k1_t<3, false, true>(a, d, threads, st) : launch_k1_t<3, false, false>(a, d, threads, st);
+}
+
+}  // namespace tapt_dev
+
+// ---------------------------------------------------------------------------
+// Decision-rate probe: the irreducible per-update work of K1 with no stencil and no
+// memory traffic -- one counter-addressed splitmix64 draw (high word), one threshold
+// lookup in shared memory, one compare, one bit insert -- in the same unrolled 2x32
+// form as the sweep loop.  Its rate is the measured ALU ceiling used as the roofline
+// denominator by bench.py.
+namespace tapt_dev {
+
+__global__ void __launch_bounds__(512) k_decision_probe(uint32_t iters, uint32_t* sink) {
+    __shared__ uint32_t Uhi[kW][8];
+    __shared__ uint64_t sb[kW];
+    const int tid = threadIdx.x;
+    for (int e = tid; e < kW * 8; e += blockDim.x) Uhi[e >> 3][e & 7] = 0x80000000u + (uint32_t)e * 977u;
+    for (int e = tid; e < kW; e += blockDim.x) sb[e] = 0x1234567ull * (e + 1);
+    __syncthreads();
+    const uint32_t gid = blockIdx.x * blockDim.x + tid;
+    uint32_t N0 = gid * 0x9E3779B9u, N1 = gid * 0x85EBCA6Bu;
+    uint32_t acc = 0;
+    bool tie = false;
+    for (uint32_t it = 0; it < iters; ++it) {
+        const uint64_t ph0 = (uint64_t)(2 * gid + it * 7919u) * kPhi;
+        const uint64_t ph1 = ph0 + kPhi;
+        uint32_t w0 = 0, w1 = 0;
+#pragma unroll
+        for (int b = 0; b < kW; ++b) {
+            const uint64_t base = sb[b];
+            const int sh = 4 * (b >> 2);
+            const uint32_t i0 = (N0 >> sh) & 7u, i1 = (N1 >> sh) & 7u;
+            const uint32_t u0 = Uhi[b][i0], u1 = Uhi[b][i1];
+            const uint32_t x0 = mix_final_hi(base + ph0), x1 = mix_final_hi(base + ph1);
+            w0 |= (x0 < u0) ? (1u << b) : 0u;
+            w1 |= (x1 < u1) ? (1u << b) : 0u;
+            tie |= (x0 == u0) | (x1 == u1);
+        }
+        N0 = w0 ^ (N1 >> 3);
+        N1 = w1 ^ (N0 << 1);
+        acc += w0 ^ w1;
+    }
+    sink[gid] = acc + (tie ? 1u : 0u);
+}
+
+cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st) {
+    k_decision_probe<<<blocks, threads, 0, st>>>(iters, sink);
+    return cudaGetLastError();
+}
+
+}  // namespace tapt_dev

@@ -1,0 +1,79 @@
+// kernels.h -- argument blocks shared by the host driver (engine.cpp) and the CUDA kernels.
+//
+// State layout in HBM (one ensemble = I instances x B buffers):
+//   words [I][G][n] uint32  -- multi-replica spin coding: bit b of word (i, g, site)
+//                              is the spin (1 = +1) of buffer g*W+b at that site.
+//   E     [I][B]    int32   -- energy of each buffer (integer couplings, exact)
+//   slot_of [I][B], buf_of [I][R]  uint8 -- the slot<->buffer permutation.  A swap
+//                               exchanges two entries; no spins move.
+// The dynamics stream and the beta of a buffer are those of the ladder slot it
+// currently occupies.
+#pragma once
+#include <cstdint>
+
+#include "common.cuh"
+
+namespace tapt_dev {
+
+constexpr int kMaxR = 256;   // ladder slots per instance (uint8 permutation)
+constexpr int kW = 32;       // replicas per group (bits per word)
+constexpr int kCnt = 8;      // planes of the sliced per-thread counters
+
+struct LatDims {
+    int dim;              // 2 or 3
+    int log2Lx, log2Ly;   // 2D: Lx, Ly; 3D: L = Lx = Ly = Lz
+    int log2hx;           // log2(Lx/2): colour sites per row
+    int J0;               // |J|
+};
+
+// Everything one fused PT launch needs (lattice K1 and CSR K2 share it).
+struct PTArgs {
+    uint32_t* words;
+    int I, G, W, B;            // instances, groups per instance, replicas per group, buffers
+    int n;                     // sites per replica
+    const uint8_t* bonds;      // [I][n] lattice bond-sign bytes (bit d: bond in direction d is -J0), or null
+    uint32_t n_free;           // free sites (draw counter stride per sweep)
+    int R;                     // ladder slots
+    const uint64_t* streams;   // [I][R] dynamics stream state by ladder slot
+    uint8_t* slot_of;          // [I][B]
+    uint8_t* buf_of;           // [I][R]
+    const uint64_t* thr;       // [R][nidx] heat-bath thresholds T = ceil(p*2^53)
+    int nidx;                  // entries per slot
+    uint64_t draw_base;        // extra offset of every dynamics draw counter
+    uint64_t t0;               // global index of the first sweep of this launch
+    int n_sweeps;
+    int32_t* E;                // [I][B] out
+    int energy_only;           // recompute energies, no sweeps
+    // replica exchange
+    int swap_every;            // 0: no swaps
+    uint64_t p0;               // global index of the first swap pass in this launch
+    const uint64_t* coord;     // [I] coordinator stream states
+    MetroTable swap_tab;       // rows = pairs (r, r+1)
+    uint64_t* swap_att;        // [I][R-1]
+    uint64_t* swap_acc;
+    // observables (by slot)
+    int measure_every;
+    uint64_t measure_from;
+    long long* obs;            // [I][R][5]: count, sum E, sum E^2, sum |M|, sum M^2
+    unsigned long long* hist;  // [R][nbins] (summed over instances)
+    long long e_lo, width;
+    int nbins;
+    int* best;                 // [I] lowest energy seen (atomicMin)
+};
+
+// CSR graph (K2): shared structure; couplings may be per instance.
+struct CsrArgs {
+    const uint32_t* rowptr;    // [n+1]
+    const uint32_t* col;       // [nnz]
+    const int8_t* J;           // [nJ][nnz]
+    int nJ;                    // 1 (shared) or I (per instance)
+    int nnz;
+    const int32_t* h;          // [n]
+    const uint32_t* rank;      // [n] position in the ascending free list
+    const uint32_t* class_ptr; // [n_classes+1] into class_sites
+    const uint32_t* class_sites;
+    int n_classes;
+    int lmin;                  // thresholds indexed by (l - lmin)
+};
+
+}  // namespace tapt_dev

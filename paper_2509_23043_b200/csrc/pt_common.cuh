@@ -1,0 +1,147 @@
+// pt_common.cuh -- the per-sweep epilogue shared by the fused PT kernels:
+// energy gather across the CTAs of an instance (thread-block cluster / DSMEM),
+// replica-exchange pass (Eq. 1), best-energy tracking and the
+// per-slot observables (magnetization() numerator, spin_model.cpp:109-114).
+#pragma once
+#include <cooperative_groups.h>
+
+#include "kernels.h"
+
+namespace tapt_dev {
+
+namespace cg = cooperative_groups;
+
+struct PTShared {
+    uint64_t sb[kW];        // stream base of each own buffer for the current sweep
+    int32_t Eown[2][kW];    // energies of own buffers, double-buffered by sweep parity
+    uint32_t Ucnt[kW];      // per-buffer unsatisfied-bond (or energy) accumulators
+    uint32_t Mcnt[kW];      // per-buffer up-spin counts (measurement)
+    int32_t Eall[kMaxR];    // energies of all buffers of the instance
+    uint8_t slot_of[kMaxR];
+    uint8_t buf_of[kMaxR];
+    int best;
+    int tie;
+};
+
+// Load the permutation of instance `inst` into shared memory.
+__device__ __forceinline__ void pt_load_perm(const PTArgs& a, PTShared& S, int inst) {
+    for (int k = threadIdx.x; k < a.B; k += blockDim.x) S.slot_of[k] = a.slot_of[(size_t)inst * a.B + k];
+    if (a.buf_of)
+        for (int k = threadIdx.x; k < a.R; k += blockDim.x) S.buf_of[k] = a.buf_of[(size_t)inst * a.R + k];
+    if (threadIdx.x == 0) {
+        S.best = a.best ? a.best[inst] : 0x7FFFFFFF;
+        S.tie = 0;
+    }
+    for (int k = threadIdx.x; k < kW; k += blockDim.x) {
+        S.Ucnt[k] = 0;
+        S.Mcnt[k] = 0;
+    }
+}
+
+// Per-buffer stream base for sweep t: S_slot + (draw_base + t*n_free + 1)*phi.
+__device__ __forceinline__ void pt_stream_bases(const PTArgs& a, PTShared& S, int inst, int grp, uint64_t t) {
+    for (int b = threadIdx.x; b < a.W; b += blockDim.x) {
+        const int slot = S.slot_of[grp * a.W + b];
+        const uint64_t k0 = a.draw_base + t * (uint64_t)a.n_free + 1ull;
+        S.sb[b] = a.streams[(size_t)inst * a.R + slot] + k0 * kPhi;
+    }
+}
+
+// After Eown[par] is final for this CTA: gather, best, swap, measure.
+// `words` = this CTA's group spins in shared memory (n words).
+template <bool CLU>
+__device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words, int inst, int grp, uint64_t t,
+                            uint64_t& pass) {
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const int par = (int)(t & 1);
+    if constexpr (CLU) {
+        cg::cluster_group cl = cg::this_cluster();
+        cl.sync();
+        for (int gb = tid; gb < a.B; gb += nt) {
+            const int r = gb / a.W;
+            const int32_t* peer = cl.map_shared_rank(&S.Eown[par][0], r);
+            S.Eall[gb] = peer[gb - r * a.W];
+        }
+    } else {
+        // Without a cluster only this CTA's buffers are visible; the host never asks
+        // for swaps or best-energy tracking when an instance spans several CTAs here.
+        __syncthreads();
+        for (int b = tid; b < a.W; b += nt) S.Eall[grp * a.W + b] = S.Eown[par][b];
+    }
+    __syncthreads();
+    const uint64_t T = t + 1;
+    if (tid == 0 && a.best) {
+        int m = S.best;
+        for (int b = 0; b < a.B; ++b) m = min(m, S.Eall[b]);
+        S.best = m;
+    }
+    if (a.swap_every > 0 && (T % (uint64_t)a.swap_every) == 0) {
+        const int parity = (int)(pass & 1);
+        const uint64_t c0 = a.coord[inst];
+        for (int r = parity + 2 * tid; r + 1 < a.R; r += 2 * nt) {
+            const int b0 = S.buf_of[r], b1 = S.buf_of[r + 1];
+            const int64_t dE = (int64_t)S.Eall[b1] - (int64_t)S.Eall[b0];
+            const uint64_t x = draw(c0, pass * (uint64_t)a.R + (uint64_t)r + 1ull);
+            const bool acc = metro_accept(a.swap_tab, r, dE, x);
+            if (grp == 0) {
+                const size_t q = (size_t)inst * (a.R - 1) + r;
+                a.swap_att[q] += 1;
+                if (acc) a.swap_acc[q] += 1;
+            }
+            if (acc) {
+                S.buf_of[r] = (uint8_t)b1;
+                S.buf_of[r + 1] = (uint8_t)b0;
+                S.slot_of[b1] = (uint8_t)r;
+                S.slot_of[b0] = (uint8_t)(r + 1);
+            }
+        }
+        ++pass;
+        __syncthreads();
+    }
+    if (a.measure_every > 0 && T > a.measure_from && (T % (uint64_t)a.measure_every) == 0) {
+        uint32_t C[kCnt];
+#pragma unroll
+        for (int k = 0; k < kCnt; ++k) C[k] = 0;
+        for (int i = tid; i < a.n; i += nt) sliced_add1<kCnt>(C, words[i]);
+        const uint32_t tot = warp_sliced_total<kCnt>(C);
+        if (lane < a.W) atomicAdd(&S.Mcnt[lane], tot);
+        __syncthreads();
+        if (tid < a.W) {
+            const int gb = grp * a.W + tid;
+            const int slot = S.slot_of[gb];
+            const long long e = S.Eall[gb];
+            const long long m = 2ll * (long long)S.Mcnt[tid] - a.n;
+            long long* o = a.obs + ((size_t)inst * a.R + slot) * 5;
+            atomicAdd((unsigned long long*)&o[0], 1ull);
+            atomicAdd((unsigned long long*)&o[1], (unsigned long long)e);
+            atomicAdd((unsigned long long*)&o[2], (unsigned long long)(e * e));
+            atomicAdd((unsigned long long*)&o[3], (unsigned long long)(m < 0 ? -m : m));
+            atomicAdd((unsigned long long*)&o[4], (unsigned long long)(m * m));
+            if (a.hist && a.nbins > 0) {
+                long long bin = e < a.e_lo ? 0 : (e - a.e_lo) / a.width;
+                if (bin >= a.nbins) bin = a.nbins - 1;
+                atomicAdd(&a.hist[(size_t)slot * a.nbins + bin], 1ull);
+            }
+            S.Mcnt[tid] = 0;
+        }
+        __syncthreads();
+    }
+}
+
+// End of launch: persist permutation, energies of own buffers and best energy.
+template <bool CLU>
+__device__ void pt_finish(const PTArgs& a, PTShared& S, int inst, int grp, int last_par) {
+    const int tid = threadIdx.x;
+    __syncthreads();
+    if (a.E)
+        for (int b = tid; b < a.W; b += blockDim.x) a.E[(size_t)inst * a.B + grp * a.W + b] = S.Eown[last_par][b];
+    if (grp == 0) {
+        for (int k = tid; k < a.B; k += blockDim.x) a.slot_of[(size_t)inst * a.B + k] = S.slot_of[k];
+        if (a.buf_of)
+            for (int k = tid; k < a.R; k += blockDim.x) a.buf_of[(size_t)inst * a.R + k] = S.buf_of[k];
+        if (tid == 0 && a.best) atomicMin(&a.best[inst], S.best);
+    }
+    if constexpr (CLU) cg::this_cluster().sync();  // peers may still read our Eown
+}
+
+}  // namespace tapt_dev

@@ -1,0 +1,371 @@
+"""GPU parity tests: the sm_100a kernels (through the C ABI) against the oracle
+restatement and the reference golden vectors -- bit-exact spins, energies, swap and
+proposal decisions, observables.  Marked `gpu`."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2509_23043_b200 as T
+from oracle import oracle as O
+import tapt_helpers as H
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def unpack(bits, n):
+    return np.where(np.unpackbits(bits)[:n] > 0, 1, -1).astype(np.int8)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if T.device_count() == 0:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+
+
+def compare(ens, pts, check_counts=True):
+    S = ens.spins()
+    E = ens.energies()
+    sa, sc, pa, pc = ens.acceptance()
+    for k, pt in enumerate(pts):
+        assert np.array_equal(E[k], pt.E), f"energies differ, instance {k}"
+        assert np.array_equal(S[k], pt.spins), f"spins differ, instance {k}"
+        if check_counts:
+            assert np.array_equal(sc[k], pt.swap_acc[: ens.R - 1]), f"swap accepts differ, instance {k}"
+            assert np.array_equal(sa[k], pt.swap_att[: ens.R - 1])
+            assert np.array_equal(pc[k], pt.prop_acc)
+
+
+# ------------------------------------------------------------ K1 lattice ----
+
+def test_cfg1_geometry_checkerboard_pt_bit_exact():
+    """Config 1 shape: 2D L=32 ferro, 32 slots geometric [0.2, 1.0], swap every sweep."""
+    betas = H.geometric(0.2, 1.0, 32)
+    m = T.Model.lattice((32, 32))
+    e = T.Ensemble(m, betas, n_instances=2, seed=2024)
+    assert e.kernel == "lattice"
+    e.init_random()
+    e.run(300, swap_every=1)
+    pts = H.run_oracle([O.lattice_graph((32, 32))] * 2, betas, 2024, 0, H.checkerboard_order((32, 32)), 300)
+    compare(e, pts)
+
+
+def test_ea3d_cluster_pt_bit_exact():
+    """3D EA +-J, 64 slots (2-CTA cluster per instance), device-generated disorder."""
+    L, R = 8, 64
+    betas = H.linear(0.2, 3.0, R)
+    m = T.Model.lattice((L,))
+    e = T.Ensemble(m, betas, n_instances=3, seed=77, instance_offset=5)
+    e.generate_ea_disorder(1234)
+    graphs = [O.ea_graph((L,), 1234, 5 + k) for k in range(3)]
+    n, ci, cj, _ = O.lattice_couplings((L,), 1.0, True)
+    signs = e.bond_signs(len(ci))
+    for k in range(3):
+        assert np.array_equal(signs[k].astype(float), O.ea_signs((L,), 1234, 5 + k))
+    e.init_random()
+    e.run(120, swap_every=1)
+    pts = H.run_oracle(graphs, betas, 77, 5, H.checkerboard_order((L,)), 120)
+    compare(e, pts)
+
+
+def test_2d64_two_groups_and_measurements():
+    """2D L=64 (config 2 geometry) with 40 slots (partial second group) and observables."""
+    betas = H.geometric(0.3, 0.6, 40)
+    m = T.Model.lattice((64, 64))
+    e = T.Ensemble(m, betas, n_instances=1, seed=9)
+    e.init_random()
+    e.run(60, swap_every=1, measure_every=3, measure_from=10)
+    pts = H.run_oracle([O.lattice_graph((64, 64))], betas, 9, 0, H.checkerboard_order((64, 64)), 60,
+                       measure_every=3, measure_from=10)
+    compare(e, pts)
+    obs = e.observables()[0]
+    mm = pts[0].meas
+    for j, key in enumerate(("cnt", "sumE", "sumE2", "sumAbsM", "sumM2")):
+        assert np.array_equal(obs[:, j], mm[key]), key
+
+
+def test_histograms_and_best():
+    L, R = 6, 12
+    betas = H.linear(0.2, 3.0, R)
+    m = T.Model.lattice((8,))
+    e = T.Ensemble(m, betas, n_instances=2, seed=3)
+    e.generate_ea_disorder(8)
+    e.set_histogram(-3 * 512, 64, 48)
+    e.init_random()
+    e.run(80, swap_every=1, measure_every=10, measure_from=20)
+    graphs = [O.ea_graph((8,), 8, k) for k in range(2)]
+    pts = H.run_oracle(graphs, betas, 3, 0, H.checkerboard_order((8,)), 80, measure_every=10, measure_from=20,
+                       e_lo=-3 * 512, width=64, nbins=48)
+    compare(e, pts)
+    hist = e.histogram()
+    assert np.array_equal(hist.astype(np.int64), pts[0].hist + pts[1].hist)
+    assert np.array_equal(e.best(), [pt.best for pt in pts])
+    del L
+
+
+def test_sweep_and_standalone_swap_compose():
+    """tapt_sweep + tapt_swap_pass reproduce the fused run."""
+    betas = H.geometric(0.2, 1.0, 16)
+    m = T.Model.lattice((16, 16))
+    a = T.Ensemble(m, betas, seed=1)
+    b = T.Ensemble(m, betas, seed=1)
+    a.init_random()
+    b.init_random()
+    a.run(30, swap_every=1)
+    for t in range(30):
+        b.sweep(1)
+        b.swap_pass(t & 1)
+    assert np.array_equal(a.spins(), b.spins())
+    assert np.array_equal(a.energies(), b.energies())
+    assert np.array_equal(a.acceptance()[1], b.acceptance()[1])
+
+
+# ------------------------------------------------------------ K2 CSR --------
+
+def test_reference_order_pt_matches_reference_golden():
+    """Index-order PT on the device == the reference's own gibbs_sweep driven PT (golden)."""
+    f = np.load(os.path.join(GOLD, "pt_cfg1_200.npz"))
+    I, R, n = (int(x) for x in f["shape"])
+    m = T.Model.lattice((32, 32))
+    e = T.Ensemble(m, f["betas"], n_instances=I, seed=int(f["seed"]), instance_offset=int(f["gid0"]),
+                   order="reference")
+    assert e.kernel == "csr"
+    e.init_random()
+    e.run(int(f["n_sweeps"]), swap_every=int(f["swap_every"]))
+    spins = unpack(f["spins"], I * R * n).reshape(I, R, n)
+    assert np.array_equal(e.spins(), spins)
+    assert np.array_equal(e.energies().astype(np.float64), f["E"])
+    assert np.array_equal(e.acceptance()[1], f["swap_acc"][:, : R - 1])
+
+
+@pytest.mark.parametrize("tag", ["2d32", "ea3d8", "2d6clamped"])
+def test_dropin_gibbs_sweep_matches_reference_golden(tag):
+    f = np.load(os.path.join(GOLD, f"sweep_{tag}.npz"))
+    if tag == "2d32":
+        g = O.lattice_graph((32, 32))
+        m = T.Model.lattice((32, 32))
+    elif tag == "ea3d8":
+        g = O.ea_graph((8,), 7, 0)
+        m = T.Model.graph(g.n, g.ci, g.cj, g.J)
+    else:
+        cl = np.array([1, -1, -1, 1, 1, -1] + [0] * 30, np.int8)
+        g = O.lattice_graph((6, 6), 1.0, False, cl)
+        m = T.Model.graph(g.n, g.ci, g.cj, g.J, None, cl)
+    seed = int(f["seed"])
+    for r, beta in enumerate(f["betas"]):
+        s = unpack(f["init"][r], g.n).copy()
+        st = O.derive(seed, [0x22, 0, r])
+        st2, dE = T.gibbs_sweep(m, s, float(beta), st, int(f["n_sweeps"]))
+        assert np.array_equal(dE, f["dE"][r])
+        assert np.array_equal(s, unpack(f["final"][r], g.n))
+        assert st2 == (st + int(f["n_sweeps"]) * len(g.free) * O.PHI) % 2**64
+
+
+def _random_circuit(seed, n=60):
+    rs = np.random.default_rng(seed)
+    m = 4 * n
+    ci, cj = rs.integers(0, n, m), rs.integers(0, n, m)
+    keep = ci != cj
+    J = rs.choice([-2, -1, 1, 2], m).astype(float)
+    h = rs.integers(-3, 4, n).astype(float)
+    cl = np.where(rs.random(n) < 0.1, rs.choice([-1, 1], n), 0).astype(np.int8)
+    return O.Graph.from_couplings(n, ci[keep], cj[keep], J[keep], h, cl)
+
+
+def test_k2_colour_order_circuit_like_graph():
+    g = _random_circuit(11)
+    m = T.Model.graph(g.n, g.ci, g.cj, g.J, g.h, g.clamp)
+    colours, _ = m.schedule()
+    assert np.array_equal(colours, O.greedy_colours(g))
+    betas = H.geometric(0.1, 5.0, 32)
+    e = T.Ensemble(m, betas, n_instances=3, seed=5)
+    e.init_random()
+    e.run(150, swap_every=1)
+    pts = H.run_oracle([g] * 3, betas, 5, 0, H.colour_order_for(colours), 150)
+    compare(e, pts)
+
+
+def test_k2_reference_order_with_clamps_and_fields():
+    g = _random_circuit(12, n=45)
+    m = T.Model.graph(g.n, g.ci, g.cj, g.J, g.h, g.clamp)
+    betas = H.linear(0.2, 2.0, 40)  # two groups -> cluster of 2
+    e = T.Ensemble(m, betas, n_instances=2, seed=6, order="reference")
+    e.init_random()
+    e.run(80, swap_every=2)
+    pts = H.run_oracle([g] * 2, betas, 6, 0, H.index_order, 80, swap_every=2)
+    compare(e, pts)
+
+
+def test_k1_and_k2_give_the_same_chain_on_a_lattice():
+    betas = H.geometric(0.2, 1.0, 32)
+    a = T.Ensemble(T.Model.lattice((16, 16)), betas, seed=4)
+    g = O.lattice_graph((16, 16))
+    b = T.Ensemble(T.Model.graph(g.n, g.ci, g.cj, g.J), betas, seed=4)
+    assert a.kernel == "lattice" and b.kernel == "csr"
+    for e in (a, b):
+        e.init_random()
+        e.run(50, swap_every=1)
+    assert np.array_equal(a.spins(), b.spins())
+    assert np.array_equal(a.energies(), b.energies())
+
+
+# ------------------------------------------------------------ proposals -----
+
+def test_synthetic_tapt_rounds_match_oracle_k1():
+    """Config 2 style: biased i.i.d. proposals + 5 refinement sweeps + Eq. 2, every 20 sweeps."""
+    R = 16
+    betas = H.geometric(0.3, 0.6, R)
+    mb = np.array([O.yang_m(b) for b in betas])
+    targets = np.arange(12)
+    m = T.Model.lattice((16, 16))
+    e = T.Ensemble(m, betas, n_instances=2, seed=77, instance_offset=5)
+    e.init_random()
+    for _ in range(6):
+        e.run(20, swap_every=1)
+        e.generate_proposals(targets, mb[:12], refine=5)
+    pts = H.run_oracle([O.lattice_graph((16, 16))] * 2, betas, 77, 5, H.checkerboard_order((16, 16)), 120,
+                       props=dict(every=20, targets=12, m_bias=mb, refine=5))
+    compare(e, pts)
+    assert e.acceptance()[3].sum() > 0
+
+
+def test_synthetic_tapt_reference_order_matches_reference_golden():
+    f = np.load(os.path.join(GOLD, "pt_tapt2d16.npz"))
+    I, R, n = (int(x) for x in f["shape"])
+    m = T.Model.lattice((16, 16))
+    e = T.Ensemble(m, f["betas"], n_instances=I, seed=int(f["seed"]), instance_offset=int(f["gid0"]),
+                   order="reference")
+    e.init_random()
+    every, nt = int(f["prop_every"]), int(f["n_targets"])
+    for _ in range(int(f["n_sweeps"]) // every):
+        e.run(every, swap_every=1)
+        e.generate_proposals(np.arange(nt), f["m_bias"][:nt], refine=int(f["refine"]))
+    spins = unpack(f["spins"], I * R * n).reshape(I, R, n)
+    assert np.array_equal(e.spins(), spins)
+    assert np.array_equal(e.energies().astype(np.float64), f["E"])
+    assert np.array_equal(e.acceptance()[3], f["prop_acc"])
+
+
+def test_ea_fair_proposals_match_reference_golden():
+    f = np.load(os.path.join(GOLD, "pt_ea3d6_tapt.npz"))
+    I, R, n = (int(x) for x in f["shape"])
+    graphs = [O.ea_graph((6,), 3, k) for k in range(I)]
+    # per-instance couplings through bond signs on a lattice model (L=6: K2 path)
+    m = T.Model.lattice((6,))
+    e = T.Ensemble(m, f["betas"], n_instances=I, seed=int(f["seed"]), order="reference")
+    e.generate_ea_disorder(3)
+    e.init_random()
+    every, nt = int(f["prop_every"]), int(f["n_targets"])
+    for _ in range(int(f["n_sweeps"]) // every):
+        e.run(every, swap_every=1)
+        e.generate_proposals(np.arange(nt), None, refine=int(f["refine"]))
+    spins = unpack(f["spins"], I * R * n).reshape(I, R, n)
+    assert np.array_equal(e.spins(), spins)
+    assert np.array_equal(e.energies().astype(np.float64), f["E"])
+    del graphs
+
+
+def test_inject_host_proposals_int8_and_packed():
+    R = 8
+    betas = H.linear(0.3, 1.5, R)
+    g = O.lattice_graph((8, 8))
+    m = T.Model.lattice((8, 8))
+    rs = np.random.default_rng(0)
+    e = T.Ensemble(m, betas, n_instances=2, seed=21)
+    e.init_random()
+    e.run(10, swap_every=1)
+    pts = H.run_oracle([g] * 2, betas, 21, 0, H.checkerboard_order((8, 8)), 10)
+    targets = np.array([0, 2, 3, 5])
+    props = rs.choice(np.array([-1, 1], np.int8), size=(2, 4, 64))
+    acc = e.inject_proposals(props, targets)
+    for k, pt in enumerate(pts):
+        full = np.zeros((R, 64), np.int8)
+        Ep = np.zeros(R, np.int64)
+        mask = np.zeros(R, np.uint8)
+        for t, r in enumerate(targets):
+            full[r] = props[k, t]
+            Ep[r] = O.lib().oc_energy(g.oc(), full[r].ctypes.data_as(O._i8p))
+            mask[r] = 1
+        dec = pt.inject(mask, full, Ep)
+        assert np.array_equal(acc[k], (dec[targets] == 1).astype(np.uint8))
+    compare(e, pts)
+    # packed path, second round
+    props2 = rs.choice(np.array([-1, 1], np.int8), size=(2, 4, 64))
+    packed = np.packbits(props2 > 0, axis=-1, bitorder="little")
+    acc2 = e.inject_proposals_packed(packed, targets)
+    for k, pt in enumerate(pts):
+        full = np.zeros((R, 64), np.int8)
+        Ep = np.zeros(R, np.int64)
+        mask = np.zeros(R, np.uint8)
+        for t, r in enumerate(targets):
+            full[r] = props2[k, t]
+            Ep[r] = O.lib().oc_energy(g.oc(), full[r].ctypes.data_as(O._i8p))
+            mask[r] = 1
+        dec = pt.inject(mask, full, Ep)
+        assert np.array_equal(acc2[k], (dec[targets] == 1).astype(np.uint8))
+    compare(e, pts)
+
+
+def test_inject_mh_corrected():
+    R = 6
+    betas = H.linear(0.5, 2.0, R)
+    g = O.lattice_graph((8, 8))
+    m = T.Model.lattice((8, 8))
+    rs = np.random.default_rng(1)
+    e = T.Ensemble(m, betas, n_instances=1, seed=3)
+    e.init_random()
+    pts = H.run_oracle([g], betas, 3, 0, H.checkerboard_order((8, 8)), 0)
+    for _ in range(5):
+        targets = np.array([0, 1, 4])
+        props = rs.choice(np.array([-1, 1], np.int8), size=(1, 3, 64))
+        lqc, lqp = rs.normal(size=(1, 3)) * 3, rs.normal(size=(1, 3)) * 3
+        acc = e.inject_proposals(props, targets, lqc, lqp)
+        full = np.zeros((R, 64), np.int8)
+        Ep = np.zeros(R, np.int64)
+        mask = np.zeros(R, np.uint8)
+        a = np.zeros(R)
+        b = np.zeros(R)
+        for t, r in enumerate(targets):
+            full[r] = props[0, t]
+            Ep[r] = O.lib().oc_energy(g.oc(), full[r].ctypes.data_as(O._i8p))
+            mask[r] = 1
+            a[r], b[r] = lqc[0, t], lqp[0, t]
+        dec = pts[0].inject(mask, full, Ep, a, b)
+        assert np.array_equal(acc[0], (dec[targets] == 1).astype(np.uint8))
+    compare(e, pts)
+
+
+# ------------------------------------------------------- full-size properties --
+
+def test_cfg5_full_size_energy_consistency_and_determinism():
+    """Config 5 geometry (3D L=32, 64 slots, cluster of 2) on a slice of instances:
+    device energies == exact recomputation, permutation valid, run is deterministic and
+    chunking-invariant (size-independent properties)."""
+    L, R, I = 32, 64, 4
+    betas = H.linear(0.2, 3.0, R)
+    m = T.Model.lattice((L,))
+    a = T.Ensemble(m, betas, n_instances=I, seed=99, instance_offset=1000)
+    b = T.Ensemble(m, betas, n_instances=I, seed=99, instance_offset=1000)
+    for e in (a, b):
+        e.generate_ea_disorder(42)
+        e.init_random()
+    a.run(40, swap_every=1)
+    b.run(15, swap_every=1)
+    b.run(25, swap_every=1)
+    S, E = a.spins(), a.energies()
+    assert np.array_equal(S, b.spins()) and np.array_equal(E, b.energies())
+    n, ci, cj, _ = O.lattice_couplings((L,), 1.0, True)
+    signs = a.bond_signs(len(ci)).astype(np.int64)
+    for k in range(I):
+        s = S[k].astype(np.int64)
+        Ek = -(signs[k][None, :] * s[:, ci] * s[:, cj]).sum(axis=1)
+        assert np.array_equal(Ek, E[k])
+        perm = a.permutation()[k]
+        assert sorted(perm.tolist()) == list(range(R))
+    # instance sharding: the last two instances computed alone give the same result
+    c = T.Ensemble(m, betas, n_instances=2, seed=99, instance_offset=1002)
+    c.generate_ea_disorder(42)
+    c.init_random()
+    c.run(40, swap_every=1)
+    assert np.array_equal(c.spins(), S[2:])
