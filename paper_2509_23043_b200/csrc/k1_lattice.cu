@@ -125,6 +125,9 @@ struct K1Smem {
     uint64_t T64[kW][8];   // per own buffer: exact thresholds (tie path)
 };
 
+// The spin words follow the control block, 128-byte aligned (vector loads/stores).
+__host__ __device__ constexpr size_t k1_words_offset() { return (sizeof(K1Smem) + 127) & ~size_t(127); }
+
 // Heat-bath decisions for one site word over the W replicas of this CTA.
 __device__ __forceinline__ uint32_t k1_decide_exact(const K1Smem& sm, int W, uint64_t phi_i, const uint32_t (&N)[4]) {
     uint32_t nw = 0;
@@ -140,11 +143,11 @@ template <int DIM, bool DIS, bool CLU>
 __global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDims d) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
-    uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K1Smem));
+    uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw + k1_words_offset());
     uint8_t* bonds = reinterpret_cast<uint8_t*>(words + a.n);
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     const int inst = blockIdx.x / a.G, grp = blockIdx.x % a.G;
-    const int n = a.n, W = a.W;
+    const int n = a.n, W = a.W, nv = own_count(a, grp);
     const int half = n >> 1, nsub = half >> 1;
 
     // ---- load this CTA's spins (and the instance's bond signs) into shared memory
@@ -168,7 +171,7 @@ __global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDi
         const uint64_t t = a.t0 + (uint64_t)s;
         par = (int)(t & 1);
         // per-buffer tables and stream bases for the slots the buffers occupy now
-        for (int e = tid; e < W * 8; e += nt) {
+        for (int e = tid; e < nv * 8; e += nt) {
             const int b = e >> 3, k = e & 7;
             const int slot = sm.S.slot_of[grp * W + b];
             const uint64_t T = k < a.nidx ? a.thr[(size_t)slot * a.nidx + k] : 0ull;
@@ -204,7 +207,7 @@ __global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDi
                     bool tie = false;
 #pragma unroll
                     for (int b = 0; b < kW; ++b) {
-                        if (b < W) {
+                        if (b < nv) {
                             const uint64_t base = sm.S.sb[b];
                             const int m = b & 3, sh = 4 * (b >> 2);
                             const uint32_t i0 = (N[0][m] >> sh) & 7u;
@@ -219,8 +222,8 @@ __global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDi
                         }
                     }
                     if (tie) {  // probability ~ 2^-32 per decision: redo both words exactly
-                        w0 = k1_decide_exact(sm, W, ph0, N[0]);
-                        w1 = k1_decide_exact(sm, W, ph1, N[1]);
+                        w0 = k1_decide_exact(sm, nv, ph0, N[0]);
+                        w1 = k1_decide_exact(sm, nv, ph1, N[1]);
                     }
                     nw[0] = w0;
                     nw[1] = w1;
@@ -241,9 +244,9 @@ __global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDi
         // exact energies: E = J0 * (2*U - n*dim)
         {
             const uint32_t tot = warp_sliced_total<kCnt>(C);
-            if (lane < W) atomicAdd(&sm.S.Ucnt[lane], tot);
+            if (lane < nv) atomicAdd(&sm.S.Ucnt[lane], tot);
             __syncthreads();
-            if (tid < W) {
+            if (tid < nv) {
                 sm.S.Eown[par][tid] = d.J0 * (2 * (int)sm.S.Ucnt[tid] - n * DIM);
                 sm.S.Ucnt[tid] = 0;
             }
@@ -253,7 +256,7 @@ __global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDi
     }
     if (a.energy_only) {
         __syncthreads();
-        for (int b = tid; b < W; b += nt) a.E[(size_t)inst * a.B + grp * W + b] = sm.S.Eown[par][b];
+        for (int b = tid; b < nv; b += nt) a.E[(size_t)inst * a.B + grp * W + b] = sm.S.Eown[par][b];
         return;
     }
     // ---- write back
@@ -266,7 +269,7 @@ __global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDi
 }
 
 size_t k1_smem_bytes(int n, bool dis) {
-    return sizeof(K1Smem) + (size_t)n * 4 + (dis ? (size_t)n : 0);
+    return k1_words_offset() + (size_t)n * 4 + (dis ? (size_t)n : 0);
 }
 
 template <int DIM, bool DIS, bool CLU>

@@ -27,17 +27,17 @@ template <bool CLU>
 __global__ void __launch_bounds__(256) k2_csr_pt(const PTArgs a, const CsrArgs g) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     K2Smem& sm = *reinterpret_cast<K2Smem*>(smem_raw);
-    uint32_t* Uhi = reinterpret_cast<uint32_t*>(smem_raw + sizeof(K2Smem));  // [R][nidx]
+    uint32_t* Uhi = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(K2Smem) + 127) & ~size_t(127)));  // [R][nidx]
     uint32_t* words = Uhi + (size_t)a.R * a.nidx;                              // [n]
     const int tid = threadIdx.x, nt = blockDim.x;
     const int inst = blockIdx.x / a.G, grp = blockIdx.x % a.G;
-    const int n = a.n, W = a.W;
+    const int n = a.n, W = a.W, nv = own_count(a, grp);
     const int8_t* Jrow = g.J + (size_t)(g.nJ > 1 ? inst : 0) * g.nnz;
 
     for (int k = tid; k < n; k += nt) words[k] = a.words[((size_t)inst * a.G + grp) * n + k];
     for (int k = tid; k < a.R * a.nidx; k += nt) Uhi[k] = thr_hi(a.thr[k]);
     pt_load_perm(a, sm.S, inst);
-    for (int b = tid; b < W; b += nt) sm.S.Eown[(a.t0 + 1) & 1][b] = a.E[(size_t)inst * a.B + grp * W + b];
+    for (int b = tid; b < nv; b += nt) sm.S.Eown[(a.t0 + 1) & 1][b] = a.E[(size_t)inst * a.B + grp * W + b];
     __syncthreads();
 
     uint64_t pass = a.p0;
@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(256) k2_csr_pt(const PTArgs a, const CsrArgs g
                 uint32_t nw = 0;
 #pragma unroll
                 for (int b = 0; b < kW; ++b) {
-                    if (b < W) {
+                    if (b < nv) {
                         const int acc = (int)((A[b & 7] >> (8 * (b >> 3))) & 0xFFu);
                         const int l = l0 + 2 * acc;
                         const int slot = sm.S.slot_of[grp * W + b];
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(256) k2_csr_pt(const PTArgs a, const CsrArgs g
                         if (up != was) dE[b] += was ? 2 * l : -2 * l;
                     }
                 }
-                words[i] = nw | (old & ~((W >= 32) ? 0xFFFFFFFFu : ((1u << W) - 1u)));
+                words[i] = nw | (old & ~((nv >= 32) ? 0xFFFFFFFFu : ((1u << nv) - 1u)));
             }
             __syncthreads();
         }
@@ -100,9 +100,9 @@ __global__ void __launch_bounds__(256) k2_csr_pt(const PTArgs a, const CsrArgs g
         {
             const int32_t tot = warp_reduce_scatter32(dE);
             const int lane = tid & 31;
-            if (lane < W) atomicAdd(&sm.S.Ucnt[lane], (uint32_t)tot);
+            if (lane < nv) atomicAdd(&sm.S.Ucnt[lane], (uint32_t)tot);
             __syncthreads();
-            if (tid < W) {
+            if (tid < nv) {
                 sm.S.Eown[par][tid] = sm.S.Eown[prev][tid] + (int32_t)sm.S.Ucnt[tid];
                 sm.S.Ucnt[tid] = 0;
             }
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(256) k2_csr_pt(const PTArgs a, const CsrArgs g
 }
 
 size_t k2_smem_bytes(int n, int R, int nidx) {
-    return sizeof(K2Smem) + (size_t)R * nidx * 4 + (size_t)n * 4;
+    return ((sizeof(K2Smem) + 127) & ~size_t(127)) + (size_t)R * nidx * 4 + (size_t)n * 4;
 }
 
 template <bool CLU>

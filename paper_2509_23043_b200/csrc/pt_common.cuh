@@ -23,6 +23,9 @@ struct PTShared {
     int tie;
 };
 
+// Number of valid buffers owned by group `grp` (the last group of an instance may be partial).
+__device__ __forceinline__ int own_count(const PTArgs& a, int grp) { return min(a.W, a.B - grp * a.W); }
+
 // Load the permutation of instance `inst` into shared memory.
 __device__ __forceinline__ void pt_load_perm(const PTArgs& a, PTShared& S, int inst) {
     for (int k = threadIdx.x; k < a.B; k += blockDim.x) S.slot_of[k] = a.slot_of[(size_t)inst * a.B + k];
@@ -40,7 +43,8 @@ __device__ __forceinline__ void pt_load_perm(const PTArgs& a, PTShared& S, int i
 
 // Per-buffer stream base for sweep t: S_slot + (draw_base + t*n_free + 1)*phi.
 __device__ __forceinline__ void pt_stream_bases(const PTArgs& a, PTShared& S, int inst, int grp, uint64_t t) {
-    for (int b = threadIdx.x; b < a.W; b += blockDim.x) {
+    const int nv = own_count(a, grp);
+    for (int b = threadIdx.x; b < nv; b += blockDim.x) {
         const int slot = S.slot_of[grp * a.W + b];
         const uint64_t k0 = a.draw_base + t * (uint64_t)a.n_free + 1ull;
         S.sb[b] = a.streams[(size_t)inst * a.R + slot] + k0 * kPhi;
@@ -66,7 +70,7 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
         // Without a cluster only this CTA's buffers are visible; the host never asks
         // for swaps or best-energy tracking when an instance spans several CTAs here.
         __syncthreads();
-        for (int b = tid; b < a.W; b += nt) S.Eall[grp * a.W + b] = S.Eown[par][b];
+        for (int b = tid; b < own_count(a, grp); b += nt) S.Eall[grp * a.W + b] = S.Eown[par][b];
     }
     __syncthreads();
     const uint64_t T = t + 1;
@@ -104,9 +108,9 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
         for (int k = 0; k < kCnt; ++k) C[k] = 0;
         for (int i = tid; i < a.n; i += nt) sliced_add1<kCnt>(C, words[i]);
         const uint32_t tot = warp_sliced_total<kCnt>(C);
-        if (lane < a.W) atomicAdd(&S.Mcnt[lane], tot);
+        if (lane < own_count(a, grp)) atomicAdd(&S.Mcnt[lane], tot);
         __syncthreads();
-        if (tid < a.W) {
+        if (tid < own_count(a, grp)) {
             const int gb = grp * a.W + tid;
             const int slot = S.slot_of[gb];
             const long long e = S.Eall[gb];
@@ -134,7 +138,8 @@ __device__ void pt_finish(const PTArgs& a, PTShared& S, int inst, int grp, int l
     const int tid = threadIdx.x;
     __syncthreads();
     if (a.E)
-        for (int b = tid; b < a.W; b += blockDim.x) a.E[(size_t)inst * a.B + grp * a.W + b] = S.Eown[last_par][b];
+        for (int b = tid; b < own_count(a, grp); b += blockDim.x)
+            a.E[(size_t)inst * a.B + grp * a.W + b] = S.Eown[last_par][b];
     if (grp == 0) {
         for (int k = tid; k < a.B; k += blockDim.x) a.slot_of[(size_t)inst * a.B + k] = S.slot_of[k];
         if (a.buf_of)
