@@ -35,6 +35,7 @@ N_SPINS = L ** 3
 BETA_MIN, BETA_MAX = 0.2, 3.0
 N_TARGETS, REFINE = 56, 5
 SEED, DISORDER_SEED = 20250923, 43
+I_U = 42  # algorithmic integer instructions per update for cfg3/cfg5
 METRIC = "spin updates/sec for PT+TAPT sweeps at 1/2/4/8 B200; % of HBM/ALU roofline"
 UNIT = "spin updates/s"
 
@@ -101,7 +102,7 @@ class ClockSampler:
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[k] for r in self.rows for k in range(4) if "Active" in r[3 + k]})
+        reasons = sorted({names[k] for r in self.rows for k in range(4) if r[3 + k].strip() == "Active"})
         pw = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "power_w_max": max(pw) if pw else None, "samples": len(self.rows)}
@@ -285,15 +286,22 @@ def main():
     k_ms = float(np.mean([a.elapsed_time(b) for a, b in k_ev]))
     k_upd = I * R * N_SPINS * S
     achieved = k_upd / (k_ms * 1e-3)
-    peak, _ = T.probe_decision_rate(1, 512, 20000)
+    probe, _ = T.probe_decision_rate(1, 512, 20000)
+    clocks = clk.summary()
+    f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
+    peak = n_sm * 128 * f_sm / I_U
     g_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs") if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     hbm_bytes = I * (2 * 4 * N_SPINS * 2 + N_SPINS)  # spins in+out (2 groups) + bond bytes, per launch
     roofline = {
         "bound": "alu", "unit": "Gupdates/s", "achieved": achieved / 1e9, "peak": peak / 1e9,
         "frac": achieved / peak, "traffic": None,
-        "peak_source": "measured on this GPU: k_decision_probe (one splitmix64 draw + threshold lookup + compare "
-                       "+ bit insert per update, no stencil, no memory traffic); BASELINE.md 4 binds the ALU roofline",
+        "peak_source": f"BASELINE.md section 4 ALU/issue bound n_SM*128*f_SM/I_u with n_SM={n_sm}, f_SM = median "
+                       f"SM clock sampled during the timed region ({f_sm / 1e6:.0f} MHz), I_u={I_U} (cfg5)",
+        "probe_ceiling": {"value": probe / 1e9, "frac": achieved / probe,
+                          "what": "k_decision_probe: the bare per-update work (splitmix64 high word + threshold "
+                                  "lookup + compare + bit insert), no stencil or memory traffic, same unroll"},
         "kernel": "k1_lattice_pt<3,true,true>", "kernel_ms_per_launch": k_ms, "updates_per_launch": k_upd,
         "hbm": {"achieved_gbs": hbm_bytes / (k_ms * 1e-3) / 1e9, "peak_gbs": g_hbm,
                 "frac": hbm_bytes / (k_ms * 1e-3) / 1e9 / g_hbm,
@@ -313,7 +321,7 @@ def main():
     }
     if not args.no_e2e:
         out["e2e"] = e2e_leg(args, T, torch, ens, stream, I, S, world)
-    out["clocks"] = clk.summary()
+    out["clocks"] = clocks
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         n_inst = max(args.cpu_sample_instances, threads)

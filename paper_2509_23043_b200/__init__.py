@@ -16,7 +16,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libtapt_b200.so")
+LIB_PATH = os.environ.get("TAPT_LIB_PATH") or os.path.join(_HERE, "lib", "libtapt_b200.so")
 
 ORDER_COLOUR, ORDER_REFERENCE = 0, 1
 BOUNDARY_OPEN, BOUNDARY_PERIODIC = 0, 1

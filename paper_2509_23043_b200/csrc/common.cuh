@@ -40,6 +40,55 @@ __host__ __device__ __forceinline__ uint32_t thr_hi(uint64_t T) {
     return T == 0 ? 0u : static_cast<uint32_t>(((T << 11) - 1ull) >> 32);
 }
 
+// Runtime copies of 4 and 32: multiplying by an opaque register keeps a right shift of the
+// high word on the FMA pipe (IMAD.HI) instead of the ALU pipe (SHF).
+struct MixConsts {
+    uint32_t k4, k32;
+};
+
+// High word of (z ^ z>>30) * M1 ^ ... * M2, i.e. mix_final(z) BEFORE its last xor-shift.
+// Variant bits (instruction-mix choices, identical results):
+//   V & 1: high-word right shifts as IMAD.HI by 4 / 32 (FMA pipe) instead of SHF (ALU pipe)
+//   V & 2: first 64-bit multiply as an explicit IMAD.WIDE + IMAD + IMAD chain (PTX)
+// The last multiply only needs its high word: IMAD.HI + IMAD + IMAD.
+template <int V>
+__device__ __forceinline__ uint32_t mix_pre_hi(uint32_t zl, uint32_t zh, const MixConsts& c) {
+    constexpr uint32_t A_LO = (uint32_t)kM1, A_HI = (uint32_t)(kM1 >> 32);
+    constexpr uint32_t B_LO = (uint32_t)kM2, B_HI = (uint32_t)(kM2 >> 32);
+    uint32_t t;
+    asm("shf.r.clamp.b32 %0, %1, %2, 30;" : "=r"(t) : "r"(zl), "r"(zh));
+    zl ^= t;
+    zh ^= (V & 1) ? __umulhi(zh, c.k4) : (zh >> 30);
+    if constexpr ((V & 2) != 0) {
+        asm("{\n\t.reg .u64 w;\n\t"
+            "mul.wide.u32 w, %2, %4;\n\t"
+            "mov.b64 {%0, %1}, w;\n\t"
+            "mad.lo.u32 %1, %2, %5, %1;\n\t"
+            "mad.lo.u32 %1, %3, %4, %1;\n\t}"
+            : "=r"(t), "=r"(zh)
+            : "r"(zl), "r"(zh), "n"(A_LO), "n"(A_HI));
+        zl = t;
+    } else {
+        const uint64_t w = (uint64_t)zl * A_LO;
+        zh = zh * A_LO + zl * A_HI + (uint32_t)(w >> 32);
+        zl = (uint32_t)w;
+    }
+    asm("shf.r.clamp.b32 %0, %1, %2, 27;" : "=r"(t) : "r"(zl), "r"(zh));
+    zl ^= t;
+    zh ^= (V & 1) ? __umulhi(zh, c.k32) : (zh >> 27);
+    return __umulhi(zl, B_LO) + zh * B_LO + zl * B_HI;
+}
+
+// Heat-bath decision on h = mix_pre_hi(z) against U = thr_hi(T):  the final xor-shift
+// of mix_final only flips bit 0 of the high word, so whenever |h - U| >= 2 the decision
+// equals (h < U).  Shifts NOT(up) into w (w = 2w + [h >= U]) via the carry of h - U and
+// returns h - U, whose value in {-1, 0, 1} flags the rare case that needs the exact test.
+__device__ __forceinline__ uint32_t decide_acc(uint32_t h, uint32_t U, uint32_t& w) {
+    uint32_t d;
+    asm("sub.cc.u32 %0, %2, %3;\n\taddc.u32 %1, %1, %1;" : "=r"(d), "+r"(w) : "r"(h), "r"(U));
+    return d;
+}
+
 // Exact decision on a full draw.
 __host__ __device__ __forceinline__ bool below(uint64_t x, uint64_t T) { return (x >> 11) < T; }
 

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -20,6 +21,10 @@
 #include <vector>
 
 #include "kernels.h"
+
+#ifndef TAPT_K1_DEFAULT_THREADS
+#define TAPT_K1_DEFAULT_THREADS 512
+#endif
 #include "tapt/errors.hpp"
 #include "tapt/rng.hpp"
 #include "tapt_gpu.h"
@@ -29,7 +34,8 @@ cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool clust
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st);
 size_t k1_smem_bytes(int n, bool dis);
 size_t k2_smem_bytes(int n, int R, int nidx);
-cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st);
+cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st,
+                                  int variant);
 __global__ void k_init_random(uint32_t*, int, int, int, int, const uint64_t*, const int8_t*, int);
 __global__ void k_energy_csr(const uint32_t*, int, int, int, int, const uint32_t*, const uint32_t*, const int8_t*, int,
                              int, const int32_t*, int32_t*);
@@ -492,6 +498,7 @@ struct tapt_ensemble_s {
         a.width = width;
         a.nbins = nbins;
         a.best = best.p;
+        a.mc = MixConsts{4u, 32u};
         return a;
     }
 
@@ -647,10 +654,12 @@ tapt_status tapt_probe_decision_rate(int blocks_per_sm, int threads, uint32_t it
         CUDA_OK(cudaEventCreate(&a));
         CUDA_OK(cudaEventCreate(&b));
         ++g_launches;
-        CUDA_OK(launch_decision_probe(blocks, threads, iters, sink.p, st));  // warm-up
+        const char* ve = std::getenv("TAPT_PROBE_VARIANT");
+        const int variant = ve ? std::atoi(ve) : -1;
+        CUDA_OK(launch_decision_probe(blocks, threads, iters, sink.p, st, variant));  // warm-up
         CUDA_OK(cudaEventRecord(a, st));
         ++g_launches;
-        CUDA_OK(launch_decision_probe(blocks, threads, iters, sink.p, st));
+        CUDA_OK(launch_decision_probe(blocks, threads, iters, sink.p, st, variant));
         CUDA_OK(cudaEventRecord(b, st));
         CUDA_OK(cudaEventSynchronize(b));
         float ms = 0;
@@ -812,7 +821,8 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
         e->use_k1 = m->k1 && d->order == TAPT_ORDER_COLOUR && !e->has_clamps();
         if (e->use_k1) {
             e->nidx = 2 * m->dim + 1;
-            int nt = std::max(32, std::min(512, n / 4));
+            int nt = std::max(32, std::min(TAPT_K1_DEFAULT_THREADS, n / 4));
+            if (const char* env = std::getenv("TAPT_K1_THREADS")) nt = std::max(32, std::min(1024, std::atoi(env)));
             nt = (nt / 32) * 32;
             e->k1_threads = nt;
             if (k1_smem_bytes(n, true) > 227 * 1024) throw tapt::SizeError("lattice too large for shared memory");

@@ -125,8 +125,8 @@ struct K1Smem {
     uint64_t T64[kW][8];   // per own buffer: exact thresholds (tie path)
 };
 
-// The spin words follow the control block, 128-byte aligned (vector loads/stores).
-__host__ __device__ constexpr size_t k1_words_offset() { return (sizeof(K1Smem) + 127) & ~size_t(127); }
+// Dynamic shared memory holds the spin words (and bond bytes); the control block is static.
+__host__ __device__ constexpr size_t k1_words_offset() { return 0; }
 
 // Heat-bath decisions for one site word over the W replicas of this CTA.
 __device__ __forceinline__ uint32_t k1_decide_exact(const K1Smem& sm, int W, uint64_t phi_i, const uint32_t (&N)[4]) {
@@ -139,16 +139,65 @@ __device__ __forceinline__ uint32_t k1_decide_exact(const K1Smem& sm, int W, uin
     return nw;
 }
 
-template <int DIM, bool DIS, bool CLU>
-__global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDims d) {
+// Fast-path decisions for SP site words (independent chains interleaved): replica b of
+// site u draws mix(sb[b] + i_u*phi) and compares with the threshold of its own q.  The
+// loop runs b descending so the carry chain leaves NOT(up_b) at bit b.  NV = 32: full
+// group, fully unrolled; NV = 0: partial group (runtime count nv), rolled loop.
+// V & 4: track the tie band as a running min of (h - U + 1) instead of OR-ing compares.
+template <int NV, int V, int SP>
+__device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64_t (&ph)[SP],
+                                          const uint32_t (&N)[SP][4], const MixConsts& mc, uint32_t (&w)[SP],
+                                          bool& tie) {
+    constexpr int U = NV ? NV : 1;
+    const int cnt = NV ? NV : nv;
+    uint32_t tmin = 0xFFFFFFFFu;
+#pragma unroll U
+    for (int b = cnt - 1; b >= 0; --b) {
+        const uint64_t base = sm.S.sb[b];
+        const int m = b & 3, sh = 4 * (b >> 2);
+#pragma unroll
+        for (int u = 0; u < SP; ++u) {
+            const uint32_t thr = sm.Uhi[b][(N[u][m] >> sh) & 7u];
+            const uint64_t z = base + ph[u];
+            const uint32_t h = mix_pre_hi<V>((uint32_t)z, (uint32_t)(z >> 32), mc);
+            const uint32_t dd = decide_acc(h, thr, w[u]);
+            if constexpr ((V & 4) != 0)
+                tmin = min(tmin, dd + 1u);
+            else
+                tie |= (dd + 1u <= 2u);
+        }
+    }
+    if constexpr ((V & 4) != 0) tie |= tmin <= 2u;
+}
+
+// Kept for the decision-rate probe (two interleaved site words).
+template <int NV, int V>
+__device__ __forceinline__ void k1_decide2(const K1Smem& sm, int nv, uint64_t ph0, uint64_t ph1,
+                                           const uint32_t (&N0)[4], const uint32_t (&N1)[4], const MixConsts& mc,
+                                           uint32_t& w0, uint32_t& w1, bool& tie) {
+    const uint64_t ph[2] = {ph0, ph1};
+    uint32_t N[2][4];
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        N[0][m] = N0[m];
+        N[1][m] = N1[m];
+    }
+    uint32_t w[2] = {w0, w1};
+    k1_decide<NV, V, 2>(sm, nv, ph, N, mc, w, tie);
+    w0 = w[0];
+    w1 = w[1];
+}
+
+template <int DIM, bool DIS, bool CLU, int SP>
+__global__ void __launch_bounds__(SP == 1 ? 1024 : 512, 1) k1_lattice_pt(const PTArgs a, const LatDims d) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    K1Smem& sm = *reinterpret_cast<K1Smem*>(smem_raw);
-    uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw + k1_words_offset());
+    __shared__ K1Smem sm;  // static: table addresses fold into LDS immediates
+    uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw);
     uint8_t* bonds = reinterpret_cast<uint8_t*>(words + a.n);
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     const int inst = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
-    const int half = n >> 1, nsub = half >> 1;
+    const int half = n >> 1, nsub = half / SP;
 
     // ---- load this CTA's spins (and the instance's bond signs) into shared memory
     {
@@ -187,52 +236,46 @@ __global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDi
 
         for (int c = (a.energy_only ? 1 : 0); c < 2; ++c) {
             for (int j = tid; j < nsub; j += nt) {
-                int xs[2], ys[2], zs[2], is[2];
-                is[0] = colour_site<DIM>(j, c, d, xs[0], ys[0], zs[0]);
-                is[1] = colour_site<DIM>(j + nsub, c, d, xs[1], ys[1], zs[1]);
-                uint32_t q[2][3], N[2][4];
+                // site u of this iteration: colour index j + u*nsub (a warp's lanes cover
+                // consecutive colour indices, so each shared load stays conflict-free)
+                int is[SP];
+                uint32_t q[SP][3], N[SP][4];
 #pragma unroll
-                for (int u = 0; u < 2; ++u) {
-                    k1_stencil<DIM, DIS>(words, bonds, is[u], xs[u], ys[u], zs[u], d, q[u][0], q[u][1], q[u][2]);
+                for (int u = 0; u < SP; ++u) {
+                    int x, y, z;
+                    is[u] = colour_site<DIM>(j + u * nsub, c, d, x, y, z);
+                    k1_stencil<DIM, DIS>(words, bonds, is[u], x, y, z, d, q[u][0], q[u][1], q[u][2]);
                     nibbles(q[u][0], q[u][1], q[u][2], N[u]);
                 }
-                uint32_t nw[2];
+                uint32_t nw[SP];
                 if (a.energy_only) {
-                    nw[0] = words[is[0]];
-                    nw[1] = words[is[1]];
-                } else {
-                    const uint64_t ph0 = (uint64_t)(uint32_t)is[0] * kPhi;
-                    const uint64_t ph1 = (uint64_t)(uint32_t)is[1] * kPhi;
-                    uint32_t w0 = 0, w1 = 0;
-                    bool tie = false;
 #pragma unroll
-                    for (int b = 0; b < kW; ++b) {
-                        if (b < nv) {
-                            const uint64_t base = sm.S.sb[b];
-                            const int m = b & 3, sh = 4 * (b >> 2);
-                            const uint32_t i0 = (N[0][m] >> sh) & 7u;
-                            const uint32_t i1 = (N[1][m] >> sh) & 7u;
-                            const uint32_t u0 = sm.Uhi[b][i0];
-                            const uint32_t u1 = sm.Uhi[b][i1];
-                            const uint32_t x0 = mix_final_hi(base + ph0);
-                            const uint32_t x1 = mix_final_hi(base + ph1);
-                            w0 |= (x0 < u0) ? (1u << b) : 0u;
-                            w1 |= (x1 < u1) ? (1u << b) : 0u;
-                            tie |= (x0 == u0) | (x1 == u1);
-                        }
+                    for (int u = 0; u < SP; ++u) nw[u] = words[is[u]];
+                } else {
+                    uint64_t ph[SP];
+#pragma unroll
+                    for (int u = 0; u < SP; ++u) {
+                        ph[u] = (uint64_t)(uint32_t)is[u] * kPhi;
+                        nw[u] = 0;  // NOT(up) bits, replica b at bit b
                     }
-                    if (tie) {  // probability ~ 2^-32 per decision: redo both words exactly
-                        w0 = k1_decide_exact(sm, nv, ph0, N[0]);
-                        w1 = k1_decide_exact(sm, nv, ph1, N[1]);
+                    bool tie = false;
+                    if (nv == kW)
+                        k1_decide<kW, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                    else
+                        k1_decide<0, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                    const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
+#pragma unroll
+                    for (int u = 0; u < SP; ++u) nw[u] = ~nw[u] & vmask;
+                    if (tie) {  // probability ~ 2^-31 per decision: redo the words exactly
+#pragma unroll
+                        for (int u = 0; u < SP; ++u) nw[u] = k1_decide_exact(sm, nv, ph[u], N[u]);
                     }
-                    nw[0] = w0;
-                    nw[1] = w1;
-                    words[is[0]] = w0;
-                    words[is[1]] = w1;
+#pragma unroll
+                    for (int u = 0; u < SP; ++u) words[is[u]] = nw[u];
                 }
                 if (c == 1) {
 #pragma unroll
-                    for (int u = 0; u < 2; ++u) {
+                    for (int u = 0; u < SP; ++u) {
                         uint32_t v0, v1, v2;
                         unsat_planes<DIM>(nw[u], q[u][0], q[u][1], q[u][2], v0, v1, v2);
                         sliced_add3<kCnt>(C, v0, v1, v2);
@@ -269,13 +312,15 @@ __global__ void __launch_bounds__(512) k1_lattice_pt(const PTArgs a, const LatDi
 }
 
 size_t k1_smem_bytes(int n, bool dis) {
+    // dynamic part only (the static K1Smem block is accounted by the compiler)
     return k1_words_offset() + (size_t)n * 4 + (dis ? (size_t)n : 0);
 }
 
 template <int DIM, bool DIS, bool CLU>
 static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st) {
     const size_t smem = k1_smem_bytes(a.n, DIS);
-    auto fn = k1_lattice_pt<DIM, DIS, CLU>;
+    // SP = 1 site word per thread-iteration at 1024 threads, else 2 interleaved at <= 512
+    auto fn = threads > 512 ? k1_lattice_pt<DIM, DIS, CLU, 1> : k1_lattice_pt<DIM, DIS, CLU, 2>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -315,41 +360,46 @@ cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool clust
 // denominator by bench.py.
 namespace tapt_dev {
 
-__global__ void __launch_bounds__(512) k_decision_probe(uint32_t iters, uint32_t* sink) {
-    __shared__ uint32_t Uhi[kW][8];
-    __shared__ uint64_t sb[kW];
+template <int V>
+__global__ void __launch_bounds__(512) k_decision_probe(uint32_t iters, uint32_t* sink, MixConsts mc) {
+    __shared__ K1Smem sm;
     const int tid = threadIdx.x;
-    for (int e = tid; e < kW * 8; e += blockDim.x) Uhi[e >> 3][e & 7] = 0x80000000u + (uint32_t)e * 977u;
-    for (int e = tid; e < kW; e += blockDim.x) sb[e] = 0x1234567ull * (e + 1);
+    for (int e = tid; e < kW * 8; e += blockDim.x) sm.Uhi[e >> 3][e & 7] = 0x80000000u + (uint32_t)e * 977u;
+    for (int e = tid; e < kW; e += blockDim.x) sm.S.sb[e] = 0x1234567ull * (e + 1);
     __syncthreads();
     const uint32_t gid = blockIdx.x * blockDim.x + tid;
-    uint32_t N0 = gid * 0x9E3779B9u, N1 = gid * 0x85EBCA6Bu;
+    uint32_t N0[4], N1[4];
+    for (int m = 0; m < 4; ++m) {
+        N0[m] = gid * 0x9E3779B9u + m;
+        N1[m] = gid * 0x85EBCA6Bu + m;
+    }
     uint32_t acc = 0;
     bool tie = false;
     for (uint32_t it = 0; it < iters; ++it) {
         const uint64_t ph0 = (uint64_t)(2 * gid + it * 7919u) * kPhi;
         const uint64_t ph1 = ph0 + kPhi;
         uint32_t w0 = 0, w1 = 0;
-#pragma unroll
-        for (int b = 0; b < kW; ++b) {
-            const uint64_t base = sb[b];
-            const int sh = 4 * (b >> 2);
-            const uint32_t i0 = (N0 >> sh) & 7u, i1 = (N1 >> sh) & 7u;
-            const uint32_t u0 = Uhi[b][i0], u1 = Uhi[b][i1];
-            const uint32_t x0 = mix_final_hi(base + ph0), x1 = mix_final_hi(base + ph1);
-            w0 |= (x0 < u0) ? (1u << b) : 0u;
-            w1 |= (x1 < u1) ? (1u << b) : 0u;
-            tie |= (x0 == u0) | (x1 == u1);
-        }
-        N0 = w0 ^ (N1 >> 3);
-        N1 = w1 ^ (N0 << 1);
+        k1_decide2<kW, V>(sm, kW, ph0, ph1, N0, N1, mc, w0, w1, tie);
+        N0[it & 3] ^= w0 >> 3;
+        N1[it & 3] ^= w1 << 1;
         acc += w0 ^ w1;
     }
     sink[gid] = acc + (tie ? 1u : 0u);
 }
 
-cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st) {
-    k_decision_probe<<<blocks, threads, 0, st>>>(iters, sink);
+cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st,
+                                  int variant) {
+    const MixConsts mc{4u, 32u};
+    switch (variant < 0 ? TAPT_K1_VARIANT : variant) {
+        case 0: k_decision_probe<0><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+        case 1: k_decision_probe<1><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+        case 2: k_decision_probe<2><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+        case 3: k_decision_probe<3><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+        case 4: k_decision_probe<4><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+        case 5: k_decision_probe<5><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+        case 6: k_decision_probe<6><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+        default: k_decision_probe<7><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+    }
     return cudaGetLastError();
 }
 

@@ -18,6 +18,9 @@ namespace tapt_dev {
 constexpr int kMaxR = 256;   // ladder slots per instance (uint8 permutation)
 constexpr int kW = 32;       // replicas per group (bits per word)
 constexpr int kCnt = 8;      // planes of the sliced per-thread counters
+#ifndef TAPT_K1_VARIANT
+#define TAPT_K1_VARIANT 4    // instruction-mix variant of the decision loop (common.cuh)
+#endif
 
 struct LatDims {
     int dim;              // 2 or 3
@@ -59,6 +62,7 @@ struct PTArgs {
     long long e_lo, width;
     int nbins;
     int* best;                 // [I] lowest energy seen (atomicMin)
+    MixConsts mc;              // {4, 32}, opaque to the compiler (see common.cuh)
 };
 
 // CSR graph (K2): shared structure; couplings may be per instance.

@@ -51,9 +51,13 @@ def test_cfg1_geometry_checkerboard_pt_bit_exact():
     compare(e, pts)
 
 
-def test_ea3d_cluster_pt_bit_exact():
-    """3D EA +-J, 64 slots (2-CTA cluster per instance), device-generated disorder."""
-    L, R = 8, 64
+@pytest.mark.parametrize("threads", [None, "1024", "128"])
+def test_ea3d_cluster_pt_bit_exact(threads, monkeypatch):
+    """3D EA +-J, 64 slots (2-CTA cluster per instance), device-generated disorder; also with
+    the 1-site/1024-thread and small-CTA launch shapes of K1 (results must not depend on them)."""
+    if threads:
+        monkeypatch.setenv("TAPT_K1_THREADS", threads)
+    L, R = 16 if threads == "1024" else 8, 64
     betas = H.linear(0.2, 3.0, R)
     m = T.Model.lattice((L,))
     e = T.Ensemble(m, betas, n_instances=3, seed=77, instance_offset=5)
