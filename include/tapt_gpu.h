@@ -205,6 +205,31 @@ tapt_status tapt_inject_proposals_packed(tapt_ensemble_t e, const uint8_t* propo
 tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, uint32_t n_targets,
                                     const double* m_bias, uint32_t refine, uint8_t* accepted);
 
+/* ------------------------------------------------------ problem suite -- */
+/* Instance construction for BASELINE config 4 (proj/src/problems.cpp:1 is a
+ * placeholder).  Host-only, never on the timed path.  Spin +1 = logical 1. */
+
+const char* tapt_problem_last_error(void);
+/* 3n^2 + n. */
+uint32_t tapt_multiplier_spins(uint32_t n);
+/* build_multiplier(n): AND gates + n-1 ripple rows of full adders with spin identification.
+ * Outputs the un-merged coupling list (3n^2 + 10n(n-1) entries; CouplingGraph::Builder sums
+ * shared wire pairs), fields [3n^2+n], the clamp set (product bits and carry-ins, values for
+ * C = 0) and wires (nullable): A[n], B[n], C[2n], carry-in[n]. */
+tapt_status tapt_multiplier_build(uint32_t n, uint32_t* n_couplings, uint32_t* ci, uint32_t* cj, double* J,
+                                  double* h, int8_t* clamp, uint32_t* wires);
+/* Consistent wire assignment for inputs (a, b) (forward evaluation). */
+tapt_status tapt_multiplier_forward(uint32_t n, uint64_t a, uint64_t b, int8_t* spins);
+/* clamp_product: clamp values for product C ([3n^2+n], 0 = free). */
+tapt_status tapt_multiplier_clamps(uint32_t n, uint64_t C, int8_t* clamp);
+/* decode_and_check. */
+tapt_status tapt_multiplier_decode(uint32_t n, const int8_t* spins, uint64_t C, uint64_t* a, uint64_t* b,
+                                   int* success);
+/* enumerate_semiprimes. */
+tapt_status tapt_enumerate_semiprimes(uint32_t n, uint64_t* out, uint32_t cap, uint32_t* count);
+/* p, q: first primes among 2^(bits-1) + below(2^(bits-1)) draws of derive(seed, {0x99, gid}). */
+tapt_status tapt_random_semiprime(uint64_t seed, uint64_t gid, uint32_t bits, uint64_t* p, uint64_t* q);
+
 #ifdef __cplusplus
 }
 #endif

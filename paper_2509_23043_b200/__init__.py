@@ -132,6 +132,14 @@ _SIGS = {
     "tapt_inject_proposals": (C.c_int, [_vp, _vp, C.c_int, _u32p, C.c_uint32, _f64p, _f64p, _u8p]),
     "tapt_inject_proposals_packed": (C.c_int, [_vp, _vp, C.c_int, _u32p, C.c_uint32, _u8p]),
     "tapt_generate_proposals": (C.c_int, [_vp, _u32p, C.c_uint32, _f64p, C.c_uint32, _u8p]),
+    "tapt_problem_last_error": (C.c_char_p, []),
+    "tapt_multiplier_spins": (C.c_uint32, [C.c_uint32]),
+    "tapt_multiplier_build": (C.c_int, [C.c_uint32, _u32p, _u32p, _u32p, _f64p, _f64p, _i8p, _u32p]),
+    "tapt_multiplier_forward": (C.c_int, [C.c_uint32, C.c_uint64, C.c_uint64, _i8p]),
+    "tapt_multiplier_clamps": (C.c_int, [C.c_uint32, C.c_uint64, _i8p]),
+    "tapt_multiplier_decode": (C.c_int, [C.c_uint32, _i8p, C.c_uint64, _u64p, _u64p, C.POINTER(C.c_int)]),
+    "tapt_enumerate_semiprimes": (C.c_int, [C.c_uint32, _u64p, C.c_uint32, _u32p]),
+    "tapt_random_semiprime": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, _u64p, _u64p]),
 }
 
 _lib = None
@@ -157,9 +165,10 @@ def exported_symbols():
     return list(_SIGS)
 
 
-def _check(status):
+def _check(status, problem=False):
     if status != 0:
-        msg = lib().tapt_last_error().decode(errors="replace")
+        f = lib().tapt_problem_last_error if problem else lib().tapt_last_error
+        msg = f().decode(errors="replace")
         raise _BY_STATUS.get(status, TaptError)(msg)
 
 
@@ -423,3 +432,61 @@ class Ensemble:
         _check(lib().tapt_generate_proposals(self._h, _p(t, _u32p), len(t), _p(mb, _f64p), int(refine),
                                              _p(acc, _u8p)))
         return acc
+
+
+# ------------------------------------------------------------- problem suite --
+
+class Multiplier:
+    """build_multiplier(n): 3n^2+n spins, AND gates + full adders with
+    spin identification; product bits and carry-ins clamped."""
+
+    def __init__(self, n):
+        self.n = int(n)
+        self.n_spins = int(lib().tapt_multiplier_spins(self.n))
+        m = C.c_uint32()
+        _check(lib().tapt_multiplier_build(self.n, C.byref(m), None, None, None, None, None, None), True)
+        k = m.value
+        self.ci, self.cj = np.zeros(k, np.uint32), np.zeros(k, np.uint32)
+        self.J, self.h = np.zeros(k), np.zeros(self.n_spins)
+        self.clamp = np.zeros(self.n_spins, np.int8)
+        self.wires = np.zeros(5 * self.n, np.uint32)
+        _check(lib().tapt_multiplier_build(self.n, C.byref(m), _p(self.ci, _u32p), _p(self.cj, _u32p),
+                                           _p(self.J, _f64p), _p(self.h, _f64p), _p(self.clamp, _i8p),
+                                           _p(self.wires, _u32p)), True)
+        n_ = self.n
+        self.A, self.B = self.wires[:n_], self.wires[n_:2 * n_]
+        self.C, self.carry = self.wires[2 * n_:4 * n_], self.wires[4 * n_:]
+
+    def model(self):
+        return Model.graph(self.n_spins, self.ci, self.cj, self.J, self.h, self.clamp)
+
+    def forward(self, a, b):
+        s = np.zeros(self.n_spins, np.int8)
+        _check(lib().tapt_multiplier_forward(self.n, int(a), int(b), _p(s, _i8p)), True)
+        return s
+
+    def clamps(self, product):
+        c = np.zeros(self.n_spins, np.int8)
+        _check(lib().tapt_multiplier_clamps(self.n, int(product), _p(c, _i8p)), True)
+        return c
+
+    def decode(self, s, product):
+        s = np.ascontiguousarray(s, np.int8)
+        a, b, ok = C.c_uint64(), C.c_uint64(), C.c_int()
+        _check(lib().tapt_multiplier_decode(self.n, _p(s, _i8p), int(product), C.byref(a), C.byref(b),
+                                            C.byref(ok)), True)
+        return a.value, b.value, bool(ok.value)
+
+
+def enumerate_semiprimes(n):
+    cnt = C.c_uint32()
+    _check(lib().tapt_enumerate_semiprimes(int(n), None, 0, C.byref(cnt)), True)
+    out = np.zeros(cnt.value, np.uint64)
+    _check(lib().tapt_enumerate_semiprimes(int(n), _p(out, _u64p), cnt.value, C.byref(cnt)), True)
+    return out
+
+
+def random_semiprime(seed, gid, bits=16):
+    p, q = C.c_uint64(), C.c_uint64()
+    _check(lib().tapt_random_semiprime(int(seed), int(gid), int(bits), C.byref(p), C.byref(q)), True)
+    return p.value, q.value
