@@ -223,10 +223,8 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    if args.instances % world:
-        raise SystemExit("instances must divide evenly over the ranks")
-    I = args.instances // world
-    off = rank * I
+    from paper_2509_23043_b200 import sharding
+    off, I = sharding.shard(args.instances, world, rank)  # contiguous global instance ids
     S = args.sweeps_per_step
 
     model = T.Model.lattice((L,))
@@ -278,8 +276,7 @@ def main():
     if world > 1:
         dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
     ms = float(ms_t.item())
-    upd_step_local = I * (R * N_SPINS * S + N_TARGETS * N_SPINS * REFINE)
-    upd_step = upd_step_local * world
+    upd_step = args.instances * (R * N_SPINS * S + N_TARGETS * N_SPINS * REFINE)
     value = upd_step * args.steps / (ms * 1e-3)
 
     # roofline of the dominant kernel (K1, one launch per step, measured on its stream)
@@ -369,7 +366,7 @@ def e2e_leg(args, T, torch, ens, stream, I, S, world):
         import torch.distributed as dist
         dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
     dt = float(dt_t.item())
-    upd = I * R * N_SPINS * S * world * args.steps
+    upd = args.instances * R * N_SPINS * S * args.steps
     return {"value": upd / dt, "unit": UNIT, "h2d_bytes_per_step": int(host.numel()),
             "d2h_bytes_per_step": int(I * R * 8),
             "path": "tapt_inject_proposals_packed (host-supplied proposals) + tapt_run + tapt_ensemble_get_energies"}

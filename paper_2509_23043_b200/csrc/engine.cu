@@ -177,6 +177,7 @@ uint64_t fnv1a(const void* data, size_t n, uint64_t h) {
 
 // Host table for the Metropolis rule  accept iff uniform < exp(c * dE)  (dE integer <= 0).
 struct HostMetro {
+    bool oversize = false;
     std::vector<uint64_t> tab;
     std::vector<uint32_t> off, K;
     std::vector<int64_t> kz;
@@ -190,15 +191,22 @@ struct HostMetro {
             tab.push_back(1ull << 53);
             return;
         }
-        always.push_back(0);
         uint32_t k = 0;
         for (;; ++k) {
             const double e = std::exp(c * -static_cast<double>(k));
             const uint64_t T = threshold_of(e);
             tab.push_back(T);
             if (T <= 1) break;
-            if (tab.size() > (64u << 20)) throw tapt::ConfigError("beta spacing too fine for exact Metropolis tables");
+            if (tab.size() > (64u << 20)) {
+                oversize = true;  // reported when a swap / proposal actually needs this table
+                tab.resize(off.back());
+                always.push_back(0);
+                K.push_back(0);
+                kz.push_back(-1);
+                return;
+            }
         }
+        always.push_back(0);
         K.push_back(k + 1);
         // largest k with exp(-c k) > 0 (threshold 1 between K and kz, 0 beyond)
         int64_t lo = k, hi = int64_t(1) << 40;
@@ -426,6 +434,7 @@ struct tapt_ensemble_s {
     int clamp_sets = 1;
     bool have_disorder = false;
     uint32_t launch_chunk = 2000;
+    bool swap_oversize = false, prop_oversize = false;  // exact tables too large for this ladder
 
     DevBuf<uint32_t> words;
     DevBuf<int32_t> E;
@@ -544,6 +553,8 @@ struct tapt_ensemble_s {
     void run(uint32_t n_sweeps, uint32_t swap_every, uint32_t measure_every, uint64_t measure_from) {
         if (n_sweeps == 0) return;
         if (swap_every && R < 2) swap_every = 0;
+        if (swap_every && swap_oversize)
+            throw tapt::ConfigError("beta spacing too fine for exact swap tables (adjacent betas closer than ~1e-5)");
         const bool cluster = G > 1;
         uint32_t done = 0;
         while (done < n_sweeps) {
@@ -851,6 +862,8 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
         for (int r = 0; r < e->R; ++r) pr.add_row(e->betas[r]);
         e->swap_tab.upload(sw, e->stream);
         e->prop_tab.upload(pr, e->stream);
+        e->swap_oversize = sw.oversize;
+        e->prop_oversize = pr.oversize;
         // streams
         std::vector<uint64_t> st((size_t)e->I * e->R), co(e->I);
         for (uint32_t i = 0; i < e->I; ++i) {
@@ -1196,6 +1209,7 @@ tapt_status tapt_swap_pass(tapt_ensemble_t e, int parity) {
     return guard([&] {
         check_ens(e);
         if (parity != 0 && parity != 1) throw tapt::ConfigError("parity must be 0 or 1");
+        if (e->swap_oversize) throw tapt::ConfigError("beta spacing too fine for exact swap tables");
         if (e->R >= 2) {
             ++g_launches;
             k_swap_pass<<<e->I, std::max(32, (e->R / 2 + 31) / 32 * 32), 0, e->stream>>>(
@@ -1300,6 +1314,7 @@ void finish_proposals(tapt_ensemble_s* e, const uint32_t* targets, uint32_t T, b
 }
 
 void prepare_targets(tapt_ensemble_s* e, const uint32_t* targets, uint32_t T) {
+    if (e->prop_oversize) throw tapt::ConfigError("beta too small for exact proposal tables");
     if (T == 0 || T > (uint32_t)e->R) throw tapt::ConfigError("n_targets must be in [1, n_slots]");
     std::vector<uint8_t> seen(e->R, 0);
     for (uint32_t t = 0; t < T; ++t) {

@@ -373,3 +373,67 @@ def test_cfg5_full_size_energy_consistency_and_determinism():
     c.init_random()
     c.run(40, swap_every=1)
     assert np.array_equal(c.spins(), S[2:])
+
+
+# ------------------------------------------------------- factorization circuits --
+
+def _mult_graph(M, clamp):
+    return O.Graph.from_couplings(M.n_spins, M.ci, M.cj, M.J, M.h, clamp)
+
+
+def test_multiplier_pt_per_instance_clamps_bit_exact():
+    """Config 4 shape at n=8: colour-class K2 sweeps + swaps, each instance its own semiprime."""
+    M = T.Multiplier(8)
+    m = M.model()
+    prods = [T.random_semiprime(5, k, 8) for k in range(3)]
+    clamps = np.stack([M.clamps(p * q) for p, q in prods])
+    betas = H.geometric(0.1, 5.0, 32)
+    e = T.Ensemble(m, betas, n_instances=3, seed=8)
+    e.set_clamps(clamps)
+    e.init_random()
+    e.run(200, swap_every=1)
+    colours, _ = m.schedule()
+    graphs = [_mult_graph(M, clamps[k]) for k in range(3)]
+    pts = H.run_oracle(graphs, betas, 8, 0, H.colour_order_for(colours), 200)
+    compare(e, pts)
+    S = e.spins()
+    for k in range(3):                       # clamped wires hold their values in every slot
+        nz = np.nonzero(clamps[k])[0]
+        assert np.all(S[k][:, nz] == clamps[k][nz])
+
+
+def test_multiplier_forward_mode_samples_the_product():
+    """n=4, A=0110, B=0101 clamped, Gibbs at beta=3 for 1e3 sweeps -> C = 30 in
+    >= 95% of chains (here: 64 independent chains as instances x slots)."""
+    M = T.Multiplier(4)
+    cl = np.zeros(M.n_spins, np.int8)
+    for i in range(4):
+        cl[M.A[i]] = 1 if (6 >> i) & 1 else -1
+        cl[M.B[i]] = 1 if (5 >> i) & 1 else -1
+    cl[M.carry] = -1
+    m = T.Model.graph(M.n_spins, M.ci, M.cj, M.J, M.h, cl)
+    e = T.Ensemble(m, [3.0, 3.5], n_instances=32, seed=123)
+    e.init_random()
+    e.run(1000, swap_every=0)
+    S = e.spins().reshape(-1, M.n_spins)
+    prod = ((S[:, M.C] > 0) * (1 << np.arange(8))).sum(axis=1)
+    assert (prod == 30).mean() >= 0.95
+
+
+def test_factorization_finds_factors_4bit():
+    """Inverse mode (8-bit products, section 5.2): C = 11*13 = 143 clamped; PT over 32
+    slots finds A*B = C in the coldest slots for most of 16 independent seeds.  (The 16-bit
+    product 44969 = 193*233 is hard: the paper reports 7% PT success in 1e4 sweeps.)"""
+    M = T.Multiplier(4)
+    m = M.model()
+    C = 11 * 13
+    e = T.Ensemble(m, H.geometric(0.1, 5.0, 32), n_instances=16, seed=2)
+    e.set_clamps(np.stack([M.clamps(C)] * 16))
+    e.init_random()
+    found = np.zeros(16, bool)
+    for _ in range(10):
+        e.run(500, swap_every=1)
+        S = e.spins()
+        for k in range(16):
+            found[k] |= any(M.decode(S[k][r], C)[2] for r in range(26, 32))
+    assert found.mean() >= 0.75
