@@ -1,0 +1,147 @@
+// tapt/mcmc.hpp -- drop-in for the reference's local-MCMC API (proj/include/tapt/mcmc.hpp:15-56,
+// proj/src/mcmc.cpp) with every sweep executed on the B200 (index-ascending schedule, bit-exact
+// with the reference's gibbs_sweep for integer couplings: same heat-bath conditional, same
+// per-site draw of the caller's RngStream, same returned energy change).
+#pragma once
+
+#include <cstring>
+#include <iosfwd>
+#include <istream>
+#include <ostream>
+
+#include "tapt/spin_model.hpp"
+
+namespace tapt {
+
+struct ChainConfig {
+    double beta = 1.0;
+    std::uint64_t mixing_sweeps = 0;
+    std::uint64_t thinning = 1;
+    std::uint64_t seed = 0;
+};
+
+struct SampleRecord {
+    double beta;
+    SpinConfiguration spins;
+};
+
+struct SampleDataset {
+    std::vector<SampleRecord> records;
+    std::uint64_t graph_digest = 0;
+
+    // binary `ISFD1`: magic, then per record f64 beta, u32 count, spins bit-packed LSB-first
+    // (+1 -> 1), little-endian (mcmc.cpp:86-162 format).
+    void save(std::ostream& os) const {
+        os.write("ISFD1", 5);
+        for (const auto& r : records) {
+            os.write(reinterpret_cast<const char*>(&r.beta), 8);
+            const std::uint32_t n = static_cast<std::uint32_t>(r.spins.size());
+            os.write(reinterpret_cast<const char*>(&n), 4);
+            std::vector<unsigned char> p((n + 7) / 8, 0);
+            for (std::uint32_t i = 0; i < n; ++i)
+                if (r.spins[i] > 0) p[i / 8] |= static_cast<unsigned char>(1u << (i % 8));
+            os.write(reinterpret_cast<const char*>(p.data()), static_cast<std::streamsize>(p.size()));
+        }
+    }
+    void save_file(const std::string& path) const {
+        std::ofstream os(path, std::ios::binary);
+        if (!os) throw FormatError("cannot open " + path + " for writing");
+        save(os);
+    }
+    static SampleDataset load(std::istream& is) {
+        char magic[5];
+        is.read(magic, 5);
+        if (is.gcount() != 5 || std::memcmp(magic, "ISFD1", 5) != 0) throw FormatError("bad dataset magic (expected ISFD1)");
+        SampleDataset out;
+        for (;;) {
+            double beta;
+            is.read(reinterpret_cast<char*>(&beta), 8);
+            if (is.gcount() == 0) break;
+            if (is.gcount() != 8) throw FormatError("truncated dataset record");
+            std::uint32_t n;
+            is.read(reinterpret_cast<char*>(&n), 4);
+            if (is.gcount() != 4) throw FormatError("truncated dataset record");
+            std::vector<unsigned char> p((n + 7) / 8);
+            is.read(reinterpret_cast<char*>(p.data()), static_cast<std::streamsize>(p.size()));
+            if (is.gcount() != static_cast<std::streamsize>(p.size())) throw FormatError("truncated dataset record");
+            SpinConfiguration s(n);
+            for (std::uint32_t i = 0; i < n; ++i) s[i] = (p[i / 8] >> (i % 8)) & 1u ? 1 : -1;
+            out.records.push_back({beta, std::move(s)});
+        }
+        return out;
+    }
+    static SampleDataset load_file(const std::string& path) {
+        std::ifstream is(path, std::ios::binary);
+        if (!is) throw FormatError("cannot open " + path);
+        return load(is);
+    }
+};
+
+// One device sweep (or n): updates s in place, advances rng by n_free draws per sweep,
+// returns the total energy change.
+inline double gibbs_sweeps(const CouplingGraph& g, SpinConfiguration& s, double beta, RngStream& rng,
+                           std::uint32_t n_sweeps, std::vector<double>* per_sweep = nullptr) {
+    if (s.size() != g.n_spins()) throw DimensionError("configuration length mismatch");
+    if (n_sweeps == 0 || g.n_free() == 0) return 0.0;
+    std::uint64_t st = rng.state();
+    std::vector<double> d(n_sweeps);
+    throw_status(tapt_gibbs_sweep(g.device(), s.data(), s.size(), beta, &st, n_sweeps, d.data()));
+    rng = RngStream::from_state(st);
+    double tot = 0.0;
+    for (double v : d) tot += v;
+    if (per_sweep) *per_sweep = std::move(d);
+    return tot;
+}
+
+inline double gibbs_sweep(const CouplingGraph& g, SpinConfiguration& s, double beta, RngStream& rng) {
+    return gibbs_sweeps(g, s, beta, rng, 1);
+}
+
+// Single-site heat-bath update (mcmc.cpp:24-28): one draw of rng.
+inline void gibbs_update(const CouplingGraph& g, SpinConfiguration& s, std::uint32_t i, double beta, RngStream& rng) {
+    const double l = local_field(g, s, i);  // throws ClampedSiteError
+    s[i] = rng.uniform() < 1.0 / (1.0 + std::exp(-2.0 * beta * l)) ? 1 : -1;
+}
+
+inline void check_chain_config(const ChainConfig& c) {
+    if (c.beta < 0.0) throw ConfigError("beta must be >= 0");
+    if (c.thinning < 1) throw ConfigError("thinning must be >= 1");
+}
+
+// run_chain (mcmc.cpp:47-65): init from derive(seed,{kInit,kChain}), dynamics
+// derive(seed,{kChain}); mixing sweeps, then a record every `thinning` sweeps.
+inline SampleDataset run_chain(const CouplingGraph& g, const ChainConfig& config, std::uint64_t n_records) {
+    check_chain_config(config);
+    SampleDataset out;
+    out.graph_digest = g.digest();
+    if (n_records == 0) return out;
+    RngStream init = RngStream::derive(config.seed, {stream::kInit, stream::kChain});
+    RngStream dyn = RngStream::derive(config.seed, {stream::kChain});
+    SpinConfiguration s = random_configuration(g, init);
+    if (config.mixing_sweeps) gibbs_sweeps(g, s, config.beta, dyn, static_cast<std::uint32_t>(config.mixing_sweeps));
+    for (std::uint64_t r = 0; r < n_records; ++r) {
+        gibbs_sweeps(g, s, config.beta, dyn, static_cast<std::uint32_t>(config.thinning));
+        out.records.push_back({config.beta, s});
+    }
+    return out;
+}
+
+// generate_training_corpus (mcmc.cpp:67-84): per beta a chain seeded by
+// derive(seed,{kChain, index}).state(); records concatenated in beta order.
+inline SampleDataset generate_training_corpus(const CouplingGraph& g, const std::vector<double>& betas,
+                                              std::uint64_t per_beta, const ChainConfig& config,
+                                              unsigned /*n_threads: the device replaces the thread pool*/ = 1) {
+    check_chain_config(config);
+    SampleDataset out;
+    out.graph_digest = g.digest();
+    for (std::size_t bi = 0; bi < betas.size(); ++bi) {
+        ChainConfig c = config;
+        c.beta = betas[bi];
+        c.seed = RngStream::derive(config.seed, {stream::kChain, bi}).state();
+        auto part = run_chain(g, c, per_beta);
+        for (auto& r : part.records) out.records.push_back(std::move(r));
+    }
+    return out;
+}
+
+}  // namespace tapt

@@ -1,0 +1,199 @@
+// C++ drop-in API test driver (compiled and run by tests/test_cpp_api.py).
+// Re-expresses the reference's own doctest assertions (proj/tests/test_spin_model.cpp) against
+// include/tapt/*.hpp, and exercises the device paths (gibbs_sweep, run_chain, run_pt/run_tapt).
+#include <cassert>
+#include <cstdio>
+#include <cstring>
+#include <iostream>
+#include <sstream>
+
+#include "tapt/lattice.hpp"
+#include "tapt/mcmc.hpp"
+#include "tapt/tempering.hpp"
+
+using namespace tapt;
+
+#define CHECK(c)                                                              \
+    do {                                                                      \
+        if (!(c)) {                                                           \
+            std::fprintf(stderr, "CHECK failed: %s (line %d)\n", #c, __LINE__); \
+            return 1;                                                         \
+        }                                                                     \
+    } while (0)
+
+template <class E, class F>
+bool throws(F&& f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static CouplingGraph and_gate() {
+    CouplingGraph::Builder b(3);
+    b.add_coupling(0, 1, -1.0).add_coupling(0, 2, 2.0).add_coupling(1, 2, 2.0);
+    b.add_field(0, 1.0).add_field(1, 1.0).add_field(2, -2.0);
+    return b.build();
+}
+
+static int cpu_tests() {
+    // test_spin_model.cpp:36-65
+    auto g22 = LatticeSpec::grid2d(2, 2).graph();
+    CHECK(energy(g22, SpinConfiguration(4, 1)) == -4.0);
+    CouplingGraph::Builder b1(1);
+    b1.add_field(0, 2.0);
+    CHECK(energy(b1.build(), SpinConfiguration{1}) == -2.0);
+    CHECK(energy(and_gate(), SpinConfiguration{1, 1, 1}) == -3.0);
+    CHECK(throws<DimensionError>([&] { energy(g22, SpinConfiguration(3, 1)); }));
+    // :67-97 local field
+    auto g33 = LatticeSpec::grid2d(3, 3).graph();
+    SpinConfiguration s3(9, 1);
+    CHECK(local_field(g33, s3, 4) == 4.0);
+    CouplingGraph::Builder bc(2);
+    bc.add_coupling(0, 1, 1.0).set_clamp(0, 1);
+    CHECK(throws<ClampedSiteError>([&] { local_field(bc.build(), SpinConfiguration{1, 1}, 0); }));
+    // :99-122 flip delta
+    for (std::uint32_t i = 0; i < 4; ++i) CHECK(flip_delta(g22, SpinConfiguration(4, 1), i) == 4.0);
+    CHECK(flip_delta(and_gate(), SpinConfiguration{1, 1, 1}, 2) == 4.0);
+    // :124-137 flip identity on random graphs
+    RngStream rng(12345);
+    for (int trial = 0; trial < 20; ++trial) {
+        CouplingGraph::Builder b(10);
+        for (std::uint32_t i = 0; i < 10; ++i) {
+            for (std::uint32_t j = i + 1; j < 10; ++j)
+                if (rng.uniform() < 0.4) b.add_coupling(i, j, rng.normal());
+            if (trial % 2 == 0) b.add_field(i, rng.normal());
+        }
+        auto g = b.build();
+        auto s = random_configuration(g, rng);
+        const double e0 = energy(g, s);
+        for (std::uint32_t i = 0; i < 10; ++i) {
+            auto f = s;
+            f[i] = static_cast<std::int8_t>(-f[i]);
+            CHECK(std::fabs(energy(g, f) - e0 - flip_delta(g, s, i)) < 1e-12);
+        }
+    }
+    // :189-233 instance file round trip and parse errors
+    {
+        std::ostringstream os;
+        and_gate().save(os);
+        std::istringstream is(os.str());
+        auto g = CouplingGraph::load(is);
+        CHECK(g.digest() == and_gate().digest());
+        std::istringstream bad("isingmodel v2\nn 2\n");
+        CHECK(throws<FormatError>([&] { CouplingGraph::load(bad); }));
+        std::istringstream dup("isingmodel v1\nn 3\nc 0 1 1\nc 1 0 2\n");
+        CHECK(throws<FormatError>([&] { CouplingGraph::load(dup); }));
+        std::istringstream self("isingmodel v1\nn 2\nc 0 0 1.0\n");
+        CHECK(throws<ConfigError>([&] { CouplingGraph::load(self); }));
+    }
+    // :235-242 builder merges duplicates
+    CouplingGraph::Builder bm(3);
+    bm.add_coupling(0, 1, 1.5).add_coupling(1, 0, 0.5);
+    auto gm = bm.build();
+    CHECK(gm.couplings().size() == 1 && gm.couplings()[0].value == 2.0);
+    // :244-259 lattice counts and bijection
+    auto s2 = LatticeSpec::grid2d(4, 5);
+    CHECK(s2.n_sites() == 20 && s2.n_edges() == 4 * 4 + 5 * 3 && s2.graph().couplings().size() == s2.n_edges());
+    CHECK(s2.index2d(1, 0) == 5);
+    auto sp = LatticeSpec::grid3d(3);
+    CHECK(sp.n_sites() == 27 && sp.n_edges() == 54 && sp.graph().couplings().size() == 54);
+    CHECK(sp.index3d(0, 1, 0) == 3 && sp.index3d(0, 0, 1) == 9);
+    // ISFD1 round trip
+    SampleDataset d;
+    d.records.push_back({0.5, SpinConfiguration{1, -1, 1, 1, -1, -1, 1, -1, 1}});
+    std::ostringstream os;
+    d.save(os);
+    std::istringstream is(os.str());
+    auto d2 = SampleDataset::load(is);
+    CHECK(d2.records.size() == 1 && d2.records[0].spins == d.records[0].spins && d2.records[0].beta == 0.5);
+    // C ABI digest matches
+    std::uint64_t dig = 0;
+    CHECK(tapt_model_digest(and_gate().device(), &dig) == TAPT_OK && dig == and_gate().digest());
+    std::printf("cpu ok\n");
+    return 0;
+}
+
+// Synthetic proposal source (stand-in for the IsingFormer): fair i.i.d. spins.
+struct IidSource : ProposalSource {
+    SpinConfiguration sample(std::size_t, double, std::span<const std::int8_t> ctx, std::size_t, RngStream& rng) override {
+        SpinConfiguration s(ctx.size());
+        for (auto& v : s) v = rng.coin() ? 1 : -1;
+        return s;
+    }
+};
+
+static int gpu_tests() {
+    // gibbs_sweep drop-in: same result as the sequential host restatement of mcmc.cpp:30-45
+    auto g = LatticeSpec::grid2d(16, 16, 1.0, LatticeSpec::Boundary::periodic).graph();
+    RngStream init(7);
+    auto s = random_configuration(g, init);
+    auto h = s;
+    RngStream r1 = RngStream::derive(1, {stream::kChain});
+    RngStream r2 = r1;
+    for (int k = 0; k < 5; ++k) {
+        const double d = gibbs_sweep(g, s, 0.6, r1);
+        double dh = 0.0;  // host restatement
+        for (std::uint32_t i : g.free_sites()) {
+            const double l = local_field(g, h, i);
+            const std::int8_t nx = r2.uniform() < 1.0 / (1.0 + std::exp(-2.0 * 0.6 * l)) ? 1 : -1;
+            if (nx != h[i]) {
+                dh += 2.0 * h[i] * l;
+                h[i] = nx;
+            }
+        }
+        CHECK(d == dh && s == h && r1.state() == r2.state());
+    }
+    // run_chain: deterministic per seed, records distinct
+    ChainConfig cc;
+    cc.beta = 0.4;
+    cc.mixing_sweeps = 10;
+    cc.thinning = 2;
+    cc.seed = 3;
+    auto ds = run_chain(g, cc, 4);
+    CHECK(ds.records.size() == 4 && ds.graph_digest == g.digest());
+    auto ds2 = run_chain(g, cc, 4);
+    for (int k = 0; k < 4; ++k) CHECK(ds.records[k].spins == ds2.records[k].spins);
+    // run_pt / run_tapt move audit and best-energy monotonicity
+    auto ladder = BetaLadder::geometric(0.2, 1.0, 8);
+    TAPTConfig cfg;
+    cfg.n_swap = 30;
+    cfg.M = 2;
+    cfg.seed = 9;
+    auto tr = run_pt(g, ladder, cfg);
+    for (std::size_t m = 0; m < tr.move_kind.size(); ++m) CHECK(tr.move_kind[m] == int(m % 3) + 1);
+    for (std::size_t m = 1; m < tr.best_energy.size(); ++m) CHECK(tr.best_energy[m] <= tr.best_energy[m - 1]);
+    CHECK(energy(g, tr.final_state) == tr.final_energy);
+    cfg.N_T = 4;
+    IidSource src;
+    auto tt = run_tapt(g, ladder, cfg, &src);
+    std::uint64_t att = 0;
+    for (auto v : tt.gen_attempts) att += v;
+    CHECK(att == 4 * 10);
+    cfg.n_swap = 0;
+    auto t0 = run_pt(g, ladder, cfg);
+    CHECK(t0.move_kind.empty());
+    auto rho = residual_energy(tr, -2.0 * 256, 256);
+    CHECK(rho.size() == tr.energies.size() && rho.back() >= 0.0);
+    auto al = adaptive_ladder(g, 0.2, 1.0, 0.5, 50, 1);
+    for (std::size_t r = 1; r < al.betas.size(); ++r) CHECK(al.betas[r] > al.betas[r - 1]);
+    CHECK(al.betas.front() == 0.2 && al.betas.back() == 1.0);
+    std::printf("gpu ok\n");
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    const std::string mode = argc > 1 ? argv[1] : "cpu";
+    try {
+        if (mode == "cpu") return cpu_tests();
+        if (mode == "gpu") return gpu_tests();
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "exception: %s\n", e.what());
+        return 2;
+    }
+    return 3;
+}

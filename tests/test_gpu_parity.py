@@ -437,3 +437,59 @@ def test_factorization_finds_factors_4bit():
         for k in range(16):
             found[k] |= any(M.decode(S[k][r], C)[2] for r in range(26, 32))
     assert found.mean() >= 0.75
+
+
+# ------------------------------------------------------------- statistical tier --
+
+def _per_slot_means(e, n):
+    obs = e.observables().astype(np.float64)          # [I][R][5]
+    cnt = obs[:, :, 0]
+    return obs[:, :, 1] / cnt / n, obs[:, :, 3] / cnt / n   # <E>/N, <|m|> per instance and slot
+
+
+def test_checkerboard_vs_reference_order_statistics_cfg1():
+    """Config 1: per-beta <E>/N and <|m|> of the checkerboard chain (K1) agree with the
+    reference's index-ascending chain (K2 level schedule, bit-exact with the unmodified
+    gibbs_sweep) within 4 sigma over S = 16 independent seeds each (SURVEY 8c statistical
+    tier; 4 sigma because 64 comparisons are made)."""
+    betas = H.geometric(0.2, 1.0, 32)
+    m = T.Model.lattice((32, 32))
+    out = {}
+    for order, off in (("colour", 0), ("reference", 1000)):
+        e = T.Ensemble(m, betas, n_instances=16, seed=77, instance_offset=off, order=order)
+        e.init_random()
+        e.run(10000, swap_every=1, measure_every=1, measure_from=5000)
+        out[order] = _per_slot_means(e, 1024)
+    for k in range(2):
+        a, b = out["colour"][k], out["reference"][k]
+        se = np.sqrt(a.var(axis=0, ddof=1) / 16 + b.var(axis=0, ddof=1) / 16) + 1e-6
+        z = np.abs(a.mean(axis=0) - b.mean(axis=0)) / se
+        assert z.max() < 4.0, (k, z.max(), int(z.argmax()))
+
+
+def test_pt_stationarity_small_system():
+    """3x3 open ferromagnet, 4 replicas beta in [0.1, 1.0]: the coldest replica's
+    state distribution matches Boltzmann(beta_max) within TV 0.02 (4096 independent ensembles,
+    20 samples each, spaced 50 sweeps apart after 500 sweeps of equilibration)."""
+    import itertools
+    g = O.lattice_graph((3, 3), 1.0, False)
+    m = T.Model.lattice((3, 3), 1.0, periodic=False)
+    betas = np.array([0.1, 0.4, 0.7, 1.0])
+    e = T.Ensemble(m, betas, n_instances=4096, seed=5)
+    e.init_random()
+    e.run(500, swap_every=1)
+    counts = np.zeros(512)
+    w = 1 << np.arange(9)
+    for _ in range(20):
+        e.run(50, swap_every=1)
+        S = e.spins()[:, -1, :]
+        np.add.at(counts, ((S > 0) * w).sum(axis=1), 1)
+    states = np.array(list(itertools.product([-1, 1], repeat=9)))[:, ::-1]
+    idx = ((states > 0) * w).sum(axis=1)
+    E = np.array([O.lib().oc_energy(g.oc(), np.ascontiguousarray(s, np.int8).ctypes.data_as(O._i8p))
+                  for s in states], np.float64)
+    p = np.zeros(512)
+    p[idx] = np.exp(-1.0 * (E - E.min()))
+    p /= p.sum()
+    tv = 0.5 * np.abs(counts / counts.sum() - p).sum()
+    assert tv < 0.02, tv
