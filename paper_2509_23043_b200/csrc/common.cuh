@@ -44,12 +44,22 @@ __host__ __device__ __forceinline__ uint32_t thr_hi(uint64_t T) {
 // high word on the FMA pipe (IMAD.HI) instead of the ALU pipe (SHF).
 struct MixConsts {
     uint32_t k4, k32;
+    uint32_t nib[8];  // nib[k] = 2^(34-4k) (k >= 1): hi(N * nib[k]) = N >> (4k-2)
 };
 
+inline MixConsts make_mix_consts() {
+    MixConsts c{4u, 32u, {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}};
+    for (int k = 1; k < 8; ++k) c.nib[k] = 1u << (34 - 4 * k);
+    return c;
+}
+
 // High word of (z ^ z>>30) * M1 ^ ... * M2, i.e. mix_final(z) BEFORE its last xor-shift.
-// Variant bits (instruction-mix choices, identical results):
-//   V & 1: high-word right shifts as IMAD.HI by 4 / 32 (FMA pipe) instead of SHF (ALU pipe)
-//   V & 2: first 64-bit multiply as an explicit IMAD.WIDE + IMAD + IMAD chain (PTX)
+// Variant bits (instruction-mix choices, identical results; measured on B200 with
+// tools/probe_variants.sh and tools/k1_variants.sh, default 12 = bits 4|8):
+//   V & 1: high-word right shifts as IMAD.HI by 4 / 32 (FMA pipe) instead of SHF (ALU pipe)  [slower]
+//   V & 2: first 64-bit multiply as an explicit IMAD.WIDE + IMAD + IMAD chain (PTX)           [neutral]
+//   V & 4: tie band tracked as a running min (k1_lattice.cu)                                   [+4%]
+//   V & 8: threshold-index shift as IMAD.HI on the FMA pipe (k1_lattice.cu)                    [+3%]
 // The last multiply only needs its high word: IMAD.HI + IMAD + IMAD.
 template <int V>
 __device__ __forceinline__ uint32_t mix_pre_hi(uint32_t zl, uint32_t zh, const MixConsts& c) {

@@ -507,7 +507,7 @@ struct tapt_ensemble_s {
         a.width = width;
         a.nbins = nbins;
         a.best = best.p;
-        a.mc = MixConsts{4u, 32u};
+        a.mc = make_mix_consts();
         return a;
     }
 

@@ -157,7 +157,13 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
         const int m = b & 3, sh = 4 * (b >> 2);
 #pragma unroll
         for (int u = 0; u < SP; ++u) {
-            const uint32_t thr = sm.Uhi[b][(N[u][m] >> sh) & 7u];
+            uint32_t thr;
+            if constexpr ((V & 8) != 0) {  // shift on the FMA pipe: (N >> sh) << 2 == hi(N * 2^(34-sh)) & 0x1C
+                const uint32_t ix = (sh >= 4 ? __umulhi(N[u][m], mc.nib[sh >> 2]) : (N[u][m] << 2)) & 0x1Cu;
+                thr = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(&sm.Uhi[b][0]) + ix);
+            } else {
+                thr = sm.Uhi[b][(N[u][m] >> sh) & 7u];
+            }
             const uint64_t z = base + ph[u];
             const uint32_t h = mix_pre_hi<V>((uint32_t)z, (uint32_t)(z >> 32), mc);
             const uint32_t dd = decide_acc(h, thr, w[u]);
@@ -189,7 +195,7 @@ __device__ __forceinline__ void k1_decide2(const K1Smem& sm, int nv, uint64_t ph
 }
 
 template <int DIM, bool DIS, bool CLU, int SP>
-__global__ void __launch_bounds__(SP == 1 ? 1024 : 512, 1) k1_lattice_pt(const PTArgs a, const LatDims d) {
+__global__ void __launch_bounds__(SP == 1 ? 1024 : (SP == 2 ? 512 : 256), 1) k1_lattice_pt(const PTArgs a, const LatDims d) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ K1Smem sm;  // static: table addresses fold into LDS immediates
     uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw);
@@ -320,7 +326,9 @@ template <int DIM, bool DIS, bool CLU>
 static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st) {
     const size_t smem = k1_smem_bytes(a.n, DIS);
     // SP = 1 site word per thread-iteration at 1024 threads, else 2 interleaved at <= 512
-    auto fn = threads > 512 ? k1_lattice_pt<DIM, DIS, CLU, 1> : k1_lattice_pt<DIM, DIS, CLU, 2>;
+    auto fn = threads > 512   ? k1_lattice_pt<DIM, DIS, CLU, 1>
+              : threads > 256 ? k1_lattice_pt<DIM, DIS, CLU, 2>
+                              : k1_lattice_pt<DIM, DIS, CLU, 4>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -389,7 +397,7 @@ __global__ void __launch_bounds__(512) k_decision_probe(uint32_t iters, uint32_t
 
 cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st,
                                   int variant) {
-    const MixConsts mc{4u, 32u};
+    const MixConsts mc = make_mix_consts();
     switch (variant < 0 ? TAPT_K1_VARIANT : variant) {
         case 0: k_decision_probe<0><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
         case 1: k_decision_probe<1><<<blocks, threads, 0, st>>>(iters, sink, mc); break;

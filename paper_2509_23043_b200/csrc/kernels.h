@@ -19,7 +19,7 @@ constexpr int kMaxR = 256;   // ladder slots per instance (uint8 permutation)
 constexpr int kW = 32;       // replicas per group (bits per word)
 constexpr int kCnt = 8;      // planes of the sliced per-thread counters
 #ifndef TAPT_K1_VARIANT
-#define TAPT_K1_VARIANT 4    // instruction-mix variant of the decision loop (common.cuh)
+#define TAPT_K1_VARIANT 12   // instruction-mix variant of the decision loop (common.cuh)
 #endif
 
 struct LatDims {
