@@ -34,6 +34,7 @@ cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool clust
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st);
 size_t k1_smem_bytes(int n, bool dis);
 size_t k2_smem_bytes(int n, int R, int nidx);
+size_t k2_smem_bytes_graph(int n, int R, int nidx, int nnz, int nfree);
 cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st,
                                   int variant);
 __global__ void k_init_random(uint32_t*, int, int, int, int, const uint64_t*, const int8_t*, int);
@@ -426,7 +427,7 @@ struct tapt_ensemble_s {
     std::vector<double> betas;
     uint64_t seed = 0;
     bool use_k1 = false;
-    int k1_threads = 0, k2_threads = 256;
+    int k1_threads = 0, k2_threads = 512;
     int nidx = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -477,6 +478,8 @@ struct tapt_ensemble_s {
         g.class_sites = level_order ? m->d_levsites.p : m->d_colsites.p;
         g.n_classes = (int)((level_order ? m->lev_ptr.size() : m->col_ptr.size()) - 1);
         g.lmin = m->lmin;
+        g.n_free = (uint32_t)m->free_sites.size();
+        g.smem_graph = k2_smem_bytes_graph(n(), R, nidx, g.nnz, (int)g.n_free) <= 200 * 1024 ? 1 : 0;
         return g;
     }
 

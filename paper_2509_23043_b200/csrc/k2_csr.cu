@@ -23,19 +23,67 @@ struct K2Smem {
     PTShared S;
 };
 
-template <bool CLU>
-__global__ void __launch_bounds__(256) k2_csr_pt(const PTArgs a, const CsrArgs g) {
+// Four lanes share one site word; lane `sub` owns the 8 replicas 8k + 2*sub + {0,1}
+// (k = 0..3), i.e. byte lanes of the two byte-SWAR accumulators A[2*sub], A[2*sub+1].
+constexpr int kTPS = 4;
+
+// Shared-memory image of the graph (the whole CSR is staged once per launch when it fits):
+//   rowptr [n+1] u32 | col [nnz] u32 | h [n] i32 | rank [n] u32 | class_sites [n_free] u32 | J [nnz] i8
+__host__ __device__ inline size_t k2_graph_bytes(int n, int nnz, int nfree) {
+    return ((size_t)(n + 1) + nnz + 2 * (size_t)n + nfree) * 4 + (((size_t)nnz + 15) & ~size_t(15));
+}
+
+// Graph arrays as seen by the sweep: shared-memory copies (SMEMG) or the global CSR.
+struct K2Graph {
+    const uint32_t* rowptr;
+    const uint32_t* col;
+    const int8_t* J;
+    const int32_t* h;
+    const uint32_t* rank;
+    const uint32_t* class_sites;
+};
+
+template <bool CLU, bool SMEMG>
+__global__ void __launch_bounds__(512, 2) k2_csr_pt(const PTArgs a, const CsrArgs g) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    K2Smem& sm = *reinterpret_cast<K2Smem*>(smem_raw);
-    uint32_t* Uhi = reinterpret_cast<uint32_t*>(smem_raw + ((sizeof(K2Smem) + 127) & ~size_t(127)));  // [R][nidx]
-    uint32_t* words = Uhi + (size_t)a.R * a.nidx;                              // [n]
-    const int tid = threadIdx.x, nt = blockDim.x;
+    __shared__ K2Smem sm;
+    const int nidx = a.nidx;
+    uint32_t* Uslot = reinterpret_cast<uint32_t*>(smem_raw);  // [R][nidx] high threshold words by slot
+    uint32_t* words = Uslot + (size_t)a.R * nidx;               // [n]
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     const int inst = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
-    const int8_t* Jrow = g.J + (size_t)(g.nJ > 1 ? inst : 0) * g.nnz;
+    const int8_t* Jglob = g.J + (size_t)(g.nJ > 1 ? inst : 0) * g.nnz;
+    const int nfree = (int)g.n_free;
+    K2Graph G;
+    if constexpr (SMEMG) {  // stage the CSR next to the spins: every neighbour walk stays on-chip
+        uint32_t* rp = words + n;
+        uint32_t* cl = rp + (n + 1);
+        int32_t* hh = reinterpret_cast<int32_t*>(cl + g.nnz);
+        uint32_t* rk = reinterpret_cast<uint32_t*>(hh + n);
+        uint32_t* cs = rk + n;
+        int8_t* jj = reinterpret_cast<int8_t*>(cs + nfree);
+        for (int k = tid; k <= n; k += nt) rp[k] = g.rowptr[k];
+        for (int k = tid; k < g.nnz; k += nt) {
+            cl[k] = g.col[k];
+            jj[k] = Jglob[k];
+        }
+        for (int k = tid; k < n; k += nt) {
+            hh[k] = g.h[k];
+            rk[k] = g.rank[k];
+        }
+        for (int k = tid; k < nfree; k += nt) cs[k] = g.class_sites[k];
+        G = K2Graph{rp, cl, jj, hh, rk, cs};
+    } else {
+        G = K2Graph{g.rowptr, g.col, Jglob, g.h, g.rank, g.class_sites};
+    }
+    const int sub = tid & (kTPS - 1), m0 = 2 * sub;
+    const uint32_t gmask = 0xFu << (lane & ~(kTPS - 1));
+    const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
+    const uint32_t mine = (0x03030303u << m0) & vmask;  // replicas of this lane
 
     for (int k = tid; k < n; k += nt) words[k] = a.words[((size_t)inst * a.G + grp) * n + k];
-    for (int k = tid; k < a.R * a.nidx; k += nt) Uhi[k] = thr_hi(a.thr[k]);
+    for (int k = tid; k < a.R * nidx; k += nt) Uslot[k] = thr_hi(a.thr[k]);
     pt_load_perm(a, sm.S, inst);
     for (int b = tid; b < nv; b += nt) sm.S.Eown[(a.t0 + 1) & 1][b] = a.E[(size_t)inst * a.B + grp * W + b];
     __syncthreads();
@@ -48,59 +96,96 @@ __global__ void __launch_bounds__(256) k2_csr_pt(const PTArgs a, const CsrArgs g
         par = (int)(t & 1);
         pt_stream_bases(a, sm.S, inst, grp, t);
         __syncthreads();
-        int32_t dE[kW];
+        // this lane's 8 replicas: threshold-row offsets of their current slots
+        int trow[8];
 #pragma unroll
-        for (int b = 0; b < kW; ++b) dE[b] = 0;
+        for (int j = 0; j < 8; ++j) {
+            const int b = 8 * (j >> 1) + m0 + (j & 1);
+            trow[j] = b < nv ? sm.S.slot_of[grp * W + b] * nidx : 0;
+        }
+        int32_t dE[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dE[j] = 0;
 
         for (int c = 0; c < g.n_classes; ++c) {
             const uint32_t c0 = g.class_ptr[c], c1 = g.class_ptr[c + 1];
-            for (uint32_t q = c0 + tid; q < c1; q += nt) {
-                const uint32_t i = g.class_sites[q];
+            for (uint32_t q = c0 + (uint32_t)(tid / kTPS); q < c1; q += (uint32_t)(nt / kTPS)) {
+                const uint32_t i = G.class_sites[q];
+                // neighbour walk split over the 4 lanes, byte-SWAR accumulators reduced after
                 uint32_t A[8];
 #pragma unroll
                 for (int m = 0; m < 8; ++m) A[m] = 0;
                 int sumabs = 0;
-                for (uint32_t k = g.rowptr[i]; k < g.rowptr[i + 1]; ++k) {
-                    const int J = Jrow[k];
-                    const uint32_t v = words[g.col[k]] ^ (J < 0 ? 0xFFFFFFFFu : 0u);
+                const uint32_t r1 = G.rowptr[i + 1];
+                for (uint32_t k = G.rowptr[i] + sub; k < r1; k += kTPS) {
+                    const int J = G.J[k];
+                    const uint32_t v = words[G.col[k]] ^ (J < 0 ? 0xFFFFFFFFu : 0u);
                     const uint32_t mag = (uint32_t)(J < 0 ? -J : J);
                     sumabs += (int)mag;
 #pragma unroll
                     for (int m = 0; m < 8; ++m) A[m] += mag * ((v >> m) & 0x01010101u);
                 }
-                const int l0 = g.h[i] - sumabs;            // l = l0 + 2*acc
-                const uint32_t old = words[i];
-                const uint64_t ph = (uint64_t)g.rank[i] * kPhi;
-                uint32_t nw = 0;
 #pragma unroll
-                for (int b = 0; b < kW; ++b) {
+                for (int m = 0; m < 8; ++m) {
+                    A[m] += __shfl_xor_sync(gmask, A[m], 1);
+                    A[m] += __shfl_xor_sync(gmask, A[m], 2);
+                }
+                sumabs += __shfl_xor_sync(gmask, sumabs, 1);
+                sumabs += __shfl_xor_sync(gmask, sumabs, 2);
+                const uint32_t A0 = A[m0], A1 = A[m0 + 1];
+                const int off = G.h[i] - sumabs - g.lmin;  // idx = l - lmin = off + 2*acc
+                const uint32_t old = words[i];
+                const uint64_t ph = (uint64_t)G.rank[i] * kPhi;
+                uint32_t nw = 0, tmin = 0xFFFFFFFFu;
+                int idx[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int b = 8 * (j >> 1) + m0 + (j & 1);
+                    idx[j] = off + 2 * (int)((((j & 1) ? A1 : A0) >> (8 * (j >> 1))) & 0xFFu);
                     if (b < nv) {
-                        const int acc = (int)((A[b & 7] >> (8 * (b >> 3))) & 0xFFu);
-                        const int l = l0 + 2 * acc;
-                        const int slot = sm.S.slot_of[grp * W + b];
-                        const int idx = l - g.lmin;
+                        const uint32_t thr = Uslot[trow[j] + idx[j]];
                         const uint64_t z = sm.S.sb[b] + ph;
-                        const uint32_t xh = mix_final_hi(z);
-                        const uint32_t U = Uhi[slot * a.nidx + idx];
-                        bool up;
-                        if (xh != U)
-                            up = xh < U;
-                        else
-                            up = below(mix_final(z), a.thr[(size_t)slot * a.nidx + idx]);
-                        const bool was = (old >> b) & 1u;
-                        if (up) nw |= 1u << b;
-                        if (up != was) dE[b] += was ? 2 * l : -2 * l;
+                        const uint32_t h = mix_pre_hi<TAPT_K1_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), a.mc);
+                        tmin = min(tmin, h - thr + 1u);
+                        if (h < thr) nw |= 1u << b;
                     }
                 }
-                words[i] = nw | (old & ~((nv >= 32) ? 0xFFFFFFFFu : ((1u << nv) - 1u)));
+                if (tmin <= 2u) {  // |h - U| <= 1 somewhere (p ~ 2^-31): exact 64-bit decisions
+                    nw = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int b = 8 * (j >> 1) + m0 + (j & 1);
+                        if (b < nv && below(mix_final(sm.S.sb[b] + ph), a.thr[(size_t)trow[j] + idx[j]])) nw |= 1u << b;
+                    }
+                }
+                const uint32_t flips = (nw ^ old) & mine;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int b = 8 * (j >> 1) + m0 + (j & 1);
+                    const int l2 = 2 * (g.lmin + idx[j]);  // dE of a flip = 2 s_old l
+                    if ((flips >> b) & 1u) dE[j] += ((old >> b) & 1u) ? l2 : -l2;
+                }
+                nw |= __shfl_xor_sync(gmask, nw, 1);
+                nw |= __shfl_xor_sync(gmask, nw, 2);
+                if (sub == 0) words[i] = nw | (old & ~vmask);
             }
             __syncthreads();
         }
-        // per-replica dE summed over the CTA
+        // per-replica dE: reduce over the lanes owning the same replicas, then over warps
         {
-            const int32_t tot = warp_reduce_scatter32(dE);
-            const int lane = tid & 31;
-            if (lane < nv) atomicAdd(&sm.S.Ucnt[lane], (uint32_t)tot);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                dE[j] += __shfl_xor_sync(0xFFFFFFFFu, dE[j], 4);
+                dE[j] += __shfl_xor_sync(0xFFFFFFFFu, dE[j], 8);
+                dE[j] += __shfl_xor_sync(0xFFFFFFFFu, dE[j], 16);
+            }
+            if (lane < kTPS) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int b = 8 * (j >> 1) + m0 + (j & 1);
+                    if (b < nv) atomicAdd(&sm.S.Ucnt[b], (uint32_t)dE[j]);
+                }
+            }
             __syncthreads();
             if (tid < nv) {
                 sm.S.Eown[par][tid] = sm.S.Eown[prev][tid] + (int32_t)sm.S.Ucnt[tid];
@@ -114,13 +199,19 @@ __global__ void __launch_bounds__(256) k2_csr_pt(const PTArgs a, const CsrArgs g
 }
 
 size_t k2_smem_bytes(int n, int R, int nidx) {
-    return ((sizeof(K2Smem) + 127) & ~size_t(127)) + (size_t)R * nidx * 4 + (size_t)n * 4;
+    // dynamic part: per-slot threshold rows + spin words (control block is static)
+    return (size_t)R * nidx * 4 + (size_t)n * 4;
+}
+
+size_t k2_smem_bytes_graph(int n, int R, int nidx, int nnz, int nfree) {
+    return k2_smem_bytes(n, R, nidx) + k2_graph_bytes(n, nnz, nfree);
 }
 
 template <bool CLU>
 static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, cudaStream_t st) {
-    const size_t smem = k2_smem_bytes(a.n, a.R, a.nidx);
-    auto fn = k2_csr_pt<CLU>;
+    const size_t smem = g.smem_graph ? k2_smem_bytes_graph(a.n, a.R, a.nidx, g.nnz, (int)g.n_free)
+                                     : k2_smem_bytes(a.n, a.R, a.nidx);
+    auto fn = g.smem_graph ? k2_csr_pt<CLU, true> : k2_csr_pt<CLU, false>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};

@@ -78,6 +78,8 @@ struct CsrArgs {
     const uint32_t* class_sites;
     int n_classes;
     int lmin;                  // thresholds indexed by (l - lmin)
+    int smem_graph;            // stage the CSR in shared memory (it fits)
+    uint32_t n_free;
 };
 
 }  // namespace tapt_dev
