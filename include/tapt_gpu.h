@@ -168,6 +168,10 @@ tapt_status tapt_get_histogram(tapt_ensemble_t e, uint64_t* dst, int dst_on_devi
 tapt_status tapt_get_best(tapt_ensemble_t e, int64_t* best /* [I] */);
 tapt_status tapt_reset_observables(tapt_ensemble_t e);
 
+/* Replace the ladder values (thresholds re-tabulated); allow_flat permits equal neighbours
+ * (annealing stages: every slot at one beta, swaps disabled). */
+tapt_status tapt_ensemble_set_betas(tapt_ensemble_t e, const double* betas, int allow_flat);
+
 /* n_sweeps sweeps of every slot, no swaps (Alg. 1 lines 21-25). */
 tapt_status tapt_sweep(tapt_ensemble_t e, uint32_t n_sweeps);
 /* One swap pass over pairs (r, r+1), r = parity, parity+2, ... (Eq. 1). */

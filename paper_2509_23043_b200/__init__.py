@@ -126,6 +126,7 @@ _SIGS = {
     "tapt_get_histogram": (C.c_int, [_vp, _vp, C.c_int]),
     "tapt_get_best": (C.c_int, [_vp, _i64p]),
     "tapt_reset_observables": (C.c_int, [_vp]),
+    "tapt_ensemble_set_betas": (C.c_int, [_vp, _f64p, C.c_int]),
     "tapt_sweep": (C.c_int, [_vp, C.c_uint32]),
     "tapt_swap_pass": (C.c_int, [_vp, C.c_int]),
     "tapt_run": (C.c_int, [_vp, C.POINTER(Schedule)]),
@@ -390,6 +391,11 @@ class Ensemble:
     def reset_observables(self):
         _check(lib().tapt_reset_observables(self._h))
 
+    def set_betas(self, betas, allow_flat=False):
+        b = np.ascontiguousarray(betas, np.float64)
+        _check(lib().tapt_ensemble_set_betas(self._h, _p(b, _f64p), int(bool(allow_flat))))
+        self.betas = b
+
     # -- dynamics
     def sweep(self, n_sweeps=1):
         _check(lib().tapt_sweep(self._h, int(n_sweeps)))
@@ -490,3 +496,42 @@ def random_semiprime(seed, gid, bits=16):
     p, q = C.c_uint64(), C.c_uint64()
     _check(lib().tapt_random_semiprime(int(seed), int(gid), int(bits), C.byref(p), C.byref(q)), True)
     return p.value, q.value
+
+
+def estimate_ground_energy(model, restarts, sweeps, seed, beta_start=0.1, beta_end=5.0, stages=50,
+                           n_instances=1, instance_offset=0, signs=None, disorder_seed=None, clamps=None):
+    """estimate_ground_energy: best energy over `restarts` geometric-annealing
+    runs of `sweeps` sweeps each, on the device (restarts = slots of one ensemble, all at the
+    same beta per stage, no swaps; streams keyed by derive(seed,{kAnneal}) as the root)."""
+    R = int(restarts)
+    if R > 256:
+        raise ConfigError("at most 256 restarts per call")
+    root = _derive_root(seed, 0x55)
+    ens = Ensemble(model, beta_start + np.arange(R, dtype=np.float64), n_instances, root, instance_offset)
+    if signs is not None:
+        ens.set_bond_signs(signs)
+    elif disorder_seed is not None:
+        ens.generate_ea_disorder(disorder_seed)
+    if clamps is not None:
+        ens.set_clamps(clamps)
+    ens.init_random()
+    per = max(1, int(sweeps) // int(stages))
+    for k in range(int(stages)):
+        b = beta_start * (beta_end / beta_start) ** (k / max(int(stages) - 1, 1))
+        ens.set_betas(np.full(R, b), allow_flat=True)
+        ens.run(per, swap_every=0)
+    return ens.best()
+
+
+def _derive_root(seed, tag):
+    """derive(seed, {tag}).state() (rng.hpp:21-27), host-side."""
+    M = (1 << 64) - 1
+    PHI = 0x9E3779B97F4A7C15
+
+    def mix(z):
+        z = (z + PHI) & M
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
+        return z ^ (z >> 31)
+    s = mix((int(seed) ^ PHI) & M)
+    return mix(s ^ ((tag + PHI) & M))

@@ -553,6 +553,26 @@ struct tapt_ensemble_s {
         best.upload(b, stream);
     }
 
+    // Heat-bath thresholds [R][nidx] and the swap (rows = pairs) / proposal (rows = slots)
+    // Metropolis tables for the current ladder.
+    void build_tables() {
+        std::vector<uint64_t> th((size_t)R * nidx);
+        for (int r = 0; r < R; ++r)
+            for (int k = 0; k < nidx; ++k) {
+                const double l = use_k1 ? (double)(m->J0 * (2 * k - 2 * m->dim)) : (double)(m->lmin + k);
+                th[(size_t)r * nidx + k] = threshold_of(conditional_up(betas[r], l));
+            }
+        thr.upload(th, stream);
+        HostMetro sw, pr;
+        for (int r = 0; r + 1 < R; ++r) sw.add_row(betas[r + 1] - betas[r]);
+        if (R < 2) sw.add_row(0.0);
+        for (int r = 0; r < R; ++r) pr.add_row(betas[r]);
+        swap_tab.upload(sw, stream);
+        prop_tab.upload(pr, stream);
+        swap_oversize = sw.oversize;
+        prop_oversize = pr.oversize;
+    }
+
     void run(uint32_t n_sweeps, uint32_t swap_every, uint32_t measure_every, uint64_t measure_from) {
         if (n_sweeps == 0) return;
         if (swap_every && R < 2) swap_every = 0;
@@ -846,27 +866,7 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
             if (k2_smem_bytes(n, e->R, e->nidx) > 227 * 1024) throw tapt::SizeError("graph too large for shared memory");
         }
         if (e->G > 8) throw tapt::ConfigError("at most 256 slots");
-        // heat-bath thresholds [R][nidx]
-        std::vector<uint64_t> thr((size_t)e->R * e->nidx);
-        for (int r = 0; r < e->R; ++r)
-            for (int k = 0; k < e->nidx; ++k) {
-                double l;
-                if (e->use_k1)
-                    l = (double)(m->Jsign * 0 + m->J0 * (2 * k - 2 * m->dim));
-                else
-                    l = (double)(m->lmin + k);
-                thr[(size_t)r * e->nidx + k] = threshold_of(conditional_up(e->betas[r], l));
-            }
-        e->thr.upload(thr, e->stream);
-        // swap (rows = pairs) and proposal (rows = slots) Metropolis tables
-        HostMetro sw, pr;
-        for (int r = 0; r + 1 < e->R; ++r) sw.add_row(e->betas[r + 1] - e->betas[r]);
-        if (e->R < 2) sw.add_row(0.0);
-        for (int r = 0; r < e->R; ++r) pr.add_row(e->betas[r]);
-        e->swap_tab.upload(sw, e->stream);
-        e->prop_tab.upload(pr, e->stream);
-        e->swap_oversize = sw.oversize;
-        e->prop_oversize = pr.oversize;
+        e->build_tables();
         // streams
         std::vector<uint64_t> st((size_t)e->I * e->R), co(e->I);
         for (uint32_t i = 0; i < e->I; ++i) {
@@ -911,6 +911,24 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
                 throw tapt::CudaError(msg);
             }
         }
+    });
+}
+
+// New ladder values for the same slots (e.g. a simulated-annealing stage).  A ladder that is
+// not strictly increasing is accepted only with allow_flat (swaps must then stay disabled:
+// equal neighbours have c = 0 rows that accept every swap).
+tapt_status tapt_ensemble_set_betas(tapt_ensemble_t e, const double* betas, int allow_flat) {
+    return guard([&] {
+        check_ens(e);
+        for (int r = 0; r < e->R; ++r) {
+            if (!(betas[r] >= 0.0) || !std::isfinite(betas[r])) throw tapt::ConfigError("beta must be >= 0");
+            if (r && !(betas[r] > betas[r - 1]) && !(allow_flat && betas[r] >= betas[r - 1]))
+                throw tapt::ConfigError("beta ladder must be strictly increasing (SPEC.md:388)");
+        }
+        CUDA_OK(cudaStreamSynchronize(e->stream));
+        e->betas.assign(betas, betas + e->R);
+        e->build_tables();
+        sync_if(e->stream);
     });
 }
 

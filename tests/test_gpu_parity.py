@@ -495,3 +495,22 @@ def test_pt_stationarity_small_system():
     p /= p.sum()
     tv = 0.5 * np.abs(counts / counts.sum() - p).sum()
     assert tv < 0.02, tv
+
+
+# ------------------------------------------------------- annealing --
+
+def test_estimate_ground_energy_ferromagnet_and_small_glass():
+    m = T.Model.lattice((16, 16))
+    best = T.estimate_ground_energy(m, restarts=8, sweeps=2000, seed=1)
+    assert best[0] == -2 * 256                      # ferromagnet: -|edges| J recovered exactly
+    # 3x4 open +-J glass: best of 8 restarts equals the brute-force ground energy
+    rs = np.random.default_rng(3)
+    n, ci, cj, _ = O.lattice_couplings((3, 4), 1.0, False)
+    J = rs.choice([-1.0, 1.0], len(ci))
+    g = O.Graph.from_couplings(n, ci, cj, J)
+    mg = T.Model.graph(n, ci, cj, J)
+    states = ((np.arange(2 ** n)[:, None] >> np.arange(n)) & 1) * 2 - 1
+    E = -(J[None, :] * states[:, ci] * states[:, cj]).sum(1)
+    best = T.estimate_ground_energy(mg, restarts=8, sweeps=1000, seed=2)
+    assert best[0] == E.min()
+    del g
