@@ -240,7 +240,13 @@ __global__ void __launch_bounds__(SP == 1 ? 1024 : (SP == 2 ? 512 : 256), 1) k1_
 #pragma unroll
         for (int k = 0; k < kCnt; ++k) C[k] = 0;
 
-        for (int c = (a.energy_only ? 1 : 0); c < 2; ++c) {
+        const int c_end = TAPT_K1_EPOST ? 3 : 2;
+        for (int cc = (a.energy_only ? (TAPT_K1_EPOST ? 2 : 1) : 0); cc < c_end; ++cc) {
+            // cc = 0, 1: colour halves; with TAPT_K1_EPOST the energy is a third pass (cc = 2)
+            // over colour 1, so no energy state stays live across the decision loop
+            const int c = cc > 1 ? 1 : cc;
+            const bool decide = !a.energy_only && cc < 2;
+            const bool count = TAPT_K1_EPOST ? (cc == 2) : (c == 1);
             for (int j = tid; j < nsub; j += nt) {
                 // site u of this iteration: colour index j + u*nsub (a warp's lanes cover
                 // consecutive colour indices, so each shared load stays conflict-free)
@@ -254,7 +260,7 @@ __global__ void __launch_bounds__(SP == 1 ? 1024 : (SP == 2 ? 512 : 256), 1) k1_
                     nibbles(q[u][0], q[u][1], q[u][2], N[u]);
                 }
                 uint32_t nw[SP];
-                if (a.energy_only) {
+                if (!decide) {
 #pragma unroll
                     for (int u = 0; u < SP; ++u) nw[u] = words[is[u]];
                 } else {
@@ -279,7 +285,7 @@ __global__ void __launch_bounds__(SP == 1 ? 1024 : (SP == 2 ? 512 : 256), 1) k1_
 #pragma unroll
                     for (int u = 0; u < SP; ++u) words[is[u]] = nw[u];
                 }
-                if (c == 1) {
+                if (count) {
 #pragma unroll
                     for (int u = 0; u < SP; ++u) {
                         uint32_t v0, v1, v2;

@@ -18,6 +18,9 @@ namespace tapt_dev {
 constexpr int kMaxR = 256;   // ladder slots per instance (uint8 permutation)
 constexpr int kW = 32;       // replicas per group (bits per word)
 constexpr int kCnt = 8;      // planes of the sliced per-thread counters
+#ifndef TAPT_K1_EPOST
+#define TAPT_K1_EPOST 0      // 1: energies in a separate pass after the two colour halves
+#endif
 #ifndef TAPT_K1_VARIANT
 #define TAPT_K1_VARIANT 12   // instruction-mix variant of the decision loop (common.cuh)
 #endif
