@@ -405,14 +405,14 @@ cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint3
                                   int variant) {
     const MixConsts mc = make_mix_consts();
     switch (variant < 0 ? TAPT_K1_VARIANT : variant) {
-        case 0: k_decision_probe<0><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
-        case 1: k_decision_probe<1><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
-        case 2: k_decision_probe<2><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
-        case 3: k_decision_probe<3><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
-        case 4: k_decision_probe<4><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
-        case 5: k_decision_probe<5><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
-        case 6: k_decision_probe<6><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
-        default: k_decision_probe<7><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+#define TAPT_PROBE_CASE(v) \
+    case v: k_decision_probe<v><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
+        TAPT_PROBE_CASE(0) TAPT_PROBE_CASE(1) TAPT_PROBE_CASE(2) TAPT_PROBE_CASE(3)
+        TAPT_PROBE_CASE(4) TAPT_PROBE_CASE(5) TAPT_PROBE_CASE(6) TAPT_PROBE_CASE(7)
+        TAPT_PROBE_CASE(8) TAPT_PROBE_CASE(9) TAPT_PROBE_CASE(10) TAPT_PROBE_CASE(11)
+        TAPT_PROBE_CASE(12) TAPT_PROBE_CASE(13) TAPT_PROBE_CASE(14) TAPT_PROBE_CASE(15)
+#undef TAPT_PROBE_CASE
+        default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
 }
