@@ -517,10 +517,13 @@ struct tapt_ensemble_s {
     void launch(const PTArgs& a, bool cluster) {
         ++g_launches;
         cudaError_t e;
-        if (use_k1)
+        if (use_k1) {
             e = launch_k1(a, m->ld, k1_threads, cluster, stream);
-        else
-            e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_threads, cluster, stream);
+        } else {
+            int nt = k2_threads;
+            if (const char* env = std::getenv("TAPT_K2_THREADS")) nt = std::max(128, std::min(1024, std::atoi(env)));
+            e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), nt, cluster, stream);
+        }
         if (e != cudaSuccess) throw tapt::CudaError(std::string("sweep kernel launch: ") + cudaGetErrorString(e));
         CUDA_OK(cudaGetLastError());
     }

@@ -13,19 +13,23 @@
 // J < 0, acc = sum |J| * bit  counts into 8 words x 4 byte lanes (replica 8k+m in byte k
 // of A[m]); then l = h_i - sum|J| + 2*acc exactly, and the threshold table is indexed by
 // l - lmin.  Energies are tracked per replica by exact integer dE = 2*s_old*l on flips.
+//
+// Work split: four lanes share one site word (lane `sub` owns replicas 8k + 2*sub + {0,1});
+// the neighbour walk is split over the four lanes and reduced with shuffles.  When an
+// instance fits one CTA (R <= 32) a CTA carries up to kIPB instances that share the staged
+// CSR and the threshold table; lane group q works on instance q % ipb, so every colour class
+// gives each group several sites and the class barriers are amortised.
 #include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
 
 #include "pt_common.cuh"
 
 namespace tapt_dev {
 
-struct K2Smem {
-    PTShared S;
-};
-
-// Four lanes share one site word; lane `sub` owns the 8 replicas 8k + 2*sub + {0,1}
-// (k = 0..3), i.e. byte lanes of the two byte-SWAR accumulators A[2*sub], A[2*sub+1].
-constexpr int kTPS = 4;
+constexpr int kTPS = 4;  // lanes per site word
+constexpr int kIPB = 4;  // max instances per CTA
 
 // Shared-memory image of the graph (the whole CSR is staged once per launch when it fits):
 //   rowptr [n+1] u32 | col [nnz] u32 | h [n] i32 | rank [n] u32 | class_sites [n_free] u32 | J [nnz] i8
@@ -44,20 +48,31 @@ struct K2Graph {
 };
 
 template <bool CLU, bool SMEMG>
-__global__ void __launch_bounds__(512, 2) k2_csr_pt(const PTArgs a, const CsrArgs g) {
+__global__ void __launch_bounds__(1024, 1) k2_csr_pt(const PTArgs a, const CsrArgs g, const int ipb) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
-    __shared__ K2Smem sm;
-    const int nidx = a.nidx;
-    uint32_t* Uslot = reinterpret_cast<uint32_t*>(smem_raw);  // [R][nidx] high threshold words by slot
-    uint32_t* words = Uslot + (size_t)a.R * nidx;               // [n]
+    __shared__ PTShared SS[kIPB];
+    const int nidx = a.nidx, n = a.n, W = a.W;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
-    const int inst = blockIdx.x / a.G, grp = blockIdx.x % a.G;
-    const int n = a.n, W = a.W, nv = own_count(a, grp);
-    const int8_t* Jglob = g.J + (size_t)(g.nJ > 1 ? inst : 0) * g.nnz;
+    // instances [inst0, inst0 + nin) of this CTA (ipb > 1 only without clusters: G == 1)
+    const int grp = ipb > 1 ? 0 : (int)(blockIdx.x % a.G);
+    const int inst0 = ipb > 1 ? (int)blockIdx.x * ipb : (int)(blockIdx.x / a.G);
+    const int nin = min(ipb, a.I - inst0);
+    const int nv = own_count(a, grp);
+    uint32_t* Uslot = reinterpret_cast<uint32_t*>(smem_raw);  // [R][nidx] high threshold words by slot
+    uint32_t* wbase = Uslot + (size_t)a.R * nidx;               // [ipb][n]
     const int nfree = (int)g.n_free;
+    // this thread's lane group, instance and position among that instance's groups
+    const int grp_id = tid / kTPS, ngroups = nt / kTPS;
+    const int mykin = grp_id % ipb;  // instance slot inside the CTA
+    const int gi = grp_id / ipb, ngi = ngroups / ipb;
+    const bool active = mykin < nin;
+    const int inst = inst0 + (active ? mykin : 0);
+    PTShared& S = SS[active ? mykin : 0];
+    uint32_t* words = wbase + (size_t)(active ? mykin : 0) * n;
+    const int8_t* Jglob = g.J + (size_t)(g.nJ > 1 ? inst : 0) * g.nnz;
     K2Graph G;
     if constexpr (SMEMG) {  // stage the CSR next to the spins: every neighbour walk stays on-chip
-        uint32_t* rp = words + n;
+        uint32_t* rp = wbase + (size_t)ipb * n;
         uint32_t* cl = rp + (n + 1);
         int32_t* hh = reinterpret_cast<int32_t*>(cl + g.nnz);
         uint32_t* rk = reinterpret_cast<uint32_t*>(hh + n);
@@ -66,14 +81,14 @@ __global__ void __launch_bounds__(512, 2) k2_csr_pt(const PTArgs a, const CsrArg
         for (int k = tid; k <= n; k += nt) rp[k] = g.rowptr[k];
         for (int k = tid; k < g.nnz; k += nt) {
             cl[k] = g.col[k];
-            jj[k] = Jglob[k];
+            jj[k] = g.J[k];  // shared couplings; per-instance couplings stay in global memory
         }
         for (int k = tid; k < n; k += nt) {
             hh[k] = g.h[k];
             rk[k] = g.rank[k];
         }
         for (int k = tid; k < nfree; k += nt) cs[k] = g.class_sites[k];
-        G = K2Graph{rp, cl, jj, hh, rk, cs};
+        G = K2Graph{rp, cl, g.nJ > 1 ? Jglob : jj, hh, rk, cs};
     } else {
         G = K2Graph{g.rowptr, g.col, Jglob, g.h, g.rank, g.class_sites};
     }
@@ -82,10 +97,14 @@ __global__ void __launch_bounds__(512, 2) k2_csr_pt(const PTArgs a, const CsrArg
     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
     const uint32_t mine = (0x03030303u << m0) & vmask;  // replicas of this lane
 
-    for (int k = tid; k < n; k += nt) words[k] = a.words[((size_t)inst * a.G + grp) * n + k];
+    for (int kin = 0; kin < nin; ++kin) {
+        const int ik = inst0 + kin;
+        uint32_t* wk = wbase + (size_t)kin * n;
+        for (int k = tid; k < n; k += nt) wk[k] = a.words[((size_t)ik * a.G + grp) * n + k];
+        pt_load_perm(a, SS[kin], ik);
+        for (int b = tid; b < nv; b += nt) SS[kin].Eown[(a.t0 + 1) & 1][b] = a.E[(size_t)ik * a.B + grp * W + b];
+    }
     for (int k = tid; k < a.R * nidx; k += nt) Uslot[k] = thr_hi(a.thr[k]);
-    pt_load_perm(a, sm.S, inst);
-    for (int b = tid; b < nv; b += nt) sm.S.Eown[(a.t0 + 1) & 1][b] = a.E[(size_t)inst * a.B + grp * W + b];
     __syncthreads();
 
     uint64_t pass = a.p0;
@@ -94,14 +113,14 @@ __global__ void __launch_bounds__(512, 2) k2_csr_pt(const PTArgs a, const CsrArg
         const uint64_t t = a.t0 + (uint64_t)s;
         const int prev = par;
         par = (int)(t & 1);
-        pt_stream_bases(a, sm.S, inst, grp, t);
+        for (int kin = 0; kin < nin; ++kin) pt_stream_bases(a, SS[kin], inst0 + kin, grp, t);
         __syncthreads();
         // this lane's 8 replicas: threshold-row offsets of their current slots
         int trow[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int b = 8 * (j >> 1) + m0 + (j & 1);
-            trow[j] = b < nv ? sm.S.slot_of[grp * W + b] * nidx : 0;
+            trow[j] = b < nv ? S.slot_of[grp * W + b] * nidx : 0;
         }
         int32_t dE[8];
 #pragma unroll
@@ -109,7 +128,7 @@ __global__ void __launch_bounds__(512, 2) k2_csr_pt(const PTArgs a, const CsrArg
 
         for (int c = 0; c < g.n_classes; ++c) {
             const uint32_t c0 = g.class_ptr[c], c1 = g.class_ptr[c + 1];
-            for (uint32_t q = c0 + (uint32_t)(tid / kTPS); q < c1; q += (uint32_t)(nt / kTPS)) {
+            for (uint32_t q = c0 + (uint32_t)gi; active && q < c1; q += (uint32_t)ngi) {
                 const uint32_t i = G.class_sites[q];
                 // neighbour walk split over the 4 lanes, byte-SWAR accumulators reduced after
                 uint32_t A[8];
@@ -144,7 +163,7 @@ __global__ void __launch_bounds__(512, 2) k2_csr_pt(const PTArgs a, const CsrArg
                     idx[j] = off + 2 * (int)((((j & 1) ? A1 : A0) >> (8 * (j >> 1))) & 0xFFu);
                     if (b < nv) {
                         const uint32_t thr = Uslot[trow[j] + idx[j]];
-                        const uint64_t z = sm.S.sb[b] + ph;
+                        const uint64_t z = S.sb[b] + ph;
                         const uint32_t h = mix_pre_hi<TAPT_K1_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), a.mc);
                         tmin = min(tmin, h - thr + 1u);
                         if (h < thr) nw |= 1u << b;
@@ -155,7 +174,7 @@ __global__ void __launch_bounds__(512, 2) k2_csr_pt(const PTArgs a, const CsrArg
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         const int b = 8 * (j >> 1) + m0 + (j & 1);
-                        if (b < nv && below(mix_final(sm.S.sb[b] + ph), a.thr[(size_t)trow[j] + idx[j]])) nw |= 1u << b;
+                        if (b < nv && below(mix_final(S.sb[b] + ph), a.thr[(size_t)trow[j] + idx[j]])) nw |= 1u << b;
                     }
                 }
                 const uint32_t flips = (nw ^ old) & mine;
@@ -171,35 +190,48 @@ __global__ void __launch_bounds__(512, 2) k2_csr_pt(const PTArgs a, const CsrArg
             }
             __syncthreads();
         }
-        // per-replica dE: reduce over the lanes owning the same replicas, then over warps
+        // per-replica dE: reduce over the lanes of this warp that own the same (instance,
+        // replicas) -- group ids equal mod ipb -- then over warps with shared atomics
         {
+            const int gw = lane >> 2;  // group index inside the warp (0..7)
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                dE[j] += __shfl_xor_sync(0xFFFFFFFFu, dE[j], 4);
-                dE[j] += __shfl_xor_sync(0xFFFFFFFFu, dE[j], 8);
-                dE[j] += __shfl_xor_sync(0xFFFFFFFFu, dE[j], 16);
+            for (int bit = 0; bit < 3; ++bit) {
+                const int d = 1 << bit;  // partner group gw ^ d has the same instance iff d % ipb == 0
+                if ((d % ipb) == 0) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) dE[j] += __shfl_xor_sync(0xFFFFFFFFu, dE[j], d * kTPS);
+                }
             }
-            if (lane < kTPS) {
+            if (active && gw < ipb) {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int b = 8 * (j >> 1) + m0 + (j & 1);
-                    if (b < nv) atomicAdd(&sm.S.Ucnt[b], (uint32_t)dE[j]);
+                    if (b < nv) atomicAdd(&S.Ucnt[b], (uint32_t)dE[j]);
                 }
             }
             __syncthreads();
-            if (tid < nv) {
-                sm.S.Eown[par][tid] = sm.S.Eown[prev][tid] + (int32_t)sm.S.Ucnt[tid];
-                sm.S.Ucnt[tid] = 0;
+            for (int e = tid; e < nin * nv; e += nt) {
+                const int kin = e / nv, b = e - kin * nv;
+                SS[kin].Eown[par][b] = SS[kin].Eown[prev][b] + (int32_t)SS[kin].Ucnt[b];
+                SS[kin].Ucnt[b] = 0;
             }
         }
-        pt_epilogue<CLU>(a, sm.S, words, inst, grp, t, pass);
+        uint64_t pass_k = pass;
+        for (int kin = 0; kin < nin; ++kin) {
+            pass_k = pass;
+            pt_epilogue<CLU>(a, SS[kin], wbase + (size_t)kin * n, inst0 + kin, grp, t, pass_k);
+        }
+        pass = pass_k;
     }
-    for (int k = tid; k < n; k += nt) a.words[((size_t)inst * a.G + grp) * n + k] = words[k];
-    pt_finish<CLU>(a, sm.S, inst, grp, par);
+    for (int kin = 0; kin < nin; ++kin) {
+        const uint32_t* wk = wbase + (size_t)kin * n;
+        for (int k = tid; k < n; k += nt) a.words[((size_t)(inst0 + kin) * a.G + grp) * n + k] = wk[k];
+    }
+    for (int kin = 0; kin < nin; ++kin) pt_finish<CLU>(a, SS[kin], inst0 + kin, grp, par);
 }
 
 size_t k2_smem_bytes(int n, int R, int nidx) {
-    // dynamic part: per-slot threshold rows + spin words (control block is static)
+    // dynamic part for one instance: per-slot threshold rows + spin words (control blocks are static)
     return (size_t)R * nidx * 4 + (size_t)n * 4;
 }
 
@@ -207,15 +239,15 @@ size_t k2_smem_bytes_graph(int n, int R, int nidx, int nnz, int nfree) {
     return k2_smem_bytes(n, R, nidx) + k2_graph_bytes(n, nnz, nfree);
 }
 
-template <bool CLU>
-static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, cudaStream_t st) {
-    const size_t smem = g.smem_graph ? k2_smem_bytes_graph(a.n, a.R, a.nidx, g.nnz, (int)g.n_free)
-                                     : k2_smem_bytes(a.n, a.R, a.nidx);
-    auto fn = g.smem_graph ? k2_csr_pt<CLU, true> : k2_csr_pt<CLU, false>;
+template <bool CLU, bool SMEMG>
+static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, int ipb, cudaStream_t st) {
+    size_t smem = (size_t)a.R * a.nidx * 4 + (size_t)ipb * a.n * 4;
+    if (SMEMG) smem += k2_graph_bytes(a.n, g.nnz, (int)g.n_free);
+    auto fn = k2_csr_pt<CLU, SMEMG>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(a.I * a.G));
+    cfg.gridDim = dim3(ipb > 1 ? (unsigned)((a.I + ipb - 1) / ipb) : (unsigned)(a.I * a.G));
     cfg.blockDim = dim3((unsigned)threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -228,11 +260,24 @@ static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, c
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     }
-    return cudaLaunchKernelEx(&cfg, fn, a, g);
+    return cudaLaunchKernelEx(&cfg, fn, a, g, ipb);
+}
+
+// Instances per CTA when one CTA holds a whole instance (G == 1, no cluster): 2 measured best
+// on config 4 (tools/k2_shapes.sh: 512 threads x {1,2,4} instances -> 2.0 / 2.3 / 2.0e11 updates/s).
+int k2_instances_per_cta(const PTArgs& a, const CsrArgs& g) {
+    if (a.G != 1) return 1;
+    if (const char* e = std::getenv("TAPT_K2_IPB")) return std::max(1, std::min(kIPB, std::atoi(e)));
+    const size_t fixed = (size_t)a.R * a.nidx * 4 + (g.smem_graph ? k2_graph_bytes(a.n, g.nnz, (int)g.n_free) : 0);
+    if (fixed + 2 * (size_t)a.n * 4 <= 110 * 1024 && a.I >= 2) return 2;
+    return 1;
 }
 
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st) {
-    return cluster ? launch_k2_t<true>(a, g, threads, st) : launch_k2_t<false>(a, g, threads, st);
+    const int ipb = cluster ? 1 : k2_instances_per_cta(a, g);
+    if (g.smem_graph)
+        return cluster ? launch_k2_t<true, true>(a, g, threads, 1, st) : launch_k2_t<false, true>(a, g, threads, ipb, st);
+    return cluster ? launch_k2_t<true, false>(a, g, threads, 1, st) : launch_k2_t<false, false>(a, g, threads, ipb, st);
 }
 
 }  // namespace tapt_dev
