@@ -168,9 +168,14 @@ tapt_status tapt_get_histogram(tapt_ensemble_t e, uint64_t* dst, int dst_on_devi
 tapt_status tapt_get_best(tapt_ensemble_t e, int64_t* best /* [I] */);
 tapt_status tapt_reset_observables(tapt_ensemble_t e);
 
-/* Replace the ladder values (thresholds re-tabulated); allow_flat permits equal neighbours
- * (annealing stages: every slot at one beta, swaps disabled). */
+/* Replace the ladder values (thresholds re-tabulated); allow_flat = 1 permits equal neighbours
+ * (annealing stages), 2 any order (independent chains, e.g. a training corpus); swaps must then
+ * stay disabled. */
 tapt_status tapt_ensemble_set_betas(tapt_ensemble_t e, const double* betas, int allow_flat);
+/* Override the per-slot dynamics stream states [I][R] (e.g. run_chain's derive(seed,{kChain})). */
+tapt_status tapt_ensemble_set_streams(tapt_ensemble_t e, const uint64_t* states);
+/* random_configuration of every slot from the given init stream states [I][R]. */
+tapt_status tapt_ensemble_init_from_streams(tapt_ensemble_t e, const uint64_t* init_states);
 
 /* n_sweeps sweeps of every slot, no swaps (Alg. 1 lines 21-25). */
 tapt_status tapt_sweep(tapt_ensemble_t e, uint32_t n_sweeps);

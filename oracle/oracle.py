@@ -130,6 +130,8 @@ def ref():
         L.ref_gibbs_sweeps.argtypes = [C.c_void_p, _i8p, C.c_double, C.c_uint64, _u64p, C.c_int, C.c_uint64,
                                        _f64p]
         L.ref_run_chain.argtypes = [C.c_void_p, C.c_double, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, _i8p]
+        L.ref_generate_corpus.argtypes = [C.c_void_p, _f64p, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64,
+                                          C.c_uint64, _i8p]
         L.ref_pt_run.argtypes = [C.POINTER(C.c_void_p), C.c_int, C.c_uint64, C.c_int, _f64p, C.c_uint64,
                                  C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _f64p, C.c_int, C.c_uint, _i8p,
                                  _f64p, _u64p, _u64p]

@@ -131,6 +131,20 @@ void ref_run_chain(void* g, double beta, std::uint64_t mixing, std::uint64_t thi
         std::memcpy(out + r * G->n_spins(), d.records[r].spins.data(), G->n_spins());
 }
 
+// generate_training_corpus (mcmc.cpp:67-84): records [n_betas * per_beta][n] in reference order.
+void ref_generate_corpus(void* g, const double* betas, int nb, std::uint64_t per_beta, std::uint64_t mixing,
+                         std::uint64_t thinning, std::uint64_t seed, std::int8_t* out) {
+    auto* G = static_cast<CouplingGraph*>(g);
+    ChainConfig c;
+    c.mixing_sweeps = mixing;
+    c.thinning = thinning;
+    c.seed = seed;
+    std::vector<double> b(betas, betas + nb);
+    SampleDataset d = generate_training_corpus(*G, b, per_beta, c, 1);
+    for (std::size_t r = 0; r < d.records.size(); ++r)
+        std::memcpy(out + r * G->n_spins(), d.records[r].spins.data(), G->n_spins());
+}
+
 // Restated PT/TAPT schedule over the reference's sweep, for
 // n_inst instances (gids gid0..gid0+n_inst-1), each with its own graph graphs[k].
 // Per global sweep T (1-based): every slot sweeps; if swap_every | T a swap pass

@@ -127,6 +127,8 @@ _SIGS = {
     "tapt_get_best": (C.c_int, [_vp, _i64p]),
     "tapt_reset_observables": (C.c_int, [_vp]),
     "tapt_ensemble_set_betas": (C.c_int, [_vp, _f64p, C.c_int]),
+    "tapt_ensemble_set_streams": (C.c_int, [_vp, _u64p]),
+    "tapt_ensemble_init_from_streams": (C.c_int, [_vp, _u64p]),
     "tapt_sweep": (C.c_int, [_vp, C.c_uint32]),
     "tapt_swap_pass": (C.c_int, [_vp, C.c_int]),
     "tapt_run": (C.c_int, [_vp, C.POINTER(Schedule)]),
@@ -392,9 +394,18 @@ class Ensemble:
         _check(lib().tapt_reset_observables(self._h))
 
     def set_betas(self, betas, allow_flat=False):
+        """allow_flat: False/0 strictly increasing, 1 non-decreasing, 2 any order (no swaps)."""
         b = np.ascontiguousarray(betas, np.float64)
-        _check(lib().tapt_ensemble_set_betas(self._h, _p(b, _f64p), int(bool(allow_flat))))
+        _check(lib().tapt_ensemble_set_betas(self._h, _p(b, _f64p), int(allow_flat)))
         self.betas = b
+
+    def set_streams(self, states):
+        st = np.ascontiguousarray(states, np.uint64).reshape(self.I, self.R)
+        _check(lib().tapt_ensemble_set_streams(self._h, _p(st, _u64p)))
+
+    def init_from_streams(self, init_states):
+        st = np.ascontiguousarray(init_states, np.uint64).reshape(self.I, self.R)
+        _check(lib().tapt_ensemble_init_from_streams(self._h, _p(st, _u64p)))
 
     # -- dynamics
     def sweep(self, n_sweeps=1):
@@ -506,7 +517,7 @@ def estimate_ground_energy(model, restarts, sweeps, seed, beta_start=0.1, beta_e
     R = int(restarts)
     if R > 256:
         raise ConfigError("at most 256 restarts per call")
-    root = _derive_root(seed, 0x55)
+    root = derive_state(seed, [0x55])
     ens = Ensemble(model, beta_start + np.arange(R, dtype=np.float64), n_instances, root, instance_offset)
     if signs is not None:
         ens.set_bond_signs(signs)
@@ -523,8 +534,9 @@ def estimate_ground_energy(model, restarts, sweeps, seed, beta_start=0.1, beta_e
     return ens.best()
 
 
-def _derive_root(seed, tag):
-    """derive(seed, {tag}).state() (rng.hpp:21-27), host-side."""
+
+def derive_state(root, path):
+    """RngStream::derive(root, path).state() (rng.hpp:21-27), host-side."""
     M = (1 << 64) - 1
     PHI = 0x9E3779B97F4A7C15
 
@@ -533,5 +545,33 @@ def _derive_root(seed, tag):
         z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M
         z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M
         return z ^ (z >> 31)
-    s = mix((int(seed) ^ PHI) & M)
-    return mix(s ^ ((tag + PHI) & M))
+    s = mix((int(root) ^ PHI) & M)
+    for p in path:
+        s = mix(s ^ ((int(p) + PHI) & M))
+    return s
+
+
+def generate_training_corpus(model, betas, per_beta, mixing_sweeps, thinning, seed):
+    """generate_training_corpus (mcmc.cpp:67-84) on the device, bit-exact with the reference:
+    chain b runs at betas[b] with c.seed = derive(seed,{kChain,b}).state(), initial state from
+    derive(c.seed,{kInit,kChain}), dynamics derive(c.seed,{kChain}), index-ascending sweeps
+    (run_chain, mcmc.cpp:47-65).  All chains advance together as the slots of one ensemble.
+    Returns (beta of each record, spins [n_betas*per_beta, n]) in the reference's record order."""
+    betas = np.asarray(betas, np.float64)
+    nb = len(betas)
+    out = np.zeros((nb, int(per_beta), model.n_spins), np.int8)
+    for c0 in range(0, nb, 256):
+        bs = betas[c0:c0 + 256]
+        R = len(bs)
+        cs = [derive_state(seed, [0x44, c0 + r]) for r in range(R)]
+        ens = Ensemble(model, 0.5 + np.arange(R, dtype=np.float64), 1, 0, 0, order="reference")
+        ens.set_betas(bs, allow_flat=2)
+        ens.init_from_streams(np.array([[derive_state(c, [0x11, 0x44]) for c in cs]], np.uint64))
+        ens.set_streams(np.array([[derive_state(c, [0x44]) for c in cs]], np.uint64))
+        if mixing_sweeps:
+            ens.run(int(mixing_sweeps), swap_every=0)
+        for k in range(int(per_beta)):
+            ens.run(int(thinning), swap_every=0)
+            out[c0:c0 + R, k] = ens.spins()[0]
+        ens.close()
+    return np.repeat(betas, int(per_beta)), out.reshape(nb * int(per_beta), model.n_spins)

@@ -925,12 +925,43 @@ tapt_status tapt_ensemble_set_betas(tapt_ensemble_t e, const double* betas, int 
         check_ens(e);
         for (int r = 0; r < e->R; ++r) {
             if (!(betas[r] >= 0.0) || !std::isfinite(betas[r])) throw tapt::ConfigError("beta must be >= 0");
-            if (r && !(betas[r] > betas[r - 1]) && !(allow_flat && betas[r] >= betas[r - 1]))
+            if (r && !(betas[r] > betas[r - 1]) && !(allow_flat == 1 && betas[r] >= betas[r - 1]) && allow_flat != 2)
                 throw tapt::ConfigError("beta ladder must be strictly increasing (SPEC.md:388)");
         }
         CUDA_OK(cudaStreamSynchronize(e->stream));
         e->betas.assign(betas, betas + e->R);
         e->build_tables();
+        sync_if(e->stream);
+    });
+}
+
+tapt_status tapt_ensemble_set_streams(tapt_ensemble_t e, const uint64_t* states) {
+    return guard([&] {
+        check_ens(e);
+        if (!states) throw tapt::ConfigError("null stream states");
+        e->streams.upload(states, (size_t)e->I * e->R, e->stream);
+        sync_if(e->stream);
+    });
+}
+
+tapt_status tapt_ensemble_init_from_streams(tapt_ensemble_t e, const uint64_t* init_states) {
+    return guard([&] {
+        check_ens(e);
+        if (!init_states) throw tapt::ConfigError("null stream states");
+        DevBuf<uint64_t> ds;
+        ds.upload(init_states, (size_t)e->I * e->R, e->stream);
+        std::vector<uint8_t> perm((size_t)e->I * e->R);
+        for (uint32_t i = 0; i < e->I; ++i)
+            for (int r = 0; r < e->R; ++r) perm[(size_t)i * e->R + r] = (uint8_t)r;
+        e->slot_of.upload(perm, e->stream);
+        e->buf_of.upload(perm, e->stream);
+        const int n = e->n();
+        ++g_launches;
+        k_init_random<<<dim3((n + 255) / 256, e->G, e->I), 256, 0, e->stream>>>(e->words.p, n, e->G, e->W, e->R, ds.p,
+                                                                                e->clamp_ptr(), e->clamp_count());
+        CUDA_OK(cudaGetLastError());
+        e->recompute_energies();
+        e->update_best_from_E();
         sync_if(e->stream);
     });
 }

@@ -86,6 +86,18 @@ def pt_fixture(tag, graphs, betas, seed, gid0, n_sweeps, swap_every, prop_every,
                         E=E, swap_acc=sacc, prop_acc=pacc)
 
 
+def corpus_fixture(tag, g: O.Graph, betas, per_beta, mixing, thinning, seed):
+    """Reference generate_training_corpus (mcmc.cpp:67-84) records."""
+    rg = ref_graph(g)
+    b = np.ascontiguousarray(betas, np.float64)
+    out = np.zeros((len(b) * per_beta, g.n), np.int8)
+    R().ref_generate_corpus(rg, O._p(b, O._f64p), len(b), per_beta, mixing, thinning, seed, O._p(out, O._i8p))
+    R().ref_graph_free(rg)
+    np.savez_compressed(os.path.join(HERE, f"corpus_{tag}.npz"), betas=b, per_beta=np.int64(per_beta),
+                        mixing=np.int64(mixing), thinning=np.int64(thinning), seed=np.uint64(seed),
+                        spins=pack(out.reshape(-1)), shape=np.array(out.shape))
+
+
 def main():
     if not O.have_ref():
         raise SystemExit("build oracle/_ref first: make -C oracle all")
@@ -113,6 +125,10 @@ def main():
     gs = [O.ea_graph((6,), 3, k) for k in range(2)]
     betas3 = np.linspace(0.2, 3.0, 12)
     pt_fixture("ea3d6_tapt", gs, betas3, 31, 0, 90, 1, 30, 8, np.zeros(12), 5)
+    # training corpus (run_chain per beta) on a clamped 8x8 open lattice
+    cl = np.zeros(64, np.int8)
+    cl[:8] = [1, 1, -1, -1, 1, -1, 1, -1]
+    corpus_fixture("2d8clamped", O.lattice_graph((8, 8), 1.0, False, cl), [0.2, 0.44, 0.7, 1.5], 3, 20, 5, 99)
     print("golden fixtures written to", HERE)
 
 

@@ -514,3 +514,18 @@ def test_estimate_ground_energy_ferromagnet_and_small_glass():
     best = T.estimate_ground_energy(mg, restarts=8, sweeps=1000, seed=2)
     assert best[0] == E.min()
     del g
+
+
+# ------------------------------------------------------- training corpus (mcmc.cpp:67-84) --
+
+def test_generate_training_corpus_matches_reference_golden():
+    f = np.load(os.path.join(GOLD, "corpus_2d8clamped.npz"))
+    cl = np.zeros(64, np.int8)
+    cl[:8] = [1, 1, -1, -1, 1, -1, 1, -1]
+    g = O.lattice_graph((8, 8), 1.0, False, cl)
+    m = T.Model.graph(g.n, g.ci, g.cj, g.J, None, cl)
+    b, S = T.generate_training_corpus(m, f["betas"], int(f["per_beta"]), int(f["mixing"]), int(f["thinning"]),
+                                      int(f["seed"]))
+    shape = tuple(int(x) for x in f["shape"])
+    assert np.array_equal(S, unpack(f["spins"], shape[0] * shape[1]).reshape(shape))
+    assert np.array_equal(b, np.repeat(f["betas"], int(f["per_beta"])))
