@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cstring>
+#include <memory>
 #include <iosfwd>
 #include <istream>
 #include <ostream>
@@ -127,20 +128,52 @@ inline SampleDataset run_chain(const CouplingGraph& g, const ChainConfig& config
 }
 
 // generate_training_corpus (mcmc.cpp:67-84): per beta a chain seeded by
-// derive(seed,{kChain, index}).state(); records concatenated in beta order.
+// derive(seed,{kChain, index}).state(); records concatenated in beta order.  All chains run
+// together as the slots of one device ensemble (index-ascending sweeps, per-slot streams
+// overridden to run_chain's), so the corpus is bit-identical to the reference's.
 inline SampleDataset generate_training_corpus(const CouplingGraph& g, const std::vector<double>& betas,
                                               std::uint64_t per_beta, const ChainConfig& config,
                                               unsigned /*n_threads: the device replaces the thread pool*/ = 1) {
     check_chain_config(config);
+    for (double b : betas)
+        if (b < 0.0) throw ConfigError("beta must be >= 0");
     SampleDataset out;
     out.graph_digest = g.digest();
-    for (std::size_t bi = 0; bi < betas.size(); ++bi) {
-        ChainConfig c = config;
-        c.beta = betas[bi];
-        c.seed = RngStream::derive(config.seed, {stream::kChain, bi}).state();
-        auto part = run_chain(g, c, per_beta);
-        for (auto& r : part.records) out.records.push_back(std::move(r));
+    const std::size_t n = g.n_spins();
+    std::vector<std::vector<SpinConfiguration>> rec(betas.size());
+    for (std::size_t c0 = 0; c0 < betas.size(); c0 += 256) {
+        const std::size_t R = std::min<std::size_t>(256, betas.size() - c0);
+        std::vector<double> dummy(R), bs(betas.begin() + c0, betas.begin() + c0 + R);
+        for (std::size_t r = 0; r < R; ++r) dummy[r] = 0.5 + double(r);
+        tapt_ensemble_desc d{1, 0, static_cast<std::uint32_t>(R), dummy.data(), 0, TAPT_ORDER_REFERENCE};
+        tapt_ensemble_t e = nullptr;
+        throw_status(tapt_ensemble_create(g.device(), &d, &e));
+        std::unique_ptr<tapt_ensemble_s, tapt_status (*)(tapt_ensemble_t)> hold(e, tapt_ensemble_destroy);
+        throw_status(tapt_ensemble_set_betas(e, bs.data(), 2));
+        std::vector<std::uint64_t> init(R), dyn(R);
+        for (std::size_t r = 0; r < R; ++r) {
+            const std::uint64_t cs = RngStream::derive(config.seed, {stream::kChain, c0 + r}).state();
+            init[r] = RngStream::derive(cs, {stream::kInit, stream::kChain}).state();
+            dyn[r] = RngStream::derive(cs, {stream::kChain}).state();
+        }
+        throw_status(tapt_ensemble_init_from_streams(e, init.data()));
+        throw_status(tapt_ensemble_set_streams(e, dyn.data()));
+        tapt_schedule sch{0, 0, 0, 0};
+        if (config.mixing_sweeps) {
+            sch.n_sweeps = static_cast<std::uint32_t>(config.mixing_sweeps);
+            throw_status(tapt_run(e, &sch));
+        }
+        std::vector<std::int8_t> flat(R * n);
+        for (std::uint64_t k = 0; k < per_beta; ++k) {
+            sch.n_sweeps = static_cast<std::uint32_t>(config.thinning);
+            throw_status(tapt_run(e, &sch));
+            throw_status(tapt_ensemble_get_spins(e, flat.data()));
+            for (std::size_t r = 0; r < R; ++r)
+                rec[c0 + r].emplace_back(flat.begin() + r * n, flat.begin() + (r + 1) * n);
+        }
     }
+    for (std::size_t bi = 0; bi < betas.size(); ++bi)
+        for (auto& s : rec[bi]) out.records.push_back({betas[bi], std::move(s)});
     return out;
 }
 
