@@ -158,6 +158,23 @@ static int gpu_tests() {
     CHECK(ds.records.size() == 4 && ds.graph_digest == g.digest());
     auto ds2 = run_chain(g, cc, 4);
     for (int k = 0; k < 4; ++k) CHECK(ds.records[k].spins == ds2.records[k].spins);
+    // batched corpus == per-beta run_chain (mcmc.cpp:67-84 semantics, two device paths)
+    {
+        ChainConfig c2;
+        c2.mixing_sweeps = 5;
+        c2.thinning = 3;
+        c2.seed = 11;
+        std::vector<double> bs{0.3, 0.9, 0.5};
+        auto corpus = generate_training_corpus(g, bs, 2, c2);
+        CHECK(corpus.records.size() == 6);
+        for (std::size_t bi = 0; bi < bs.size(); ++bi) {
+            ChainConfig c = c2;
+            c.beta = bs[bi];
+            c.seed = RngStream::derive(c2.seed, {stream::kChain, bi}).state();
+            auto one = run_chain(g, c, 2);
+            for (int k = 0; k < 2; ++k) CHECK(one.records[k].spins == corpus.records[bi * 2 + k].spins);
+        }
+    }
     // run_pt / run_tapt move audit and best-energy monotonicity
     auto ladder = BetaLadder::geometric(0.2, 1.0, 8);
     TAPTConfig cfg;

@@ -16,7 +16,9 @@ def binary():
     os.makedirs(os.path.dirname(BIN), exist_ok=True)
     if not os.path.exists(os.path.join(LIBDIR, "libtapt_b200.so")):
         subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "paper_2509_23043_b200", "csrc")], check=True)
-    if not os.path.exists(BIN) or os.path.getmtime(BIN) < os.path.getmtime(src):
+    deps = [src] + [os.path.join(ROOT, "include", "tapt", f) for f in os.listdir(os.path.join(ROOT, "include", "tapt"))]
+    deps.append(os.path.join(ROOT, "include", "tapt_gpu.h"))
+    if not os.path.exists(BIN) or os.path.getmtime(BIN) < max(os.path.getmtime(d) for d in deps):
         subprocess.run(["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), src, "-L", LIBDIR,
                         "-ltapt_b200", f"-Wl,-rpath,{LIBDIR}", "-o", BIN], check=True)
     return BIN
