@@ -89,6 +89,37 @@ __device__ __forceinline__ uint32_t mix_pre_hi(uint32_t zl, uint32_t zh, const M
     return __umulhi(zl, B_LO) + zh * B_LO + zl * B_HI;
 }
 
+// K independent chains of mix_pre_hi, written stage by stage so the instruction stream
+// interleaves the chains (ptxas otherwise tends to emit one dependent chain at a time).
+template <int K>
+__device__ __forceinline__ void mix_pre_hi_k(const uint32_t (&zl0)[K], const uint32_t (&zh0)[K], uint32_t (&out)[K]) {
+    constexpr uint32_t A_LO = (uint32_t)kM1, A_HI = (uint32_t)(kM1 >> 32);
+    constexpr uint32_t B_LO = (uint32_t)kM2, B_HI = (uint32_t)(kM2 >> 32);
+    uint32_t zl[K], zh[K], t[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) asm("shf.r.clamp.b32 %0, %1, %2, 30;" : "=r"(t[c]) : "r"(zl0[c]), "r"(zh0[c]));
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        zl[c] = zl0[c] ^ t[c];
+        zh[c] = zh0[c] ^ (zh0[c] >> 30);
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        const uint64_t w = (uint64_t)zl[c] * A_LO;
+        zh[c] = zh[c] * A_LO + zl[c] * A_HI + (uint32_t)(w >> 32);
+        zl[c] = (uint32_t)w;
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) asm("shf.r.clamp.b32 %0, %1, %2, 27;" : "=r"(t[c]) : "r"(zl[c]), "r"(zh[c]));
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+        zl[c] ^= t[c];
+        zh[c] ^= zh[c] >> 27;
+    }
+#pragma unroll
+    for (int c = 0; c < K; ++c) out[c] = __umulhi(zl[c], B_LO) + zh[c] * B_LO + zl[c] * B_HI;
+}
+
 // Heat-bath decision on h = mix_pre_hi(z) against U = thr_hi(T):  the final xor-shift
 // of mix_final only flips bit 0 of the high word, so whenever |h - U| >= 2 the decision
 // equals (h < U).  Shifts NOT(up) into w (w = 2w + [h >= U]) via the carry of h - U and

@@ -861,6 +861,9 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
             int nt = std::max(32, std::min(TAPT_K1_DEFAULT_THREADS, n / 4));
             if (const char* env = std::getenv("TAPT_K1_THREADS")) nt = std::max(32, std::min(1024, std::atoi(env)));
             nt = (nt / 32) * 32;
+            // the per-thread bit-sliced counters hold < 256: unsatisfied bonds of this thread's
+            // colour-1 sites (2*dim each) and up-spins of its share of all sites
+            while (nt < 1024 && ((n / 2 + nt - 1) / nt * 2 * m->dim >= 256 || (n + nt - 1) / nt >= 256)) nt *= 2;
             e->k1_threads = nt;
             if (k1_smem_bytes(n, true) > 227 * 1024) throw tapt::SizeError("lattice too large for shared memory");
         } else {

@@ -151,6 +151,43 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
     constexpr int U = NV ? NV : 1;
     const int cnt = NV ? NV : nv;
     uint32_t tmin = 0xFFFFFFFFu;
+    if constexpr (NV == kW && (V & 16) != 0) {
+        // two replicas (b, b-1) x SP sites per step: 2*SP chains interleaved stage by stage
+#pragma unroll
+        for (int b = kW - 1; b >= 1; b -= 2) {
+            constexpr int K = 2 * SP;
+            uint32_t zl[K], zh[K], h[K], thr[K];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int bb = b - e;
+                const uint64_t base = sm.S.sb[bb];
+                const int m = bb & 3, sh = 4 * (bb >> 2);
+#pragma unroll
+                for (int u = 0; u < SP; ++u) {
+                    const uint64_t z = base + ph[u];
+                    zl[e * SP + u] = (uint32_t)z;
+                    zh[e * SP + u] = (uint32_t)(z >> 32);
+                    if constexpr ((V & 8) != 0) {
+                        const uint32_t ix = (sh >= 4 ? __umulhi(N[u][m], mc.nib[sh >> 2]) : (N[u][m] << 2)) & 0x1Cu;
+                        thr[e * SP + u] =
+                            *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(&sm.Uhi[bb][0]) + ix);
+                    } else {
+                        thr[e * SP + u] = sm.Uhi[bb][(N[u][m] >> sh) & 7u];
+                    }
+                }
+            }
+            mix_pre_hi_k<K>(zl, zh, h);
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+#pragma unroll
+                for (int u = 0; u < SP; ++u) {
+                    const uint32_t dd = decide_acc(h[e * SP + u], thr[e * SP + u], w[u]);
+                    tmin = min(tmin, dd + 1u);
+                }
+        }
+        tie |= tmin <= 2u;
+        return;
+    }
 #pragma unroll U
     for (int b = cnt - 1; b >= 0; --b) {
         const uint64_t base = sm.S.sb[b];
@@ -247,18 +284,25 @@ __global__ void __launch_bounds__(SP == 1 ? 1024 : (SP == 2 ? 512 : 256), 1) k1_
             const int c = cc > 1 ? 1 : cc;
             const bool decide = !a.energy_only && cc < 2;
             const bool count = TAPT_K1_EPOST ? (cc == 2) : (c == 1);
-            for (int j = tid; j < nsub; j += nt) {
-                // site u of this iteration: colour index j + u*nsub (a warp's lanes cover
-                // consecutive colour indices, so each shared load stays conflict-free)
-                int is[SP];
-                uint32_t q[SP][3], N[SP][4];
+            // Software-pipelined over this thread's site pairs: the neighbour sums of the next
+            // pair (other-colour words, not written during this half) are formed before the
+            // decisions of the current pair, hiding the shared-memory latency of the stencil.
+            int is[SP];
+            uint32_t q[SP][3], N[SP][4];
+            auto stencil = [&](int jj, int (&is_)[SP], uint32_t (&q_)[SP][3], uint32_t (&N_)[SP][4]) {
 #pragma unroll
                 for (int u = 0; u < SP; ++u) {
                     int x, y, z;
-                    is[u] = colour_site<DIM>(j + u * nsub, c, d, x, y, z);
-                    k1_stencil<DIM, DIS>(words, bonds, is[u], x, y, z, d, q[u][0], q[u][1], q[u][2]);
-                    nibbles(q[u][0], q[u][1], q[u][2], N[u]);
+                    is_[u] = colour_site<DIM>(jj + u * nsub, c, d, x, y, z);
+                    k1_stencil<DIM, DIS>(words, bonds, is_[u], x, y, z, d, q_[u][0], q_[u][1], q_[u][2]);
+                    nibbles(q_[u][0], q_[u][1], q_[u][2], N_[u]);
                 }
+            };
+            if (tid < nsub) stencil(tid, is, q, N);
+            for (int j = tid; j < nsub; j += nt) {
+                int isn[SP];
+                uint32_t qn[SP][3], Nn[SP][4];
+                if (TAPT_K1_PIPE && j + nt < nsub) stencil(j + nt, isn, qn, Nn);
                 uint32_t nw[SP];
                 if (!decide) {
 #pragma unroll
@@ -291,6 +335,17 @@ __global__ void __launch_bounds__(SP == 1 ? 1024 : (SP == 2 ? 512 : 256), 1) k1_
                         uint32_t v0, v1, v2;
                         unsat_planes<DIM>(nw[u], q[u][0], q[u][1], q[u][2], v0, v1, v2);
                         sliced_add3<kCnt>(C, v0, v1, v2);
+                    }
+                }
+                if (j + nt < nsub) {
+                    if (!TAPT_K1_PIPE) stencil(j + nt, isn, qn, Nn);
+#pragma unroll
+                    for (int u = 0; u < SP; ++u) {
+                        is[u] = isn[u];
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) q[u][k] = qn[u][k];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) N[u][k] = Nn[u][k];
                     }
                 }
             }
@@ -411,6 +466,7 @@ cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint3
         TAPT_PROBE_CASE(4) TAPT_PROBE_CASE(5) TAPT_PROBE_CASE(6) TAPT_PROBE_CASE(7)
         TAPT_PROBE_CASE(8) TAPT_PROBE_CASE(9) TAPT_PROBE_CASE(10) TAPT_PROBE_CASE(11)
         TAPT_PROBE_CASE(12) TAPT_PROBE_CASE(13) TAPT_PROBE_CASE(14) TAPT_PROBE_CASE(15)
+        TAPT_PROBE_CASE(28)
 #undef TAPT_PROBE_CASE
         default: return cudaErrorInvalidValue;
     }

@@ -18,6 +18,9 @@ namespace tapt_dev {
 constexpr int kMaxR = 256;   // ladder slots per instance (uint8 permutation)
 constexpr int kW = 32;       // replicas per group (bits per word)
 constexpr int kCnt = 8;      // planes of the sliced per-thread counters
+#ifndef TAPT_K1_PIPE
+#define TAPT_K1_PIPE 0       // 1: software-pipeline the stencil of the next site pair
+#endif
 #ifndef TAPT_K1_EPOST
 #define TAPT_K1_EPOST 0      // 1: energies in a separate pass after the two colour halves
 #endif
