@@ -529,3 +529,72 @@ def test_generate_training_corpus_matches_reference_golden():
     shape = tuple(int(x) for x in f["shape"])
     assert np.array_equal(S, unpack(f["spins"], shape[0] * shape[1]).reshape(shape))
     assert np.array_equal(b, np.repeat(f["betas"], int(f["per_beta"])))
+
+
+# ------------------------------------------------- proposal-path stationarity --
+
+def _five_spin():
+    ci = [0, 0, 1, 1, 2, 3, 0]
+    cj = [1, 2, 2, 3, 4, 4, 4]
+    J = [1.0, -1.0, 2.0, 1.0, -1.0, 1.0, 1.0]
+    h = [0.0, 1.0, 0.0, -1.0, 0.0]
+    return O.Graph.from_couplings(5, ci, cj, J, h), (ci, cj, J, h)
+
+
+def _boltzmann5(g, beta):
+    import itertools
+    states = np.array(list(itertools.product([-1, 1], repeat=5)), np.int8)
+    E = np.array([O.lib().oc_energy(g.oc(), np.ascontiguousarray(s).ctypes.data_as(O._i8p)) for s in states], float)
+    p = np.exp(-beta * (E - E.min()))
+    return states, p / p.sum()
+
+
+def _run_independence_sampler(mh, bias):
+    """Per round: one Gibbs sweep (preserves Boltzmann, provides mixing) then three proposal
+    rounds into every slot.  With uniform proposals Eq. 2 leaves Boltzmann invariant; with
+    biased i.i.d. proposals only the MH-corrected rule does."""
+    g, (ci, cj, J, h) = _five_spin()
+    m = T.Model.graph(5, ci, cj, J, h)
+    betas = np.array([0.5, 1.0, 1.5, 2.0])
+    I = 4096
+    e = T.Ensemble(m, betas, n_instances=I, seed=31)
+    e.init_random()
+    rs = np.random.default_rng(7)
+    targets = np.arange(4)
+    w = 1 << np.arange(5)
+    counts = np.zeros((4, 32))
+    for rnd in range(80):
+        e.sweep(1)
+        for _ in range(3):
+            props = np.where(rs.random((I, 4, 5)) < bias, 1, -1).astype(np.int8)
+            if mh:
+                nplus_cur = (e.spins() > 0).sum(axis=2)
+                lq_cur = nplus_cur * np.log(bias) + (5 - nplus_cur) * np.log(1 - bias)
+                nplus = (props > 0).sum(axis=2)
+                lq_prop = nplus * np.log(bias) + (5 - nplus) * np.log(1 - bias)
+                e.inject_proposals(props, targets, lq_cur, lq_prop)
+            else:
+                e.inject_proposals(props, targets)
+        if rnd >= 40:
+            S = e.spins()
+            for r in range(4):
+                np.add.at(counts[r], ((S[:, r, :] > 0) * w).sum(axis=1), 1)
+    tvs = []
+    for r, b in enumerate(betas):
+        states, p = _boltzmann5(g, b)
+        idx = ((states > 0) * w).sum(axis=1)
+        q = np.zeros(32)
+        q[idx] = p
+        tvs.append(0.5 * np.abs(counts[r] / counts[r].sum() - q).sum())
+    return np.array(tvs)
+
+
+def test_uniform_proposals_keep_boltzmann():
+    assert _run_independence_sampler(False, 0.5).max() < 0.02
+
+
+def test_mh_correction_removes_generator_bias():
+    corrected = _run_independence_sampler(True, 0.8)
+    biased = _run_independence_sampler(False, 0.8)
+    assert corrected.max() < 0.02
+    assert biased.max() > 2 * corrected.max() and biased.max() > 0.03   # Eq. 2 alone keeps the bias
