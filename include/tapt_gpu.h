@@ -94,6 +94,10 @@ tapt_status tapt_model_create_lattice(int dim, int ly, int lx, int lz, double J,
 tapt_status tapt_model_create_graph(uint32_t n, uint32_t n_couplings, const uint32_t* ci, const uint32_t* cj,
                                     const double* J, const double* h, const int8_t* clamp, tapt_model_t* out);
 tapt_status tapt_model_destroy(tapt_model_t m);
+/* CouplingGraph::load_file / save_file: the `isingmodel v1` text format (spin_model.cpp:123-226);
+ * parse errors -> TAPT_ERR_FORMAT, invalid records -> TAPT_ERR_CONFIG, as the reference throws. */
+tapt_status tapt_model_load_file(const char* path, tapt_model_t* out);
+tapt_status tapt_model_save_file(tapt_model_t m, const char* path);
 tapt_status tapt_model_info(tapt_model_t m, uint32_t* n_spins, uint32_t* n_free, uint32_t* n_couplings,
                             int32_t* lmin, int32_t* lmax, uint32_t* n_colours, uint32_t* n_levels);
 /* Couplings after merging/sorting (CouplingGraph::couplings(), spin_model.hpp:57). */

@@ -98,6 +98,8 @@ _SIGS = {
     "tapt_model_create_lattice": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(_vp)]),
     "tapt_model_create_graph": (C.c_int, [C.c_uint32, C.c_uint32, _u32p, _u32p, _f64p, _f64p, _i8p, C.POINTER(_vp)]),
     "tapt_model_destroy": (C.c_int, [_vp]),
+    "tapt_model_load_file": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "tapt_model_save_file": (C.c_int, [_vp, C.c_char_p]),
     "tapt_model_info": (C.c_int, [_vp, _u32p, _u32p, _u32p, _i32p, _i32p, _u32p, _u32p]),
     "tapt_model_couplings": (C.c_int, [_vp, _u32p, _u32p, _f64p]),
     "tapt_model_schedule": (C.c_int, [_vp, _i32p, _i32p]),
@@ -238,6 +240,16 @@ class Model:
         _check(lib().tapt_model_create_graph(int(n), len(ci), _p(ci, _u32p), _p(cj, _u32p), _p(J, _f64p),
                                              _p(hh, _f64p), _p(cl, _i8p), C.byref(hdl)))
         return cls(hdl, "graph")
+
+    @classmethod
+    def load_file(cls, path):
+        """CouplingGraph::load_file (`isingmodel v1`)."""
+        hdl = _vp()
+        _check(lib().tapt_model_load_file(os.fsencode(path), C.byref(hdl)))
+        return cls(hdl, "graph")
+
+    def save_file(self, path):
+        _check(lib().tapt_model_save_file(self._h, os.fsencode(path)))
 
     def couplings(self):
         m = self.n_couplings

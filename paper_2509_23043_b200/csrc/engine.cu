@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "tapt/spin_model.hpp"
 
 #ifndef TAPT_K1_DEFAULT_THREADS
 #define TAPT_K1_DEFAULT_THREADS 512
@@ -764,6 +765,40 @@ tapt_status tapt_model_create_graph(uint32_t n, uint32_t nc, const uint32_t* ci,
         std::vector<double> v(J, J + nc);
         build_model(*m, n, a, b, v, h, clamp);
         *out = m.release();
+    });
+}
+
+// `isingmodel v1` text files (spin_model.cpp:123-226 format and errors).
+tapt_status tapt_model_load_file(const char* path, tapt_model_t* out) {
+    return guard([&] {
+        if (!path || !out) throw tapt::ConfigError("null path / output");
+        const tapt::CouplingGraph g = tapt::CouplingGraph::load_file(path);
+        std::vector<uint32_t> ci, cj;
+        std::vector<double> J;
+        for (const auto& c : g.couplings()) {
+            ci.push_back(c.i);
+            cj.push_back(c.j);
+            J.push_back(c.value);
+        }
+        std::vector<int8_t> cl(g.n_spins());
+        for (uint32_t i = 0; i < g.n_spins(); ++i) cl[i] = g.clamp_value(i);
+        auto m = std::make_unique<tapt_model_s>();
+        build_model(*m, (uint32_t)g.n_spins(), ci, cj, J, g.fields().data(), cl.data());
+        *out = m.release();
+    });
+}
+
+tapt_status tapt_model_save_file(tapt_model_t m, const char* path) {
+    return guard([&] {
+        check_model(m);
+        if (!path) throw tapt::ConfigError("null path");
+        tapt::CouplingGraph::Builder b(m->n);
+        for (size_t k = 0; k < m->ci.size(); ++k) b.add_coupling(m->ci[k], m->cj[k], m->J[k]);
+        for (uint32_t i = 0; i < m->n; ++i) {
+            if (m->h[i] != 0.0) b.add_field(i, m->h[i]);
+            if (m->clamp[i]) b.set_clamp(i, m->clamp[i]);
+        }
+        b.build().save_file(path);
     });
 }
 

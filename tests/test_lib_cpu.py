@@ -128,3 +128,33 @@ def test_ensemble_argument_validation():
         T.Ensemble(m, [0.5, 0.4])        # ladder must increase
     with pytest.raises(T.ConfigError):
         T.Ensemble(m, [-0.1, 0.4])       # beta >= 0
+
+
+def test_isingmodel_v1_round_trip_and_errors(tmp_path):
+    """CouplingGraph save/load (spin_model.cpp:123-226) through the C ABI, incl. the
+    reference's parse errors (test_spin_model.cpp:189-233)."""
+    M = T.Multiplier(4)
+    m = M.model()
+    p = tmp_path / "mult.ising"
+    m.save_file(str(p))
+    text = p.read_text()
+    assert text.startswith("isingmodel v1\nn 52\n")
+    m2 = T.Model.load_file(str(p))
+    assert m2.digest() == m.digest()
+    assert all(np.array_equal(a, b) for a, b in zip(m.couplings(), m2.couplings()))
+    bad = tmp_path / "bad.ising"
+    for body, err in (("isingmodel v2\nn 2\n", T.FormatError), ("isingmodel v1\nc 0 1 1\n", T.FormatError),
+                      ("isingmodel v1\nn 3\nc 0 1 1\nc 1 0 2\n", T.FormatError),
+                      ("isingmodel v1\nn 2\nq 1\n", T.FormatError), ("isingmodel v1\nn 2\nc 0 0 1\n", T.ConfigError),
+                      ("isingmodel v1\nn 2\nx 0 2\n", T.FormatError)):
+        bad.write_text(body)
+        with pytest.raises(err):
+            T.Model.load_file(str(bad))
+    if O.have_ref():
+        import ctypes as C
+        # the reference loader reads our file to the same graph (digest)
+        g = O.Graph.from_couplings(52, M.ci, M.cj, M.J, M.h, M.clamp)
+        rg = O.ref_graph(g)
+        assert O.ref().ref_graph_digest(rg) == m.digest()
+        O.ref().ref_graph_free(rg)
+        del C
