@@ -598,3 +598,29 @@ def test_mh_correction_removes_generator_bias():
     biased = _run_independence_sampler(False, 0.8)
     assert corrected.max() < 0.02
     assert biased.max() > 2 * corrected.max() and biased.max() > 0.03   # Eq. 2 alone keeps the bias
+
+
+@pytest.mark.parametrize("kernel", ["lattice", "csr"])
+def test_tapt_rounds_with_two_proposal_groups(kernel):
+    """56 targets (two 32-replica proposal groups, as in the config-5 bench) on a 64-slot ladder."""
+    R, L = 64, 8
+    betas = H.linear(0.2, 3.0, R)
+    if kernel == "lattice":
+        m = T.Model.lattice((L,))
+    else:
+        g0 = O.lattice_graph((L,))
+        m = T.Model.graph(g0.n, g0.ci, g0.cj, g0.J)
+    e = T.Ensemble(m, betas, n_instances=2, seed=12, instance_offset=3)
+    assert e.kernel == kernel
+    if kernel == "lattice":
+        e.generate_ea_disorder(9)
+        graphs = [O.ea_graph((L,), 9, 3 + k) for k in range(2)]
+    else:
+        graphs = [O.lattice_graph((L,))] * 2
+    e.init_random()
+    for _ in range(3):
+        e.run(15, swap_every=1)
+        e.generate_proposals(np.arange(56), None, refine=5)
+    order = H.checkerboard_order((L,)) if kernel == "lattice" else H.colour_order_for(m.schedule()[0])
+    pts = H.run_oracle(graphs, betas, 12, 3, order, 45, props=dict(every=15, targets=56, m_bias=np.zeros(R), refine=5))
+    compare(e, pts)
