@@ -85,6 +85,12 @@ inline double gibbs_sweeps(const CouplingGraph& g, SpinConfiguration& s, double 
     if (s.size() != g.n_spins()) throw DimensionError("configuration length mismatch");
     if (n_sweeps == 0 || g.n_free() == 0) return 0.0;
     std::uint64_t st = rng.state();
+    if (!per_sweep && n_sweeps > 1) {  // one device launch for all sweeps; total from the energies
+        const double e0 = energy(g, s);
+        throw_status(tapt_gibbs_sweep(g.device(), s.data(), s.size(), beta, &st, n_sweeps, nullptr));
+        rng = RngStream::from_state(st);
+        return energy(g, s) - e0;
+    }
     std::vector<double> d(n_sweeps);
     throw_status(tapt_gibbs_sweep(g.device(), s.data(), s.size(), beta, &st, n_sweeps, d.data()));
     rng = RngStream::from_state(st);

@@ -247,6 +247,10 @@ struct DevMetro {
 // =================================================================== model ===
 
 struct tapt_model_s {
+    // single-replica ensemble reused by the drop-in tapt_gibbs_sweep (created lazily)
+    tapt_ensemble_t dropin = nullptr;
+    std::mutex dropin_mu;
+    ~tapt_model_s();
     uint32_t n = 0;
     std::vector<uint32_t> ci, cj;  // merged, sorted (i<j)
     std::vector<double> J;
@@ -805,6 +809,14 @@ tapt_status tapt_model_save_file(tapt_model_t m, const char* path) {
 tapt_status tapt_model_destroy(tapt_model_t m) {
     return guard([&] { delete m; });
 }
+
+}  // extern "C"
+
+tapt_model_s::~tapt_model_s() {
+    if (dropin) tapt_ensemble_destroy(dropin);
+}
+
+extern "C" {
 
 tapt_status tapt_model_info(tapt_model_t m, uint32_t* n_spins, uint32_t* n_free, uint32_t* n_couplings, int32_t* lmin,
                             int32_t* lmax, uint32_t* n_colours, uint32_t* n_levels) {
@@ -1543,27 +1555,37 @@ tapt_status tapt_gibbs_sweep(tapt_model_t m, int8_t* s, size_t len, double beta,
         if (!(beta >= 0.0)) throw tapt::ConfigError("beta must be >= 0");
         if (!rng_state) throw tapt::ConfigError("null rng state");
         if (n_sweeps == 0) return;
-        tapt_ensemble_desc d{};
-        d.n_instances = 1;
-        d.n_slots = 1;
-        d.betas = &beta;
-        d.seed = 0;
-        d.order = TAPT_ORDER_REFERENCE;
-        tapt_ensemble_t e = nullptr;
-        if (tapt_ensemble_create(m, &d, &e) != TAPT_OK) throw tapt::CudaError(g_last_error);
-        std::unique_ptr<tapt_ensemble_s, tapt_status (*)(tapt_ensemble_t)> hold(e, tapt_ensemble_destroy);
+        std::lock_guard<std::mutex> lock(m->dropin_mu);
+        if (!m->dropin) {
+            tapt_ensemble_desc d{};
+            d.n_instances = 1;
+            d.n_slots = 1;
+            d.betas = &beta;
+            d.seed = 0;
+            d.order = TAPT_ORDER_REFERENCE;
+            if (tapt_ensemble_create(m, &d, &m->dropin) != TAPT_OK) throw tapt::CudaError(g_last_error);
+        } else if (m->dropin->betas[0] != beta) {
+            if (tapt_ensemble_set_betas(m->dropin, &beta, 0) != TAPT_OK) throw tapt::ConfigError(g_last_error);
+        }
+        tapt_ensemble_t e = m->dropin;
+        e->T = 0;  // draws are addressed from the caller's stream state
+        e->P = 0;
         const uint64_t st = *rng_state;
         e->streams.upload(&st, 1, e->stream);
         // gibbs_sweep never writes clamped sites and reads whatever they hold (mcmc.cpp:34-37)
         set_spins_impl(e, s, false);
         int64_t e0 = 0;
         tapt_ensemble_get_energies(e, &e0);
-        for (uint32_t k = 0; k < n_sweeps; ++k) {
-            e->run(1, 0, 0, 0);
-            int64_t e1 = 0;
-            if (tapt_ensemble_get_energies(e, &e1) != TAPT_OK) throw tapt::CudaError(g_last_error);
-            if (dE) dE[k] = (double)(e1 - e0);
-            e0 = e1;
+        if (dE) {
+            for (uint32_t k = 0; k < n_sweeps; ++k) {
+                e->run(1, 0, 0, 0);
+                int64_t e1 = 0;
+                if (tapt_ensemble_get_energies(e, &e1) != TAPT_OK) throw tapt::CudaError(g_last_error);
+                dE[k] = (double)(e1 - e0);
+                e0 = e1;
+            }
+        } else {
+            e->run(n_sweeps, 0, 0, 0);
         }
         if (tapt_ensemble_get_spins(e, s) != TAPT_OK) throw tapt::CudaError(g_last_error);
         *rng_state = st + (uint64_t)n_sweeps * (uint64_t)m->free_sites.size() * tapt_dev::kPhi;
