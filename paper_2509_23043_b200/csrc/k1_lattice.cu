@@ -45,6 +45,23 @@ __device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const
                                            int x, int y, int z, const LatDims& d, uint32_t& q0, uint32_t& q1,
                                            uint32_t& q2) {
     const int Lx = 1 << d.log2Lx, Ly = 1 << d.log2Ly;
+#if TAPT_K1_IDX2
+    // periodic neighbours by masked add on the packed index (power-of-two extents)
+    const int mx = Lx - 1, my = (Ly - 1) << d.log2Lx;
+    uint32_t p0 = w[(i & ~mx) | ((i + 1) & mx)];
+    uint32_t p1 = w[(i & ~mx) | ((i - 1) & mx)];
+    uint32_t p2 = w[(i & ~my) | ((i + Lx) & my)];
+    uint32_t p3 = w[(i & ~my) | ((i - Lx) & my)];
+    uint32_t p4 = 0, p5 = 0;
+    if constexpr (DIM == 3) {
+        const int P = Lx * Ly, mz = (Ly - 1) << (d.log2Lx + d.log2Ly);
+        p4 = w[(i & ~mz) | ((i + P) & mz)];
+        p5 = w[(i & ~mz) | ((i - P) & mz)];
+    }
+    (void)x;
+    (void)y;
+    (void)z;
+#else
     const int rowb = i - x;
     uint32_t p0 = w[rowb + ((x + 1) & (Lx - 1))];
     uint32_t p1 = w[rowb + ((x - 1) & (Lx - 1))];
@@ -60,6 +77,7 @@ __device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const
         p4 = w[kp];
         p5 = w[km];
     }
+#endif
     if constexpr (DIS) {
         const uint32_t bb = bonds[i];  // bit d set: bond in direction d has J = -J0
         p0 ^= 0u - (bb & 1u);
@@ -107,8 +125,18 @@ __device__ __forceinline__ void unsat_planes(uint32_t s, uint32_t q0, uint32_t q
     u2 = (s & r2) | (~s & q2);
 }
 
-// Nibble spread: nibble k of N[m] = q of replica 4k+m.
+// Nibble spread: bits 0..2 of nibble k of N[m] = q of replica 4k+m (bit 3 is don't-care:
+// every reader masks with 7).  Pairs (q0,q1) of even / odd replicas are formed first.
 __device__ __forceinline__ void nibbles(uint32_t q0, uint32_t q1, uint32_t q2, uint32_t (&N)[4]) {
+#if TAPT_K1_NIB2
+    const uint32_t e01 = (q0 & 0x55555555u) | ((q1 << 1) & 0xAAAAAAAAu);
+    const uint32_t o01 = ((q0 >> 1) & 0x55555555u) | (q1 & 0xAAAAAAAAu);
+    constexpr uint32_t M = 0x33333333u;
+    N[0] = (e01 & M) | ((q2 << 2) & ~M);
+    N[1] = (o01 & M) | ((q2 << 1) & ~M);
+    N[2] = ((e01 >> 2) & M) | (q2 & ~M);
+    N[3] = ((o01 >> 2) & M) | ((q2 >> 1) & ~M);
+#else
     constexpr uint32_t K1 = 0x11111111u;
 #pragma unroll
     for (int m = 0; m < 4; ++m) {
@@ -117,6 +145,7 @@ __device__ __forceinline__ void nibbles(uint32_t q0, uint32_t q1, uint32_t q2, u
         const uint32_t c = (m >= 2 ? (q2 >> (m - 2)) : (q2 << (2 - m))) & (K1 << 2);
         N[m] = a | b | c;
     }
+#endif
 }
 
 struct K1Smem {
@@ -186,8 +215,7 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
                 }
         }
         tie |= tmin <= 2u;
-        return;
-    }
+    } else {
 #pragma unroll U
     for (int b = cnt - 1; b >= 0; --b) {
         const uint64_t base = sm.S.sb[b];
@@ -211,6 +239,7 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
         }
     }
     if constexpr ((V & 4) != 0) tie |= tmin <= 2u;
+    }
 }
 
 // Kept for the decision-rate probe (two interleaved site words).

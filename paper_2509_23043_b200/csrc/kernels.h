@@ -18,6 +18,12 @@ namespace tapt_dev {
 constexpr int kMaxR = 256;   // ladder slots per instance (uint8 permutation)
 constexpr int kW = 32;       // replicas per group (bits per word)
 constexpr int kCnt = 8;      // planes of the sliced per-thread counters
+#ifndef TAPT_K1_NIB2
+#define TAPT_K1_NIB2 1       // 1: 13-op nibble spread (measured +0.5..1%)
+#endif
+#ifndef TAPT_K1_IDX2
+#define TAPT_K1_IDX2 1       // 1: masked-add periodic neighbour indices
+#endif
 #ifndef TAPT_K1_PIPE
 #define TAPT_K1_PIPE 0       // 1: software-pipeline the stencil of the next site pair
 #endif
