@@ -526,7 +526,7 @@ struct tapt_ensemble_s {
             e = launch_k1(a, m->ld, k1_threads, cluster, stream);
         } else {
             int nt = k2_threads;
-            if (const char* env = std::getenv("TAPT_K2_THREADS")) nt = std::max(128, std::min(1024, std::atoi(env)));
+            if (const char* env = std::getenv("TAPT_K2_THREADS")) nt = std::max(128, std::min(TAPT_K2_MAXT, std::atoi(env)));
             e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), nt, cluster, stream);
         }
         if (e != cudaSuccess) throw tapt::CudaError(std::string("sweep kernel launch: ") + cudaGetErrorString(e));

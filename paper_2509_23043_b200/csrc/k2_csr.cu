@@ -12,7 +12,8 @@
 // Local fields, byte-SWAR over 32 replicas: with the neighbour word v = w_j, negated for
 // J < 0, acc = sum |J| * bit  counts into 8 words x 4 byte lanes (replica 8k+m in byte k
 // of A[m]); then l = h_i - sum|J| + 2*acc exactly, and the threshold table is indexed by
-// l - lmin.  Energies are tracked per replica by exact integer dE = 2*s_old*l on flips.
+// l - lmin.  Decisions use the carry-chain test of K1 (decide_acc).  Energies are tracked per
+// replica by exact integer dE = 2*s_old*l on flips.
 //
 // Work split: four lanes share one site word (lane `sub` owns replicas 8k + 2*sub + {0,1});
 // the neighbour walk is split over the four lanes and reduced with shuffles.  When an
@@ -31,6 +32,12 @@ namespace tapt_dev {
 constexpr int kTPS = 4;  // lanes per site word
 constexpr int kIPB = 4;  // max instances per CTA
 
+__device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t y, uint32_t sel) {
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(y), "r"(sel));
+    return r;
+}
+
 // Shared-memory image of the graph (the whole CSR is staged once per launch when it fits):
 //   rowptr [n+1] u32 | col [nnz] u32 | h [n] i32 | rank [n] u32 | class_sites [n_free] u32 | J [nnz] i8
 __host__ __device__ inline size_t k2_graph_bytes(int n, int nnz, int nfree) {
@@ -48,7 +55,7 @@ struct K2Graph {
 };
 
 template <bool CLU, bool SMEMG>
-__global__ void __launch_bounds__(1024, 1) k2_csr_pt(const PTArgs a, const CsrArgs g, const int ipb) {
+__global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, const CsrArgs g, const int ipb) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ PTShared SS[kIPB];
     const int nidx = a.nidx, n = a.n, W = a.W;
@@ -93,7 +100,6 @@ __global__ void __launch_bounds__(1024, 1) k2_csr_pt(const PTArgs a, const CsrAr
         G = K2Graph{g.rowptr, g.col, Jglob, g.h, g.rank, g.class_sites};
     }
     const int sub = tid & (kTPS - 1), m0 = 2 * sub;
-    const uint32_t gmask = 0xFu << (lane & ~(kTPS - 1));
     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
     const uint32_t mine = (0x03030303u << m0) & vmask;  // replicas of this lane
 
@@ -116,11 +122,11 @@ __global__ void __launch_bounds__(1024, 1) k2_csr_pt(const PTArgs a, const CsrAr
         for (int kin = 0; kin < nin; ++kin) pt_stream_bases(a, SS[kin], inst0 + kin, grp, t);
         __syncthreads();
         // this lane's 8 replicas: threshold-row offsets of their current slots
-        int trow[8];
+        int trl[8];  // slot row - lmin, so that Uslot[trl + l] is the entry of local field l
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int b = 8 * (j >> 1) + m0 + (j & 1);
-            trow[j] = b < nv ? S.slot_of[grp * W + b] * nidx : 0;
+            trl[j] = (b < nv ? S.slot_of[grp * W + b] * nidx : 0) - g.lmin;
         }
         int32_t dE[8];
 #pragma unroll
@@ -128,65 +134,89 @@ __global__ void __launch_bounds__(1024, 1) k2_csr_pt(const PTArgs a, const CsrAr
 
         for (int c = 0; c < g.n_classes; ++c) {
             const uint32_t c0 = g.class_ptr[c], c1 = g.class_ptr[c + 1];
-            for (uint32_t q = c0 + (uint32_t)gi; active && q < c1; q += (uint32_t)ngi) {
-                const uint32_t i = G.class_sites[q];
-                // neighbour walk split over the 4 lanes, byte-SWAR accumulators reduced after
+            // warp-uniform trip count (full-mask shuffles stay legal); lane groups past the end
+            // of the class or without an instance run predicated off
+            for (uint32_t base = c0; base < c1; base += (uint32_t)ngi) {
+                const uint32_t q = base + (uint32_t)gi;
+                const bool on = active && q < c1;
+                const uint32_t i = on ? G.class_sites[q] : 0u;
+                // neighbour walk split over the 4 lanes, byte-SWAR accumulators
                 uint32_t A[8];
 #pragma unroll
                 for (int m = 0; m < 8; ++m) A[m] = 0;
                 int sumabs = 0;
-                const uint32_t r1 = G.rowptr[i + 1];
-                for (uint32_t k = G.rowptr[i] + sub; k < r1; k += kTPS) {
-                    const int J = G.J[k];
-                    const uint32_t v = words[G.col[k]] ^ (J < 0 ? 0xFFFFFFFFu : 0u);
-                    const uint32_t mag = (uint32_t)(J < 0 ? -J : J);
-                    sumabs += (int)mag;
+                if (on) {
+                    const uint32_t r1 = G.rowptr[i + 1];
+                    for (uint32_t k = G.rowptr[i] + sub; k < r1; k += kTPS) {
+                        const int J = G.J[k];
+                        const uint32_t v = words[G.col[k]] ^ (J < 0 ? 0xFFFFFFFFu : 0u);
+                        const uint32_t mag = (uint32_t)(J < 0 ? -J : J);
+                        sumabs += (int)mag;
 #pragma unroll
-                    for (int m = 0; m < 8; ++m) A[m] += mag * ((v >> m) & 0x01010101u);
-                }
-#pragma unroll
-                for (int m = 0; m < 8; ++m) {
-                    A[m] += __shfl_xor_sync(gmask, A[m], 1);
-                    A[m] += __shfl_xor_sync(gmask, A[m], 2);
-                }
-                sumabs += __shfl_xor_sync(gmask, sumabs, 1);
-                sumabs += __shfl_xor_sync(gmask, sumabs, 2);
-                const uint32_t A0 = A[m0], A1 = A[m0 + 1];
-                const int off = G.h[i] - sumabs - g.lmin;  // idx = l - lmin = off + 2*acc
-                const uint32_t old = words[i];
-                const uint64_t ph = (uint64_t)G.rank[i] * kPhi;
-                uint32_t nw = 0, tmin = 0xFFFFFFFFu;
-                int idx[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int b = 8 * (j >> 1) + m0 + (j & 1);
-                    idx[j] = off + 2 * (int)((((j & 1) ? A1 : A0) >> (8 * (j >> 1))) & 0xFFu);
-                    if (b < nv) {
-                        const uint32_t thr = Uslot[trow[j] + idx[j]];
-                        const uint64_t z = S.sb[b] + ph;
-                        const uint32_t h = mix_pre_hi<TAPT_K1_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), a.mc);
-                        tmin = min(tmin, h - thr + 1u);
-                        if (h < thr) nw |= 1u << b;
+                        for (int m = 0; m < 8; ++m) A[m] += mag * ((v >> m) & 0x01010101u);
                     }
                 }
-                if (tmin <= 2u) {  // |h - U| <= 1 somewhere (p ~ 2^-31): exact 64-bit decisions
-                    nw = 0;
+                // 4-lane reduce-scatter: lane `sub` ends with A[2 sub] and A[2 sub + 1] summed
+                uint32_t Bh[4];
+                const bool h2 = (sub & 2) != 0, h1 = (sub & 1) != 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const uint32_t send = h2 ? A[k] : A[k + 4];
+                    Bh[k] = (h2 ? A[k + 4] : A[k]) + __shfl_xor_sync(0xFFFFFFFFu, send, 2);
+                }
+                uint32_t A0, A1;
+                {
+                    const uint32_t s0 = h1 ? Bh[0] : Bh[2], s1 = h1 ? Bh[1] : Bh[3];
+                    const uint32_t r0 = __shfl_xor_sync(0xFFFFFFFFu, s0, 1);
+                    const uint32_t r1 = __shfl_xor_sync(0xFFFFFFFFu, s1, 1);
+                    A0 = (h1 ? Bh[2] : Bh[0]) + r0;
+                    A1 = (h1 ? Bh[3] : Bh[1]) + r1;
+                }
+                sumabs += __shfl_xor_sync(0xFFFFFFFFu, sumabs, 1);
+                sumabs += __shfl_xor_sync(0xFFFFFFFFu, sumabs, 2);
+                uint32_t nw = 0, old = 0;
+                if (on) {
+                    const int hs = G.h[i] - sumabs;  // l_j = hs + 2*acc_j, table index l_j - lmin
+                    old = words[i];
+                    const uint64_t ph = (uint64_t)G.rank[i] * kPhi;
+                    uint32_t tmin = 0xFFFFFFFFu, w = 0;
+                    int l[8];
+                    // descending j: the carry chain leaves NOT(up_j) in bit j of w.  Replicas past
+                    // nv read a valid row and a spare stream slot; their bits are masked below.
+#pragma unroll
+                    for (int j = 7; j >= 0; --j) {
+                        l[j] = hs + 2 * (int)prmt((j & 1) ? A1 : A0, 0u, 0x4440u | (uint32_t)(j >> 1));
+                        const uint32_t thr = Uslot[trl[j] + l[j]];
+                        const uint64_t z = S.sb[8 * (j >> 1) + m0 + (j & 1)] + ph;
+                        const uint32_t hh = mix_pre_hi<TAPT_K1_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), a.mc);
+                        tmin = min(tmin, decide_acc(hh, thr, w) + 1u);
+                    }
+                    if (tmin > 2u) {
+                        // bits j -> positions 8*(j>>1) + (j&1), then shift to this lane's replicas
+                        const uint32_t u = ~w & 0xFFu;
+                        const uint32_t y = (u | (u << 12)) & 0x000F000Fu;
+                        nw = (((y | (y << 6)) & 0x03030303u) << m0) & mine;
+                    } else {  // |h - U| <= 1 somewhere (p ~ 2^-31): exact 64-bit decisions
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            const int b = 8 * (j >> 1) + m0 + (j & 1);
+                            if (b < nv && below(mix_final(S.sb[b] + ph), a.thr[(size_t)(trl[j] + l[j])])) nw |= 1u << b;
+                        }
+                    }
+                    // flip energy 2 s_old l = 2 l (old - new) per replica: byte-wise old - new in
+                    // {-1, 0, 1}, sign-extended by PRMT, times l (the factor 2 is applied at the end)
+                    const uint32_t O = (old & mine) >> m0, N = nw >> m0;
+                    const uint32_t X0 = (((O & 0x01010101u) | 0x80808080u) - (N & 0x01010101u)) ^ 0x80808080u;
+                    const uint32_t X1 = ((((O >> 1) & 0x01010101u) | 0x80808080u) - ((N >> 1) & 0x01010101u)) ^ 0x80808080u;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
-                        const int b = 8 * (j >> 1) + m0 + (j & 1);
-                        if (b < nv && below(mix_final(S.sb[b] + ph), a.thr[(size_t)trow[j] + idx[j]])) nw |= 1u << b;
+                        constexpr uint32_t kSx[4] = {0x8880u, 0x9991u, 0xAAA2u, 0xBBB3u};
+                        dE[j] += l[j] * (int)prmt((j & 1) ? X1 : X0, 0u, kSx[j >> 1]);
                     }
                 }
-                const uint32_t flips = (nw ^ old) & mine;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const int b = 8 * (j >> 1) + m0 + (j & 1);
-                    const int l2 = 2 * (g.lmin + idx[j]);  // dE of a flip = 2 s_old l
-                    if ((flips >> b) & 1u) dE[j] += ((old >> b) & 1u) ? l2 : -l2;
-                }
-                nw |= __shfl_xor_sync(gmask, nw, 1);
-                nw |= __shfl_xor_sync(gmask, nw, 2);
-                if (sub == 0) words[i] = nw | (old & ~vmask);
+                nw |= __shfl_xor_sync(0xFFFFFFFFu, nw, 1);
+                nw |= __shfl_xor_sync(0xFFFFFFFFu, nw, 2);
+                if (on && sub == 0) words[i] = nw | (old & ~vmask);
             }
             __syncthreads();
         }
@@ -206,7 +236,7 @@ __global__ void __launch_bounds__(1024, 1) k2_csr_pt(const PTArgs a, const CsrAr
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const int b = 8 * (j >> 1) + m0 + (j & 1);
-                    if (b < nv) atomicAdd(&S.Ucnt[b], (uint32_t)dE[j]);
+                    if (b < nv) atomicAdd(&S.Ucnt[b], (uint32_t)(2 * dE[j]));
                 }
             }
             __syncthreads();

@@ -24,6 +24,9 @@ constexpr int kCnt = 8;      // planes of the sliced per-thread counters
 #ifndef TAPT_K1_IDX2
 #define TAPT_K1_IDX2 1       // 1: masked-add periodic neighbour indices
 #endif
+#ifndef TAPT_K2_MAXT
+#define TAPT_K2_MAXT 1024    // K2 launch bound (threads per CTA); 512 lifts the register cap to 128
+#endif
 #ifndef TAPT_K1_PIPE
 #define TAPT_K1_PIPE 0       // 1: software-pipeline the stencil of the next site pair
 #endif
