@@ -304,7 +304,11 @@ def ea_graph(dims, seed, gid) -> Graph:
 
 def greedy_colours(g: Graph) -> np.ndarray:
     """Greedy colouring in ascending site order (smallest colour unused by
-    already-coloured neighbours); clamped sites get colour -1."""
+    already-coloured neighbours), then equitable rebalancing: repeated passes in
+    ascending order move a site out of a class larger than T = ceil(n_free / k)
+    into the smallest class below T that none of its neighbours uses.  Clamped
+    sites get colour -1.  (The reference has no colouring; this is the schedule
+    of the parallel chain.)"""
     col = np.full(g.n, -1, np.int32)
     for i in range(g.n):
         if g.clamp[i]:
@@ -314,6 +318,28 @@ def greedy_colours(g: Graph) -> np.ndarray:
         while c in used:
             c += 1
         col[i] = c
+    free = np.nonzero(col >= 0)[0]
+    k = int(col.max()) + 1 if len(free) else 0
+    if k > 1:
+        size = np.bincount(col[free], minlength=k)
+        T = -(-len(free) // k)
+        changed = True
+        while changed:
+            changed = False
+            for i in free:
+                c = col[i]
+                if size[c] <= T:
+                    continue
+                used = {int(col[j]) for j in g.col[g.rowptr[i]:g.rowptr[i + 1]] if col[j] >= 0}
+                best = -1
+                for d in range(k):
+                    if d != c and size[d] < T and d not in used and (best < 0 or size[d] < size[best]):
+                        best = d
+                if best >= 0:
+                    col[i] = best
+                    size[c] -= 1
+                    size[best] += 1
+                    changed = True
     return col
 
 

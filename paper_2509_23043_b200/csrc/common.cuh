@@ -45,11 +45,13 @@ __host__ __device__ __forceinline__ uint32_t thr_hi(uint64_t T) {
 struct MixConsts {
     uint32_t k4, k32;
     uint32_t nib[8];  // nib[k] = 2^(34-4k) (k >= 1): hi(N * nib[k]) = N >> (4k-2)
+    uint32_t sh[8];   // sh[m] = 2^(32-m) (m >= 1): hi(v * sh[m]) = v >> m
 };
 
 inline MixConsts make_mix_consts() {
-    MixConsts c{4u, 32u, {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}};
+    MixConsts c{4u, 32u, {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}, {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u}};
     for (int k = 1; k < 8; ++k) c.nib[k] = 1u << (34 - 4 * k);
+    for (int m = 1; m < 8; ++m) c.sh[m] = 1u << (32 - m);
     return c;
 }
 

@@ -274,7 +274,7 @@ struct tapt_model_s {
     bool on_device = false;
     DevBuf<uint32_t> d_rowptr, d_col, d_rank, d_colptr, d_colsites, d_levptr, d_levsites, d_adjbond;
     DevBuf<int8_t> d_J, d_clamp;
-    DevBuf<int32_t> d_h;
+    DevBuf<int32_t> d_h, d_hs;
 
     void ensure_device(cudaStream_t st) {
         if (on_device) return;
@@ -289,6 +289,12 @@ struct tapt_model_s {
         d_J.upload(adjJ, st);
         d_clamp.upload(clamp, st);
         d_h.upload(hi, st);
+        {  // h_i - sum_k |J_ik|: the local field of the all-down neighbourhood (K2 adds 2*acc)
+            std::vector<int32_t> hs(hi);
+            for (size_t i = 0; i + 1 < rowptr.size(); ++i)
+                for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) hs[i] -= std::abs((int)adjJ[k]);
+            d_hs.upload(hs, st);
+        }
         CUDA_OK(cudaStreamSynchronize(st));
         on_device = true;
     }
@@ -407,6 +413,34 @@ void build_model(tapt_model_s& m, uint32_t n, const std::vector<uint32_t>& ai, c
         ncol = std::max(ncol, c + 1);
         nlev = std::max(nlev, lv + 1);
     }
+    // equitable rebalancing: move sites (ascending index, repeated passes) out of classes larger
+    // than T = ceil(n_free / ncol) into the smallest class below T that no neighbour uses.  The
+    // sweep processes a class in rounds of one site per lane group, so the round count
+    // sum_c ceil(|c| / groups) is what a sweep costs (multiplier 16: 15 -> 12 rounds at 64 groups).
+    if (ncol > 1) {
+        std::vector<uint32_t> size(ncol, 0);
+        for (uint32_t i : m.free_sites) ++size[m.colour[i]];
+        const uint32_t T = (uint32_t)((m.free_sites.size() + ncol - 1) / ncol);
+        for (bool changed = true; changed;) {
+            changed = false;
+            for (uint32_t i : m.free_sites) {
+                const int c = m.colour[i];
+                if (size[c] <= T) continue;
+                mark.assign(ncol, 0);
+                for (uint32_t k = m.rowptr[i]; k < m.rowptr[i + 1]; ++k)
+                    if (m.colour[m.col[k]] >= 0) mark[m.colour[m.col[k]]] = 1;
+                int best = -1;
+                for (int d = 0; d < ncol; ++d)
+                    if (d != c && size[d] < T && !mark[d] && (best < 0 || size[d] < size[best])) best = d;
+                if (best >= 0) {
+                    m.colour[i] = best;
+                    --size[c];
+                    ++size[best];
+                    changed = true;
+                }
+            }
+        }
+    }
     auto classes = [&](const std::vector<int32_t>& cls, int nc, std::vector<uint32_t>& ptr,
                        std::vector<uint32_t>& sites) {
         ptr.assign(nc + 1, 0);
@@ -478,6 +512,7 @@ struct tapt_ensemble_s {
         g.nJ = csrJ.p ? (int)I : 1;
         g.nnz = (int)m->col.size();
         g.h = m->d_h.p;
+        g.hs = m->d_hs.p;
         g.rank = m->d_rank.p;
         g.class_ptr = level_order ? m->d_levptr.p : m->d_colptr.p;
         g.class_sites = level_order ? m->d_levsites.p : m->d_colsites.p;

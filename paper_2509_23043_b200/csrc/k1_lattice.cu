@@ -211,7 +211,7 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
 #pragma unroll
                 for (int u = 0; u < SP; ++u) {
                     const uint32_t dd = decide_acc(h[e * SP + u], thr[e * SP + u], w[u]);
-                    tmin = min(tmin, dd + 1u);
+                    tmin = min(tmin, dd + (TAPT_K1_UM1 ? 0u : 1u));
                 }
         }
         tie |= tmin <= 2u;
@@ -233,9 +233,9 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
             const uint32_t h = mix_pre_hi<V>((uint32_t)z, (uint32_t)(z >> 32), mc);
             const uint32_t dd = decide_acc(h, thr, w[u]);
             if constexpr ((V & 4) != 0)
-                tmin = min(tmin, dd + 1u);
+                tmin = min(tmin, dd + (TAPT_K1_UM1 ? 0u : 1u));
             else
-                tie |= (dd + 1u <= 2u);
+                tie |= (dd + (TAPT_K1_UM1 ? 0u : 1u) <= 2u);
         }
     }
     if constexpr ((V & 4) != 0) tie |= tmin <= 2u;
@@ -296,7 +296,9 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
             const int b = e >> 3, k = e & 7;
             const int slot = sm.S.slot_of[grp * W + b];
             const uint64_t T = k < a.nidx ? a.thr[(size_t)slot * a.nidx + k] : 0ull;
-            sm.Uhi[b][k] = thr_hi(T);
+            // UM1: store U - 1 (clamped at 0) so that h - (U - 1) is both the carry of the decision
+            // and the tie band {0, 1, 2} (h = U - 1 falls in the band and is redone exactly)
+            sm.Uhi[b][k] = TAPT_K1_UM1 ? max(thr_hi(T), 1u) - 1u : thr_hi(T);
             sm.T64[b][k] = T;
         }
         pt_stream_bases(a, sm.S, inst, grp, t);

@@ -39,7 +39,7 @@ __device__ __forceinline__ uint32_t prmt(uint32_t x, uint32_t y, uint32_t sel) {
 }
 
 // Shared-memory image of the graph (the whole CSR is staged once per launch when it fits):
-//   rowptr [n+1] u32 | col [nnz] u32 | h [n] i32 | rank [n] u32 | class_sites [n_free] u32 | J [nnz] i8
+//   rowptr [n+1] u32 | col [nnz] u32 | hs [n] i32 | rank [n] u32 | class_sites [n_free] u32 | J [nnz] i8
 __host__ __device__ inline size_t k2_graph_bytes(int n, int nnz, int nfree) {
     return ((size_t)(n + 1) + nnz + 2 * (size_t)n + nfree) * 4 + (((size_t)nnz + 15) & ~size_t(15));
 }
@@ -49,12 +49,14 @@ struct K2Graph {
     const uint32_t* rowptr;
     const uint32_t* col;
     const int8_t* J;
-    const int32_t* h;
+    const int32_t* hs;  // h_i - sum |J_ik|
     const uint32_t* rank;
     const uint32_t* class_sites;
 };
 
-template <bool CLU, bool SMEMG>
+// US > 0: per-sweep copy of the threshold rows indexed by buffer, row stride US (compile time),
+// so a decision's table address is l*4 + a per-replica immediate (no per-replica row registers).
+template <bool CLU, bool SMEMG, int US>
 __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, const CsrArgs g, const int ipb) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ PTShared SS[kIPB];
@@ -91,14 +93,16 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
             jj[k] = g.J[k];  // shared couplings; per-instance couplings stay in global memory
         }
         for (int k = tid; k < n; k += nt) {
-            hh[k] = g.h[k];
+            hh[k] = TAPT_K2_HS ? g.hs[k] : g.h[k];
             rk[k] = g.rank[k];
         }
         for (int k = tid; k < nfree; k += nt) cs[k] = g.class_sites[k];
         G = K2Graph{rp, cl, g.nJ > 1 ? Jglob : jj, hh, rk, cs};
     } else {
-        G = K2Graph{g.rowptr, g.col, Jglob, g.h, g.rank, g.class_sites};
+        G = K2Graph{g.rowptr, g.col, Jglob, TAPT_K2_HS ? g.hs : g.h, g.rank, g.class_sites};
     }
+    // [ipb][32][US] threshold rows by buffer (US > 0), after the spins and the staged graph
+    uint32_t* Ubuf = wbase + (size_t)ipb * n + (SMEMG ? k2_graph_bytes(n, g.nnz, nfree) / 4 : 0);
     const int sub = tid & (kTPS - 1), m0 = 2 * sub;
     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
     const uint32_t mine = (0x03030303u << m0) & vmask;  // replicas of this lane
@@ -110,7 +114,9 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
         pt_load_perm(a, SS[kin], ik);
         for (int b = tid; b < nv; b += nt) SS[kin].Eown[(a.t0 + 1) & 1][b] = a.E[(size_t)ik * a.B + grp * W + b];
     }
-    for (int k = tid; k < a.R * nidx; k += nt) Uslot[k] = thr_hi(a.thr[k]);
+    // U - 1 (clamped at 0): the carry of h - (U - 1) and the tie band h - (U - 1) in {0, 1, 2}
+    // come out of one subtraction (decisions with h = U - 1 fall in the band and are redone)
+    for (int k = tid; k < a.R * nidx; k += nt) Uslot[k] = max(thr_hi(a.thr[k]), 1u) - 1u;
     __syncthreads();
 
     uint64_t pass = a.p0;
@@ -120,13 +126,21 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
         const int prev = par;
         par = (int)(t & 1);
         for (int kin = 0; kin < nin; ++kin) pt_stream_bases(a, SS[kin], inst0 + kin, grp, t);
+        if constexpr (US > 0) {
+            for (int e = tid; e < nin * 32 * US; e += nt) {
+                const int kin = e / (32 * US), b = (e / US) & 31, x = e % US;
+                Ubuf[e] = (b < nv && x < nidx) ? Uslot[SS[kin].slot_of[grp * W + b] * nidx + x] : 0u;
+            }
+        }
         __syncthreads();
-        // this lane's 8 replicas: threshold-row offsets of their current slots
-        int trl[8];  // slot row - lmin, so that Uslot[trl + l] is the entry of local field l
+        // this lane's 8 replicas: threshold rows of their current slots, offset by -lmin so that
+        // row[l] is the entry of local field l
+        int trl[8];  // (US == 0 only)
+        const uint32_t* Ub = Ubuf + (size_t)((active ? mykin : 0) * 32 + m0) * US - g.lmin;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int b = 8 * (j >> 1) + m0 + (j & 1);
-            trl[j] = (b < nv ? S.slot_of[grp * W + b] * nidx : 0) - g.lmin;
+            trl[j] = US > 0 ? 0 : (b < nv ? S.slot_of[grp * W + b] * nidx : 0) - g.lmin;
         }
         int32_t dE[8];
 #pragma unroll
@@ -144,16 +158,28 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
                 uint32_t A[8];
 #pragma unroll
                 for (int m = 0; m < 8; ++m) A[m] = 0;
+#if !TAPT_K2_HS
                 int sumabs = 0;
+#endif
                 if (on) {
                     const uint32_t r1 = G.rowptr[i + 1];
                     for (uint32_t k = G.rowptr[i] + sub; k < r1; k += kTPS) {
                         const int J = G.J[k];
                         const uint32_t v = words[G.col[k]] ^ (J < 0 ? 0xFFFFFFFFu : 0u);
                         const uint32_t mag = (uint32_t)(J < 0 ? -J : J);
+#if !TAPT_K2_HS
                         sumabs += (int)mag;
+#endif
 #pragma unroll
-                        for (int m = 0; m < 8; ++m) A[m] += mag * ((v >> m) & 0x01010101u);
+                        for (int m = 0; m < 8; ++m) {
+#if TAPT_K2_WALKHI
+                            // shifts as IMAD.HI by runtime powers of two: FMA pipe instead of ALU
+                            const uint32_t vm = m == 0 ? v : __umulhi(v, a.mc.sh[m]);
+#else
+                            const uint32_t vm = v >> m;
+#endif
+                            A[m] += mag * (vm & 0x01010101u);
+                        }
                     }
                 }
                 // 4-lane reduce-scatter: lane `sub` ends with A[2 sub] and A[2 sub + 1] summed
@@ -172,11 +198,17 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
                     A0 = (h1 ? Bh[2] : Bh[0]) + r0;
                     A1 = (h1 ? Bh[3] : Bh[1]) + r1;
                 }
+#if !TAPT_K2_HS
                 sumabs += __shfl_xor_sync(0xFFFFFFFFu, sumabs, 1);
                 sumabs += __shfl_xor_sync(0xFFFFFFFFu, sumabs, 2);
+#endif
                 uint32_t nw = 0, old = 0;
                 if (on) {
-                    const int hs = G.h[i] - sumabs;  // l_j = hs + 2*acc_j, table index l_j - lmin
+#if TAPT_K2_HS
+                    const int hs = G.hs[i];  // l_j = hs + 2*acc_j, table index l_j - lmin
+#else
+                    const int hs = G.hs[i] - sumabs;  // G.hs holds h here
+#endif
                     old = words[i];
                     const uint64_t ph = (uint64_t)G.rank[i] * kPhi;
                     uint32_t tmin = 0xFFFFFFFFu, w = 0;
@@ -186,10 +218,10 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
 #pragma unroll
                     for (int j = 7; j >= 0; --j) {
                         l[j] = hs + 2 * (int)prmt((j & 1) ? A1 : A0, 0u, 0x4440u | (uint32_t)(j >> 1));
-                        const uint32_t thr = Uslot[trl[j] + l[j]];
+                        const uint32_t thr = US > 0 ? Ub[(8 * (j >> 1) + (j & 1)) * US + l[j]] : Uslot[trl[j] + l[j]];
                         const uint64_t z = S.sb[8 * (j >> 1) + m0 + (j & 1)] + ph;
-                        const uint32_t hh = mix_pre_hi<TAPT_K1_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), a.mc);
-                        tmin = min(tmin, decide_acc(hh, thr, w) + 1u);
+                        const uint32_t hh = mix_pre_hi<TAPT_K2_MIXV>((uint32_t)z, (uint32_t)(z >> 32), a.mc);
+                        tmin = min(tmin, decide_acc(hh, thr, w));
                     }
                     if (tmin > 2u) {
                         // bits j -> positions 8*(j>>1) + (j&1), then shift to this lane's replicas
@@ -200,7 +232,9 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
                             const int b = 8 * (j >> 1) + m0 + (j & 1);
-                            if (b < nv && below(mix_final(S.sb[b] + ph), a.thr[(size_t)(trl[j] + l[j])])) nw |= 1u << b;
+                            if (b >= nv) continue;
+                            const int row = US > 0 ? S.slot_of[grp * W + b] * nidx - g.lmin : trl[j];
+                            if (below(mix_final(S.sb[b] + ph), a.thr[(size_t)(row + l[j])])) nw |= 1u << b;
                         }
                     }
                     // flip energy 2 s_old l = 2 l (old - new) per replica: byte-wise old - new in
@@ -260,20 +294,25 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
     for (int kin = 0; kin < nin; ++kin) pt_finish<CLU>(a, SS[kin], inst0 + kin, grp, par);
 }
 
+// per-instance buffer-indexed threshold rows (US path)
+static size_t k2_ubuf_bytes(int nidx) { return (TAPT_K2_US > 0 && nidx <= TAPT_K2_US) ? 32 * TAPT_K2_US * 4 : 0; }
+
 size_t k2_smem_bytes(int n, int R, int nidx) {
-    // dynamic part for one instance: per-slot threshold rows + spin words (control blocks are static)
-    return (size_t)R * nidx * 4 + (size_t)n * 4;
+    // dynamic part for one instance: per-slot threshold rows + spin words (+ buffer rows; control
+    // blocks are static)
+    return (size_t)R * nidx * 4 + (size_t)n * 4 + k2_ubuf_bytes(nidx);
 }
 
 size_t k2_smem_bytes_graph(int n, int R, int nidx, int nnz, int nfree) {
     return k2_smem_bytes(n, R, nidx) + k2_graph_bytes(n, nnz, nfree);
 }
 
-template <bool CLU, bool SMEMG>
+template <bool CLU, bool SMEMG, int US>
 static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, int ipb, cudaStream_t st) {
     size_t smem = (size_t)a.R * a.nidx * 4 + (size_t)ipb * a.n * 4;
     if (SMEMG) smem += k2_graph_bytes(a.n, g.nnz, (int)g.n_free);
-    auto fn = k2_csr_pt<CLU, SMEMG>;
+    smem += (size_t)ipb * 32 * US * 4;
+    auto fn = k2_csr_pt<CLU, SMEMG, US>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -294,20 +333,27 @@ static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, i
 }
 
 // Instances per CTA when one CTA holds a whole instance (G == 1, no cluster): 2 measured best
-// on config 4 (tools/k2_shapes.sh: 512 threads x {1,2,4} instances -> 2.0 / 2.3 / 2.0e11 updates/s).
+// on config 4 (tools/k2_shapes.sh, updates/s: 512 threads x {1,2,4} -> 2.93 / 3.20 / 2.90e11; 256 threads
+// x {1,2,4} -> 2.81 / 2.93 / 2.17e11).
 int k2_instances_per_cta(const PTArgs& a, const CsrArgs& g) {
     if (a.G != 1) return 1;
     if (const char* e = std::getenv("TAPT_K2_IPB")) return std::max(1, std::min(kIPB, std::atoi(e)));
     const size_t fixed = (size_t)a.R * a.nidx * 4 + (g.smem_graph ? k2_graph_bytes(a.n, g.nnz, (int)g.n_free) : 0);
-    if (fixed + 2 * (size_t)a.n * 4 <= 110 * 1024 && a.I >= 2) return 2;
+    if (fixed + 2 * ((size_t)a.n * 4 + k2_ubuf_bytes(a.nidx)) <= 110 * 1024 && a.I >= 2) return 2;
     return 1;
+}
+
+template <int US>
+static cudaError_t launch_k2_us(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, int ipb, cudaStream_t st) {
+    if (g.smem_graph)
+        return cluster ? launch_k2_t<true, true, US>(a, g, threads, 1, st) : launch_k2_t<false, true, US>(a, g, threads, ipb, st);
+    return cluster ? launch_k2_t<true, false, US>(a, g, threads, 1, st) : launch_k2_t<false, false, US>(a, g, threads, ipb, st);
 }
 
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st) {
     const int ipb = cluster ? 1 : k2_instances_per_cta(a, g);
-    if (g.smem_graph)
-        return cluster ? launch_k2_t<true, true>(a, g, threads, 1, st) : launch_k2_t<false, true>(a, g, threads, ipb, st);
-    return cluster ? launch_k2_t<true, false>(a, g, threads, 1, st) : launch_k2_t<false, false>(a, g, threads, ipb, st);
+    if (TAPT_K2_US > 0 && a.nidx <= TAPT_K2_US) return launch_k2_us<TAPT_K2_US>(a, g, threads, cluster, ipb, st);
+    return launch_k2_us<0>(a, g, threads, cluster, ipb, st);
 }
 
 }  // namespace tapt_dev

@@ -24,6 +24,21 @@ constexpr int kCnt = 8;      // planes of the sliced per-thread counters
 #ifndef TAPT_K1_IDX2
 #define TAPT_K1_IDX2 1       // 1: masked-add periodic neighbour indices
 #endif
+#ifndef TAPT_K1_UM1
+#define TAPT_K1_UM1 0        // 1: tables hold U - 1, tie band without the +1 (measured 0.8% slower on K1)
+#endif
+#ifndef TAPT_K2_MIXV
+#define TAPT_K2_MIXV TAPT_K1_VARIANT  // mix_pre_hi variant of the K2 decisions
+#endif
+#ifndef TAPT_K2_HS
+#define TAPT_K2_HS 0         // 1: precomputed h - sum|J| per site (0: accumulate in the walk; 3% faster, config 4)
+#endif
+#ifndef TAPT_K2_US
+#define TAPT_K2_US 64        // buffer-indexed threshold rows of this stride when nidx fits (0: off)
+#endif
+#ifndef TAPT_K2_WALKHI
+#define TAPT_K2_WALKHI 0     // 1: neighbour-walk bit-plane shifts as IMAD.HI (FMA pipe)
+#endif
 #ifndef TAPT_K2_MAXT
 #define TAPT_K2_MAXT 1024    // K2 launch bound (threads per CTA); 512 lifts the register cap to 128
 #endif
@@ -88,6 +103,7 @@ struct CsrArgs {
     int nJ;                    // 1 (shared) or I (per instance)
     int nnz;
     const int32_t* h;          // [n]
+    const int32_t* hs;         // [n] h_i - sum_k |J_ik| (per-instance couplings only flip signs)
     const uint32_t* rank;      // [n] position in the ascending free list
     const uint32_t* class_ptr; // [n_classes+1] into class_sites
     const uint32_t* class_sites;

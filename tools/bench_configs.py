@@ -38,6 +38,7 @@ def timed(torch, stream, fn):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", default="1,2,3,4")
+    ap.add_argument("--swap-every", type=int, default=1, help="configs 3/4: swap cadence (0: none; diagnostics)")
     ap.add_argument("--sweeps", type=int, default=2000)
     args = ap.parse_args()
     import torch
@@ -95,7 +96,7 @@ def main():
             e.set_clamps(np.stack([M.clamps(p * q) for p, q in prods]))
             e.init_random()
             e.run(100, swap_every=1)
-            dt = timed(torch, stream, lambda: e.run(S, swap_every=1))
+            dt = timed(torch, stream, lambda: e.run(S, swap_every=args.swap_every))
             upd = I * R * m.n_free * S
             Sp = e.spins()
             succ = np.mean([M.decode(Sp[k][R - 1], prods[k][0] * prods[k][1])[2] for k in range(I)])
