@@ -54,9 +54,7 @@ struct K2Graph {
     const uint32_t* class_sites;
 };
 
-// US > 0: per-sweep copy of the threshold rows indexed by buffer, row stride US (compile time),
-// so a decision's table address is l*4 + a per-replica immediate (no per-replica row registers).
-template <bool CLU, bool SMEMG, int US>
+template <bool CLU, bool SMEMG>
 __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, const CsrArgs g, const int ipb) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ PTShared SS[kIPB];
@@ -101,8 +99,6 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
     } else {
         G = K2Graph{g.rowptr, g.col, Jglob, TAPT_K2_HS ? g.hs : g.h, g.rank, g.class_sites};
     }
-    // [ipb][32][US] threshold rows by buffer (US > 0), after the spins and the staged graph
-    uint32_t* Ubuf = wbase + (size_t)ipb * n + (SMEMG ? k2_graph_bytes(n, g.nnz, nfree) / 4 : 0);
     const int sub = tid & (kTPS - 1), m0 = 2 * sub;
     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
     const uint32_t mine = (0x03030303u << m0) & vmask;  // replicas of this lane
@@ -126,21 +122,16 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
         const int prev = par;
         par = (int)(t & 1);
         for (int kin = 0; kin < nin; ++kin) pt_stream_bases(a, SS[kin], inst0 + kin, grp, t);
-        if constexpr (US > 0) {
-            for (int e = tid; e < nin * 32 * US; e += nt) {
-                const int kin = e / (32 * US), b = (e / US) & 31, x = e % US;
-                Ubuf[e] = (b < nv && x < nidx) ? Uslot[SS[kin].slot_of[grp * W + b] * nidx + x] : 0u;
-            }
-        }
         __syncthreads();
         // this lane's 8 replicas: threshold rows of their current slots, offset by -lmin so that
-        // row[l] is the entry of local field l
-        int trl[8];  // (US == 0 only)
-        const uint32_t* Ub = Ubuf + (size_t)((active ? mykin : 0) * 32 + m0) * US - g.lmin;
+        // Uslot[trl + l] is the entry of local field l.  (A per-sweep copy of the rows indexed by
+        // buffer with a compile-time stride, making the address 4l + an immediate, measured 4-9 %
+        // slower on config 4: 32 KB more shared memory per CTA and bank conflicts.)
+        int trl[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
             const int b = 8 * (j >> 1) + m0 + (j & 1);
-            trl[j] = US > 0 ? 0 : (b < nv ? S.slot_of[grp * W + b] * nidx : 0) - g.lmin;
+            trl[j] = (b < nv ? S.slot_of[grp * W + b] * nidx : 0) - g.lmin;
         }
         int32_t dE[8];
 #pragma unroll
@@ -218,7 +209,7 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
 #pragma unroll
                     for (int j = 7; j >= 0; --j) {
                         l[j] = hs + 2 * (int)prmt((j & 1) ? A1 : A0, 0u, 0x4440u | (uint32_t)(j >> 1));
-                        const uint32_t thr = US > 0 ? Ub[(8 * (j >> 1) + (j & 1)) * US + l[j]] : Uslot[trl[j] + l[j]];
+                        const uint32_t thr = Uslot[trl[j] + l[j]];
                         const uint64_t z = S.sb[8 * (j >> 1) + m0 + (j & 1)] + ph;
                         const uint32_t hh = mix_pre_hi<TAPT_K2_MIXV>((uint32_t)z, (uint32_t)(z >> 32), a.mc);
                         tmin = min(tmin, decide_acc(hh, thr, w));
@@ -232,9 +223,7 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
                             const int b = 8 * (j >> 1) + m0 + (j & 1);
-                            if (b >= nv) continue;
-                            const int row = US > 0 ? S.slot_of[grp * W + b] * nidx - g.lmin : trl[j];
-                            if (below(mix_final(S.sb[b] + ph), a.thr[(size_t)(row + l[j])])) nw |= 1u << b;
+                            if (b < nv && below(mix_final(S.sb[b] + ph), a.thr[(size_t)(trl[j] + l[j])])) nw |= 1u << b;
                         }
                     }
                     // flip energy 2 s_old l = 2 l (old - new) per replica: byte-wise old - new in
@@ -294,25 +283,20 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
     for (int kin = 0; kin < nin; ++kin) pt_finish<CLU>(a, SS[kin], inst0 + kin, grp, par);
 }
 
-// per-instance buffer-indexed threshold rows (US path)
-static size_t k2_ubuf_bytes(int nidx) { return (TAPT_K2_US > 0 && nidx <= TAPT_K2_US) ? 32 * TAPT_K2_US * 4 : 0; }
-
 size_t k2_smem_bytes(int n, int R, int nidx) {
-    // dynamic part for one instance: per-slot threshold rows + spin words (+ buffer rows; control
-    // blocks are static)
-    return (size_t)R * nidx * 4 + (size_t)n * 4 + k2_ubuf_bytes(nidx);
+    // dynamic part for one instance: per-slot threshold rows + spin words (control blocks are static)
+    return (size_t)R * nidx * 4 + (size_t)n * 4;
 }
 
 size_t k2_smem_bytes_graph(int n, int R, int nidx, int nnz, int nfree) {
     return k2_smem_bytes(n, R, nidx) + k2_graph_bytes(n, nnz, nfree);
 }
 
-template <bool CLU, bool SMEMG, int US>
+template <bool CLU, bool SMEMG>
 static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, int ipb, cudaStream_t st) {
     size_t smem = (size_t)a.R * a.nidx * 4 + (size_t)ipb * a.n * 4;
     if (SMEMG) smem += k2_graph_bytes(a.n, g.nnz, (int)g.n_free);
-    smem += (size_t)ipb * 32 * US * 4;
-    auto fn = k2_csr_pt<CLU, SMEMG, US>;
+    auto fn = k2_csr_pt<CLU, SMEMG>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -339,21 +323,15 @@ int k2_instances_per_cta(const PTArgs& a, const CsrArgs& g) {
     if (a.G != 1) return 1;
     if (const char* e = std::getenv("TAPT_K2_IPB")) return std::max(1, std::min(kIPB, std::atoi(e)));
     const size_t fixed = (size_t)a.R * a.nidx * 4 + (g.smem_graph ? k2_graph_bytes(a.n, g.nnz, (int)g.n_free) : 0);
-    if (fixed + 2 * ((size_t)a.n * 4 + k2_ubuf_bytes(a.nidx)) <= 110 * 1024 && a.I >= 2) return 2;
+    if (fixed + 2 * (size_t)a.n * 4 <= 110 * 1024 && a.I >= 2) return 2;
     return 1;
-}
-
-template <int US>
-static cudaError_t launch_k2_us(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, int ipb, cudaStream_t st) {
-    if (g.smem_graph)
-        return cluster ? launch_k2_t<true, true, US>(a, g, threads, 1, st) : launch_k2_t<false, true, US>(a, g, threads, ipb, st);
-    return cluster ? launch_k2_t<true, false, US>(a, g, threads, 1, st) : launch_k2_t<false, false, US>(a, g, threads, ipb, st);
 }
 
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st) {
     const int ipb = cluster ? 1 : k2_instances_per_cta(a, g);
-    if (TAPT_K2_US > 0 && a.nidx <= TAPT_K2_US) return launch_k2_us<TAPT_K2_US>(a, g, threads, cluster, ipb, st);
-    return launch_k2_us<0>(a, g, threads, cluster, ipb, st);
+    if (g.smem_graph)
+        return cluster ? launch_k2_t<true, true>(a, g, threads, 1, st) : launch_k2_t<false, true>(a, g, threads, ipb, st);
+    return cluster ? launch_k2_t<true, false>(a, g, threads, 1, st) : launch_k2_t<false, false>(a, g, threads, ipb, st);
 }
 
 }  // namespace tapt_dev

@@ -33,9 +33,6 @@ constexpr int kCnt = 8;      // planes of the sliced per-thread counters
 #ifndef TAPT_K2_HS
 #define TAPT_K2_HS 0         // 1: precomputed h - sum|J| per site (0: accumulate in the walk; 3% faster, config 4)
 #endif
-#ifndef TAPT_K2_US
-#define TAPT_K2_US 64        // buffer-indexed threshold rows of this stride when nidx fits (0: off)
-#endif
 #ifndef TAPT_K2_WALKHI
 #define TAPT_K2_WALKHI 0     // 1: neighbour-walk bit-plane shifts as IMAD.HI (FMA pipe)
 #endif
