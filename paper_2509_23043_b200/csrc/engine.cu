@@ -913,6 +913,7 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
         check_model(m);
         if (!d || !out) throw tapt::ConfigError("null descriptor / output");
         if (d->n_instances == 0) throw tapt::ConfigError("n_instances must be >= 1");
+        if (m->n == 0) throw tapt::ConfigError("model has no spins");
         if (d->n_slots < 1 || d->n_slots > (uint32_t)kMaxR) throw tapt::ConfigError("n_slots must be in [1, 256]");
         if (!d->betas) throw tapt::ConfigError("null beta ladder");
         for (uint32_t r = 0; r < d->n_slots; ++r) {
@@ -1590,6 +1591,10 @@ tapt_status tapt_gibbs_sweep(tapt_model_t m, int8_t* s, size_t len, double beta,
         if (!(beta >= 0.0)) throw tapt::ConfigError("beta must be >= 0");
         if (!rng_state) throw tapt::ConfigError("null rng state");
         if (n_sweeps == 0) return;
+        if (m->free_sites.empty()) {  // nothing to visit: no draws, dE = 0 (mcmc.cpp:34 loops over free_sites)
+            if (dE) std::fill(dE, dE + n_sweeps, 0.0);
+            return;
+        }
         std::lock_guard<std::mutex> lock(m->dropin_mu);
         if (!m->dropin) {
             tapt_ensemble_desc d{};

@@ -1,0 +1,217 @@
+"""Edge cases of the device engine against the oracle restatement (bit-exact) and the
+reference's own semantics: graphs without couplings, everything clamped, a single slot,
+wide threshold tables (large |J| and h), the 256-slot maximum, ragged replica groups, odd
+and L=2 periodic lattices, open boundaries, beta = 0, and the empty model.  Marked `gpu`."""
+import numpy as np
+import pytest
+
+import paper_2509_23043_b200 as T
+from oracle import oracle as O
+import tapt_helpers as H
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if T.device_count() == 0:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+
+
+def compare(ens, pts):
+    S, E = ens.spins(), ens.energies()
+    sa, sc, pa, pc = ens.acceptance()
+    for k, pt in enumerate(pts):
+        assert np.array_equal(E[k], pt.E), f"energies differ, instance {k}"
+        assert np.array_equal(S[k], pt.spins), f"spins differ, instance {k}"
+        assert np.array_equal(sc[k], pt.swap_acc[: ens.R - 1]), f"swap accepts differ, instance {k}"
+        assert np.array_equal(pc[k], pt.prop_acc), f"proposal accepts differ, instance {k}"
+
+
+def run_both(g, betas, seed, order, n_sweeps=60, n_inst=2, swap_every=1, props=None):
+    """Device ensemble and oracle on the same graph/schedule; proposals every props['every']."""
+    m = T.Model.graph(g.n, g.ci, g.cj, g.J, g.h, g.clamp)
+    e = T.Ensemble(m, betas, n_instances=n_inst, seed=seed, order=order)
+    e.init_random()
+    if props:
+        for _ in range(n_sweeps // props["every"]):
+            e.run(props["every"], swap_every=swap_every)
+            e.generate_proposals(np.arange(props["targets"]), props.get("m_bias"), refine=props["refine"])
+    else:
+        e.run(n_sweeps, swap_every=swap_every)
+    if order == "reference":
+        fn = H.index_order
+    else:
+        fn = H.colour_order_for(m.schedule()[0])
+    pts = H.run_oracle([g] * n_inst, betas, seed, 0, fn, n_sweeps, swap_every=swap_every, props=props)
+    return e, pts
+
+
+@pytest.mark.parametrize("order", ["colour", "reference"])
+def test_fields_only_no_couplings(order):
+    rs = np.random.default_rng(1)
+    n = 37
+    h = rs.integers(-4, 5, n).astype(float)
+    cl = np.where(rs.random(n) < 0.2, rs.choice([-1, 1], n), 0).astype(np.int8)
+    g = O.Graph.from_couplings(n, np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0), h, cl)
+    e, pts = run_both(g, H.geometric(0.1, 3.0, 8), 3, order,
+                      props=dict(every=20, targets=4, m_bias=np.full(8, 0.3), refine=2))
+    compare(e, pts)
+
+
+def test_everything_clamped():
+    """n_free = 0: sweeps draw nothing and change nothing; equal energies make every swap
+    accepted (dE = 0), exactly as the restated driver."""
+    n = 12
+    ci, cj = np.arange(n - 1), np.arange(1, n)
+    cl = np.where(np.arange(n) % 3 == 0, -1, 1).astype(np.int8)
+    g = O.Graph.from_couplings(n, ci, cj, np.ones(n - 1), np.ones(n), cl)
+    e, pts = run_both(g, H.linear(0.2, 1.0, 6), 4, "reference", n_sweeps=10)
+    compare(e, pts)
+    assert np.all(e.spins() == g.clamp)
+    assert e.acceptance()[1].sum() > 0
+
+
+@pytest.mark.parametrize("kernel_dims", [(8, 8), None])
+def test_single_slot_no_swap_pairs(kernel_dims):
+    betas = np.array([0.7])
+    if kernel_dims:
+        g = O.lattice_graph(kernel_dims)
+        m = T.Model.lattice(kernel_dims)
+        e = T.Ensemble(m, betas, n_instances=3, seed=9)
+        assert e.kernel == "lattice"
+        e.init_random()
+        for _ in range(3):
+            e.run(10, swap_every=1)
+            e.generate_proposals(np.arange(1), np.array([0.4]), refine=3)
+        pts = H.run_oracle([g] * 3, betas, 9, 0, H.checkerboard_order(kernel_dims), 30,
+                           props=dict(every=10, targets=1, m_bias=np.array([0.4]), refine=3))
+    else:
+        rs = np.random.default_rng(2)
+        n = 30
+        ci, cj = rs.integers(0, n, 90), rs.integers(0, n, 90)
+        keep = ci != cj
+        g = O.Graph.from_couplings(n, ci[keep], cj[keep], rs.choice([-1.0, 1.0], 90)[keep])
+        e, pts = run_both(g, betas, 9, "colour", n_sweeps=30, n_inst=3,
+                          props=dict(every=10, targets=1, m_bias=np.array([0.4]), refine=3))
+    compare(e, pts)
+
+
+def test_wide_threshold_tables_large_couplings():
+    """|J| up to 60 and |h| up to 40: local fields span ~[-280, 280], hundreds of table rows
+    per slot (exact thresholds near 0 and 1 as well as the tails)."""
+    rs = np.random.default_rng(5)
+    n = 24
+    ci = np.arange(n)
+    cj = (ci + 1) % n
+    ck = (ci + 5) % n
+    a = np.concatenate([ci, ci])
+    b = np.concatenate([cj, ck])
+    J = rs.integers(1, 61, len(a)) * rs.choice([-1, 1], len(a))
+    h = rs.integers(-40, 41, n).astype(float)
+    g = O.Graph.from_couplings(n, a, b, J.astype(float), h)
+    m = T.Model.graph(g.n, g.ci, g.cj, g.J, g.h)
+    assert m.lmax - m.lmin > 300
+    for order in ("colour", "reference"):
+        e, pts = run_both(g, H.geometric(0.01, 0.5, 16), 11, order, n_sweeps=40)
+        compare(e, pts)
+
+
+def test_256_slots_maximum_ladder():
+    """The largest ladder (8 replica groups in one cluster on K1, 256-entry permutations)."""
+    dims = (8, 8)
+    R = 256
+    betas = H.linear(0.05, 2.0, R)
+    m = T.Model.lattice(dims)
+    e = T.Ensemble(m, betas, n_instances=1, seed=21)
+    assert e.kernel == "lattice"
+    e.init_random()
+    e.run(12, swap_every=1)
+    pts = H.run_oracle([O.lattice_graph(dims)], betas, 21, 0, H.checkerboard_order(dims), 12)
+    compare(e, pts)
+    with pytest.raises(T.ConfigError):
+        T.Ensemble(m, H.linear(0.05, 2.0, 257))
+
+
+@pytest.mark.parametrize("R", [33, 63])
+def test_ragged_replica_groups(R):
+    dims = (4,)
+    betas = H.linear(0.1, 1.2, R)
+    g = O.lattice_graph(dims)
+    e = T.Ensemble(T.Model.lattice(dims), betas, n_instances=2, seed=R)
+    e.init_random()
+    e.run(25, swap_every=1)
+    pts = H.run_oracle([g] * 2, betas, R, 0, H.checkerboard_order(dims), 25)
+    compare(e, pts)
+
+
+@pytest.mark.parametrize("dims", [(3, 3, 3), (5, 7), (2, 2), (2,), (1, 6)])
+def test_odd_and_tiny_periodic_lattices(dims):
+    """Odd periodic lattices are not bipartite (greedy colouring on K2); L=2 adds no wrap bonds
+    (lattice.cpp:63,67,76-80) -- the model must hold exactly the reference's couplings."""
+    dims3 = (dims[0],) if len(dims) == 3 else dims
+    m = T.Model.lattice(dims3)
+    g = O.lattice_graph(dims3)
+    ci, cj, J = m.couplings()[:3]
+    rg = O.ref().ref_graph_lattice(3 if len(dims3) == 1 else 2, dims3[0] if len(dims3) == 2 else 0,
+                                   dims3[1] if len(dims3) == 2 else 0, dims3[0] if len(dims3) == 1 else 0, 1.0, 1)
+    assert m.digest() == O.ref().ref_graph_digest(rg)
+    O.ref().ref_graph_free(rg)
+    assert len(ci) == len(g.ci)
+    betas = H.geometric(0.2, 1.5, 8)
+    for order in ("colour", "reference"):
+        e = T.Ensemble(m, betas, n_instances=2, seed=13, order=order)
+        e.init_random()
+        e.run(30, swap_every=1)
+        if order == "reference":
+            fn = H.index_order
+        elif e.kernel == "lattice":
+            fn = H.checkerboard_order(dims3)
+        else:
+            fn = H.colour_order_for(m.schedule()[0])
+        compare(e, H.run_oracle([g] * 2, betas, 13, 0, fn, 30))
+
+
+def test_open_boundary_lattice():
+    dims = (6, 9)
+    m = T.Model.lattice(dims, periodic=False)
+    g = O.lattice_graph(dims, periodic=False)
+    betas = H.geometric(0.2, 1.5, 12)
+    e = T.Ensemble(m, betas, n_instances=2, seed=17)
+    e.init_random()
+    e.run(40, swap_every=1)
+    fn = H.checkerboard_order(dims) if e.kernel == "lattice" else H.colour_order_for(m.schedule()[0])
+    compare(e, H.run_oracle([g] * 2, betas, 17, 0, fn, 40))
+
+
+def test_beta_zero_slot():
+    """beta = 0: P(+1) = 1/2 for every local field, swap acceptance
+    exp(beta diff * dE) with the hottest slot at 0."""
+    dims = (8, 8)
+    betas = np.concatenate([[0.0], H.linear(0.1, 1.0, 7)])
+    e = T.Ensemble(T.Model.lattice(dims), betas, n_instances=2, seed=23)
+    e.init_random()
+    for _ in range(2):
+        e.run(15, swap_every=1)
+        e.generate_proposals(np.arange(3), np.zeros(3), refine=2)
+    pts = H.run_oracle([O.lattice_graph(dims)] * 2, betas, 23, 0, H.checkerboard_order(dims), 30,
+                       props=dict(every=15, targets=3, m_bias=np.zeros(8), refine=2))
+    compare(e, pts)
+
+
+def test_empty_model_dropin_sweep():
+    """gibbs_sweep on a 0-spin graph visits nothing, draws nothing and returns dE = 0
+    (mcmc.cpp:30-45 loops over an empty free list)."""
+    m = T.Model.graph(0, np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0))
+    s = np.zeros(0, np.int8)
+    st, dE = T.gibbs_sweep(m, s, 1.0, 12345, n_sweeps=3)
+    assert st == 12345 and np.all(dE == 0)
+    with pytest.raises(T.DimensionError):
+        T.gibbs_sweep(m, np.zeros(2, np.int8), 1.0, 1)
+    with pytest.raises(T.ConfigError):
+        T.Ensemble(m, np.array([1.0]))
+    # all spins clamped: same contract, the spins are left as they are
+    c = T.Model.graph(3, np.array([0, 1]), np.array([1, 2]), np.ones(2), None, np.array([1, -1, 1], np.int8))
+    s = np.array([1, -1, 1], np.int8)
+    st, dE = T.gibbs_sweep(c, s, 2.0, 99, n_sweeps=2)
+    assert st == 99 and np.all(dE == 0) and list(s) == [1, -1, 1]
