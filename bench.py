@@ -291,15 +291,16 @@ def main():
     g_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs") if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     hbm_bytes = I * (2 * 4 * N_SPINS * 2 + N_SPINS)  # spins in+out (2 groups) + bond bytes, per launch
-    traffic = None
+    traffic, traffic_detail = None, None
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
     if os.path.exists(tpath):  # dram bytes per instance-launch from the committed ncu --set full capture
         tr = json.load(open(tpath))
-        traffic = {"bytes_per_launch": tr["dram_bytes_per_instance_launch"] * I,
-                   "algorithmic_bytes_per_launch": hbm_bytes, "source": tr["source"]}
+        traffic = tr["dram_bytes_per_instance_launch"] * I
+        traffic_detail = {"dram_bytes_per_launch": traffic, "algorithmic_bytes_per_launch": hbm_bytes,
+                          "source": tr["source"]}
     roofline = {
         "bound": "alu", "unit": "Gupdates/s", "achieved": achieved / 1e9, "peak": peak / 1e9,
-        "frac": achieved / peak, "traffic": traffic,
+        "frac": achieved / peak, "traffic": traffic, "traffic_detail": traffic_detail,
         "peak_source": f"BASELINE.md section 4 ALU/issue bound n_SM*128*f_SM/I_u with n_SM={n_sm}, f_SM = median "
                        f"SM clock sampled during the timed region ({f_sm / 1e6:.0f} MHz), I_u={I_U} (cfg5)",
         "probe_ceiling": {"value": probe / 1e9, "frac": achieved / probe,

@@ -19,6 +19,8 @@
  *   tapt_get_energies/_spins    energy(g, s) / magnetization(s) readout      proj/src/spin_model.cpp:79-89,109-114
  *   tapt_get_observables        RunTrace accumulators
  *   tapt_last_error / status    tapt::*Error exceptions                      proj/include/tapt/errors.hpp:11-41
+ *   tapt_former_*               IsingFormer forward_logits / sample /        SPEC.md:275-379 (generator module;
+ *                               log_prob / save/load_checkpoint (ISFW1)      proj/src/generator.cpp:1 is a placeholder)
  *
  * Conventions
  *   - Every function returns a tapt_status (0 = OK); no C++ exception crosses this
@@ -242,6 +244,49 @@ tapt_status tapt_multiplier_decode(uint32_t n, const int8_t* spins, uint64_t C, 
 tapt_status tapt_enumerate_semiprimes(uint32_t n, uint64_t* out, uint32_t cap, uint32_t* count);
 /* p, q: first primes among 2^(bits-1) + below(2^(bits-1)) draws of derive(seed, {0x99, gid}). */
 tapt_status tapt_random_semiprime(uint64_t seed, uint64_t gid, uint32_t bits, uint64_t* p, uint64_t* q);
+
+/* ------------------------------------------------ IsingFormer generator -- */
+/* Decoder-only autoregressive proposal model over spin tokens conditioned on beta
+ * (Appendix F), inference on the device.  Token 1 = spin +1.
+ * Architecture and the SPEC's open choices are fixed in DESIGN.md section 10 (pre-LN blocks,
+ * sinusoidal positions, sinusoidal beta features + linear map added at every position, GELU
+ * (tanh), one Bernoulli logit per position).  Parameters are fp32 in the canonical ISFW1
+ * order.  The device kernels support d_model = 64 with 32-wide heads and ffn = 128 (the
+ * SPEC default); layers, beta_features and max_len are free. */
+typedef struct tapt_former_s* tapt_former_t;
+
+typedef struct {
+    uint32_t d_model;       /* 64 */
+    uint32_t heads;         /* 2 */
+    uint32_t ffn;           /* 128 */
+    uint32_t layers;        /* 2 */
+    uint32_t max_len;       /* longest token sequence */
+    uint32_t beta_features; /* even, sin/cos pairs */
+} tapt_former_config;
+
+/* Number of fp32 parameters of a configuration (68 353 at the SPEC default). */
+size_t tapt_former_param_count(const tapt_former_config* c);
+/* Seeded initialisation (host): matrices N(0, scale^2 / fan_in) from derive(seed, {0x77}),
+ * biases 0, LayerNorm gains 1.  params: [tapt_former_param_count]. */
+tapt_status tapt_former_init_params(const tapt_former_config* c, uint64_t seed, double scale, float* params);
+tapt_status tapt_former_create(const tapt_former_config* c, const float* params, tapt_former_t* out);
+tapt_status tapt_former_destroy(tapt_former_t f);
+tapt_status tapt_former_get(tapt_former_t f, tapt_former_config* c, float* params /* nullable */);
+/* save/load_checkpoint: magic "ISFW1", u32 version (1), u32 config block (d_model, heads,
+ * ffn, layers, max_len, beta_features), u32 parameter count, then little-endian fp32
+ * parameters.  Bad magic / truncation -> TAPT_ERR_FORMAT. */
+tapt_status tapt_former_save(tapt_former_t f, const char* path);
+tapt_status tapt_former_load(const char* path, tapt_former_t* out);
+/* forward_logits / log_prob: tokens [B][T] (0/1, host), betas [B]; log_q [B] sums the
+ * Bernoulli log-probabilities of positions >= n_prefix; logits [B][T] (nullable). */
+tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_t B, uint32_t T, const double* betas,
+                                 uint32_t n_prefix, double* log_q, float* logits);
+/* sample: B sequences of T tokens; positions < n_prefix are forced to prefix[b][t]
+ * (prefix [B][n_prefix], nullable when n_prefix = 0); position t >= n_prefix draws
+ * u = (x >> 11) 2^-53 with x = draw t+1 of stream state streams[b] and takes token 1 iff
+ * u < sigmoid(logit_t).  tokens [B][T] and log_q [B] out (host). */
+tapt_status tapt_former_sample(tapt_former_t f, uint32_t B, uint32_t T, const double* betas, const uint8_t* prefix,
+                               uint32_t n_prefix, const uint64_t* streams, uint8_t* tokens, double* log_q);
 
 #ifdef __cplusplus
 }

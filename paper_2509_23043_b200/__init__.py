@@ -77,11 +77,17 @@ _i8p = C.POINTER(C.c_int8)
 _u8p = C.POINTER(C.c_uint8)
 _f64p = C.POINTER(C.c_double)
 _vp = C.c_void_p
+_f32p = C.POINTER(C.c_float)
 
 
 class EnsembleDesc(C.Structure):
     _fields_ = [("n_instances", C.c_uint32), ("instance_offset", C.c_uint64), ("n_slots", C.c_uint32),
                 ("betas", _f64p), ("seed", C.c_uint64), ("order", C.c_int)]
+
+
+class FormerConfig(C.Structure):
+    _fields_ = [("d_model", C.c_uint32), ("heads", C.c_uint32), ("ffn", C.c_uint32), ("layers", C.c_uint32),
+                ("max_len", C.c_uint32), ("beta_features", C.c_uint32)]
 
 
 class Schedule(C.Structure):
@@ -145,6 +151,15 @@ _SIGS = {
     "tapt_multiplier_decode": (C.c_int, [C.c_uint32, _i8p, C.c_uint64, _u64p, _u64p, C.POINTER(C.c_int)]),
     "tapt_enumerate_semiprimes": (C.c_int, [C.c_uint32, _u64p, C.c_uint32, _u32p]),
     "tapt_random_semiprime": (C.c_int, [C.c_uint64, C.c_uint64, C.c_uint32, _u64p, _u64p]),
+    "tapt_former_param_count": (C.c_size_t, [C.POINTER(FormerConfig)]),
+    "tapt_former_init_params": (C.c_int, [C.POINTER(FormerConfig), C.c_uint64, C.c_double, _f32p]),
+    "tapt_former_create": (C.c_int, [C.POINTER(FormerConfig), _f32p, C.POINTER(_vp)]),
+    "tapt_former_destroy": (C.c_int, [_vp]),
+    "tapt_former_get": (C.c_int, [_vp, C.POINTER(FormerConfig), _f32p]),
+    "tapt_former_save": (C.c_int, [_vp, C.c_char_p]),
+    "tapt_former_load": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
+    "tapt_former_log_prob": (C.c_int, [_vp, _u8p, C.c_uint32, C.c_uint32, _f64p, C.c_uint32, _f64p, _f32p]),
+    "tapt_former_sample": (C.c_int, [_vp, C.c_uint32, C.c_uint32, _f64p, _u8p, C.c_uint32, _u64p, _u8p, _f64p]),
 }
 
 _lib = None
@@ -461,6 +476,101 @@ class Ensemble:
         _check(lib().tapt_generate_proposals(self._h, _p(t, _u32p), len(t), _p(mb, _f64p), int(refine),
                                              _p(acc, _u8p)))
         return acc
+
+
+# -------------------------------------------------------------- IsingFormer --
+
+class Former:
+    """IsingFormer proposal model on the device: forward_logits, log_prob,
+    sample, save/load_checkpoint (ISFW1).  Token 1 = spin +1; parameters fp32 in the
+    canonical ISFW1 order."""
+
+    DEFAULT = dict(d_model=64, heads=2, ffn=128, layers=2, max_len=1024, beta_features=16)
+
+    def __init__(self, params=None, seed=0, scale=1.0, _handle=None, **cfg):
+        if _handle is not None:
+            self._h = _handle
+            c = FormerConfig()
+            _check(lib().tapt_former_get(self._h, C.byref(c), None))
+            self.config = {k: getattr(c, k) for k, _ in FormerConfig._fields_}
+            return
+        conf = dict(self.DEFAULT)
+        conf.update(cfg)
+        self.config = conf
+        c = FormerConfig(**conf)
+        if params is None:
+            params = Former.init_params(seed=seed, scale=scale, **conf)
+        p = np.ascontiguousarray(params, np.float32)
+        if len(p) != Former.param_count(**conf):
+            raise DimensionError("parameter vector length does not match the configuration")
+        h = _vp()
+        _check(lib().tapt_former_create(C.byref(c), _p(p, _f32p), C.byref(h)))
+        self._h = h
+
+    @staticmethod
+    def param_count(**cfg):
+        conf = dict(Former.DEFAULT)
+        conf.update(cfg)
+        return int(lib().tapt_former_param_count(C.byref(FormerConfig(**conf))))
+
+    @staticmethod
+    def init_params(seed=0, scale=1.0, **cfg):
+        conf = dict(Former.DEFAULT)
+        conf.update(cfg)
+        c = FormerConfig(**conf)
+        p = np.zeros(int(lib().tapt_former_param_count(C.byref(c))), np.float32)
+        _check(lib().tapt_former_init_params(C.byref(c), int(seed), float(scale), _p(p, _f32p)))
+        return p
+
+    @property
+    def cfg_tuple(self):
+        c = self.config
+        return (c["d_model"], c["heads"], c["ffn"], c["layers"], c["beta_features"])
+
+    def params(self):
+        p = np.zeros(Former.param_count(**self.config), np.float32)
+        _check(lib().tapt_former_get(self._h, None, _p(p, _f32p)))
+        return p
+
+    def save(self, path):
+        _check(lib().tapt_former_save(self._h, str(path).encode()))
+
+    @classmethod
+    def load(cls, path):
+        h = _vp()
+        _check(lib().tapt_former_load(str(path).encode(), C.byref(h)))
+        return cls(_handle=h)
+
+    def log_prob(self, tokens, betas, n_prefix=0, return_logits=False):
+        t = np.ascontiguousarray(tokens, np.uint8)
+        if t.ndim == 1:
+            t = t[None, :]
+        B, T = t.shape
+        b = np.ascontiguousarray(np.broadcast_to(np.asarray(betas, np.float64), (B,)))
+        lq = np.zeros(B)
+        z = np.zeros((B, T), np.float32) if return_logits else None
+        _check(lib().tapt_former_log_prob(self._h, _p(t, _u8p), B, T, _p(b, _f64p), int(n_prefix), _p(lq, _f64p),
+                                          _p(z, _f32p)))
+        return (lq, z) if return_logits else lq
+
+    def sample(self, B, T, betas, streams, prefix=None):
+        b = np.ascontiguousarray(np.broadcast_to(np.asarray(betas, np.float64), (B,)))
+        s = np.ascontiguousarray(streams, np.uint64)
+        if prefix is None:
+            pre, npre = None, 0
+        else:
+            pre = np.ascontiguousarray(prefix, np.uint8).reshape(B, -1)
+            npre = pre.shape[1]
+        tok = np.zeros((B, T), np.uint8)
+        lq = np.zeros(B)
+        _check(lib().tapt_former_sample(self._h, B, T, _p(b, _f64p), _p(pre, _u8p), npre, _p(s, _u64p),
+                                        _p(tok, _u8p), _p(lq, _f64p)))
+        return tok, lq
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tapt_former_destroy(self._h)
+            self._h = None
 
 
 # ------------------------------------------------------------- problem suite --

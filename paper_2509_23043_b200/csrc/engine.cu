@@ -108,6 +108,17 @@ tapt_status guard(F&& f) {
     }
 }
 
+}  // namespace
+
+// Hooks for the other translation units of the library (former.cu): shared last-error
+// message and launch counter.
+namespace tapt_host {
+void set_last_error(const std::string& m) { g_last_error = m; }
+void note_launches(unsigned n) { g_launches += n; }
+}  // namespace tapt_host
+
+namespace {
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;

@@ -1,0 +1,730 @@
+// former.cu -- IsingFormer proposal model on the device (Appendix F;
+// the reference's proj/src/generator.cpp:1 is a placeholder).  Inference only: forward logits,
+// exact log q (the MH-corrected acceptance of tapt_inject_proposals consumes it) and ancestral
+// sampling from counter-based splitmix64 streams.  Host side: configuration, seeded parameter
+// initialisation and the ISFW1 checkpoint format.
+//
+// Kernel ("row engine"): a CTA of 256 threads advances a block of 32 ROWS through the decoder.
+// A row is one (sequence, position).  Forward/log_prob: the rows are 32 consecutive positions of
+// one sequence.  Sampling: the rows are 32 sequences at the same position.  Per row the layer
+// computes LN1 -> QKV (K, V appended to the row's cache in HBM) -> causal attention over the
+// row's cached keys (one warp per (row, head), online softmax over 32-key chunks, lane = key
+// for the scores and lane = head dimension for P.V) -> out-projection + residual -> LN2 ->
+// FFN (GELU) + residual.  The dense products read fp32 weights from global memory (L1/L2
+// resident, 267 KB) with one column per lane and 8 rows per thread, so every weight load is
+// shared by 8 rows.  Sampling is bound by the K/V cache reads: sum over t of t x 2 layers x
+// (K + V) x 64 x 4 B per sequence.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "tapt/errors.hpp"
+#include "tapt/rng.hpp"
+#include "tapt_gpu.h"
+
+namespace tapt_host {
+void set_last_error(const std::string& m);
+void note_launches(unsigned n);
+}  // namespace tapt_host
+
+namespace tapt_former_dev {
+
+constexpr int D = 64, F = 128, DH = 32, RB = 32, NT = 256, kMaxL = 16;
+
+struct LayerOff {
+    int ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_1, b_1, w_2, b_2;
+};
+
+struct FArgs {
+    const float* W;  // parameters (canonical ISFW1 order)
+    int tok_emb, beta_w, beta_b, lnf_g, lnf_b, head_w, head_b;
+    LayerOff lay[kMaxL];
+    int L, fb;
+    const float* pos;  // [max_len][D] sinusoidal positions
+    int T, n_prefix, B;
+    float* cache;  // [slots][L][T][2][D]: K then V of every cached position
+    const uint8_t* tokens;     // forward: [B][T]; sample: prefix [B][n_prefix]
+    const double* betas;       // [B]
+    float* logits;             // forward: [B][T] (nullable)
+    double* log_q;             // [B]
+    uint8_t* tok_out;          // sample: [B][T]
+    const uint64_t* streams;   // sample: [B]
+};
+
+struct Smem {
+    float X[RB][D];   // residual stream
+    float A[RB][D];   // LayerNorm output
+    float Q[RB][D];   // queries
+    float O[RB][D];   // attention output
+    float Fh[RB][F];  // FFN hidden
+    float Eb[RB][D];  // beta embedding of each row's sequence
+    float z[RB];      // logits
+    int t[RB];        // position of each row
+    int slot[RB];     // cache slot of each row
+    int valid[RB];
+    int tokprev[RB];
+    double lq[RB];
+};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xFFFFFFFFu, v, o));
+    return v;
+}
+
+// LayerNorm of every row (eps 1e-5): warp w handles rows w, w+8, ...; lane holds 2 values.
+__device__ void rows_ln(const float (&X)[RB][D], float (&A)[RB][D], const float* g, const float* b) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int r = w; r < RB; r += NT / 32) {
+        const float x0 = X[r][lane], x1 = X[r][lane + 32];
+        const float mu = warp_sum(x0 + x1) * (1.0f / D);
+        const float d0 = x0 - mu, d1 = x1 - mu;
+        const float var = warp_sum(d0 * d0 + d1 * d1) * (1.0f / D);
+        const float inv = rsqrtf(var + 1e-5f);
+        A[r][lane] = d0 * inv * __ldg(g + lane) + __ldg(b + lane);
+        A[r][lane + 32] = d1 * inv * __ldg(g + lane + 32) + __ldg(b + lane + 32);
+    }
+}
+
+__device__ __forceinline__ float gelu(float x) {
+    return 0.5f * x * (1.0f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
+}
+
+// Out[r][c] = sum_k In[r][k] W[k][c] + b[c] for the 32 rows: lane group (tid & 63) owns
+// columns c0 + 64j, tid >> 6 selects rows rg + 4i.  EPI: 0 store, 1 residual add into Out,
+// 2 GELU then store.
+template <int N, int K, int EPI>
+__device__ void rows_gemm(const float* In, const float* W, const float* bias, float* Out) {
+    constexpr int NC = N / 64;
+    const int c0 = threadIdx.x & 63, rg = threadIdx.x >> 6;
+    float acc[8][NC];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) acc[i][j] = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < K; ++k) {
+        float w[NC];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) w[j] = __ldg(W + (size_t)k * N + c0 + 64 * j);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float a = In[(rg + 4 * i) * K + k];
+#pragma unroll
+            for (int j = 0; j < NC; ++j) acc[i][j] = fmaf(a, w[j], acc[i][j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+            const int r = rg + 4 * i, c = c0 + 64 * j;
+            const float v = acc[i][j] + __ldg(bias + c);
+            if constexpr (EPI == 0) Out[r * N + c] = v;
+            if constexpr (EPI == 1) Out[r * N + c] += v;
+            if constexpr (EPI == 2) Out[r * N + c] = gelu(v);
+        }
+}
+
+// QKV projection: Q to shared memory, K and V appended to each valid row's cache.
+__device__ void rows_qkv(Smem& s, const FArgs& a, int l) {
+    const LayerOff& o = a.lay[l];
+    const float* W = a.W + o.w_qkv;
+    const float* bias = a.W + o.b_qkv;
+    const int c0 = threadIdx.x & 63, rg = threadIdx.x >> 6;
+    float acc[8][3];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) acc[i][j] = 0.f;
+#pragma unroll 4
+    for (int k = 0; k < D; ++k) {
+        float w[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) w[j] = __ldg(W + (size_t)k * 3 * D + c0 + 64 * j);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float x = s.A[rg + 4 * i][k];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) acc[i][j] = fmaf(x, w[j], acc[i][j]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int r = rg + 4 * i;
+        s.Q[r][c0] = acc[i][0] + __ldg(bias + c0);
+        if (s.valid[r]) {
+            float* kv = a.cache + ((((size_t)s.slot[r] * a.L + l) * a.T + s.t[r]) * 2) * D;
+            kv[c0] = acc[i][1] + __ldg(bias + D + c0);
+            kv[D + c0] = acc[i][2] + __ldg(bias + 2 * D + c0);
+        }
+    }
+}
+
+// Causal attention of every valid row over its cached positions 0..t (2 heads of 32).
+__device__ void rows_attention(Smem& s, const FArgs& a, int l, int H) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const float scale = rsqrtf((float)DH);
+    for (int task = w; task < RB * H; task += NT / 32) {
+        const int r = task / H, h = task - r * H;
+        if (!s.valid[r]) {
+            s.O[r][h * DH + lane] = 0.f;
+            continue;
+        }
+        const int tr = s.t[r];
+        const float* base = a.cache + (((size_t)s.slot[r] * a.L + l) * a.T) * 2 * D + h * DH;
+        float m = -INFINITY, lsum = 0.f, o = 0.f;
+        for (int c = 0; c <= tr; c += 32) {
+            const int j = c + lane;
+            float sc = -INFINITY;
+            if (j <= tr) {
+                const float4* kr = reinterpret_cast<const float4*>(base + (size_t)j * 2 * D);
+                float acc = 0.f;
+#pragma unroll
+                for (int q4 = 0; q4 < DH / 4; ++q4) {
+                    const float4 kk = kr[q4];
+                    acc = fmaf(s.Q[r][h * DH + 4 * q4 + 0], kk.x, acc);
+                    acc = fmaf(s.Q[r][h * DH + 4 * q4 + 1], kk.y, acc);
+                    acc = fmaf(s.Q[r][h * DH + 4 * q4 + 2], kk.z, acc);
+                    acc = fmaf(s.Q[r][h * DH + 4 * q4 + 3], kk.w, acc);
+                }
+                sc = acc * scale;
+            }
+            const float mn = fmaxf(m, warp_max(sc));
+            const float corr = __expf(m - mn);  // m = -inf on the first chunk -> 0
+            const float p = j <= tr ? __expf(sc - mn) : 0.f;
+            lsum = lsum * corr + warp_sum(p);
+            o *= corr;
+            const int nk = min(32, tr + 1 - c);
+            const float* vb = base + (size_t)c * 2 * D + D + lane;
+            for (int jj = 0; jj < nk; ++jj) o = fmaf(__shfl_sync(0xFFFFFFFFu, p, jj), vb[(size_t)jj * 2 * D], o);
+            m = mn;
+        }
+        s.O[r][h * DH + lane] = o / lsum;
+    }
+}
+
+// All decoder layers + final LayerNorm + head for the current row block; logits in s.z.
+__device__ void rows_forward(Smem& s, const FArgs& a) {
+    const int H = D / DH;
+    for (int l = 0; l < a.L; ++l) {
+        const LayerOff& o = a.lay[l];
+        rows_ln(s.X, s.A, a.W + o.ln1_g, a.W + o.ln1_b);
+        __syncthreads();
+        rows_qkv(s, a, l);
+        __syncthreads();
+        rows_attention(s, a, l, H);
+        __syncthreads();
+        rows_gemm<D, D, 1>(&s.O[0][0], a.W + o.w_o, a.W + o.b_o, &s.X[0][0]);
+        __syncthreads();
+        rows_ln(s.X, s.A, a.W + o.ln2_g, a.W + o.ln2_b);
+        __syncthreads();
+        rows_gemm<F, D, 2>(&s.A[0][0], a.W + o.w_1, a.W + o.b_1, &s.Fh[0][0]);
+        __syncthreads();
+        rows_gemm<D, F, 1>(&s.Fh[0][0], a.W + o.w_2, a.W + o.b_2, &s.X[0][0]);
+        __syncthreads();
+    }
+    rows_ln(s.X, s.A, a.W + a.lnf_g, a.W + a.lnf_b);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int r = w; r < RB; r += NT / 32) {
+        const float v = warp_sum(s.A[r][lane] * __ldg(a.W + a.head_w + lane) +
+                                 s.A[r][lane + 32] * __ldg(a.W + a.head_w + lane + 32));
+        if (lane == 0) s.z[r] = v + __ldg(a.W + a.head_b);
+    }
+    __syncthreads();
+}
+
+// e_beta for a row: W_beta . [sin(w_k beta), cos(w_k beta)] + b_beta, w_k = 2^k / 4.
+__device__ void beta_embed(const FArgs& a, double beta, float* out) {
+    for (int c = threadIdx.x; c < D; c += NT) {
+        float acc = __ldg(a.W + a.beta_b + c);
+        const int half = a.fb / 2;
+        for (int k = 0; k < half; ++k) {
+            const double wk = ldexp(1.0, k) / 4.0;
+            acc = fmaf((float)sin(wk * beta), __ldg(a.W + a.beta_w + k * D + c), acc);
+            acc = fmaf((float)cos(wk * beta), __ldg(a.W + a.beta_w + (half + k) * D + c), acc);
+        }
+        out[c] = acc;
+    }
+}
+
+__device__ __forceinline__ double log_sigmoid(double z) { return z >= 0 ? -log1p(exp(-z)) : z - log1p(exp(z)); }
+
+// Build the rows' inputs: x = E[tok_prev] (t > 0) + P_t + e_beta.
+__device__ void rows_input(Smem& s, const FArgs& a) {
+    for (int e = threadIdx.x; e < RB * D; e += NT) {
+        const int r = e / D, c = e - r * D;
+        float x = 0.f;
+        if (s.valid[r]) {
+            const int t = s.t[r];
+            x = __ldg(a.pos + (size_t)t * D + c) + s.Eb[r][c];
+            if (t > 0) x += __ldg(a.W + a.tok_emb + s.tokprev[r] * D + c);
+        }
+        s.X[r][c] = x;
+    }
+}
+
+__global__ void __launch_bounds__(NT) k_former_forward(const FArgs a) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    Smem& s = *reinterpret_cast<Smem*>(fsm);
+    const int tid = threadIdx.x;
+    for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
+        beta_embed(a, a.betas[b], &s.Eb[0][0]);
+        __syncthreads();
+        if (tid < RB) s.lq[tid] = 0.0;
+        for (int e = tid + D; e < RB * D; e += NT) (&s.Eb[0][0])[e] = s.Eb[0][e % D];  // same beta for all rows
+        for (int t0 = 0; t0 < a.T; t0 += RB) {
+            if (tid < RB) {
+                const int t = t0 + tid;
+                s.t[tid] = t;
+                s.slot[tid] = blockIdx.x;
+                s.valid[tid] = t < a.T;
+                s.tokprev[tid] = (t > 0 && t < a.T) ? a.tokens[(size_t)b * a.T + t - 1] : 0;
+            }
+            __syncthreads();
+            rows_input(s, a);
+            __syncthreads();
+            rows_forward(s, a);
+            if (tid < RB && s.valid[tid]) {
+                const int t = s.t[tid];
+                const float z = s.z[tid];
+                if (a.logits) a.logits[(size_t)b * a.T + t] = z;
+                if (t >= a.n_prefix) s.lq[tid] += a.tokens[(size_t)b * a.T + t] ? log_sigmoid(z) : log_sigmoid(-z);
+            }
+            __syncthreads();
+        }
+        if (tid == 0) {
+            double q = 0.0;
+            for (int r = 0; r < RB; ++r) q += s.lq[r];
+            a.log_q[b] = q;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(NT) k_former_sample(const FArgs a) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    Smem& s = *reinterpret_cast<Smem*>(fsm);
+    const int tid = threadIdx.x;
+    const int nblk = (a.B + RB - 1) / RB;
+    for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        if (tid < RB) {
+            const int b = blk * RB + tid;
+            s.slot[tid] = blockIdx.x * RB + tid;
+            s.valid[tid] = b < a.B;
+            s.lq[tid] = 0.0;
+            s.tokprev[tid] = 0;
+        }
+        for (int r = 0; r < RB; ++r) {
+            const int b = min(blk * RB + r, a.B - 1);
+            beta_embed(a, a.betas[b], &s.Eb[r][0]);
+        }
+        __syncthreads();
+        for (int t = 0; t < a.T; ++t) {
+            if (tid < RB) s.t[tid] = t;
+            __syncthreads();
+            rows_input(s, a);
+            __syncthreads();
+            rows_forward(s, a);
+            if (tid < RB && s.valid[tid]) {
+                const int b = blk * RB + tid;
+                const double z = s.z[tid];
+                int tok;
+                if (t < a.n_prefix) {
+                    tok = a.tokens[(size_t)b * a.n_prefix + t] ? 1 : 0;
+                } else {
+                    const uint64_t x = tapt_dev::draw(a.streams[b], (uint64_t)t + 1ull);
+                    const double u = (double)(x >> 11) * 0x1.0p-53;
+                    tok = u < 1.0 / (1.0 + exp(-z)) ? 1 : 0;
+                    s.lq[tid] += tok ? log_sigmoid(z) : log_sigmoid(-z);
+                }
+                a.tok_out[(size_t)b * a.T + t] = (uint8_t)tok;
+                s.tokprev[tid] = tok;
+            }
+            __syncthreads();
+        }
+        if (tid < RB && s.valid[tid]) a.log_q[blk * RB + tid] = s.lq[tid];
+        __syncthreads();
+    }
+}
+
+}  // namespace tapt_former_dev
+
+using namespace tapt_former_dev;
+
+// ==================================================================== host ===
+
+namespace {
+
+#define FCUDA(expr)                                                                                      \
+    do {                                                                                                 \
+        cudaError_t e_ = (expr);                                                                         \
+        if (e_ != cudaSuccess) throw tapt::CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+template <class Fn>
+tapt_status fguard(Fn&& f) {
+    try {
+        f();
+        return TAPT_OK;
+    } catch (const tapt::ConfigError& e) {
+        tapt_host::set_last_error(e.what());
+        return TAPT_ERR_CONFIG;
+    } catch (const tapt::DimensionError& e) {
+        tapt_host::set_last_error(e.what());
+        return TAPT_ERR_DIMENSION;
+    } catch (const tapt::SizeError& e) {
+        tapt_host::set_last_error(e.what());
+        return TAPT_ERR_SIZE;
+    } catch (const tapt::FormatError& e) {
+        tapt_host::set_last_error(e.what());
+        return TAPT_ERR_FORMAT;
+    } catch (const tapt::NumericError& e) {
+        tapt_host::set_last_error(e.what());
+        return TAPT_ERR_NUMERIC;
+    } catch (const tapt::CudaError& e) {
+        tapt_host::set_last_error(e.what());
+        return TAPT_ERR_CUDA;
+    } catch (const std::exception& e) {
+        tapt_host::set_last_error(e.what());
+        return TAPT_ERR_INTERNAL;
+    }
+}
+
+struct Layout {
+    size_t total = 0;
+    int tok_emb, beta_w, beta_b, lnf_g, lnf_b, head_w, head_b;
+    std::vector<LayerOff> lay;
+    // (offset, size, fan_in; fan_in 0 = bias/zero, -1 = LN gain/one) for initialisation
+    struct Item {
+        size_t off, size;
+        int fan_in;
+    };
+    std::vector<Item> items;
+};
+
+void check_config(const tapt_former_config* c) {
+    if (!c) throw tapt::ConfigError("null former config");
+    if (c->d_model == 0 || c->heads == 0 || c->ffn == 0 || c->layers == 0 || c->max_len == 0)
+        throw tapt::ConfigError("former dimensions must be >= 1");
+    if (c->d_model % c->heads) throw tapt::ConfigError("d_model must be divisible by heads");
+    if (c->beta_features == 0 || c->beta_features % 2) throw tapt::ConfigError("beta_features must be even and >= 2");
+}
+
+Layout make_layout(const tapt_former_config& c) {
+    Layout L;
+    const int d = (int)c.d_model, f = (int)c.ffn, fb = (int)c.beta_features;
+    size_t o = 0;
+    auto put = [&](size_t n, int fan) {
+        const size_t at = o;
+        L.items.push_back({at, n, fan});
+        o += n;
+        return (int)at;
+    };
+    L.tok_emb = put(2 * (size_t)d, 1);
+    L.beta_w = put((size_t)fb * d, fb);
+    L.beta_b = put(d, 0);
+    for (uint32_t l = 0; l < c.layers; ++l) {
+        LayerOff y;
+        y.ln1_g = put(d, -1);
+        y.ln1_b = put(d, 0);
+        y.w_qkv = put((size_t)d * 3 * d, d);
+        y.b_qkv = put(3 * (size_t)d, 0);
+        y.w_o = put((size_t)d * d, d);
+        y.b_o = put(d, 0);
+        y.ln2_g = put(d, -1);
+        y.ln2_b = put(d, 0);
+        y.w_1 = put((size_t)d * f, d);
+        y.b_1 = put(f, 0);
+        y.w_2 = put((size_t)f * d, f);
+        y.b_2 = put(d, 0);
+        L.lay.push_back(y);
+    }
+    L.lnf_g = put(d, -1);
+    L.lnf_b = put(d, 0);
+    L.head_w = put(d, d);
+    L.head_b = put(1, 0);
+    L.total = o;
+    return L;
+}
+
+}  // namespace
+
+struct tapt_former_s {
+    tapt_former_config cfg{};
+    Layout lay;
+    std::vector<float> params;
+    float* dW = nullptr;
+    float* dpos = nullptr;
+    float* cache = nullptr;
+    size_t cache_n = 0;
+    void* tmp = nullptr;
+    size_t tmp_n = 0;
+    ~tapt_former_s() {
+        if (dW) cudaFree(dW);
+        if (dpos) cudaFree(dpos);
+        if (cache) cudaFree(cache);
+        if (tmp) cudaFree(tmp);
+    }
+    void upload() {
+        if (dW) return;
+        FCUDA(cudaMalloc(&dW, params.size() * sizeof(float)));
+        FCUDA(cudaMemcpy(dW, params.data(), params.size() * sizeof(float), cudaMemcpyHostToDevice));
+        const int d = (int)cfg.d_model;
+        std::vector<float> P((size_t)cfg.max_len * d);
+        for (uint32_t t = 0; t < cfg.max_len; ++t)
+            for (int i = 0; i < d / 2; ++i) {
+                const double ang = (double)t / std::pow(10000.0, 2.0 * i / d);
+                P[(size_t)t * d + 2 * i] = (float)std::sin(ang);
+                P[(size_t)t * d + 2 * i + 1] = (float)std::cos(ang);
+            }
+        FCUDA(cudaMalloc(&dpos, P.size() * sizeof(float)));
+        FCUDA(cudaMemcpy(dpos, P.data(), P.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    float* need_cache(size_t n) {
+        if (n > cache_n) {
+            if (cache) cudaFree(cache);
+            cache = nullptr;
+            FCUDA(cudaMalloc(&cache, n * sizeof(float)));
+            cache_n = n;
+        }
+        return cache;
+    }
+    uint8_t* need_tmp(size_t bytes) {
+        if (bytes > tmp_n) {
+            if (tmp) cudaFree(tmp);
+            tmp = nullptr;
+            FCUDA(cudaMalloc(&tmp, bytes));
+            tmp_n = bytes;
+        }
+        return static_cast<uint8_t*>(tmp);
+    }
+    FArgs args() const {
+        FArgs a{};
+        a.W = dW;
+        a.tok_emb = lay.tok_emb;
+        a.beta_w = lay.beta_w;
+        a.beta_b = lay.beta_b;
+        a.lnf_g = lay.lnf_g;
+        a.lnf_b = lay.lnf_b;
+        a.head_w = lay.head_w;
+        a.head_b = lay.head_b;
+        for (size_t l = 0; l < lay.lay.size(); ++l) a.lay[l] = lay.lay[l];
+        a.L = (int)cfg.layers;
+        a.fb = (int)cfg.beta_features;
+        a.pos = dpos;
+        return a;
+    }
+};
+
+namespace {
+
+void check_device_shape(const tapt_former_config& c) {
+    if (c.d_model != (uint32_t)D || c.d_model / c.heads != (uint32_t)DH || c.ffn != (uint32_t)F)
+        throw tapt::SizeError("device kernels support d_model = 64, 32-wide heads, ffn = 128 (the SPEC default)");
+    if (c.layers > (uint32_t)kMaxL) throw tapt::SizeError("at most 16 layers");
+}
+
+int sm_count() {
+    int dev = 0, n = 0;
+    FCUDA(cudaGetDevice(&dev));
+    FCUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    return n;
+}
+
+tapt_former_s* check_former(tapt_former_t f) {
+    if (!f) throw tapt::ConfigError("null former handle");
+    return f;
+}
+
+tapt_former_s* create_former(const tapt_former_config* c, const float* params) {
+    check_config(c);
+    if (!params) throw tapt::ConfigError("null parameters");
+    auto f = std::make_unique<tapt_former_s>();
+    f->cfg = *c;
+    f->lay = make_layout(*c);
+    f->params.assign(params, params + f->lay.total);
+    for (float v : f->params)
+        if (!std::isfinite(v)) throw tapt::NumericError("non-finite parameter");
+    check_device_shape(*c);
+    return f.release();  // device copies are made on first use (create/save/load work without a GPU)
+}
+
+template <class K>
+void launch_rows(K kernel, int grid, const FArgs& a) {
+    const int smem = (int)sizeof(Smem);
+    FCUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kernel<<<grid, NT, smem>>>(a);
+    tapt_host::note_launches(1);
+    FCUDA(cudaGetLastError());
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t tapt_former_param_count(const tapt_former_config* c) {
+    if (!c || c->d_model == 0 || c->beta_features == 0) return 0;
+    return make_layout(*c).total;
+}
+
+tapt_status tapt_former_init_params(const tapt_former_config* c, uint64_t seed, double scale, float* params) {
+    return fguard([&] {
+        check_config(c);
+        if (!params) throw tapt::ConfigError("null parameter buffer");
+        const Layout L = make_layout(*c);
+        tapt::RngStream r = tapt::RngStream::derive(seed, {0x77});
+        for (const auto& it : L.items) {
+            for (size_t k = 0; k < it.size; ++k) {
+                float v;
+                if (it.fan_in == 0) {
+                    v = 0.f;
+                } else if (it.fan_in < 0) {
+                    v = 1.f;
+                } else {  // Box-Muller on two 53-bit uniforms
+                    const double u1 = 1.0 - r.uniform(), u2 = r.uniform();
+                    const double g = std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
+                    v = (float)(scale * g / std::sqrt((double)it.fan_in));
+                }
+                params[it.off + k] = v;
+            }
+        }
+    });
+}
+
+tapt_status tapt_former_create(const tapt_former_config* c, const float* params, tapt_former_t* out) {
+    return fguard([&] {
+        if (!out) throw tapt::ConfigError("null output handle");
+        *out = create_former(c, params);
+    });
+}
+
+tapt_status tapt_former_destroy(tapt_former_t f) {
+    delete f;
+    return TAPT_OK;
+}
+
+tapt_status tapt_former_get(tapt_former_t f, tapt_former_config* c, float* params) {
+    return fguard([&] {
+        check_former(f);
+        if (c) *c = f->cfg;
+        if (params) std::memcpy(params, f->params.data(), f->params.size() * sizeof(float));
+    });
+}
+
+tapt_status tapt_former_save(tapt_former_t f, const char* path) {
+    return fguard([&] {
+        check_former(f);
+        if (!path) throw tapt::ConfigError("null path");
+        std::ofstream o(path, std::ios::binary);
+        if (!o) throw tapt::FormatError(std::string("cannot open ") + path);
+        o.write("ISFW1", 5);
+        const uint32_t hdr[8] = {1u, f->cfg.d_model, f->cfg.heads, f->cfg.ffn, f->cfg.layers, f->cfg.max_len,
+                                 f->cfg.beta_features, (uint32_t)f->params.size()};
+        o.write(reinterpret_cast<const char*>(hdr), sizeof(hdr));  // little-endian hosts only (x86-64, aarch64)
+        o.write(reinterpret_cast<const char*>(f->params.data()), (std::streamsize)(f->params.size() * sizeof(float)));
+        if (!o) throw tapt::FormatError("write failed");
+    });
+}
+
+tapt_status tapt_former_load(const char* path, tapt_former_t* out) {
+    return fguard([&] {
+        if (!path || !out) throw tapt::ConfigError("null path / output");
+        std::ifstream in(path, std::ios::binary);
+        if (!in) throw tapt::FormatError(std::string("cannot open ") + path);
+        char magic[5];
+        in.read(magic, 5);
+        if (!in || std::memcmp(magic, "ISFW1", 5) != 0) throw tapt::FormatError("bad ISFW1 magic");
+        uint32_t hdr[8];
+        in.read(reinterpret_cast<char*>(hdr), sizeof(hdr));
+        if (!in) throw tapt::FormatError("truncated ISFW1 header");
+        if (hdr[0] != 1u) throw tapt::FormatError("unsupported ISFW1 version");
+        tapt_former_config c{hdr[1], hdr[2], hdr[3], hdr[4], hdr[5], hdr[6]};
+        check_config(&c);
+        const size_t n = make_layout(c).total;
+        if (hdr[7] != n) throw tapt::FormatError("ISFW1 parameter count does not match its config");
+        std::vector<float> p(n);
+        in.read(reinterpret_cast<char*>(p.data()), (std::streamsize)(n * sizeof(float)));
+        if (!in) throw tapt::FormatError("truncated ISFW1 parameters");
+        *out = create_former(&c, p.data());
+    });
+}
+
+tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_t B, uint32_t T, const double* betas,
+                                 uint32_t n_prefix, double* log_q, float* logits) {
+    return fguard([&] {
+        check_former(f);
+        if (!tokens || !betas || !log_q) throw tapt::ConfigError("null tokens / betas / log_q");
+        if (T == 0 || T > f->cfg.max_len) throw tapt::SizeError("sequence length must be in [1, max_len]");
+        if (n_prefix > T) throw tapt::DimensionError("prefix longer than the sequence");
+        if (B == 0) return;
+        const int grid = (int)std::min<uint32_t>(B, (uint32_t)sm_count() * 4);
+        f->upload();
+        FArgs a = f->args();
+        a.T = (int)T;
+        a.n_prefix = (int)n_prefix;
+        a.B = (int)B;
+        a.cache = f->need_cache((size_t)grid * f->cfg.layers * T * 2 * D);
+        const size_t tb = (size_t)B * T, off_b = (tb + 255) & ~size_t(255), off_q = off_b + (size_t)B * 8,
+                     off_z = off_q + (size_t)B * 8;
+        uint8_t* tmp = f->need_tmp(off_z + (logits ? tb * 4 : 0));
+        FCUDA(cudaMemcpy(tmp, tokens, tb, cudaMemcpyHostToDevice));
+        FCUDA(cudaMemcpy(tmp + off_b, betas, (size_t)B * 8, cudaMemcpyHostToDevice));
+        a.tokens = tmp;
+        a.betas = reinterpret_cast<const double*>(tmp + off_b);
+        a.log_q = reinterpret_cast<double*>(tmp + off_q);
+        a.logits = logits ? reinterpret_cast<float*>(tmp + off_z) : nullptr;
+        launch_rows(k_former_forward, grid, a);
+        FCUDA(cudaMemcpy(log_q, a.log_q, (size_t)B * 8, cudaMemcpyDeviceToHost));
+        if (logits) FCUDA(cudaMemcpy(logits, a.logits, tb * 4, cudaMemcpyDeviceToHost));
+    });
+}
+
+tapt_status tapt_former_sample(tapt_former_t f, uint32_t B, uint32_t T, const double* betas, const uint8_t* prefix,
+                               uint32_t n_prefix, const uint64_t* streams, uint8_t* tokens, double* log_q) {
+    return fguard([&] {
+        check_former(f);
+        if (!betas || !streams || !tokens || !log_q) throw tapt::ConfigError("null betas / streams / outputs");
+        if (T == 0 || T > f->cfg.max_len) throw tapt::SizeError("sequence length must be in [1, max_len]");
+        if (n_prefix > T) throw tapt::DimensionError("prefix longer than the sequence");
+        if (n_prefix && !prefix) throw tapt::ConfigError("null prefix");
+        if (B == 0) return;
+        const int nblk = (int)((B + RB - 1) / RB);
+        const int grid = std::min(nblk, sm_count() * 4);
+        f->upload();
+        FArgs a = f->args();
+        a.T = (int)T;
+        a.n_prefix = (int)n_prefix;
+        a.B = (int)B;
+        a.cache = f->need_cache((size_t)grid * RB * f->cfg.layers * T * 2 * D);
+        const size_t pb = (size_t)B * n_prefix, off_b = (pb + 255) & ~size_t(255), off_s = off_b + (size_t)B * 8,
+                     off_q = off_s + (size_t)B * 8, off_t = off_q + (size_t)B * 8;
+        uint8_t* tmp = f->need_tmp(off_t + (size_t)B * T);
+        if (pb) FCUDA(cudaMemcpy(tmp, prefix, pb, cudaMemcpyHostToDevice));
+        FCUDA(cudaMemcpy(tmp + off_b, betas, (size_t)B * 8, cudaMemcpyHostToDevice));
+        FCUDA(cudaMemcpy(tmp + off_s, streams, (size_t)B * 8, cudaMemcpyHostToDevice));
+        a.tokens = tmp;
+        a.betas = reinterpret_cast<const double*>(tmp + off_b);
+        a.streams = reinterpret_cast<const uint64_t*>(tmp + off_s);
+        a.log_q = reinterpret_cast<double*>(tmp + off_q);
+        a.tok_out = tmp + off_t;
+        launch_rows(k_former_sample, grid, a);
+        FCUDA(cudaMemcpy(tokens, a.tok_out, (size_t)B * T, cudaMemcpyDeviceToHost));
+        FCUDA(cudaMemcpy(log_q, a.log_q, (size_t)B * 8, cudaMemcpyDeviceToHost));
+    });
+}
+
+}  // extern "C"
