@@ -36,7 +36,7 @@ void note_launches(unsigned n);
 
 namespace tapt_former_dev {
 
-constexpr int D = 64, F = 128, DH = 32, RB = 32, NT = 256, kMaxL = 16;
+constexpr int D = 64, F = 128, DH = 32, NT = 256, kMaxL = 16;
 
 struct LayerOff {
     int ln1_g, ln1_b, w_qkv, b_qkv, w_o, b_o, ln2_g, ln2_b, w_1, b_1, w_2, b_2;
@@ -58,6 +58,7 @@ struct FArgs {
     const uint64_t* streams;   // sample: [B]
 };
 
+template <int RB>
 struct Smem {
     float X[RB][D];   // residual stream
     float A[RB][D];   // LayerNorm output
@@ -85,6 +86,7 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // LayerNorm of every row (eps 1e-5): warp w handles rows w, w+8, ...; lane holds 2 values.
+template <int RB>
 __device__ void rows_ln(const float (&X)[RB][D], float (&A)[RB][D], const float* g, const float* b) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int r = w; r < RB; r += NT / 32) {
@@ -102,32 +104,39 @@ __device__ __forceinline__ float gelu(float x) {
     return 0.5f * x * (1.0f + tanhf(0.7978845608028654f * (x + 0.044715f * x * x * x)));
 }
 
-// Out[r][c] = sum_k In[r][k] W[k][c] + b[c] for the 32 rows: lane group (tid & 63) owns
-// columns c0 + 64j, tid >> 6 selects rows rg + 4i.  EPI: 0 store, 1 residual add into Out,
-// 2 GELU then store.
-template <int N, int K, int EPI>
+// Out[r][c] = sum_k In[r][k] W[k][c] + b[c] for the RB rows: lane group (tid & 63) owns
+// columns c0 + 64j, tid >> 6 selects rows rg + 4i; A is read 4 k at a time (LDS.128,
+// broadcast within a warp).  EPI: 0 store, 1 residual add into Out, 2 GELU then store.
+template <int RB, int N, int K, int EPI>
 __device__ void rows_gemm(const float* In, const float* W, const float* bias, float* Out) {
-    constexpr int NC = N / 64;
+    constexpr int NC = N / 64, NR = RB / 4;
     const int c0 = threadIdx.x & 63, rg = threadIdx.x >> 6;
-    float acc[8][NC];
+    float acc[NR][NC];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < NR; ++i)
 #pragma unroll
         for (int j = 0; j < NC; ++j) acc[i][j] = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < K; ++k) {
-        float w[NC];
+#pragma unroll 2
+    for (int k = 0; k < K; k += 4) {
+        float w[4][NC];
 #pragma unroll
-        for (int j = 0; j < NC; ++j) w[j] = __ldg(W + (size_t)k * N + c0 + 64 * j);
+        for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float a = In[(rg + 4 * i) * K + k];
+            for (int j = 0; j < NC; ++j) w[kk][j] = __ldg(W + (size_t)(k + kk) * N + c0 + 64 * j);
 #pragma unroll
-            for (int j = 0; j < NC; ++j) acc[i][j] = fmaf(a, w[j], acc[i][j]);
+        for (int i = 0; i < NR; ++i) {
+            const float4 a = *reinterpret_cast<const float4*>(In + (rg + 4 * i) * K + k);
+#pragma unroll
+            for (int j = 0; j < NC; ++j) {
+                acc[i][j] = fmaf(a.x, w[0][j], acc[i][j]);
+                acc[i][j] = fmaf(a.y, w[1][j], acc[i][j]);
+                acc[i][j] = fmaf(a.z, w[2][j], acc[i][j]);
+                acc[i][j] = fmaf(a.w, w[3][j], acc[i][j]);
+            }
         }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < NR; ++i)
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
             const int r = rg + 4 * i, c = c0 + 64 * j;
@@ -139,30 +148,39 @@ __device__ void rows_gemm(const float* In, const float* W, const float* bias, fl
 }
 
 // QKV projection: Q to shared memory, K and V appended to each valid row's cache.
-__device__ void rows_qkv(Smem& s, const FArgs& a, int l) {
+template <int RB>
+__device__ void rows_qkv(Smem<RB>& s, const FArgs& a, int l) {
+    constexpr int NR = RB / 4;
     const LayerOff& o = a.lay[l];
     const float* W = a.W + o.w_qkv;
     const float* bias = a.W + o.b_qkv;
     const int c0 = threadIdx.x & 63, rg = threadIdx.x >> 6;
-    float acc[8][3];
+    float acc[NR][3];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < NR; ++i)
 #pragma unroll
         for (int j = 0; j < 3; ++j) acc[i][j] = 0.f;
-#pragma unroll 4
-    for (int k = 0; k < D; ++k) {
-        float w[3];
+#pragma unroll 2
+    for (int k = 0; k < D; k += 4) {
+        float w[4][3];
 #pragma unroll
-        for (int j = 0; j < 3; ++j) w[j] = __ldg(W + (size_t)k * 3 * D + c0 + 64 * j);
+        for (int kk = 0; kk < 4; ++kk)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float x = s.A[rg + 4 * i][k];
+            for (int j = 0; j < 3; ++j) w[kk][j] = __ldg(W + (size_t)(k + kk) * 3 * D + c0 + 64 * j);
 #pragma unroll
-            for (int j = 0; j < 3; ++j) acc[i][j] = fmaf(x, w[j], acc[i][j]);
+        for (int i = 0; i < NR; ++i) {
+            const float4 x = *reinterpret_cast<const float4*>(&s.A[rg + 4 * i][k]);
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                acc[i][j] = fmaf(x.x, w[0][j], acc[i][j]);
+                acc[i][j] = fmaf(x.y, w[1][j], acc[i][j]);
+                acc[i][j] = fmaf(x.z, w[2][j], acc[i][j]);
+                acc[i][j] = fmaf(x.w, w[3][j], acc[i][j]);
+            }
         }
     }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < NR; ++i) {
         const int r = rg + 4 * i;
         s.Q[r][c0] = acc[i][0] + __ldg(bias + c0);
         if (s.valid[r]) {
@@ -174,7 +192,8 @@ __device__ void rows_qkv(Smem& s, const FArgs& a, int l) {
 }
 
 // Causal attention of every valid row over its cached positions 0..t (2 heads of 32).
-__device__ void rows_attention(Smem& s, const FArgs& a, int l, int H) {
+template <int RB>
+__device__ void rows_attention(Smem<RB>& s, const FArgs& a, int l, int H) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const float scale = rsqrtf((float)DH);
     for (int task = w; task < RB * H; task += NT / 32) {
@@ -209,7 +228,12 @@ __device__ void rows_attention(Smem& s, const FArgs& a, int l, int H) {
             o *= corr;
             const int nk = min(32, tr + 1 - c);
             const float* vb = base + (size_t)c * 2 * D + D + lane;
-            for (int jj = 0; jj < nk; ++jj) o = fmaf(__shfl_sync(0xFFFFFFFFu, p, jj), vb[(size_t)jj * 2 * D], o);
+            if (nk == 32) {  // full chunk: unrolled so the 32 V-row loads issue ahead of the FMAs
+#pragma unroll 8
+                for (int jj = 0; jj < 32; ++jj) o = fmaf(__shfl_sync(0xFFFFFFFFu, p, jj), vb[(size_t)jj * 2 * D], o);
+            } else {
+                for (int jj = 0; jj < nk; ++jj) o = fmaf(__shfl_sync(0xFFFFFFFFu, p, jj), vb[(size_t)jj * 2 * D], o);
+            }
             m = mn;
         }
         s.O[r][h * DH + lane] = o / lsum;
@@ -217,7 +241,8 @@ __device__ void rows_attention(Smem& s, const FArgs& a, int l, int H) {
 }
 
 // All decoder layers + final LayerNorm + head for the current row block; logits in s.z.
-__device__ void rows_forward(Smem& s, const FArgs& a) {
+template <int RB>
+__device__ void rows_forward(Smem<RB>& s, const FArgs& a) {
     const int H = D / DH;
     for (int l = 0; l < a.L; ++l) {
         const LayerOff& o = a.lay[l];
@@ -227,13 +252,13 @@ __device__ void rows_forward(Smem& s, const FArgs& a) {
         __syncthreads();
         rows_attention(s, a, l, H);
         __syncthreads();
-        rows_gemm<D, D, 1>(&s.O[0][0], a.W + o.w_o, a.W + o.b_o, &s.X[0][0]);
+        rows_gemm<RB, D, D, 1>(&s.O[0][0], a.W + o.w_o, a.W + o.b_o, &s.X[0][0]);
         __syncthreads();
         rows_ln(s.X, s.A, a.W + o.ln2_g, a.W + o.ln2_b);
         __syncthreads();
-        rows_gemm<F, D, 2>(&s.A[0][0], a.W + o.w_1, a.W + o.b_1, &s.Fh[0][0]);
+        rows_gemm<RB, F, D, 2>(&s.A[0][0], a.W + o.w_1, a.W + o.b_1, &s.Fh[0][0]);
         __syncthreads();
-        rows_gemm<D, F, 1>(&s.Fh[0][0], a.W + o.w_2, a.W + o.b_2, &s.X[0][0]);
+        rows_gemm<RB, D, F, 1>(&s.Fh[0][0], a.W + o.w_2, a.W + o.b_2, &s.X[0][0]);
         __syncthreads();
     }
     rows_ln(s.X, s.A, a.W + a.lnf_g, a.W + a.lnf_b);
@@ -264,7 +289,8 @@ __device__ void beta_embed(const FArgs& a, double beta, float* out) {
 __device__ __forceinline__ double log_sigmoid(double z) { return z >= 0 ? -log1p(exp(-z)) : z - log1p(exp(z)); }
 
 // Build the rows' inputs: x = E[tok_prev] (t > 0) + P_t + e_beta.
-__device__ void rows_input(Smem& s, const FArgs& a) {
+template <int RB>
+__device__ void rows_input(Smem<RB>& s, const FArgs& a) {
     for (int e = threadIdx.x; e < RB * D; e += NT) {
         const int r = e / D, c = e - r * D;
         float x = 0.f;
@@ -278,8 +304,9 @@ __device__ void rows_input(Smem& s, const FArgs& a) {
 }
 
 __global__ void __launch_bounds__(NT) k_former_forward(const FArgs a) {
+    constexpr int RB = 32;
     extern __shared__ __align__(16) unsigned char fsm[];
-    Smem& s = *reinterpret_cast<Smem*>(fsm);
+    Smem<RB>& s = *reinterpret_cast<Smem<RB>*>(fsm);
     const int tid = threadIdx.x;
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
         beta_embed(a, a.betas[b], &s.Eb[0][0]);
@@ -315,9 +342,10 @@ __global__ void __launch_bounds__(NT) k_former_forward(const FArgs a) {
     }
 }
 
+template <int RB>
 __global__ void __launch_bounds__(NT) k_former_sample(const FArgs a) {
     extern __shared__ __align__(16) unsigned char fsm[];
-    Smem& s = *reinterpret_cast<Smem*>(fsm);
+    Smem<RB>& s = *reinterpret_cast<Smem<RB>*>(fsm);
     const int tid = threadIdx.x;
     const int nblk = (a.B + RB - 1) / RB;
     for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
@@ -563,9 +591,9 @@ tapt_former_s* create_former(const tapt_former_config* c, const float* params) {
     return f.release();  // device copies are made on first use (create/save/load work without a GPU)
 }
 
-template <class K>
+template <int RB, class K>
 void launch_rows(K kernel, int grid, const FArgs& a) {
-    const int smem = (int)sizeof(Smem);
+    const int smem = (int)sizeof(Smem<RB>);
     FCUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kernel<<<grid, NT, smem>>>(a);
     tapt_host::note_launches(1);
@@ -687,7 +715,7 @@ tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_
         a.betas = reinterpret_cast<const double*>(tmp + off_b);
         a.log_q = reinterpret_cast<double*>(tmp + off_q);
         a.logits = logits ? reinterpret_cast<float*>(tmp + off_z) : nullptr;
-        launch_rows(k_former_forward, grid, a);
+        launch_rows<32>(k_former_forward, grid, a);
         FCUDA(cudaMemcpy(log_q, a.log_q, (size_t)B * 8, cudaMemcpyDeviceToHost));
         if (logits) FCUDA(cudaMemcpy(logits, a.logits, tb * 4, cudaMemcpyDeviceToHost));
     });
@@ -702,14 +730,17 @@ tapt_status tapt_former_sample(tapt_former_t f, uint32_t B, uint32_t T, const do
         if (n_prefix > T) throw tapt::DimensionError("prefix longer than the sequence");
         if (n_prefix && !prefix) throw tapt::ConfigError("null prefix");
         if (B == 0) return;
-        const int nblk = (int)((B + RB - 1) / RB);
-        const int grid = std::min(nblk, sm_count() * 4);
+        // rows (sequences) per CTA: the largest of 32 / 8 / 4 that still gives two CTAs per SM
+        const int nsm = sm_count();
+        const int RBs = (B + 31) / 32 >= 2u * nsm ? 32 : ((B + 7) / 8 >= 2u * nsm ? 8 : 4);
+        const int nblk = (int)((B + RBs - 1) / RBs);
+        const int grid = std::min(nblk, nsm * (RBs == 32 ? 4 : 8));
         f->upload();
         FArgs a = f->args();
         a.T = (int)T;
         a.n_prefix = (int)n_prefix;
         a.B = (int)B;
-        a.cache = f->need_cache((size_t)grid * RB * f->cfg.layers * T * 2 * D);
+        a.cache = f->need_cache((size_t)grid * RBs * f->cfg.layers * T * 2 * D);
         const size_t pb = (size_t)B * n_prefix, off_b = (pb + 255) & ~size_t(255), off_s = off_b + (size_t)B * 8,
                      off_q = off_s + (size_t)B * 8, off_t = off_q + (size_t)B * 8;
         uint8_t* tmp = f->need_tmp(off_t + (size_t)B * T);
@@ -721,7 +752,12 @@ tapt_status tapt_former_sample(tapt_former_t f, uint32_t B, uint32_t T, const do
         a.streams = reinterpret_cast<const uint64_t*>(tmp + off_s);
         a.log_q = reinterpret_cast<double*>(tmp + off_q);
         a.tok_out = tmp + off_t;
-        launch_rows(k_former_sample, grid, a);
+        if (RBs == 32)
+            launch_rows<32>(k_former_sample<32>, grid, a);
+        else if (RBs == 8)
+            launch_rows<8>(k_former_sample<8>, grid, a);
+        else
+            launch_rows<4>(k_former_sample<4>, grid, a);
         FCUDA(cudaMemcpy(tokens, a.tok_out, (size_t)B * T, cudaMemcpyDeviceToHost));
         FCUDA(cudaMemcpy(log_q, a.log_q, (size_t)B * 8, cudaMemcpyDeviceToHost));
     });

@@ -7,6 +7,7 @@
 #include <iostream>
 #include <sstream>
 
+#include "tapt/generator.hpp"
 #include "tapt/lattice.hpp"
 #include "tapt/mcmc.hpp"
 #include "tapt/tempering.hpp"
@@ -114,6 +115,18 @@ static int cpu_tests() {
     // C ABI digest matches
     std::uint64_t dig = 0;
     CHECK(tapt_model_digest(and_gate().device(), &dig) == TAPT_OK && dig == and_gate().digest());
+    // IsingFormer host side: default parameter count, ISFW1 round trip
+    {
+        GeneratorConfig gc;
+        CHECK(gc.parameter_count() == 68353);
+        auto gl = LatticeSpec::grid2d(4, 4, 1.0, LatticeSpec::Boundary::periodic).graph();
+        IsingFormer f(gl, gc, IsingFormer::init_params(gc, 1));
+        const std::string path = "tests/cpp/build/former_cpu.isfw";
+        f.save_checkpoint(path);
+        auto f2 = IsingFormer::load_checkpoint(gl, path);
+        CHECK(f2.config().max_sequence_length == gc.max_sequence_length && f2.prefix_length() == 0);
+        CHECK(throws<DimensionError>([&] { IsingFormer(gl, gc, ParameterSet(10)); }));
+    }
     std::printf("cpu ok\n");
     return 0;
 }
@@ -196,6 +209,29 @@ static int gpu_tests() {
     CHECK(t0.move_kind.empty());
     auto rho = residual_energy(tr, -2.0 * 256, 256);
     CHECK(rho.size() == tr.energies.size() && rho.back() >= 0.0);
+    // IsingFormer as run_tapt's proposal source with the MH-corrected move
+    {
+        GeneratorConfig gc;
+        gc.max_sequence_length = 256;
+        IsingFormer gen(g, gc, IsingFormer::init_params(gc, 5, 1.0));
+        RngStream rr(3);
+        auto p = gen.sample(0, 0.5, {}, 0, rr);
+        CHECK(std::fabs(gen.last_log_q() - gen.log_prob(p, 0.5)) < 1e-4);
+        CHECK(rr.state() == RngStream(3).state() + 256 * 0x9E3779B97F4A7C15ull);
+        const std::string path = "tests/cpp/build/former_gpu.isfw";
+        gen.save_checkpoint(path);
+        auto g2 = IsingFormer::load_checkpoint(g, path);
+        CHECK(g2.forward_logits(p, 0.5) == gen.forward_logits(p, 0.5));
+        TAPTConfig c3 = cfg;
+        c3.n_swap = 30;
+        c3.N_T = 4;
+        c3.mh_corrected = true;
+        c3.context_fraction = 0.25;
+        auto tf = run_tapt(g, ladder, c3, &gen);
+        std::uint64_t a3 = 0;
+        for (auto v : tf.gen_attempts) a3 += v;
+        CHECK(a3 == 4 * 10 && energy(g, tf.final_state) == tf.final_energy);
+    }
     auto al = adaptive_ladder(g, 0.2, 1.0, 0.5, 50, 1);
     for (std::size_t r = 1; r < al.betas.size(); ++r) CHECK(al.betas[r] > al.betas[r - 1]);
     CHECK(al.betas.front() == 0.2 && al.betas.back() == 1.0);
