@@ -18,6 +18,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
 #include <memory>
@@ -732,7 +733,8 @@ tapt_status tapt_former_sample(tapt_former_t f, uint32_t B, uint32_t T, const do
         if (B == 0) return;
         // rows (sequences) per CTA: the largest of 32 / 8 / 4 that still gives two CTAs per SM
         const int nsm = sm_count();
-        const int RBs = (B + 31) / 32 >= 2u * nsm ? 32 : ((B + 7) / 8 >= 2u * nsm ? 8 : 4);
+        int RBs = (B + 31) / 32 >= 2u * nsm ? 32 : ((B + 7) / 8 >= 2u * nsm ? 8 : 4);
+        if (const char* e = std::getenv("TAPT_FORMER_RB")) RBs = std::atoi(e) >= 32 ? 32 : (std::atoi(e) >= 8 ? 8 : 4);
         const int nblk = (int)((B + RBs - 1) / RBs);
         const int grid = std::min(nblk, nsm * (RBs == 32 ? 4 : 8));
         f->upload();
