@@ -8,8 +8,8 @@
 // A row is one (sequence, position).  Forward/log_prob: the rows are 32 consecutive positions of
 // one sequence.  Sampling: the rows are 32 sequences at the same position.  Per row the layer
 // computes LN1 -> QKV (K, V appended to the row's cache in HBM) -> causal attention over the
-// row's cached keys (one warp per (row, head), online softmax over 32-key chunks, lane = key
-// for the scores and lane = head dimension for P.V) -> out-projection + residual -> LN2 ->
+// row's cached keys (one warp per (row, head), online softmax over 32-key chunks, each chunk's
+// K and V loads issued together) -> out-projection + residual -> LN2 ->
 // FFN (GELU) + residual.  The dense products read fp32 weights from global memory (L1/L2
 // resident, 267 KB) with one column per lane and 8 rows per thread, so every weight load is
 // shared by 8 rows.  Sampling is bound by the K/V cache reads: sum over t of t x 2 layers x
@@ -192,10 +192,15 @@ __device__ void rows_qkv(Smem<RB>& s, const FArgs& a, int l) {
     }
 }
 
-// Causal attention of every valid row over its cached positions 0..t (2 heads of 32).
+// Causal attention of every valid row over its cached positions 0..t (2 heads of 32): one
+// warp per (row, head), online softmax over 32-key chunks.  Per chunk every lane issues all of
+// its loads up front -- its key's K row (8 x float4) and a float4 slice of 8 V rows (keys
+// c + 4i + lane/8, dims 4*(lane%8)..+3) -- so a chunk costs one memory round trip; the lanes
+// sharing a dimension slice are reduced once per task.
 template <int RB>
 __device__ void rows_attention(Smem<RB>& s, const FArgs& a, int l, int H) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int kq = lane >> 3, dq = 4 * (lane & 7);
     const float scale = rsqrtf((float)DH);
     for (int task = w; task < RB * H; task += NT / 32) {
         const int r = task / H, h = task - r * H;
@@ -205,39 +210,60 @@ __device__ void rows_attention(Smem<RB>& s, const FArgs& a, int l, int H) {
         }
         const int tr = s.t[r];
         const float* base = a.cache + (((size_t)s.slot[r] * a.L + l) * a.T) * 2 * D + h * DH;
-        float m = -INFINITY, lsum = 0.f, o = 0.f;
+        const float4* q4 = reinterpret_cast<const float4*>(&s.Q[r][h * DH]);
+        float m = -INFINITY, lsum = 0.f;
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
         for (int c = 0; c <= tr; c += 32) {
             const int j = c + lane;
-            float sc = -INFINITY;
-            if (j <= tr) {
-                const float4* kr = reinterpret_cast<const float4*>(base + (size_t)j * 2 * D);
-                float acc = 0.f;
+            float4 kk[DH / 4], vv[8];
 #pragma unroll
-                for (int q4 = 0; q4 < DH / 4; ++q4) {
-                    const float4 kk = kr[q4];
-                    acc = fmaf(s.Q[r][h * DH + 4 * q4 + 0], kk.x, acc);
-                    acc = fmaf(s.Q[r][h * DH + 4 * q4 + 1], kk.y, acc);
-                    acc = fmaf(s.Q[r][h * DH + 4 * q4 + 2], kk.z, acc);
-                    acc = fmaf(s.Q[r][h * DH + 4 * q4 + 3], kk.w, acc);
-                }
-                sc = acc * scale;
+            for (int q = 0; q < DH / 4; ++q)
+                kk[q] = j <= tr ? reinterpret_cast<const float4*>(base + (size_t)j * 2 * D)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int key = c + 4 * i + kq;
+                vv[i] = key <= tr ? *reinterpret_cast<const float4*>(base + (size_t)key * 2 * D + D + dq)
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
             }
+            float acc = 0.f;
+#pragma unroll
+            for (int q = 0; q < DH / 4; ++q) {
+                const float4 qq = q4[q];
+                acc = fmaf(qq.x, kk[q].x, acc);
+                acc = fmaf(qq.y, kk[q].y, acc);
+                acc = fmaf(qq.z, kk[q].z, acc);
+                acc = fmaf(qq.w, kk[q].w, acc);
+            }
+            const float sc = j <= tr ? acc * scale : -INFINITY;
             const float mn = fmaxf(m, warp_max(sc));
             const float corr = __expf(m - mn);  // m = -inf on the first chunk -> 0
             const float p = j <= tr ? __expf(sc - mn) : 0.f;
             lsum = lsum * corr + warp_sum(p);
-            o *= corr;
-            const int nk = min(32, tr + 1 - c);
-            const float* vb = base + (size_t)c * 2 * D + D + lane;
-            if (nk == 32) {  // full chunk: unrolled so the 32 V-row loads issue ahead of the FMAs
-#pragma unroll 8
-                for (int jj = 0; jj < 32; ++jj) o = fmaf(__shfl_sync(0xFFFFFFFFu, p, jj), vb[(size_t)jj * 2 * D], o);
-            } else {
-                for (int jj = 0; jj < nk; ++jj) o = fmaf(__shfl_sync(0xFFFFFFFFu, p, jj), vb[(size_t)jj * 2 * D], o);
+            o.x *= corr;
+            o.y *= corr;
+            o.z *= corr;
+            o.w *= corr;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const float pk = __shfl_sync(0xFFFFFFFFu, p, 4 * i + kq);
+                o.x = fmaf(pk, vv[i].x, o.x);
+                o.y = fmaf(pk, vv[i].y, o.y);
+                o.z = fmaf(pk, vv[i].z, o.z);
+                o.w = fmaf(pk, vv[i].w, o.w);
             }
             m = mn;
         }
-        s.O[r][h * DH + lane] = o / lsum;
+#pragma unroll
+        for (int x = 8; x <= 16; x <<= 1) {
+            o.x += __shfl_xor_sync(0xFFFFFFFFu, o.x, x);
+            o.y += __shfl_xor_sync(0xFFFFFFFFu, o.y, x);
+            o.z += __shfl_xor_sync(0xFFFFFFFFu, o.z, x);
+            o.w += __shfl_xor_sync(0xFFFFFFFFu, o.w, x);
+        }
+        if (lane < 8) {
+            const float inv = 1.f / lsum;
+            *reinterpret_cast<float4*>(&s.O[r][h * DH + dq]) = make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
+        }
     }
 }
 
