@@ -50,6 +50,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+                    help="BASELINE.json config (default cfg5, the headline); cfg1-4 run on one GPU with the "
+                         "reference CPU path timed beside them at SURVEY.md 8(d)'s sub-budgets")
     ap.add_argument("--instances", type=int, default=4096)
     ap.add_argument("--sweeps-per-step", type=int, default=1000)
     ap.add_argument("--measure-every", type=int, default=10)
@@ -110,10 +113,11 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU baseline ---
 
-def ea_couplings_numpy(seed, gid):
+def ea_couplings_numpy(seed, gid, L=L):
     """EA +-1 bonds of DESIGN.md 3.4 (coin per (+x,+y,+z) bond in site order from
     derive(seed, {0x88, gid})), vectorised restatement for building reference graphs."""
     from oracle import oracle as O
+    N_SPINS = L ** 3
     s0 = np.uint64(O.derive(seed, [0x88, gid]))
     k = np.arange(1, 3 * N_SPINS + 1, dtype=np.uint64)
     with np.errstate(over="ignore"):
@@ -167,6 +171,112 @@ def cpu_reference_rate(n_inst, n_sweeps, threads, prop_every):
     return updates / dt, dt, kind, cores, updates
 
 
+def cpu_workload_rate(k, threads):
+    """The reference CPU path (unmodified gibbs_sweep in index order + the restated PT/TAPT driver,
+    oracle/_ref, parallel_for over instances) on SURVEY.md 8(d)'s sub-budget of config k:
+    cfg1 the full run of one seed, cfg2 16 chains x 10^3 sweeps, cfg3 32 instances x 10^3,
+    cfg4 64 instances x 10^3.  Returns (updates/s, seconds, threads used, sample)."""
+    import ctypes as C
+
+    import paper_2509_23043_b200 as T
+    from paper_2509_23043_b200 import workloads as WL
+    from oracle import oracle as O
+    Rf = O.ref()
+    hs, props = [], (0, 0, None, 0)
+    if k == 1:
+        hs = [Rf.ref_graph_lattice(2, 32, 32, 0, 1.0, 1)]
+        betas_, sweeps, n_free = WL.geometric(0.2, 1.0, 32), 10000, 1024
+    elif k == 2:
+        hs = [Rf.ref_graph_lattice(2, 64, 64, 0, 1.0, 1) for _ in range(16)]
+        betas_, sweeps, n_free = WL.geometric(0.3, 0.6, 64), 1000, 4096
+        mb = np.zeros(64)
+        mb[:60] = [WL.yang_m(x) for x in betas_[:60]]
+        props = (100, 60, mb, 5)
+    elif k == 3:
+        for g in range(32):
+            ci, cj, J = ea_couplings_numpy(3, g, 16)
+            hs.append(Rf.ref_graph_build(4096, len(ci), ci.ctypes.data_as(O._u32p), cj.ctypes.data_as(O._u32p),
+                                         J.ctypes.data_as(O._f64p), None, None))
+        betas_, sweeps, n_free = np.linspace(0.2, 3.0, 64), 1000, 4096
+    else:
+        M = T.Multiplier(16)
+        ci, cj = np.ascontiguousarray(M.ci, np.uint32), np.ascontiguousarray(M.cj, np.uint32)
+        J, h = np.ascontiguousarray(M.J, np.float64), np.ascontiguousarray(M.h, np.float64)
+        for g in range(64):
+            p, q = T.random_semiprime(4, g, 16)
+            cl = np.ascontiguousarray(M.clamps(p * q), np.int8)
+            hs.append(Rf.ref_graph_build(M.n_spins, len(ci), ci.ctypes.data_as(O._u32p), cj.ctypes.data_as(O._u32p),
+                                         J.ctypes.data_as(O._f64p), h.ctypes.data_as(O._f64p),
+                                         cl.ctypes.data_as(O._i8p)))
+        betas_, sweeps, n_free = WL.geometric(0.1, 5.0, 32), 1000, M.model().n_free
+    b = np.ascontiguousarray(betas_, np.float64)
+    R_, n_inst = len(b), len(hs)
+    every, nt, mb, refine = props
+    mbp = np.ascontiguousarray(mb if mb is not None else np.zeros(R_), np.float64)
+    arr = (C.c_void_p * n_inst)(*hs)
+    t0 = time.perf_counter()
+    Rf.ref_pt_run(arr, n_inst, 0, R_, b.ctypes.data_as(O._f64p), SEED, sweeps, 1, every, nt,
+                  mbp.ctypes.data_as(O._f64p), refine, threads, None, None, None, None)
+    dt = time.perf_counter() - t0
+    for hnd in hs:
+        Rf.ref_graph_free(hnd)
+    rounds = sweeps // every if every else 0
+    upd = n_inst * (R_ * n_free * sweeps + rounds * nt * n_free * refine)
+    used = min(threads, n_inst)
+    sample = f"{n_inst} instance(s) x {sweeps} sweeps of config {k}, {used} thread(s) on '{cpu_model()}'"
+    return upd / dt, dt, used, sample
+
+
+def run_workload(args):
+    """bench.py --workload cfg1..cfg4: one GPU, same JSON schema as the headline line."""
+    import torch
+
+    import paper_2509_23043_b200 as T
+    from paper_2509_23043_b200 import workloads as WL
+    k = int(args.workload[3:])
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        raise SystemExit("--workload cfg1..cfg4 runs on one GPU (config 5 is the sharded run)")
+    torch.cuda.set_device(0)
+    stream = torch.cuda.Stream()
+    w = WL.build(T, k, stream.cuda_stream)
+    for _ in range(args.warmup):
+        w["step"]()
+    torch.cuda.synchronize()
+    l0 = T.launch_count()
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    with ClockSampler(0) as clk:
+        ev[0].record(stream)
+        for _ in range(args.steps):
+            w["step"]()
+        ev[1].record(stream)
+        torch.cuda.synchronize()
+    ms = ev[0].elapsed_time(ev[1])
+    value = w["updates_per_step"] * args.steps / (ms * 1e-3)
+    clocks = clk.summary()
+    f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    n_sm = torch.cuda.get_device_properties(0).multi_processor_count
+    peak = n_sm * 128 * f_sm / WL.I_U[k]
+    probe, _ = T.probe_decision_rate(1, 512, 20000)
+    out = {
+        "metric": f"spin updates/sec, BASELINE config {k}", "value": value, "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "replicas only", "vs_baseline": None, "dtype": "u32 multi-spin words / u64 splitmix64",
+        "data": "synthetic", "config": {"workload": w["desc"], "kernel": w["kernel"],
+                                        "updates_per_step": w["updates_per_step"]},
+        "roofline": {"bound": "alu", "unit": "Gupdates/s", "achieved": value / 1e9, "peak": peak / 1e9,
+                     "frac": value / peak, "traffic": None,
+                     "peak_source": f"BASELINE.md section 4 ALU bound n_SM*128*f_SM/I_u, I_u={WL.I_U[k]}",
+                     "probe_ceiling": {"value": probe / 1e9, "frac": value / probe}},
+        "gpu_launches": T.launch_count() - l0, "clocks": clocks,
+    }
+    if not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        rate, dt, used, sample = cpu_workload_rate(k, threads)
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": used, "kind": "reference",
+                               "sample": f"{sample} ({dt:.1f} s)"}
+    print(json.dumps(out), flush=True)
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -211,6 +321,9 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.workload != "cfg5":
+        run_workload(args)
         return
     import torch
     import torch.distributed as dist
