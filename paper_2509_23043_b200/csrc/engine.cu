@@ -482,6 +482,9 @@ struct tapt_ensemble_s {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     uint64_t T = 0, P = 0, Q = 0;  // sweeps, swap passes, proposal rounds (global)
+    // swap passes run inside the fused kernel, by parity: pair r is attempted once per pass of
+    // parity r & 1 (the kernel counts only accepts; tapt_get_acceptance adds these attempts)
+    uint64_t fused_passes[2] = {0, 0};
     int clamp_sets = 1;
     bool have_disorder = false;
     uint32_t launch_chunk = 2000;
@@ -644,7 +647,13 @@ struct tapt_ensemble_s {
             a.measure_every = (int)measure_every;
             a.measure_from = measure_from;
             launch(a, cluster);
-            if (swap_every) P += (T + chunk) / swap_every - T / swap_every;
+            if (swap_every) {
+                const uint64_t P1 = P + (T + chunk) / swap_every - T / swap_every;
+                const uint64_t even = (P1 + 1) / 2 - (P + 1) / 2;  // passes p in [P, P1) with p even
+                fused_passes[0] += even;
+                fused_passes[1] += (P1 - P) - even;
+                P = P1;
+            }
             T += chunk;
             done += chunk;
         }
@@ -993,6 +1002,7 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
         e->prop_att.alloc((size_t)e->I * e->R);
         e->prop_acc.alloc((size_t)e->I * e->R);
         e->swap_att.zero(e->stream);
+        e->fused_passes[0] = e->fused_passes[1] = 0;
         e->swap_acc.zero(e->stream);
         e->prop_att.zero(e->stream);
         e->prop_acc.zero(e->stream);
@@ -1289,7 +1299,10 @@ tapt_status tapt_get_acceptance(tapt_ensemble_t e, uint64_t* sa, uint64_t* sc, u
     return guard([&] {
         check_ens(e);
         const size_t np = (size_t)e->I * (e->R - 1);
-        if (sa && np) std::copy_n(e->swap_att.download(e->stream).begin(), np, sa);
+        if (sa && np) {
+            std::copy_n(e->swap_att.download(e->stream).begin(), np, sa);
+            for (size_t q = 0; q < np; ++q) sa[q] += e->fused_passes[(q % (e->R - 1)) & 1];
+        }
         if (sc && np) std::copy_n(e->swap_acc.download(e->stream).begin(), np, sc);
         if (pa) {
             auto v = e->prop_att.download(e->stream);

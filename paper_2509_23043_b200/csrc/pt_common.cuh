@@ -19,9 +19,36 @@ struct PTShared {
     int32_t Eall[kMaxR];    // energies of all buffers of the instance
     uint8_t slot_of[kMaxR];
     uint8_t buf_of[kMaxR];
+    uint32_t sacc[kMaxR];   // swap accepts of this launch by pair (flushed by pt_finish)
     int best;
     int tie;
 };
+
+// Swap-table metadata of each ladder pair, staged in shared memory once per launch so that a
+// swap decision costs one dependent global load (the threshold) instead of four.
+struct SwapMeta {
+    uint32_t off, K;
+    int64_t kz;
+    uint32_t always;
+};
+constexpr int kSwm = 128;
+__shared__ SwapMeta g_swm[kSwm];
+
+__device__ __forceinline__ void pt_stage_swap(const PTArgs& a) {
+    if (a.swap_every <= 0 || a.R - 1 > kSwm || !a.swap_tab.off) return;
+    for (int r = threadIdx.x; r < a.R - 1; r += blockDim.x)
+        g_swm[r] = SwapMeta{a.swap_tab.off[r], a.swap_tab.K[r], a.swap_tab.kz[r], a.swap_tab.always[r]};
+}
+
+// metro_accept (common.cuh) for swap pair r with the staged metadata.
+__device__ __forceinline__ bool pt_swap_accept(const PTArgs& a, int r, int64_t dE, uint64_t x) {
+    if (a.R - 1 > kSwm) return metro_accept(a.swap_tab, r, dE, x);
+    const SwapMeta m = g_swm[r];
+    if (dE >= 0 || m.always) return true;
+    const int64_t k = -dE;
+    const uint64_t T = k < (int64_t)m.K ? a.swap_tab.tab[m.off + k] : (k <= m.kz ? 1ull : 0ull);
+    return below(x, T);
+}
 
 // Number of valid buffers owned by group `grp` (the last group of an instance may be partial).
 __device__ __forceinline__ int own_count(const PTArgs& a, int grp) { return min(a.W, a.B - grp * a.W); }
@@ -39,6 +66,8 @@ __device__ __forceinline__ void pt_load_perm(const PTArgs& a, PTShared& S, int i
         S.Ucnt[k] = 0;
         S.Mcnt[k] = 0;
     }
+    for (int k = threadIdx.x; k < a.R; k += blockDim.x) S.sacc[k] = 0;
+    pt_stage_swap(a);
 }
 
 // Per-buffer stream base for sweep t: S_slot + (draw_base + t*n_free + 1)*phi.
@@ -74,10 +103,11 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
     }
     __syncthreads();
     const uint64_t T = t + 1;
-    if (tid == 0 && a.best) {
-        int m = S.best;
-        for (int b = 0; b < a.B; ++b) m = min(m, S.Eall[b]);
-        S.best = m;
+    if (tid < 32 && a.best) {  // warp-wide min over the instance's energies
+        int m = 0x7FFFFFFF;
+        for (int b = lane; b < a.B; b += 32) m = min(m, S.Eall[b]);
+        m = __reduce_min_sync(0xFFFFFFFFu, m);
+        if (lane == 0) S.best = min(S.best, m);
     }
     if (a.swap_every > 0 && (T % (uint64_t)a.swap_every) == 0) {
         const int parity = (int)(pass & 1);
@@ -86,12 +116,10 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
             const int b0 = S.buf_of[r], b1 = S.buf_of[r + 1];
             const int64_t dE = (int64_t)S.Eall[b1] - (int64_t)S.Eall[b0];
             const uint64_t x = draw(c0, pass * (uint64_t)a.R + (uint64_t)r + 1ull);
-            const bool acc = metro_accept(a.swap_tab, r, dE, x);
-            if (grp == 0) {
-                const size_t q = (size_t)inst * (a.R - 1) + r;
-                a.swap_att[q] += 1;
-                if (acc) a.swap_acc[q] += 1;
-            }
+            const bool acc = pt_swap_accept(a, r, dE, x);
+            // attempts are deterministic (pass parity) and counted by the host; accepts are
+            // counted here and flushed once per launch
+            if (acc) S.sacc[r] += 1;
             if (acc) {
                 S.buf_of[r] = (uint8_t)b1;
                 S.buf_of[r + 1] = (uint8_t)b0;
@@ -141,6 +169,8 @@ __device__ void pt_finish(const PTArgs& a, PTShared& S, int inst, int grp, int l
         for (int b = tid; b < own_count(a, grp); b += blockDim.x)
             a.E[(size_t)inst * a.B + grp * a.W + b] = S.Eown[last_par][b];
     if (grp == 0) {
+        for (int r = tid; r + 1 < a.R; r += blockDim.x)
+            if (S.sacc[r]) a.swap_acc[(size_t)inst * (a.R - 1) + r] += S.sacc[r];
         for (int k = tid; k < a.B; k += blockDim.x) a.slot_of[(size_t)inst * a.B + k] = S.slot_of[k];
         if (a.buf_of)
             for (int k = tid; k < a.R; k += blockDim.x) a.buf_of[(size_t)inst * a.R + k] = S.buf_of[k];
