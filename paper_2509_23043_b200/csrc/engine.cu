@@ -32,6 +32,7 @@
 
 namespace tapt_dev {
 cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st);
+int k1_resident_units(const PTArgs& a, const LatDims& d, int threads, bool cluster);
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st);
 size_t k1_smem_bytes(int n, bool dis);
 size_t k2_smem_bytes(int n, int R, int nidx);
@@ -467,6 +468,49 @@ void build_model(tapt_model_s& m, uint32_t n, const std::vector<uint32_t>& ai, c
 
 }  // namespace
 
+// ========================================================= balanced schedule ===
+
+namespace {
+
+// McNaughton's wrap-around rule for I equal jobs of S sweeps on M co-resident clusters:
+// lay the jobs end to end, cut the line into M segments of C = ceil(I*S/M) sweeps.  A job
+// cut between machines k and k+1 runs its FIRST sweeps at the start of k+1's timeline
+// (signalling a flag when its state is stored) and its LAST sweeps at the end of k's timeline
+// (waiting for the flag); C >= S guarantees the first part ends before the second starts.
+struct HostSched {
+    std::vector<int> ptr;
+    std::vector<SchedItem> items;
+    int nflags = 0;
+};
+
+HostSched mcnaughton(int I, int S, int M) {
+    HostSched h;
+    const long long total = (long long)I * S, C = (total + M - 1) / M;
+    h.ptr.assign(M + 1, 0);
+    int pending = -1;
+    for (int k = 0; k < M; ++k) {
+        const long long a = k * C, b = std::min(total, (k + 1) * C);
+        for (long long pos = a; pos < b;) {
+            const int j = (int)(pos / S), s_in = (int)(pos % S);
+            const long long end = std::min(b, (long long)(j + 1) * S);
+            const int len = (int)(end - (long long)j * S) - s_in;
+            if (s_in > 0) {  // continuation of the job cut at this segment's start: its first sweeps
+                h.items.push_back({j, 0, len, -1, pending});
+            } else if (len < S) {  // cut at this segment's end: its last sweeps, after the flag
+                pending = h.nflags++;
+                h.items.push_back({j, S - len, S, pending, -1});
+            } else {
+                h.items.push_back({j, 0, S, -1, -1});
+            }
+            pos = end;
+        }
+        h.ptr[k + 1] = (int)h.items.size();
+    }
+    return h;
+}
+
+}  // namespace
+
 // ================================================================ ensemble ===
 
 struct tapt_ensemble_s {
@@ -478,6 +522,37 @@ struct tapt_ensemble_s {
     uint64_t seed = 0;
     bool use_k1 = false;
     int k1_threads = 0, k2_threads = 512;
+    // balanced persistent K1 schedule (McNaughton), cached per launch length
+    int k1_units = -1;  // co-resident clusters (or CTAs) of the K1 launch shape
+    int sched_S = -1, sched_M = 0, sched_nflags = 0;
+    DevBuf<int> sched_ptr;
+    DevBuf<SchedItem> sched_items;
+    DevBuf<uint32_t> sched_flags, sched_err;  // sched_err is sticky until checked
+    uint32_t* sched_err_host = nullptr;        // pinned copy, read once the stream has passed it
+    cudaEvent_t sched_ev = nullptr;
+    bool sched_pending = false;
+    ~tapt_ensemble_s() {
+        if (sched_ev) cudaEventDestroy(sched_ev);
+        if (sched_err_host) cudaFreeHost(sched_err_host);
+    }
+
+    // Report a timed-out wait of a balanced launch (set by the kernel, copied asynchronously after
+    // the launch).  force: wait for the copy (getters and synchronize, which sync anyway);
+    // otherwise only if the stream has already passed it (no host stall on the launch path).
+    void poll_sched(bool force) {
+        if (!sched_pending) return;
+        if (force)
+            CUDA_OK(cudaEventSynchronize(sched_ev));
+        else if (cudaEventQuery(sched_ev) != cudaSuccess)
+            return;
+        sched_pending = false;
+        if (*sched_err_host) {
+            *sched_err_host = 0;
+            sched_err.zero(stream);
+            throw tapt::CudaError("balanced K1 schedule: a split job waited > 2 s for its first part "
+                                  "(another kernel holding SMs?); results of that run are invalid; set TAPT_BALANCE=0");
+        }
+    }
     int nidx = 0;
     cudaStream_t stream = nullptr;
     bool own_stream = false;
@@ -630,6 +705,42 @@ struct tapt_ensemble_s {
         prop_oversize = pr.oversize;
     }
 
+    // When the instances (one cluster each) do not fill whole waves of co-resident clusters,
+    // launch a persistent grid that runs McNaughton's balanced schedule.
+    // TAPT_BALANCE=0 disables it.
+    bool balance(PTArgs& a, bool cluster) {
+        if (!use_k1 || a.energy_only) return false;
+        if (const char* e = std::getenv("TAPT_BALANCE"); e && std::atoi(e) == 0) return false;
+        if (k1_units < 0) k1_units = k1_resident_units(a, m->ld, k1_threads, cluster);
+        const int M = k1_units;
+        if (M <= 0 || (int)I <= M) return false;
+        const double waves = (double)I / M;
+        if (waves / std::ceil(waves) > 0.999) return false;
+        if (!sched_err_host) {
+            CUDA_OK(cudaMallocHost(&sched_err_host, 4));
+            *sched_err_host = 0;
+            CUDA_OK(cudaEventCreateWithFlags(&sched_ev, cudaEventDisableTiming));
+            sched_err.alloc(1);
+            sched_err.zero(stream);
+        }
+        if (sched_S != a.n_sweeps || sched_M != M) {
+            const HostSched h = mcnaughton((int)I, a.n_sweeps, M);
+            sched_ptr.upload(h.ptr, stream);
+            sched_items.upload(h.items, stream);
+            sched_flags.alloc(std::max(1, h.nflags));
+            sched_S = a.n_sweeps;
+            sched_M = M;
+            sched_nflags = h.nflags;
+        }
+        sched_flags.zero(stream);
+        a.sched_ptr = sched_ptr.p;
+        a.sched = sched_items.p;
+        a.flags = sched_flags.p;
+        a.sched_err = sched_err.p;
+        a.sched_clusters = M;
+        return true;
+    }
+
     void run(uint32_t n_sweeps, uint32_t swap_every, uint32_t measure_every, uint64_t measure_from) {
         if (n_sweeps == 0) return;
         if (swap_every && R < 2) swap_every = 0;
@@ -646,7 +757,13 @@ struct tapt_ensemble_s {
             a.p0 = P;
             a.measure_every = (int)measure_every;
             a.measure_from = measure_from;
+            const bool balanced = balance(a, cluster);
             launch(a, cluster);
+            if (balanced) {
+                CUDA_OK(cudaMemcpyAsync(sched_err_host, sched_err.p, 4, cudaMemcpyDeviceToHost, stream));
+                CUDA_OK(cudaEventRecord(sched_ev, stream));
+                sched_pending = true;
+            }
             if (swap_every) {
                 const uint64_t P1 = P + (T + chunk) / swap_every - T / swap_every;
                 const uint64_t even = (P1 + 1) / 2 - (P + 1) / 2;  // passes p in [P, P1) with p even
@@ -665,8 +782,9 @@ namespace {
 void check_model(const tapt_model_s* m) {
     if (!m) throw tapt::ConfigError("null model handle");
 }
-void check_ens(const tapt_ensemble_s* e) {
+void check_ens(tapt_ensemble_s* e) {
     if (!e) throw tapt::ConfigError("null ensemble handle");
+    e->poll_sched(false);
 }
 
 // LatticeSpec::graph_clamped bond list (lattice.cpp:55-87): per site, +x then +y (then +z);
@@ -1100,6 +1218,7 @@ tapt_status tapt_ensemble_set_stream(tapt_ensemble_t e, void* s) {
 tapt_status tapt_ensemble_synchronize(tapt_ensemble_t e) {
     return guard([&] {
         check_ens(e);
+        e->poll_sched(true);
         CUDA_OK(cudaStreamSynchronize(e->stream));
     });
 }
@@ -1240,6 +1359,7 @@ tapt_status tapt_ensemble_set_spins(tapt_ensemble_t e, const int8_t* spins) {
 tapt_status tapt_ensemble_get_spins(tapt_ensemble_t e, int8_t* spins) {
     return guard([&] {
         check_ens(e);
+        e->poll_sched(true);
         const int n = e->n();
         DevBuf<int8_t> d;
         d.alloc((size_t)e->I * e->R * n);
@@ -1255,6 +1375,7 @@ tapt_status tapt_ensemble_get_spins(tapt_ensemble_t e, int8_t* spins) {
 tapt_status tapt_ensemble_get_spins_packed(tapt_ensemble_t e, uint8_t* packed) {
     return guard([&] {
         check_ens(e);
+        e->poll_sched(true);
         const int n = e->n(), nb = (n + 7) / 8;
         DevBuf<uint8_t> d;
         d.alloc((size_t)e->I * e->R * nb);
@@ -1270,6 +1391,7 @@ tapt_status tapt_ensemble_get_spins_packed(tapt_ensemble_t e, uint8_t* packed) {
 tapt_status tapt_ensemble_get_energies(tapt_ensemble_t e, int64_t* out) {
     return guard([&] {
         check_ens(e);
+        e->poll_sched(true);
         auto E = e->E.download(e->stream);
         auto bo = e->buf_of.download(e->stream);
         for (uint32_t i = 0; i < e->I; ++i)
@@ -1281,6 +1403,7 @@ tapt_status tapt_ensemble_get_energies(tapt_ensemble_t e, int64_t* out) {
 tapt_status tapt_ensemble_get_permutation(tapt_ensemble_t e, uint8_t* out) {
     return guard([&] {
         check_ens(e);
+        e->poll_sched(true);
         auto bo = e->buf_of.download(e->stream);
         std::copy(bo.begin(), bo.end(), out);
     });
@@ -1298,6 +1421,7 @@ tapt_status tapt_ensemble_counters(tapt_ensemble_t e, uint64_t* sweeps, uint64_t
 tapt_status tapt_get_acceptance(tapt_ensemble_t e, uint64_t* sa, uint64_t* sc, uint64_t* pa, uint64_t* pc) {
     return guard([&] {
         check_ens(e);
+        e->poll_sched(true);
         const size_t np = (size_t)e->I * (e->R - 1);
         if (sa && np) {
             std::copy_n(e->swap_att.download(e->stream).begin(), np, sa);
@@ -1318,6 +1442,7 @@ tapt_status tapt_get_acceptance(tapt_ensemble_t e, uint64_t* sa, uint64_t* sc, u
 tapt_status tapt_get_observables(tapt_ensemble_t e, int64_t* obs) {
     return guard([&] {
         check_ens(e);
+        e->poll_sched(true);
         auto v = e->obs.download(e->stream);
         std::copy(v.begin(), v.end(), obs);
     });
@@ -1339,6 +1464,7 @@ tapt_status tapt_set_histogram(tapt_ensemble_t e, int64_t e_lo, int64_t width, u
 tapt_status tapt_get_histogram(tapt_ensemble_t e, uint64_t* dst, int on_device) {
     return guard([&] {
         check_ens(e);
+        e->poll_sched(true);
         if (!e->nbins) throw tapt::ConfigError("no histogram configured");
         CUDA_OK(cudaMemcpyAsync(dst, e->hist.p, e->hist.n * sizeof(uint64_t),
                                 on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, e->stream));
@@ -1349,6 +1475,7 @@ tapt_status tapt_get_histogram(tapt_ensemble_t e, uint64_t* dst, int on_device) 
 tapt_status tapt_get_best(tapt_ensemble_t e, int64_t* best) {
     return guard([&] {
         check_ens(e);
+        e->poll_sched(true);
         auto v = e->best.download(e->stream);
         for (uint32_t i = 0; i < e->I; ++i) best[i] = v[i];
     });

@@ -267,9 +267,14 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
     uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw);
     uint8_t* bonds = reinterpret_cast<uint8_t*>(words + a.n);
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
-    const int inst = blockIdx.x / a.G, grp = blockIdx.x % a.G;
+    const int cl = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
     const int half = n >> 1, nsub = half / SP;
+    const int it0 = a.sched ? a.sched_ptr[cl] : 0, it1 = a.sched ? a.sched_ptr[cl + 1] : 1;
+    for (int it = it0; it < it1; ++it) {
+    const SchedItem item = a.sched ? a.sched[it] : SchedItem{cl, 0, a.energy_only ? 1 : a.n_sweeps, -1, -1};
+    const int inst = item.inst;
+    if (item.wait >= 0) pt_wait_flag(a, item.wait);
 
     // ---- load this CTA's spins (and the instance's bond signs) into shared memory
     {
@@ -285,10 +290,12 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
     pt_load_perm(a, sm.S, inst);
     __syncthreads();
 
+    // swap passes before this item: sweeps T = t+1 in (t0, t0+s0] with swap_every | T
     uint64_t pass = a.p0;
+    if (a.swap_every > 0 && item.s0 > 0)
+        pass += (a.t0 + item.s0) / (uint64_t)a.swap_every - a.t0 / (uint64_t)a.swap_every;
     int par = 0;
-    const int nsw = a.energy_only ? 1 : a.n_sweeps;
-    for (int s = 0; s < nsw; ++s) {
+    for (int s = item.s0; s < item.s1; ++s) {
         const uint64_t t = a.t0 + (uint64_t)s;
         par = (int)(t & 1);
         // per-buffer tables and stream bases for the slots the buffers occupy now
@@ -398,7 +405,7 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
     if (a.energy_only) {
         __syncthreads();
         for (int b = tid; b < nv; b += nt) a.E[(size_t)inst * a.B + grp * W + b] = sm.S.Eown[par][b];
-        return;
+        continue;
     }
     // ---- write back
     {
@@ -407,6 +414,9 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
         for (int k = tid; k < (n >> 2); k += nt) dst[k] = src[k];
     }
     pt_finish<CLU>(a, sm.S, inst, grp, par);
+    if (item.signal >= 0) pt_signal_flag<CLU>(a, item.signal, grp);
+    __syncthreads();  // shared memory is reused by the next item
+    }
 }
 
 size_t k1_smem_bytes(int n, bool dis) {
@@ -414,8 +424,10 @@ size_t k1_smem_bytes(int n, bool dis) {
     return k1_words_offset() + (size_t)n * 4 + (dis ? (size_t)n : 0);
 }
 
+// resident != null: report how many clusters (or CTAs, without a cluster) of this launch shape
+// are co-resident on the device instead of launching.
 template <int DIM, bool DIS, bool CLU>
-static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st) {
+static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st, int* resident) {
     const size_t smem = k1_smem_bytes(a.n, DIS);
     // SP = 1 site word per thread-iteration at 1024 threads, else 2 interleaved at <= 512
     // launch shapes: 2 interleaved site words per thread-iteration at <= 512 threads (default),
@@ -427,7 +439,7 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(a.I * a.G));
+    cfg.gridDim = dim3((unsigned)((a.sched ? a.sched_clusters : a.I) * a.G));
     cfg.blockDim = dim3((unsigned)threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -440,17 +452,43 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
         cfg.attrs = attr;
         cfg.numAttrs = 1;
     }
+    if (resident) {
+        if (CLU) return cudaOccupancyMaxActiveClusters(resident, (const void*)fn, &cfg);
+        int per_sm = 0, dev = 0, nsm = 0;
+        cudaError_t q = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+        if (q == cudaSuccess) q = cudaGetDevice(&dev);
+        if (q == cudaSuccess) q = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        *resident = per_sm * nsm;
+        return q;
+    }
     return cudaLaunchKernelEx(&cfg, fn, a, d);
 }
 
-cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st) {
+static cudaError_t k1_dispatch(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st,
+                               int* resident) {
     const bool dis = a.bonds != nullptr;
     if (d.dim == 2) {
-        if (dis) return cluster ? launch_k1_t<2, true, true>(a, d, threads, st) : launch_k1_t<2, true, false>(a, d, threads, st);
-        return cluster ? launch_k1_t<2, false, true>(a, d, threads, st) : launch_k1_t<2, false, false>(a, d, threads, st);
+        if (dis)
+            return cluster ? launch_k1_t<2, true, true>(a, d, threads, st, resident)
+                           : launch_k1_t<2, true, false>(a, d, threads, st, resident);
+        return cluster ? launch_k1_t<2, false, true>(a, d, threads, st, resident)
+                       : launch_k1_t<2, false, false>(a, d, threads, st, resident);
     }
-    if (dis) return cluster ? launch_k1_t<3, true, true>(a, d, threads, st) : launch_k1_t<3, true, false>(a, d, threads, st);
-    return cluster ? launch_k1_t<3, false, true>(a, d, threads, st) : launch_k1_t<3, false, false>(a, d, threads, st);
+    if (dis)
+        return cluster ? launch_k1_t<3, true, true>(a, d, threads, st, resident)
+                       : launch_k1_t<3, true, false>(a, d, threads, st, resident);
+    return cluster ? launch_k1_t<3, false, true>(a, d, threads, st, resident)
+                   : launch_k1_t<3, false, false>(a, d, threads, st, resident);
+}
+
+cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st) {
+    return k1_dispatch(a, d, threads, cluster, st, nullptr);
+}
+
+// Co-resident clusters (cluster launches) or CTAs of the K1 launch shape (balanced schedule).
+int k1_resident_units(const PTArgs& a, const LatDims& d, int threads, bool cluster) {
+    int r = 0;
+    return k1_dispatch(a, d, threads, cluster, nullptr, &r) == cudaSuccess ? r : 0;
 }
 
 }  // namespace tapt_dev

@@ -56,6 +56,16 @@ struct LatDims {
     int J0;               // |J|
 };
 
+// Balanced persistent schedule (McNaughton's wrap-around rule): cluster c runs items
+// sched_ptr[c] .. sched_ptr[c+1]-1 in order; an item is sweeps [s0, s1) of the launch for
+// one instance.  A job split over two clusters runs its first sweeps at the start of one
+// timeline and its last sweeps at the end of the previous one; the later part waits for
+// flags[wait] (set by the earlier part after its state is stored) -- by construction the
+// earlier part has finished long before.
+struct SchedItem {
+    int inst, s0, s1, wait, signal;  // wait / signal: flag index or -1
+};
+
 // Everything one fused PT launch needs (lattice K1 and CSR K2 share it).
 struct PTArgs {
     uint32_t* words;
@@ -90,6 +100,12 @@ struct PTArgs {
     int nbins;
     int* best;                 // [I] lowest energy seen (atomicMin)
     MixConsts mc;              // {4, 32}, opaque to the compiler (see common.cuh)
+    // balanced persistent schedule (null: one instance per cluster, all launch sweeps)
+    const int* sched_ptr;      // [n_clusters + 1]
+    const SchedItem* sched;
+    uint32_t* flags;           // [n_split] zeroed before the launch
+    uint32_t* sched_err;       // set when a wait times out (the host raises)
+    int sched_clusters;        // clusters of the persistent grid (with sched)
 };
 
 // CSR graph (K2): shared structure; couplings may be per instance.

@@ -160,6 +160,31 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
     }
 }
 
+// Balanced schedule (SchedItem): wait for / publish the state of a split job.  The wait is
+// bounded (~2 s of clock64 at 1.9 GHz); on timeout it flags an error instead of hanging.
+__device__ __forceinline__ void pt_wait_flag(const PTArgs& a, int f) {
+    if (threadIdx.x == 0) {
+        const long long t0 = clock64();
+        while (atomicAdd(&a.flags[f], 0u) == 0u) {
+            if (clock64() - t0 > 4000000000ll) {
+                atomicExch(a.sched_err, 1u);
+                break;
+            }
+            __nanosleep(256);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <bool CLU>
+__device__ __forceinline__ void pt_signal_flag(const PTArgs& a, int f, int grp) {
+    __threadfence();  // this CTA's stores (spins, permutation, energies) before the flag
+    __syncthreads();
+    if constexpr (CLU) cg::this_cluster().sync();
+    if (grp == 0 && threadIdx.x == 0) atomicExch(&a.flags[f], 1u);
+}
+
 // End of launch: persist permutation, energies of own buffers and best energy.
 template <bool CLU>
 __device__ void pt_finish(const PTArgs& a, PTShared& S, int inst, int grp, int last_par) {

@@ -1,0 +1,70 @@
+"""The balanced persistent K1 schedule (McNaughton's wrap-around rule):
+with more instances than co-resident clusters, split jobs run their first sweeps on one
+cluster and their last sweeps on another.  Results must equal the plain one-instance-per-CTA
+launch (TAPT_BALANCE=0) bit for bit -- spins, energies, permutations, swap and proposal
+counters, observables, histograms, best energies -- and the oracle.  Marked `gpu`."""
+import numpy as np
+import pytest
+
+import paper_2509_23043_b200 as T
+from oracle import oracle as O
+import tapt_helpers as H
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if T.device_count() == 0:
+        pytest.fail("no CUDA device visible: GPU tests must run on the B200 box")
+
+
+def _state(e):
+    return (e.spins(), e.energies(), e.permutation(), e.acceptance(), e.observables(), e.histogram(), e.best())
+
+
+def _run(monkeypatch, balance, model, betas, I, ea=None, sweeps=(23, 41)):
+    monkeypatch.setenv("TAPT_BALANCE", "1" if balance else "0")
+    e = T.Ensemble(model, betas, n_instances=I, seed=17)
+    if ea is not None:
+        e.generate_ea_disorder(ea)
+    e.init_random()
+    e.set_histogram(-4 * model.n_spins, 8, 64)
+    e.run(sweeps[0], swap_every=1, measure_every=3)
+    e.generate_proposals(np.arange(8), None, refine=2)
+    e.run(sweeps[1], swap_every=2, measure_every=5, measure_from=10)
+    return e
+
+
+@pytest.mark.parametrize("case", ["2d_no_cluster", "3d_ea_cluster"])
+def test_balanced_schedule_equals_plain_launch(case, monkeypatch):
+    # 4096-site lattices: 512-thread CTAs, one per SM, so I exceeds the co-resident count
+    if case == "2d_no_cluster":
+        model, betas, I, ea = T.Model.lattice((64, 64)), H.geometric(0.2, 1.0, 32), 200, None
+    else:
+        model, betas, I, ea = T.Model.lattice((16,)), H.linear(0.2, 3.0, 64), 100, 5
+    a = _run(monkeypatch, True, model, betas, I, ea)
+    b = _run(monkeypatch, False, model, betas, I, ea)
+    assert a.kernel == "lattice"
+    for x, y in zip(_state(a), _state(b)):
+        if isinstance(x, tuple):
+            for u, v in zip(x, y):
+                assert np.array_equal(u, v)
+        else:
+            assert np.array_equal(x, y)
+    monkeypatch.delenv("TAPT_BALANCE")
+
+
+def test_balanced_schedule_matches_oracle_on_a_split_instance():
+    dims = (64, 64)
+    betas = H.geometric(0.2, 1.0, 32)
+    I = 200  # > 148 co-resident CTAs: C = ceil(200*57/148) = 78 > 57, so instance 1 is split
+    e = T.Ensemble(T.Model.lattice(dims), betas, n_instances=I, seed=19)
+    e.init_random()
+    e.run(57, swap_every=1)
+    S, E = e.spins(), e.energies()
+    g = O.lattice_graph(dims)
+    for k in (0, 1, 199):
+        pt = O.PT(g, betas, 19, k, g.colour_order(O.checkerboard_colours(dims)))
+        pt.run(57, 1)
+        assert np.array_equal(S[k], pt.spins) and np.array_equal(E[k], pt.E)
