@@ -33,6 +33,7 @@
 namespace tapt_dev {
 cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st);
 int k1_resident_units(const PTArgs& a, const LatDims& d, int threads, bool cluster);
+int k2_resident_units(const PTArgs& a, const CsrArgs& g, int threads, bool cluster);
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st);
 size_t k1_smem_bytes(int n, bool dis);
 size_t k2_smem_bytes(int n, int R, int nidx);
@@ -523,7 +524,7 @@ struct tapt_ensemble_s {
     bool use_k1 = false;
     int k1_threads = 0, k2_threads = 512;
     // balanced persistent K1 schedule (McNaughton), cached per launch length
-    int k1_units = -1;  // co-resident clusters (or CTAs) of the K1 launch shape
+    int k1_units = -1;  // co-resident clusters (or CTAs) of the sweep kernel's launch shape
     int sched_S = -1, sched_M = 0, sched_nflags = 0;
     DevBuf<int> sched_ptr;
     DevBuf<SchedItem> sched_items;
@@ -549,7 +550,7 @@ struct tapt_ensemble_s {
         if (*sched_err_host) {
             *sched_err_host = 0;
             sched_err.zero(stream);
-            throw tapt::CudaError("balanced K1 schedule: a split job waited > 2 s for its first part "
+            throw tapt::CudaError("balanced sweep schedule: a split job waited > 2 s for its first part "
                                   "(another kernel holding SMs?); results of that run are invalid; set TAPT_BALANCE=0");
         }
     }
@@ -643,15 +644,19 @@ struct tapt_ensemble_s {
         return a;
     }
 
+    int k2_nt() const {
+        int nt = k2_threads;
+        if (const char* env = std::getenv("TAPT_K2_THREADS")) nt = std::max(128, std::min(TAPT_K2_MAXT, std::atoi(env)));
+        return nt;
+    }
+
     void launch(const PTArgs& a, bool cluster) {
         ++g_launches;
         cudaError_t e;
         if (use_k1) {
             e = launch_k1(a, m->ld, k1_threads, cluster, stream);
         } else {
-            int nt = k2_threads;
-            if (const char* env = std::getenv("TAPT_K2_THREADS")) nt = std::max(128, std::min(TAPT_K2_MAXT, std::atoi(env)));
-            e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), nt, cluster, stream);
+            e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster, stream);
         }
         if (e != cudaSuccess) throw tapt::CudaError(std::string("sweep kernel launch: ") + cudaGetErrorString(e));
         CUDA_OK(cudaGetLastError());
@@ -709,9 +714,11 @@ struct tapt_ensemble_s {
     // launch a persistent grid that runs McNaughton's balanced schedule.
     // TAPT_BALANCE=0 disables it.
     bool balance(PTArgs& a, bool cluster) {
-        if (!use_k1 || a.energy_only) return false;
+        if (a.energy_only) return false;
         if (const char* e = std::getenv("TAPT_BALANCE"); e && std::atoi(e) == 0) return false;
-        if (k1_units < 0) k1_units = k1_resident_units(a, m->ld, k1_threads, cluster);
+        if (k1_units < 0)
+            k1_units = use_k1 ? k1_resident_units(a, m->ld, k1_threads, cluster)
+                              : k2_resident_units(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster);
         const int M = k1_units;
         if (M <= 0 || (int)I <= M) return false;
         const double waves = (double)I / M;

@@ -54,16 +54,18 @@ struct K2Graph {
     const uint32_t* class_sites;
 };
 
-template <bool CLU, bool SMEMG>
+// BAL: run a balanced schedule's items (one instance per CTA); otherwise one pass over this CTA's
+// instances (the loop below folds away and the register allocation is the single-pass one).
+template <bool CLU, bool SMEMG, bool BAL>
 __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, const CsrArgs g, const int ipb) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ PTShared SS[kIPB];
     const int nidx = a.nidx, n = a.n, W = a.W;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
-    // instances [inst0, inst0 + nin) of this CTA (ipb > 1 only without clusters: G == 1)
+    // instances [inst0, inst0 + nin) of this CTA (ipb > 1 only without clusters: G == 1); with a
+    // balanced schedule (ipb = 1) the cluster runs its items one after another
     const int grp = ipb > 1 ? 0 : (int)(blockIdx.x % a.G);
-    const int inst0 = ipb > 1 ? (int)blockIdx.x * ipb : (int)(blockIdx.x / a.G);
-    const int nin = min(ipb, a.I - inst0);
+    const int cl = ipb > 1 ? (int)blockIdx.x : (int)(blockIdx.x / a.G);
     const int nv = own_count(a, grp);
     uint32_t* Uslot = reinterpret_cast<uint32_t*>(smem_raw);  // [R][nidx] high threshold words by slot
     uint32_t* wbase = Uslot + (size_t)a.R * nidx;               // [ipb][n]
@@ -72,22 +74,17 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
     const int grp_id = tid / kTPS, ngroups = nt / kTPS;
     const int mykin = grp_id % ipb;  // instance slot inside the CTA
     const int gi = grp_id / ipb, ngi = ngroups / ipb;
-    const bool active = mykin < nin;
-    const int inst = inst0 + (active ? mykin : 0);
-    PTShared& S = SS[active ? mykin : 0];
-    uint32_t* words = wbase + (size_t)(active ? mykin : 0) * n;
-    const int8_t* Jglob = g.J + (size_t)(g.nJ > 1 ? inst : 0) * g.nnz;
     K2Graph G;
     if constexpr (SMEMG) {  // stage the CSR next to the spins: every neighbour walk stays on-chip
         uint32_t* rp = wbase + (size_t)ipb * n;
-        uint32_t* cl = rp + (n + 1);
-        int32_t* hh = reinterpret_cast<int32_t*>(cl + g.nnz);
+        uint32_t* co = rp + (n + 1);
+        int32_t* hh = reinterpret_cast<int32_t*>(co + g.nnz);
         uint32_t* rk = reinterpret_cast<uint32_t*>(hh + n);
         uint32_t* cs = rk + n;
         int8_t* jj = reinterpret_cast<int8_t*>(cs + nfree);
         for (int k = tid; k <= n; k += nt) rp[k] = g.rowptr[k];
         for (int k = tid; k < g.nnz; k += nt) {
-            cl[k] = g.col[k];
+            co[k] = g.col[k];
             jj[k] = g.J[k];  // shared couplings; per-instance couplings stay in global memory
         }
         for (int k = tid; k < n; k += nt) {
@@ -95,29 +92,43 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
             rk[k] = g.rank[k];
         }
         for (int k = tid; k < nfree; k += nt) cs[k] = g.class_sites[k];
-        G = K2Graph{rp, cl, g.nJ > 1 ? Jglob : jj, hh, rk, cs};
+        G = K2Graph{rp, co, jj, hh, rk, cs};  // per-instance couplings: G.J set per item
     } else {
-        G = K2Graph{g.rowptr, g.col, Jglob, TAPT_K2_HS ? g.hs : g.h, g.rank, g.class_sites};
+        G = K2Graph{g.rowptr, g.col, g.J, TAPT_K2_HS ? g.hs : g.h, g.rank, g.class_sites};
     }
     const int sub = tid & (kTPS - 1), m0 = 2 * sub;
     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
     const uint32_t mine = (0x03030303u << m0) & vmask;  // replicas of this lane
+    // U - 1 (clamped at 0): the carry of h - (U - 1) and the tie band h - (U - 1) in {0, 1, 2}
+    // come out of one subtraction (decisions with h = U - 1 fall in the band and are redone)
+    for (int k = tid; k < a.R * nidx; k += nt) Uslot[k] = max(thr_hi(a.thr[k]), 1u) - 1u;
 
+    const int it0 = BAL ? a.sched_ptr[cl] : 0, it1 = BAL ? a.sched_ptr[cl + 1] : 1;
+    for (int it = it0; it < it1; ++it) {
+    const SchedItem item = BAL ? a.sched[it] : SchedItem{ipb > 1 ? cl * ipb : cl, 0, a.n_sweeps, -1, -1};
+    const int inst0 = item.inst;
+    const int nin = min(ipb, a.I - inst0);
+    const bool active = mykin < nin;
+    const int inst = inst0 + (active ? mykin : 0);
+    PTShared& S = SS[active ? mykin : 0];
+    uint32_t* words = wbase + (size_t)(active ? mykin : 0) * n;
+    if (g.nJ > 1) G.J = g.J + (size_t)inst * g.nnz;  // per-instance couplings stay in global memory
+    if (BAL && item.wait >= 0) pt_wait_flag(a, item.wait);
+    const uint64_t t0 = a.t0 + (uint64_t)item.s0;  // first sweep of this item
     for (int kin = 0; kin < nin; ++kin) {
         const int ik = inst0 + kin;
         uint32_t* wk = wbase + (size_t)kin * n;
         for (int k = tid; k < n; k += nt) wk[k] = a.words[((size_t)ik * a.G + grp) * n + k];
         pt_load_perm(a, SS[kin], ik);
-        for (int b = tid; b < nv; b += nt) SS[kin].Eown[(a.t0 + 1) & 1][b] = a.E[(size_t)ik * a.B + grp * W + b];
+        for (int b = tid; b < nv; b += nt) SS[kin].Eown[(t0 + 1) & 1][b] = a.E[(size_t)ik * a.B + grp * W + b];
     }
-    // U - 1 (clamped at 0): the carry of h - (U - 1) and the tie band h - (U - 1) in {0, 1, 2}
-    // come out of one subtraction (decisions with h = U - 1 fall in the band and are redone)
-    for (int k = tid; k < a.R * nidx; k += nt) Uslot[k] = max(thr_hi(a.thr[k]), 1u) - 1u;
     __syncthreads();
 
+    // swap passes before this item: sweeps T = t+1 in (a.t0, t0] with swap_every | T
     uint64_t pass = a.p0;
-    int par = (int)((a.t0 + 1) & 1);
-    for (int s = 0; s < a.n_sweeps; ++s) {
+    if (a.swap_every > 0 && item.s0 > 0) pass += t0 / (uint64_t)a.swap_every - a.t0 / (uint64_t)a.swap_every;
+    int par = (int)((t0 + 1) & 1);
+    for (int s = item.s0; s < item.s1; ++s) {
         const uint64_t t = a.t0 + (uint64_t)s;
         const int prev = par;
         par = (int)(t & 1);
@@ -281,6 +292,9 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
         for (int k = tid; k < n; k += nt) a.words[((size_t)(inst0 + kin) * a.G + grp) * n + k] = wk[k];
     }
     for (int kin = 0; kin < nin; ++kin) pt_finish<CLU>(a, SS[kin], inst0 + kin, grp, par);
+    if (BAL && item.signal >= 0) pt_signal_flag<CLU>(a, item.signal, grp);
+    if (BAL) __syncthreads();  // shared memory is reused by the next item
+    }
 }
 
 size_t k2_smem_bytes(int n, int R, int nidx) {
@@ -292,15 +306,17 @@ size_t k2_smem_bytes_graph(int n, int R, int nidx, int nnz, int nfree) {
     return k2_smem_bytes(n, R, nidx) + k2_graph_bytes(n, nnz, nfree);
 }
 
-template <bool CLU, bool SMEMG>
-static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, int ipb, cudaStream_t st) {
+template <bool CLU, bool SMEMG, bool BAL>
+static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, int ipb, cudaStream_t st,
+                               int* resident) {
     size_t smem = (size_t)a.R * a.nidx * 4 + (size_t)ipb * a.n * 4;
     if (SMEMG) smem += k2_graph_bytes(a.n, g.nnz, (int)g.n_free);
-    auto fn = k2_csr_pt<CLU, SMEMG>;
+    auto fn = k2_csr_pt<CLU, SMEMG, BAL>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(ipb > 1 ? (unsigned)((a.I + ipb - 1) / ipb) : (unsigned)(a.I * a.G));
+    cfg.gridDim = dim3(a.sched ? (unsigned)(a.sched_clusters * a.G)
+                               : (ipb > 1 ? (unsigned)((a.I + ipb - 1) / ipb) : (unsigned)(a.I * a.G)));
     cfg.blockDim = dim3((unsigned)threads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
@@ -312,6 +328,15 @@ static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, i
         attr[0].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
+    }
+    if (resident) {  // co-resident clusters / CTAs of this shape (balanced schedule)
+        if (CLU) return cudaOccupancyMaxActiveClusters(resident, (const void*)fn, &cfg);
+        int per_sm = 0, dev = 0, nsm = 0;
+        cudaError_t q = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, threads, smem);
+        if (q == cudaSuccess) q = cudaGetDevice(&dev);
+        if (q == cudaSuccess) q = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        *resident = per_sm * nsm;
+        return q;
     }
     return cudaLaunchKernelEx(&cfg, fn, a, g, ipb);
 }
@@ -327,11 +352,32 @@ int k2_instances_per_cta(const PTArgs& a, const CsrArgs& g) {
     return 1;
 }
 
-cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st) {
-    const int ipb = cluster ? 1 : k2_instances_per_cta(a, g);
+static cudaError_t k2_dispatch(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st,
+                               int* resident, bool bal) {
+    // a balanced schedule runs one instance per CTA (its jobs are single instances)
+    const int ipb = (cluster || bal) ? 1 : k2_instances_per_cta(a, g);
+    if (bal) {
+        if (g.smem_graph)
+            return cluster ? launch_k2_t<true, true, true>(a, g, threads, 1, st, resident)
+                           : launch_k2_t<false, true, true>(a, g, threads, 1, st, resident);
+        return cluster ? launch_k2_t<true, false, true>(a, g, threads, 1, st, resident)
+                       : launch_k2_t<false, false, true>(a, g, threads, 1, st, resident);
+    }
     if (g.smem_graph)
-        return cluster ? launch_k2_t<true, true>(a, g, threads, 1, st) : launch_k2_t<false, true>(a, g, threads, ipb, st);
-    return cluster ? launch_k2_t<true, false>(a, g, threads, 1, st) : launch_k2_t<false, false>(a, g, threads, ipb, st);
+        return cluster ? launch_k2_t<true, true, false>(a, g, threads, 1, st, resident)
+                       : launch_k2_t<false, true, false>(a, g, threads, ipb, st, resident);
+    return cluster ? launch_k2_t<true, false, false>(a, g, threads, 1, st, resident)
+                   : launch_k2_t<false, false, false>(a, g, threads, ipb, st, resident);
+}
+
+cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st) {
+    return k2_dispatch(a, g, threads, cluster, st, nullptr, a.sched != nullptr);
+}
+
+// Co-resident clusters (or single-instance CTAs) of the K2 launch shape (balanced schedule).
+int k2_resident_units(const PTArgs& a, const CsrArgs& g, int threads, bool cluster) {
+    int r = 0;
+    return k2_dispatch(a, g, threads, cluster, nullptr, &r, true) == cudaSuccess ? r : 0;
 }
 
 }  // namespace tapt_dev

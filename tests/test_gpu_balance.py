@@ -23,11 +23,13 @@ def _state(e):
     return (e.spins(), e.energies(), e.permutation(), e.acceptance(), e.observables(), e.histogram(), e.best())
 
 
-def _run(monkeypatch, balance, model, betas, I, ea=None, sweeps=(23, 41)):
+def _run(monkeypatch, balance, model, betas, I, ea=None, sweeps=(23, 41), clamps=None):
     monkeypatch.setenv("TAPT_BALANCE", "1" if balance else "0")
     e = T.Ensemble(model, betas, n_instances=I, seed=17)
     if ea is not None:
         e.generate_ea_disorder(ea)
+    if clamps is not None:
+        e.set_clamps(clamps)
     e.init_random()
     e.set_histogram(-4 * model.n_spins, 8, 64)
     e.run(sweeps[0], swap_every=1, measure_every=3)
@@ -36,16 +38,36 @@ def _run(monkeypatch, balance, model, betas, I, ea=None, sweeps=(23, 41)):
     return e
 
 
-@pytest.mark.parametrize("case", ["2d_no_cluster", "3d_ea_cluster"])
+def _circuit(seed=3, n=60):
+    rs = np.random.default_rng(seed)
+    ci, cj = rs.integers(0, n, 4 * n), rs.integers(0, n, 4 * n)
+    keep = ci != cj
+    J = rs.choice([-2.0, -1.0, 1.0, 2.0], 4 * n)[keep]
+    h = rs.integers(-3, 4, n).astype(float)
+    cl = np.zeros(n, np.int8)
+    cl[:6] = 1  # clamped sites whose values vary per instance
+    return T.Model.graph(n, ci[keep], cj[keep], J, h, cl), rs
+
+
+@pytest.mark.parametrize("case", ["2d_no_cluster", "3d_ea_cluster", "k2_circuit_clamps", "k2_odd_ea"])
 def test_balanced_schedule_equals_plain_launch(case, monkeypatch):
-    # 4096-site lattices: 512-thread CTAs, one per SM, so I exceeds the co-resident count
+    # K1: 4096-site lattices (512-thread CTAs, one per SM); K2: 400 single-instance CTAs on
+    # ~296 co-resident -- I exceeds the co-resident count in every case
+    clamps, kern = None, "lattice"
     if case == "2d_no_cluster":
         model, betas, I, ea = T.Model.lattice((64, 64)), H.geometric(0.2, 1.0, 32), 200, None
-    else:
+    elif case == "3d_ea_cluster":
         model, betas, I, ea = T.Model.lattice((16,)), H.linear(0.2, 3.0, 64), 100, 5
-    a = _run(monkeypatch, True, model, betas, I, ea)
-    b = _run(monkeypatch, False, model, betas, I, ea)
-    assert a.kernel == "lattice"
+    elif case == "k2_circuit_clamps":
+        model, rs = _circuit()
+        betas, I, ea, kern = H.geometric(0.1, 4.0, 32), 400, None, "csr"
+        clamps = np.zeros((I, model.n_spins), np.int8)
+        clamps[:, :6] = np.where(rs.random((I, 6)) < 0.5, 1, -1)
+    else:  # odd periodic lattice: not bipartite -> K2, per-instance EA couplings
+        model, betas, I, ea, kern = T.Model.lattice((5,)), H.linear(0.2, 3.0, 32), 400, 7, "csr"
+    a = _run(monkeypatch, True, model, betas, I, ea, clamps=clamps)
+    b = _run(monkeypatch, False, model, betas, I, ea, clamps=clamps)
+    assert a.kernel == kern
     for x, y in zip(_state(a), _state(b)):
         if isinstance(x, tuple):
             for u, v in zip(x, y):
