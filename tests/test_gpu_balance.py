@@ -25,6 +25,7 @@ def _state(e):
 
 def _run(monkeypatch, balance, model, betas, I, ea=None, sweeps=(23, 41), clamps=None):
     monkeypatch.setenv("TAPT_BALANCE", "1" if balance else "0")
+    monkeypatch.setenv("TAPT_K3", "0")  # K3 runs unbalanced; these cases exercise K2's schedule
     e = T.Ensemble(model, betas, n_instances=I, seed=17)
     if ea is not None:
         e.generate_ea_disorder(ea)
@@ -75,6 +76,7 @@ def test_balanced_schedule_equals_plain_launch(case, monkeypatch):
         else:
             assert np.array_equal(x, y)
     monkeypatch.delenv("TAPT_BALANCE")
+    monkeypatch.delenv("TAPT_K3")
 
 
 def test_balanced_schedule_matches_oracle_on_a_split_instance():

@@ -201,17 +201,64 @@ def test_k2_reference_order_with_clamps_and_fields():
     compare(e, pts)
 
 
-def test_k1_and_k2_give_the_same_chain_on_a_lattice():
+def test_k1_k2_k3_give_the_same_chain_on_a_lattice(monkeypatch):
     betas = H.geometric(0.2, 1.0, 32)
     a = T.Ensemble(T.Model.lattice((16, 16)), betas, seed=4)
     g = O.lattice_graph((16, 16))
-    b = T.Ensemble(T.Model.graph(g.n, g.ci, g.cj, g.J), betas, seed=4)
-    assert a.kernel == "lattice" and b.kernel == "csr"
+    mg = T.Model.graph(g.n, g.ci, g.cj, g.J)
+    monkeypatch.setenv("TAPT_K3", "1")
+    b = T.Ensemble(mg, betas, seed=4)
+    assert a.kernel == "lattice" and b.kernel == "bitcsr"
     for e in (a, b):
         e.init_random()
         e.run(50, swap_every=1)
+    monkeypatch.setenv("TAPT_K3", "0")
+    c = T.Ensemble(mg, betas, seed=4)
+    assert c.kernel == "csr"
+    c.init_random()
+    c.run(50, swap_every=1)
+    for e in (b, c):
+        assert np.array_equal(a.spins(), e.spins())
+        assert np.array_equal(a.energies(), e.energies())
+
+
+def test_k3_circuit_with_clamps_and_fields_matches_oracle(monkeypatch):
+    monkeypatch.setenv("TAPT_K3", "1")
+    g = _random_circuit(13)
+    m = T.Model.graph(g.n, g.ci, g.cj, g.J, g.h, g.clamp)
+    betas = H.geometric(0.1, 5.0, 32)
+    e = T.Ensemble(m, betas, n_instances=3, seed=5)
+    assert e.kernel == "bitcsr"
+    e.init_random()
+    e.run(120, swap_every=1)
+    compare(e, H.run_oracle([g] * 3, betas, 5, 0, H.colour_order_for(m.schedule()[0]), 120))
+
+
+def test_k3_equals_k2_on_multiplier_instances(monkeypatch):
+    """K3 (bit-sliced, heavy sites, per-instance clamps, swaps, measurements) == K2, bit for bit."""
+    M = T.Multiplier(12)
+    m = M.model()
+    I, R = 64, 32
+    prods = [T.random_semiprime(4, k, 12) for k in range(I)]
+    cl = np.stack([M.clamps(p * q) for p, q in prods])
+
+    def run(k3):
+        monkeypatch.setenv("TAPT_K3", "1" if k3 else "0")
+        e = T.Ensemble(m, H.geometric(0.1, 5.0, R), n_instances=I, seed=8)
+        e.set_clamps(cl)
+        e.init_random()
+        e.set_histogram(-2000, 16, 256)
+        e.run(150, swap_every=1, measure_every=7)
+        return e
+    a, b = run(True), run(False)
+    assert a.kernel == "bitcsr" and b.kernel == "csr"
     assert np.array_equal(a.spins(), b.spins())
     assert np.array_equal(a.energies(), b.energies())
+    for x, y in zip(a.acceptance(), b.acceptance()):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a.observables(), b.observables())
+    assert np.array_equal(a.histogram(), b.histogram())
+    assert np.array_equal(a.best(), b.best())
 
 
 # ------------------------------------------------------------ proposals -----
