@@ -3,7 +3,7 @@ ensembles with one measured "step" each.  Product
 construction only -- no oracle, no CPU path.  Used by bench.py --workload and
 tools/bench_configs.py.
 
-  step of cfg1: 1000 checkerboard sweeps, swap pass + measurement after every sweep
+  step of cfg1: 1000 checkerboard sweeps, swap pass + measurement after every sweep (296 seeds)
   step of cfg2: 10 x (100 sweeps, swap every sweep, measure every 10; then a TAPT round into the
                 60 hottest slots: biased i.i.d. proposals, 5 refinement sweeps, Eq. 2)
   step of cfg3: 1000 sweeps, swap every sweep (EA +-1 disorder from derive(3, {0x88, gid}))
@@ -29,7 +29,10 @@ def build(T, cfg, stream_ptr=None, instances=None):
     """Returns dict(ens, step, updates_per_step, desc, kernel, shape) for BASELINE config cfg."""
     if cfg == 1:
         m = T.Model.lattice((32, 32))
-        R, I, n = 32, instances or 16, 1024
+        # BASELINE config 1 is one instance (the CPU-runnable case); its seeds are independent
+        # replicas of the whole run (SURVEY asks for >= 16), and 296 of them -- two per SM -- fill
+        # the GPU (replicas only)
+        R, I, n = 32, instances or 296, 1024
         e = T.Ensemble(m, geometric(0.2, 1.0, R), n_instances=I, seed=1)
         if stream_ptr:
             e.set_stream(stream_ptr)
