@@ -75,6 +75,13 @@ struct Smem {
     double lq[RB];
 };
 
+// K/V chunk staged by the forward kernel (rows share one sequence's keys): 32 keys x (K | V) of
+// 64 dims, row stride 65 so that lanes reading different keys fall in different banks.
+struct KVChunk {
+    float K[32][2 * 32 + 1];
+    float V[32][2 * 32 + 1];
+};
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
@@ -267,9 +274,70 @@ __device__ void rows_attention(Smem<RB>& s, const FArgs& a, int l, int H) {
     }
 }
 
+// Causal attention for the forward pass, where the 32 rows are consecutive positions of ONE
+// sequence: every 32-key chunk of the cache is staged in shared memory once per row block and
+// read by all (row, head) tasks (flash-attention style).  Warp w owns tasks w, w+8, ... and
+// keeps their online-softmax state in registers across chunks.
+template <int RB>
+__device__ void rows_attention_fwd(Smem<RB>& s, KVChunk& kv, const FArgs& a, int l) {
+    constexpr int H = D / DH, NTASK = RB * H / (NT / 32);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const float scale = rsqrtf((float)DH);
+    const float* base = a.cache + (((size_t)s.slot[0] * a.L + l) * a.T) * 2 * D;
+    int tmax = -1;
+    for (int r = 0; r < RB; ++r)
+        if (s.valid[r]) tmax = max(tmax, s.t[r]);
+    float m[NTASK], lsum[NTASK], o[NTASK];
+#pragma unroll
+    for (int k = 0; k < NTASK; ++k) {
+        m[k] = -INFINITY;
+        lsum[k] = 0.f;
+        o[k] = 0.f;
+    }
+    for (int c = 0; c <= tmax; c += 32) {
+        __syncthreads();  // previous chunk fully consumed
+        for (int e = threadIdx.x; e < 32 * 2 * D / 4; e += NT) {  // 32 keys x (K 64 | V 64), float4
+            const int key = e / (2 * D / 4), q4 = e - key * (2 * D / 4);
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (c + key <= tmax) v = reinterpret_cast<const float4*>(base + (size_t)(c + key) * 2 * D)[q4];
+            float* dst = q4 < D / 4 ? &kv.K[key][4 * q4] : &kv.V[key][4 * q4 - D];
+            dst[0] = v.x;
+            dst[1] = v.y;
+            dst[2] = v.z;
+            dst[3] = v.w;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < NTASK; ++k) {
+            const int task = w + k * (NT / 32), r = task / H, h = task - r * H;
+            const int tr = s.t[r];
+            if (!s.valid[r] || c > tr) continue;  // warp-uniform
+            const int j = c + lane;
+            float acc = 0.f;
+#pragma unroll 8
+            for (int d = 0; d < DH; ++d) acc = fmaf(s.Q[r][h * DH + d], kv.K[lane][h * DH + d], acc);
+            const float sc = j <= tr ? acc * scale : -INFINITY;
+            const float mn = fmaxf(m[k], warp_max(sc));
+            const float corr = __expf(m[k] - mn);
+            const float p = j <= tr ? __expf(sc - mn) : 0.f;
+            lsum[k] = lsum[k] * corr + warp_sum(p);
+            float oo = o[k] * corr;
+#pragma unroll 8
+            for (int jj = 0; jj < 32; ++jj) oo = fmaf(__shfl_sync(0xFFFFFFFFu, p, jj), kv.V[jj][h * DH + lane], oo);
+            o[k] = oo;
+            m[k] = mn;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < NTASK; ++k) {
+        const int task = w + k * (NT / 32), r = task / H, h = task - r * H;
+        s.O[r][h * DH + lane] = s.valid[r] ? o[k] / lsum[k] : 0.f;
+    }
+}
+
 // All decoder layers + final LayerNorm + head for the current row block; logits in s.z.
 template <int RB>
-__device__ void rows_forward(Smem<RB>& s, const FArgs& a) {
+__device__ void rows_forward(Smem<RB>& s, const FArgs& a, KVChunk* kv = nullptr) {
     const int H = D / DH;
     for (int l = 0; l < a.L; ++l) {
         const LayerOff& o = a.lay[l];
@@ -277,7 +345,14 @@ __device__ void rows_forward(Smem<RB>& s, const FArgs& a) {
         __syncthreads();
         rows_qkv(s, a, l);
         __syncthreads();
-        rows_attention(s, a, l, H);
+        if constexpr (RB == 32) {
+            if (kv)
+                rows_attention_fwd<RB>(s, *kv, a, l);
+            else
+                rows_attention(s, a, l, H);
+        } else {
+            rows_attention(s, a, l, H);
+        }
         __syncthreads();
         rows_gemm<RB, D, D, 1>(&s.O[0][0], a.W + o.w_o, a.W + o.b_o, &s.X[0][0]);
         __syncthreads();
@@ -334,6 +409,7 @@ __global__ void __launch_bounds__(NT) k_former_forward(const FArgs a) {
     constexpr int RB = 32;
     extern __shared__ __align__(16) unsigned char fsm[];
     Smem<RB>& s = *reinterpret_cast<Smem<RB>*>(fsm);
+    KVChunk& kv = *reinterpret_cast<KVChunk*>(fsm + ((sizeof(Smem<RB>) + 15) & ~size_t(15)));
     const int tid = threadIdx.x;
     for (int b = blockIdx.x; b < a.B; b += gridDim.x) {
         beta_embed(a, a.betas[b], &s.Eb[0][0]);
@@ -351,7 +427,7 @@ __global__ void __launch_bounds__(NT) k_former_forward(const FArgs a) {
             __syncthreads();
             rows_input(s, a);
             __syncthreads();
-            rows_forward(s, a);
+            rows_forward(s, a, &kv);
             if (tid < RB && s.valid[tid]) {
                 const int t = s.t[tid];
                 const float z = s.z[tid];
@@ -619,8 +695,8 @@ tapt_former_s* create_former(const tapt_former_config* c, const float* params) {
 }
 
 template <int RB, class K>
-void launch_rows(K kernel, int grid, const FArgs& a) {
-    const int smem = (int)sizeof(Smem<RB>);
+void launch_rows(K kernel, int grid, const FArgs& a, size_t extra = 0) {
+    const int smem = (int)(((sizeof(Smem<RB>) + 15) & ~size_t(15)) + extra);
     FCUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     kernel<<<grid, NT, smem>>>(a);
     tapt_host::note_launches(1);
@@ -742,7 +818,7 @@ tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_
         a.betas = reinterpret_cast<const double*>(tmp + off_b);
         a.log_q = reinterpret_cast<double*>(tmp + off_q);
         a.logits = logits ? reinterpret_cast<float*>(tmp + off_z) : nullptr;
-        launch_rows<32>(k_former_forward, grid, a);
+        launch_rows<32>(k_former_forward, grid, a, sizeof(KVChunk));
         FCUDA(cudaMemcpy(log_q, a.log_q, (size_t)B * 8, cudaMemcpyDeviceToHost));
         if (logits) FCUDA(cudaMemcpy(logits, a.logits, tb * 4, cudaMemcpyDeviceToHost));
     });
