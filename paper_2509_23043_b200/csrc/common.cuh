@@ -62,6 +62,7 @@ inline MixConsts make_mix_consts() {
 //   V & 2: first 64-bit multiply as an explicit IMAD.WIDE + IMAD + IMAD chain (PTX)           [neutral]
 //   V & 4: tie band tracked as a running min (k1_lattice.cu)                                   [+4%]
 //   V & 8: threshold-index shift as IMAD.HI on the FMA pipe (k1_lattice.cu)                    [+3%]
+//   V & 32: first 64-bit multiply as two IMAD + one IMAD.WIDE with a 64-bit addend (3 ops, not 4)
 // The last multiply only needs its high word: IMAD.HI + IMAD + IMAD.
 template <int V>
 __device__ __forceinline__ uint32_t mix_pre_hi(uint32_t zl, uint32_t zh, const MixConsts& c) {
@@ -71,7 +72,17 @@ __device__ __forceinline__ uint32_t mix_pre_hi(uint32_t zl, uint32_t zh, const M
     asm("shf.r.clamp.b32 %0, %1, %2, 30;" : "=r"(t) : "r"(zl), "r"(zh));
     zl ^= t;
     zh ^= (V & 1) ? __umulhi(zh, c.k4) : (zh >> 30);
-    if constexpr ((V & 2) != 0) {
+    if constexpr ((V & 32) != 0) {
+        asm("{\n\t.reg .u32 x;\n\t.reg .u64 c, w;\n\t"
+            "mul.lo.u32 x, %2, %5;\n\t"
+            "mad.lo.u32 x, %3, %4, x;\n\t"
+            "mov.b64 c, {0, x};\n\t"
+            "mad.wide.u32 w, %2, %4, c;\n\t"
+            "mov.b64 {%0, %1}, w;\n\t}"
+            : "=r"(t), "=r"(zh)
+            : "r"(zl), "r"(zh), "n"(A_LO), "n"(A_HI));
+        zl = t;
+    } else if constexpr ((V & 2) != 0) {
         asm("{\n\t.reg .u64 w;\n\t"
             "mul.wide.u32 w, %2, %4;\n\t"
             "mov.b64 {%0, %1}, w;\n\t"

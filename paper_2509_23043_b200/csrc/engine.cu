@@ -34,9 +34,19 @@ namespace tapt_dev {
 cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st);
 int k1_resident_units(const PTArgs& a, const LatDims& d, int threads, bool cluster);
 int k2_resident_units(const PTArgs& a, const CsrArgs& g, int threads, bool cluster);
-size_t k3_smem_bytes(int n, int R, int nidx, int nnz, int nfree);
-cudaError_t launch_k3(const PTArgs& a, const CsrArgs& g, const uint32_t* rowptr3, const uint32_t* adj3,
-                      const uint32_t* meta3, const int32_t* h, const int32_t* Ek, cudaStream_t st);
+struct Csr3 {
+    const uint4* meta;
+    const uint32_t* adj;
+    const uint32_t* class_ptr;
+    int n_classes;
+    int nadj;
+    int n2;
+    int nidx4;
+};
+size_t k3_smem_bytes(int R, int nidx, int nadj, int nfree, int n, int ncls, int ipb);
+int k3_row_stride();
+int k3_resident_units(const PTArgs& a, const Csr3& g, int ipb);
+cudaError_t launch_k3(const PTArgs& a, const Csr3& g, int ipb, cudaStream_t st);
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st);
 size_t k1_smem_bytes(int n, bool dis);
 size_t k2_smem_bytes(int n, int R, int nidx);
@@ -291,64 +301,62 @@ struct tapt_model_s {
     DevBuf<uint32_t> d_rowptr, d_col, d_rank, d_colptr, d_colsites, d_levptr, d_levsites, d_adjbond;
     DevBuf<int8_t> d_J, d_clamp;
     DevBuf<int32_t> d_h, d_hs;
-    // K3 (bit-sliced CSR, colour order): early-first adjacency, packed site metadata, heavy-first
-    // class order; built on first use (build_k3)
+    // K3 (bit-sliced CSR, colour order; k3_bitcsr.cu): unit-weight padded adjacency (byte offsets
+    // into the instance word image [w | ~w | ONES | ZEROS]) and per-position site metadata, class
+    // positions sorted by (chunks desc, threshold offset, site); built on first use (build_k3)
     int k3_state = 0;  // 0 unbuilt, 1 eligible, -1 not eligible
-    int k3_max_weight = 0;     // max over free sites of sum |J| + |h| (energy-counter bound)
-    long long k3_wsum = 0;     // sum of |J| over edges with a free end + sum of |h| over free sites
-    std::vector<uint32_t> k3_cc_i, k3_cc_j;  // clamped-clamped edges (constant energy)
-    std::vector<int> k3_cc_J;
-    DevBuf<uint32_t> d_rowptr3, d_adj3, d_meta3, d_colsites3;
+    int k3_nadj = 0, k3_max_per_thread = 0;
+    DevBuf<uint32_t> d_adj3;
+    DevBuf<uint4> d_meta3;
 
     void build_k3(cudaStream_t st) {
         if (k3_state) return;
         k3_state = -1;
-        if (n >= (1u << 24)) return;
-        std::vector<uint32_t> rp(n + 1, 0), adj, meta(n, 0);
+        const uint32_t nf = (uint32_t)free_sites.size();
+        if (nf == 0 || (size_t)(2 * n + 2) * 4 >= (1u << 31)) return;
+        std::vector<uint32_t> pos_site;
+        std::vector<int> nch_of(n, 0), off_of(n, 0), sp_of(n, 0);
         for (uint32_t i = 0; i < n; ++i) {
-            std::vector<std::pair<int, uint32_t>> early, late;  // (J, col)
-            int sa = 0;
-            for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
-                const uint32_t j = col[k];
-                const int Jk = adjJ[k];
-                if (std::abs(Jk) > 63) return;
-                if (clamp[i]) continue;
-                sa += std::abs(Jk);
-                const bool is_early = clamp[j] != 0 || colour[j] < colour[i];
-                (is_early ? early : late).push_back({Jk, j});
-                if (clamp[j] == 0 && j > i) k3_wsum += std::abs(Jk);  // free-free edge: once
-                if (clamp[j] != 0) k3_wsum += std::abs(Jk);             // free-clamped edge
-            }
-            if (clamp[i]) {
-                for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k)
-                    if (clamp[col[k]] && col[k] > i) {
-                        k3_cc_i.push_back(i);
-                        k3_cc_j.push_back(col[k]);
-                        k3_cc_J.push_back(adjJ[k]);
-                    }
-                rp[i + 1] = (uint32_t)adj.size();
-                continue;
-            }
-            if (sa > 63 || early.size() >= 32768) return;
-            k3_wsum += std::abs(hi[i]);
-            k3_max_weight = std::max(k3_max_weight, sa + std::abs(hi[i]));
-            for (auto* v : {&early, &late})
-                for (auto [Jk, j] : *v)  // col | sign << 24 | |J| << 25 (k3_bitcsr.cu)
-                    adj.push_back(j | (Jk < 0 ? 1u << 24 : 0u) | ((uint32_t)std::abs(Jk) << 25));
-            rp[i + 1] = (uint32_t)adj.size();
-            const int off = hi[i] - sa - lmin;
-            meta[i] = (uint32_t)(off + 32768) | ((uint32_t)early.size() << 16) | (sa > 15 ? 0x80000000u : 0u);
+            if (clamp[i]) continue;
+            int sp = std::abs(hi[i]);
+            for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) sp += std::abs((int)adjJ[k]);
+            if (sp > 127) return;
+            sp_of[i] = sp;
+            // one 16-entry chunk holds S' <= 15 (4 planes); heavier rows take 2..8 chunks (7 planes)
+            nch_of[i] = sp <= 15 ? 1 : std::max(2, (sp + 15) / 16);
+            off_of[i] = -sp - lmin;
         }
-        // heavy sites first inside each colour class (sites of a class are independent, so the
-        // visiting order inside a class does not change the chain)
-        std::vector<uint32_t> cs3(col_sites);
-        for (size_t c = 0; c + 1 < col_ptr.size(); ++c)
-            std::stable_sort(cs3.begin() + col_ptr[c], cs3.begin() + col_ptr[c + 1],
-                             [&](uint32_t x, uint32_t y) { return (meta[x] >> 31) > (meta[y] >> 31); });
-        d_rowptr3.upload(rp, st);
+        std::vector<uint32_t> adj;
+        std::vector<uint4> meta;
+        const uint32_t ONES = 2 * n, ZEROS = 2 * n + 1;
+        int per_thread = 0;
+        for (size_t c = 0; c + 1 < col_ptr.size(); ++c) {
+            std::vector<uint32_t> v(col_sites.begin() + col_ptr[c], col_sites.begin() + col_ptr[c + 1]);
+            std::stable_sort(v.begin(), v.end(), [&](uint32_t x, uint32_t y) {
+                if (nch_of[x] != nch_of[y]) return nch_of[x] > nch_of[y];
+                if (off_of[x] != off_of[y]) return off_of[x] < off_of[y];
+                return x < y;
+            });
+            per_thread += (int)((v.size() + 127) / 128);
+            for (uint32_t i : v) {
+                const size_t start = adj.size();
+                for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+                    const int Jk = adjJ[k];
+                    const uint32_t e = 4u * (Jk > 0 ? col[k] : n + col[k]);
+                    for (int r = 0; r < std::abs(Jk); ++r) adj.push_back(e);
+                }
+                for (int r = 0; r < std::abs(hi[i]); ++r) adj.push_back(4u * (hi[i] > 0 ? ONES : ZEROS));
+                while (adj.size() < start + 16 * (size_t)nch_of[i]) adj.push_back(4u * ZEROS);
+                if (off_of[i] + 32768 < 0 || off_of[i] + 32768 > 0xFFFF) return;
+                meta.push_back(make_uint4(i, rank[i], (uint32_t)start,
+                                          (uint32_t)(off_of[i] + 32768) | ((uint32_t)nch_of[i] << 16) |
+                                              ((uint32_t)sp_of[i] << 20)));
+            }
+        }
+        k3_nadj = (int)adj.size();
+        k3_max_per_thread = per_thread;
         d_adj3.upload(adj, st);
         d_meta3.upload(meta, st);
-        d_colsites3.upload(cs3, st);
         CUDA_OK(cudaStreamSynchronize(st));  // shared by every ensemble of the model, on any stream
         k3_state = 1;
     }
@@ -587,44 +595,54 @@ struct tapt_ensemble_s {
     uint64_t seed = 0;
     bool use_k1 = false;
     int k1_threads = 0, k2_threads = 512;
-    // K3 (bit-sliced CSR) for colour-order runs of small-coupling graphs: energy constant per
-    // instance (clamped-only terms minus the counted weights), host copy of per-instance clamps
-    DevBuf<int32_t> Ek;
-    bool Ek_dirty = true;
-    std::vector<int8_t> clamp_host;
+    // K3 (bit-sliced CSR, k3_bitcsr.cu) for colour-order runs of graphs with small integer
+    // couplings and fields; instance teams per CTA (k3_ipb), 0 = not eligible / not decided
+    int k3_ipb = -1;
 
-    bool k3_eligible() {
-        if (use_k1 || order != TAPT_ORDER_COLOUR || G != 1 || csrJ.p || nidx > 128) return false;
-        // opt-in: measured slower than K2 on config 4 (217 vs 322 G/s) and on a clamped 3D lattice
-        // (337 vs 393 G/s), DESIGN.md section 5
-        if (const char* e = std::getenv("TAPT_K3"); !e || std::atoi(e) == 0) return false;
-        m->build_k3(stream);
-        if (m->k3_state != 1) return false;
-        long long per_thread = 0;  // energy-counter bound: sites per thread per sweep x max weight
-        for (size_t c = 0; c + 1 < m->col_ptr.size(); ++c)
-            per_thread += (m->col_ptr[c + 1] - m->col_ptr[c] + 127) / 128;
-        if (per_thread * m->k3_max_weight > 1023) return false;
-        // dynamic shared memory; the static control blocks (2 x PTShared, swap metadata) need ~8 KB more
-        return k3_smem_bytes(n(), R, nidx, (int)m->col.size(), (int)m->free_sites.size()) <= 212 * 1024;
+    Csr3 k3_args() const {
+        Csr3 g{};
+        g.meta = m->d_meta3.p;
+        g.adj = m->d_adj3.p;
+        g.class_ptr = m->d_colptr.p;
+        g.n_classes = (int)(m->col_ptr.size() - 1);
+        g.nadj = m->k3_nadj;
+        g.n2 = (2 * n() + 2 + 3) & ~3;
+        g.nidx4 = (nidx + 3) & ~3;
+        return g;
     }
 
-    const int32_t* k3_energy_constants() {
-        if (Ek_dirty) {
-            std::vector<int32_t> ek(I);
-            const uint32_t nn = n();
-            for (uint32_t i = 0; i < I; ++i) {
-                const int8_t* cl = clamp_host.empty() ? m->clamp.data() : clamp_host.data() + (size_t)i * nn;
-                long long e = -m->k3_wsum;
-                for (size_t k = 0; k < m->k3_cc_i.size(); ++k)
-                    e -= (long long)m->k3_cc_J[k] * cl[m->k3_cc_i[k]] * cl[m->k3_cc_j[k]];
-                for (uint32_t s = 0; s < nn; ++s)
-                    if (cl[s]) e -= (long long)m->hi[s] * cl[s];
-                ek[i] = (int32_t)e;
+    bool k3_eligible() {
+        if (k3_ipb >= 0) return k3_ipb > 0;
+        k3_ipb = 0;
+        if (use_k1 || order != TAPT_ORDER_COLOUR || G != 1 || csrJ.p || nidx > k3_row_stride()) return false;
+        // TAPT_K3=0 selects K2 (the byte-SWAR kernel) for every CSR run
+        if (const char* e = std::getenv("TAPT_K3"); e && std::atoi(e) == 0) return false;
+        m->build_k3(stream);
+        if (m->k3_state != 1) return false;
+        // energy counters: at most 2 x 127 per site and thread per sweep into 12 planes
+        if (m->k3_max_per_thread * 254 > 4095) return false;
+        // instance teams per CTA: the most that fit the shared memory (graph staged once per CTA) and
+        // leave no more co-resident teams than instances, so that every SM gets work (the balanced
+        // schedule then spreads I > M instances evenly); fewer instances than one team per CTA can
+        // hold: one team per CTA
+        int fit = 0;
+        for (int ipb = 4; ipb >= 1 && !fit; --ipb)
+            if (k3_smem_bytes(R, nidx, m->k3_nadj, (int)m->free_sites.size(), n(), (int)m->col_ptr.size() - 1, ipb) <=
+                200 * 1024)
+                fit = ipb;
+        if (!fit) return false;
+        k3_ipb = 1;
+        PTArgs a = base_args();
+        for (int ipb = fit; ipb >= 1; --ipb) {
+            const int M = k3_resident_units(a, k3_args(), ipb);
+            if (M > 0 && M <= (int)I) {
+                k3_ipb = ipb;
+                break;
             }
-            Ek.upload(ek, stream);
-            Ek_dirty = false;
         }
-        return Ek.p;
+        if (const char* e = std::getenv("TAPT_K3_IPB"))
+            k3_ipb = std::max(1, std::min(fit, std::atoi(e)));
+        return k3_ipb > 0;
     }
 
     // balanced persistent K1 schedule (McNaughton), cached per launch length
@@ -759,10 +777,8 @@ struct tapt_ensemble_s {
         cudaError_t e;
         if (use_k1) {
             e = launch_k1(a, m->ld, k1_threads, cluster, stream);
-        } else if (!a.sched && !a.energy_only && k3_eligible()) {
-            CsrArgs g = csr_args(false);
-            g.class_sites = m->d_colsites3.p;
-            e = launch_k3(a, g, m->d_rowptr3.p, m->d_adj3.p, m->d_meta3.p, m->d_h.p, k3_energy_constants(), stream);
+        } else if (!a.energy_only && k3_eligible()) {
+            e = launch_k3(a, k3_args(), k3_ipb, stream);
         } else {
             e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster, stream);
         }
@@ -822,11 +838,12 @@ struct tapt_ensemble_s {
     // launch a persistent grid that runs McNaughton's balanced schedule.
     // TAPT_BALANCE=0 disables it.
     bool balance(PTArgs& a, bool cluster) {
-        if (a.energy_only || (!use_k1 && k3_eligible())) return false;  // K3 runs unbalanced
+        if (a.energy_only) return false;
         if (const char* e = std::getenv("TAPT_BALANCE"); e && std::atoi(e) == 0) return false;
         if (k1_units < 0)
-            k1_units = use_k1 ? k1_resident_units(a, m->ld, k1_threads, cluster)
-                              : k2_resident_units(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster);
+            k1_units = use_k1           ? k1_resident_units(a, m->ld, k1_threads, cluster)
+                       : k3_eligible() ? k3_resident_units(a, k3_args(), k3_ipb)
+                                       : k2_resident_units(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster);
         const int M = k1_units;
         if (M <= 0 || (int)I <= M) return false;
         const double waves = (double)I / M;
@@ -1376,6 +1393,8 @@ tapt_status tapt_ensemble_set_bond_signs(tapt_ensemble_t e, const int8_t* signs,
         } else {
             const int nnz = (int)m->col.size();
             e->csrJ.alloc((size_t)e->I * nnz);
+            e->k3_ipb = -1;  // per-instance couplings: K2 only
+            e->k1_units = -1;
             ++g_launches;
             k_csr_from_signs<<<dim3((nnz + 255) / 256, e->I), 256, 0, e->stream>>>(
                 e->signs.p, (int)n_bonds, m->d_adjbond.p, nnz, m->J0, e->csrJ.p);
@@ -1437,8 +1456,6 @@ tapt_status tapt_ensemble_set_clamps(tapt_ensemble_t e, const int8_t* clamps) {
                     throw tapt::ClampedSiteError("per-instance clamps must cover exactly the model's clamped sites");
             }
         e->clampval.upload(clamps, (size_t)e->I * n, e->stream);
-        e->clamp_host.assign(clamps, clamps + (size_t)e->I * n);
-        e->Ek_dirty = true;
         sync_if(e->stream);
     });
 }

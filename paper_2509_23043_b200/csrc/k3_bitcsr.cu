@@ -1,111 +1,88 @@
 // k3_bitcsr.cu -- K3: bit-sliced parallel-tempering kernel for integer CSR graphs with small
-// couplings (BASELINE config 4: |J| in {1, 2}, sum |J| per site <= 63), colour-class order.
+// couplings and fields (BASELINE config 4: |J| in {1, 2}, h in {-2, 0, 16}), colour-class order.
 //
-// K2 gives each site word to four lanes and sums the neighbour contributions of its 32
-// replicas in byte lanes (~72 instructions per update on config 4).  K3 follows K1 instead:
-// one thread owns a site word (32 replicas, bit b = replica b) and
-//   * accumulates acc_b = sum over neighbours of |J| [J s_j > 0] in bit planes (weighted
-//     ripple adds, 4 planes; 6 for "heavy" sites with sum |J| > 15),
-//   * spreads the planes into nibbles (N[m] nibble k = acc of replica 4k+m),
-//   * decides the 32 replicas with K1's carry-chain test against per-buffer threshold rows
-//     laid out with a compile-time stride, so a replica's threshold is LDS [4*idx + imm]:
-//     l = h - sum|J| + 2 acc, idx = l - lmin = off_i + 2 acc,
-//   * counts energies exactly: every edge is scored once, at its later-updated endpoint (its
-//     "early" neighbours -- earlier colour classes and clamped sites -- come first in the
-//     site's adjacency), as weighted unsatisfied-bond planes into sliced counters; plus the
-//     field terms.  E_b = 2 U_b + Ek[inst] (Ek: the clamped-only terms and -sum of weights).
-// Same streams, tables, permutation, swap epilogue and observables as K1/K2 (pt_common.cuh);
-// results are identical to K2's colour order (tests/test_gpu_parity.py).
+// One thread owns a site word (32 replicas, bit b = replica b), as in K1:
+//   * Unit-weight adjacency.  A coupling J_ij becomes |J| entries that point at w_j (J > 0) or at
+//     its complement ~w_j (J < 0); a field h_i becomes |h| entries that point at a constant
+//     all-ones (h > 0) or all-zeros word; rows are padded with the zeros word to 16 * nch
+//     entries.  An entry is a byte offset into the instance's word image [w | ~w | ONES | ZEROS],
+//     so entry e contributes bit x_e = [J s_j > 0] (or [h > 0]) and
+//         acc = sum_e x_e,   S' = sum|J| + |h|,   l = h + sum_j J s_j = 2 acc - S'.
+//   * acc is a bit-sliced popcount: a carry-save tree over each 16-entry chunk (11 full and 4 half
+//     adders, no masks, no weights), 4 planes for S' <= 15 and 7 for the "heavy" rows (S' <= 127).
+//   * Decisions: K1's carry-chain test on the pre-xorshift high word against per-buffer threshold
+//     rows with a compile-time stride; a replica's threshold is LDS [base_i + 8 acc + imm(b)].
+//   * Energies by flip bookkeeping, bit-sliced: the unsatisfied weight of site i in state s is
+//     U(s) = s ? S' - acc : acc (bonds and field), and E changes by 2 (U(new) - U(old)).  Each
+//     thread adds U(new) + (2^P - 1 - U(old)) to sliced counters and counts the constants.
+//   * Teams: 4 warps (128 threads) per instance with their own named barrier; up to 4 instances
+//     per CTA share one staged copy of the graph and of the slot threshold table, and progress
+//     independently (no CTA-wide barrier inside the sweep loop).
+// The draw of replica b at site i in sweep t is the reference's per-site stream position
+// (mcmc.cpp:30-45), so the chain is bit-identical to K2's colour order and to the oracle
+// (oracle/tapt_oracle.c): tests/test_gpu_parity.py.
 #include <cuda_runtime.h>
 
 #include "pt_common.cuh"
 
 namespace tapt_dev {
 
-constexpr int kUS = 128;     // threshold row stride (entries) of the per-buffer table
-constexpr int kC3 = 10;      // sliced energy-counter planes (per-thread unsat weight per sweep < 1024)
-constexpr int kTPI = 128;    // threads per instance
-constexpr int kIPB3 = 2;     // instances per CTA
+constexpr int kT3 = 128;     // threads per instance team
+constexpr int kIPB3 = 4;     // max instance teams per CTA
+constexpr int kRow3 = 132;   // threshold row stride (entries) of the per-buffer table
+constexpr int kC3 = 12;      // sliced energy-counter planes (per-thread weight per sweep < 4096)
+#ifndef TAPT_K3_VARIANT
+#define TAPT_K3_VARIANT TAPT_K1_VARIANT  // mix_pre_hi instruction mix (common.cuh; V & 32 measured: no gain)
+#endif
 
-// Adjacency entry: bits 0..23 neighbour index, bit 24 sign of J (1: J < 0), bits 25..30 |J|.
-__device__ __forceinline__ uint32_t adj_col(uint32_t e) { return e & 0xFFFFFFu; }
-__device__ __forceinline__ uint32_t adj_sign(uint32_t e) { return (uint32_t)((int32_t)(e << 7) >> 31); }
-__device__ __forceinline__ uint32_t adj_bit(uint32_t e, int k) { return (uint32_t)((int32_t)(e << (6 - k)) >> 31); }
-
-// P += a0 + 2 a1 (a 2-bit addend per replica): one half adder, one full adder, then the carry.
-template <int K>
-__device__ __forceinline__ void plane_add2(uint32_t (&P)[K], uint32_t a0, uint32_t a1) {
-    const uint32_t c0 = P[0] & a0;
-    P[0] ^= a0;
-    uint32_t c = maj3(P[1], a1, c0);
-    P[1] ^= a1 ^ c0;
-#pragma unroll
-    for (int p = 2; p < K; ++p) {
-        const uint32_t t = P[p] & c;
-        P[p] ^= c;
-        c = t;
-    }
+__device__ __forceinline__ void fa(uint32_t a, uint32_t b, uint32_t c, uint32_t& s, uint32_t& co) {
+    s = a ^ b ^ c;
+    co = maj3(a, b, c);
+}
+__device__ __forceinline__ void ha(uint32_t a, uint32_t b, uint32_t& s, uint32_t& co) {
+    s = a ^ b;
+    co = a & b;
 }
 
-// P += v * w for an edge entry: the |J| bits 0, 1 through plane_add2, bits 2..5 (rare) one by one.
-template <int K>
-__device__ __forceinline__ void plane_add_edge(uint32_t (&P)[K], uint32_t v, uint32_t e);
-
-// Bit-sliced add of plane v with weight 2^k into planes P[0..K).
-template <int K>
-__device__ __forceinline__ void plane_add(uint32_t (&P)[K], uint32_t v, int k) {
-    uint32_t c = v;
+// Bit-sliced popcount of the 16 entries of one chunk: P[0..4] (sum <= 16).
+__device__ __forceinline__ void chunk_count(const uint8_t* W2, const uint32_t* ap, uint32_t (&P)[5]) {
+    uint32_t x[16];
 #pragma unroll
-    for (int p = 0; p < K; ++p) {
-        if (p >= k) {
-            const uint32_t t = P[p] & c;
-            P[p] ^= c;
-            c = t;
-        }
+    for (int k = 0; k < 4; ++k) {
+        const uint4 e = *reinterpret_cast<const uint4*>(ap + 4 * k);
+        x[4 * k + 0] = *reinterpret_cast<const uint32_t*>(W2 + e.x);
+        x[4 * k + 1] = *reinterpret_cast<const uint32_t*>(W2 + e.y);
+        x[4 * k + 2] = *reinterpret_cast<const uint32_t*>(W2 + e.z);
+        x[4 * k + 3] = *reinterpret_cast<const uint32_t*>(W2 + e.w);
     }
-}
-
-template <int K>
-__device__ __forceinline__ void plane_addw(uint32_t (&P)[K], uint32_t v, uint32_t w) {
-#pragma unroll
-    for (int k = 0; k < K; ++k)
-        if ((w >> k) & 1u) plane_add<K>(P, v, k);
-}
-
-template <int K>
-__device__ __forceinline__ void plane_add_edge(uint32_t (&P)[K], uint32_t v, uint32_t e) {
-    plane_add2<K>(P, v & adj_bit(e, 0), v & adj_bit(e, 1));
-    if (e & 0x78000000u) {  // |J| >= 4
-#pragma unroll
-        for (int k = 2; k < 6 && k < K; ++k)
-            if ((e >> (25 + k)) & 1u) plane_add<K>(P, v, k);
-    }
-}
-
-// C += T for a 6-plane site sum T into the K-plane counters (ripple of full adders).
-template <int K>
-__device__ __forceinline__ void planes_accumulate(uint32_t (&C)[K], const uint32_t (&T)[6]) {
-    uint32_t c = 0;
-#pragma unroll
-    for (int p = 0; p < 6; ++p) {
-        const uint32_t s = C[p] ^ T[p] ^ c;
-        c = maj3(C[p], T[p], c);
-        C[p] = s;
-    }
-#pragma unroll
-    for (int p = 6; p < K; ++p) {
-        const uint32_t t = C[p] & c;
-        C[p] ^= c;
-        c = t;
-    }
+    uint32_t s1, s2, s3, s4, s5, c1, c2, c3, c4, c5;
+    fa(x[0], x[1], x[2], s1, c1);
+    fa(x[3], x[4], x[5], s2, c2);
+    fa(x[6], x[7], x[8], s3, c3);
+    fa(x[9], x[10], x[11], s4, c4);
+    fa(x[12], x[13], x[14], s5, c5);
+    uint32_t t1, t2, d1, d2, d3;  // ones: s1..s5, x15
+    fa(s1, s2, s3, t1, d1);
+    fa(s4, s5, x[15], t2, d2);
+    ha(t1, t2, P[0], d3);
+    uint32_t u1, u2, u3, e1, e2, e3, e4;  // twos: c1..c5, d1..d3
+    fa(c1, c2, c3, u1, e1);
+    fa(c4, c5, d1, u2, e2);
+    fa(d2, d3, u1, u3, e3);
+    ha(u2, u3, P[1], e4);
+    uint32_t v1, f1, f2;  // fours: e1..e4
+    fa(e1, e2, e3, v1, f1);
+    ha(v1, e4, P[2], f2);
+    P[3] = f1 ^ f2;  // eights
+    P[4] = f1 & f2;
 }
 
 // 4 planes -> nibbles: nibble k of N[m] = (P0..P3) of replica 4k+m.
-__device__ __forceinline__ void nibbles4(const uint32_t (&P)[4], uint32_t (&N)[4]) {
-    const uint32_t e01 = (P[0] & 0x55555555u) | ((P[1] << 1) & 0xAAAAAAAAu);
-    const uint32_t o01 = ((P[0] >> 1) & 0x55555555u) | (P[1] & 0xAAAAAAAAu);
-    const uint32_t e23 = (P[2] & 0x55555555u) | ((P[3] << 1) & 0xAAAAAAAAu);
-    const uint32_t o23 = ((P[2] >> 1) & 0x55555555u) | (P[3] & 0xAAAAAAAAu);
+__device__ __forceinline__ void nibbles4(uint32_t P0, uint32_t P1, uint32_t P2, uint32_t P3, uint32_t (&N)[4]) {
+    const uint32_t e01 = (P0 & 0x55555555u) | ((P1 << 1) & 0xAAAAAAAAu);
+    const uint32_t o01 = ((P0 >> 1) & 0x55555555u) | (P1 & 0xAAAAAAAAu);
+    const uint32_t e23 = (P2 & 0x55555555u) | ((P3 << 1) & 0xAAAAAAAAu);
+    const uint32_t o23 = ((P2 >> 1) & 0x55555555u) | (P3 & 0xAAAAAAAAu);
     constexpr uint32_t M = 0x33333333u;
     N[0] = (e01 & M) | ((e23 << 2) & ~M);
     N[1] = (o01 & M) | ((o23 << 2) & ~M);
@@ -113,175 +90,327 @@ __device__ __forceinline__ void nibbles4(const uint32_t (&P)[4], uint32_t (&N)[4
     N[3] = ((o01 >> 2) & M) | (o23 & ~M);
 }
 
-struct Csr3 {
-    const uint32_t* rowptr;  // [n+1] into adj
-    const uint32_t* adj;     // [nnz] col | sign << 24 | |J| << 25, early neighbours first
-    const uint32_t* meta;    // [n] (off_i + 32768) | n_early << 16 | heavy << 31 (free sites)
-    const int32_t* h;        // [n]
-    const uint32_t* rank;    // [n]
-};
-
-template <bool HEAVY>
-__device__ __forceinline__ uint32_t k3_decide(const uint32_t* Ub, int off, const uint32_t (&N)[4], const uint32_t (&Nh)[4],
-                                              const PTShared& S, uint64_t ph, const MixConsts& mc, bool& tie) {
-    uint32_t w = 0, tmin = 0xFFFFFFFFu;
-#pragma unroll
-    for (int b = kW - 1; b >= 0; --b) {
-        const int m = b & 3, sh = 4 * (b >> 2);
-        uint32_t acc = (N[m] >> sh) & 15u;
-        if constexpr (HEAVY) acc += ((Nh[m] >> sh) & 3u) << 4;
-        const uint32_t thr = Ub[b * kUS + off + 2 * (int)acc];
-        const uint64_t z = S.sb[b] + ph;
-        const uint32_t h = mix_pre_hi<TAPT_K1_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), mc);
-        tmin = min(tmin, decide_acc(h, thr, w) + 1u);
-    }
-    tie |= tmin <= 2u;
-    return w;  // NOT(up) bits
+// 8 * (nibble of replica b) as a byte offset (bits 3..6), and 128 * (high nibble) for heavy rows.
+template <int SH>
+__device__ __forceinline__ uint32_t nib8(uint32_t N) {
+    if constexpr (SH >= 3)
+        return (N >> (SH - 3)) & 0x78u;
+    else
+        return (N << (3 - SH)) & 0x78u;
+}
+template <int SH>
+__device__ __forceinline__ uint32_t nib128(uint32_t N) {
+    if constexpr (SH >= 7)
+        return (N >> (SH - 7)) & 0x380u;
+    else
+        return (N << (7 - SH)) & 0x380u;
 }
 
-template <bool HEAVY>
-__device__ __forceinline__ uint32_t k3_decide_exact(const PTArgs& a, const PTShared& S, int off,
-                                                    const uint32_t (&N)[4], const uint32_t (&Nh)[4], uint64_t ph, int nv) {
+// Decisions of the 32 replicas of one site word, descending b so that the carry chain leaves
+// NOT(up_b) in bit b.  Ub: byte address of this site's threshold base (per-buffer rows).
+template <bool HEAVY, int B>
+__device__ __forceinline__ void k3_decide_one(const uint8_t* Ub, const uint32_t (&N)[4], const uint32_t (&Nh)[4],
+                                              const PTShared& S, uint64_t ph, const MixConsts& mc, uint32_t& w,
+                                              uint32_t& tmin) {
+    constexpr int m = B & 3, sh = 4 * (B >> 2);
+    uint32_t ix = nib8<sh>(N[m]);
+    if constexpr (HEAVY) ix += nib128<sh>(Nh[m]);
+    const uint32_t thr = *reinterpret_cast<const uint32_t*>(Ub + ix + B * kRow3 * 4);
+    const uint64_t z = S.sb[B] + ph;
+    const uint32_t h = mix_pre_hi<TAPT_K3_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), mc);
+    tmin = min(tmin, decide_acc(h, thr, w) + 1u);
+}
+
+template <bool HEAVY, int B>
+__device__ __forceinline__ void k3_decide_rec(const uint8_t* Ub, const uint32_t (&N)[4], const uint32_t (&Nh)[4],
+                                              const PTShared& S, uint64_t ph, const MixConsts& mc, uint32_t& w,
+                                              uint32_t& tmin) {
+    k3_decide_one<HEAVY, B>(Ub, N, Nh, S, ph, mc, w, tmin);
+    if constexpr (B > 0) k3_decide_rec<HEAVY, B - 1>(Ub, N, Nh, S, ph, mc, w, tmin);
+}
+
+// Exact 64-bit decisions (tie band, p ~ 2^-31 per site word).
+__device__ __noinline__ uint32_t k3_decide_exact(const PTArgs& a, const PTShared& S, int off, uint32_t A0, uint32_t A1,
+                                                 uint32_t A2, uint32_t A3, uint32_t A4, uint32_t A5, uint32_t A6,
+                                                 uint64_t ph, int nv) {
+    const uint32_t A[7] = {A0, A1, A2, A3, A4, A5, A6};
     uint32_t up = 0;
     for (int b = 0; b < nv; ++b) {
-        const int m = b & 3, sh = 4 * (b >> 2);
-        uint32_t acc = (N[m] >> sh) & 15u;
-        if (HEAVY) acc += ((Nh[m] >> sh) & 3u) << 4;
+        int acc = 0;
+        for (int p = 0; p < 7; ++p) acc |= (int)((A[p] >> b) & 1u) << p;
         const uint64_t T = a.thr[(size_t)S.slot_of[b] * a.nidx + off + 2 * acc];
         if (below(mix_final(S.sb[b] + ph), T)) up |= 1u << b;
     }
     return up;
 }
 
-__global__ void __launch_bounds__(kTPI * kIPB3, 2) k3_bitcsr_pt(const PTArgs a, const Csr3 g3, const CsrArgs g,
-                                                                  const int32_t* Ek) {
+// Sliced U(s) = s ? S' - acc : acc over P planes, for s = new and s = old, and
+// C += U(new) + (2^P - 1 - U(old)) (P + 1 planes, one ripple through the counters).
+template <int P>
+__device__ __forceinline__ void k3_energy(uint32_t (&C)[kC3], const uint32_t (&A)[7], uint32_t sp, uint32_t nw,
+                                          uint32_t old) {
+    uint32_t T[P + 1];
+    uint32_t c = 0xFFFFFFFFu, ct = 0;  // D = S' + ~acc + 1 (carry c); T = U(new) + ~U(old) (carry ct)
+#pragma unroll
+    for (int p = 0; p < P; ++p) {
+        const uint32_t sb = (uint32_t)((int32_t)(sp << (31 - p)) >> 31);
+        const uint32_t na = ~A[p];
+        const uint32_t D = sb ^ na ^ c;
+        c = maj3(sb, na, c);
+        const uint32_t un = (nw & D) | (~nw & A[p]);
+        const uint32_t uo = ~((old & D) | (~old & A[p]));
+        if (p == 0)
+            ha(un, uo, T[0], ct);
+        else
+            fa(un, uo, ct, T[p], ct);
+    }
+    T[P] = ct;
+    uint32_t cc;
+    ha(C[0], T[0], C[0], cc);
+#pragma unroll
+    for (int k = 1; k <= P; ++k) fa(C[k], T[k], cc, C[k], cc);
+#pragma unroll
+    for (int k = P + 1; k < kC3; ++k) ha(C[k], cc, C[k], cc);
+}
+
+struct Csr3 {
+    const uint4* meta;         // [n_free] by class position: site, rank, adj start, off+32768 | nch<<16 | S'<<20
+    const uint32_t* adj;       // [nadj] byte offsets into the instance word image
+    const uint32_t* class_ptr; // [n_classes+1]
+    int n_classes;
+    int nadj;
+    int n2;                    // words of the instance image (2n + 2, rounded up to 4)
+    int nidx4;                 // staged slot-table row stride (nidx rounded up to 4)
+};
+
+// Process one class position (site) of this team's instance.
+template <bool HW>
+__device__ __forceinline__ void k3_site(const PTArgs& a, const PTShared& S, const uint4 md, uint8_t* W2,
+                                        const uint32_t* adj, const uint8_t* ub0, int n, uint32_t vmask, int nv,
+                                        uint32_t (&C)[kC3], int& corr) {
+    const uint32_t i = md.x;
+    const uint64_t ph = (uint64_t)md.y * kPhi;
+    const int off = (int)(md.w & 0xFFFFu) - 32768;
+    const int nch = (int)((md.w >> 16) & 15u);
+    const uint32_t sp = (md.w >> 20) & 127u;
+    const uint32_t* ap = adj + md.z;
+    uint32_t A[7];
+    {
+        uint32_t P[5];
+        chunk_count(W2, ap, P);
+#pragma unroll
+        for (int p = 0; p < 5; ++p) A[p] = P[p];
+        A[5] = A[6] = 0;
+    }
+    if constexpr (HW) {
+        for (int ch = 1; ch < nch; ++ch) {  // heavy rows: 7-plane ripple of each chunk's count
+            uint32_t P[5];
+            chunk_count(W2, ap + 16 * ch, P);
+            uint32_t c;
+            ha(A[0], P[0], A[0], c);
+#pragma unroll
+            for (int p = 1; p < 5; ++p) fa(A[p], P[p], c, A[p], c);
+            ha(A[5], c, A[5], c);
+            A[6] ^= c;
+        }
+    }
+    uint32_t N[4], Nh[4];
+    nibbles4(A[0], A[1], A[2], A[3], N);
+    if constexpr (HW) nibbles4(A[4], A[5], A[6], 0u, Nh);
+    const uint32_t old = *reinterpret_cast<const uint32_t*>(W2 + 4 * i);
+    // the site's threshold base as one register (otherwise 4*off is re-added in every decision)
+    uint32_t ubr = (uint32_t)__cvta_generic_to_shared(ub0) + (uint32_t)(4 * off);
+    asm("mov.b32 %0, %0;" : "+r"(ubr));
+    const uint8_t* Ub = reinterpret_cast<const uint8_t*>(__cvta_shared_to_generic(ubr));
+    uint32_t w = 0, tmin = 0xFFFFFFFFu;
+    k3_decide_rec<HW, kW - 1>(Ub, N, Nh, S, ph, a.mc, w, tmin);
+    uint32_t nw = ~w & vmask;
+    if (tmin <= 2u) nw = k3_decide_exact(a, S, off, A[0], A[1], A[2], A[3], A[4], A[5], A[6], ph, nv);
+    nw |= old & ~vmask;
+    *reinterpret_cast<uint32_t*>(W2 + 4 * i) = nw;
+    *reinterpret_cast<uint32_t*>(W2 + 4 * (n + i)) = ~nw;
+    if (HW && nch > 1) {
+        k3_energy<7>(C, A, sp, nw, old);
+        corr += 127;
+    } else {
+        k3_energy<4>(C, A, sp, nw, old);
+        corr += 15;
+    }
+}
+
+template <bool BAL>
+__global__ void __launch_bounds__(kT3 * kIPB3, 1) k3_bitcsr_pt(const PTArgs a, const Csr3 g) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ PTShared SS[kIPB3];
-    const int n = a.n, nidx = a.nidx;
+    __shared__ int corr_sh[kIPB3];
+    __shared__ uint64_t str_sh[kIPB3][kW];  // the instance's dynamics stream states by slot
+    const int n = a.n, nidx = a.nidx, n_free = (int)a.n_free;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
-    const int kin = tid / kTPI, ti = tid - kin * kTPI;  // instance slot, thread within it
-    const int inst0 = blockIdx.x * kIPB3;
-    const int nin = min(kIPB3, a.I - inst0);
-    const bool active = kin < nin;
+    const int ipb = nt / kT3, kin = tid / kT3, ti = tid - kin * kT3;
+    const SubTeam tm{ti, kT3, 1 + kin};
     const int nv = own_count(a, 0);
     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
-    // shared memory: Uslot [R][nidx] | Ubuf [ipb][32][kUS] | words [ipb][n] | staged graph
+    // shared memory: Uslot [R][nidx4] | adj [nadj] | meta [n_free] (uint4) | class_ptr [n_classes+1] |
+    // per team: Ub [32][kRow3] | W2 [n2]
     uint32_t* Uslot = reinterpret_cast<uint32_t*>(smem_raw);
-    uint32_t* Ubuf = Uslot + (size_t)a.R * nidx;
-    uint32_t* wbase = Ubuf + (size_t)kIPB3 * kW * kUS;
-    uint32_t* rp = wbase + (size_t)kIPB3 * n;
-    uint32_t* adj = rp + (n + 1);
-    uint32_t* meta = adj + g.nnz;
-    uint32_t* rk = meta + n;
-    uint32_t* cs = rk + n;
-    for (int k = tid; k <= n; k += nt) rp[k] = g3.rowptr[k];
-    for (int k = tid; k < g.nnz; k += nt) adj[k] = g3.adj[k];
-    for (int k = tid; k < n; k += nt) {
-        meta[k] = g3.meta[k];
-        rk[k] = g3.rank[k];
+    uint32_t* adj = Uslot + (size_t)a.R * g.nidx4;
+    uint4* meta = reinterpret_cast<uint4*>(adj + ((g.nadj + 3) & ~3));
+    uint32_t* cptr = reinterpret_cast<uint32_t*>(meta + n_free);
+    uint32_t* team0 = cptr + ((g.n_classes + 1 + 3) & ~3);
+    const size_t team_words = (size_t)kW * kRow3 + g.n2;
+    uint32_t* Ubuf = team0 + (size_t)kin * team_words;
+    uint32_t* W2w = Ubuf + (size_t)kW * kRow3;
+    uint8_t* W2 = reinterpret_cast<uint8_t*>(W2w);
+    PTShared& S = SS[kin];
+    for (int k = tid; k < a.R * g.nidx4; k += nt) {
+        const int r = k / g.nidx4, x = k - r * g.nidx4;
+        Uslot[k] = x < nidx ? thr_hi(a.thr[(size_t)r * nidx + x]) : 0u;
     }
-    for (int k = tid; k < (int)g.n_free; k += nt) cs[k] = g.class_sites[k];
-    for (int k = tid; k < a.R * nidx; k += nt) Uslot[k] = thr_hi(a.thr[k]);
-    for (int q = 0; q < nin; ++q) {
-        const int ik = inst0 + q;
-        for (int k = tid; k < n; k += nt) wbase[(size_t)q * n + k] = a.words[(size_t)ik * n + k];
-        pt_load_perm(a, SS[q], ik);
-    }
-    __syncthreads();
+    for (int k = tid; k < g.nadj; k += nt) adj[k] = g.adj[k];
+    for (int k = tid; k < n_free; k += nt) meta[k] = g.meta[k];
+    for (int k = tid; k <= g.n_classes; k += nt) cptr[k] = g.class_ptr[k];
+    pt_stage_swap(a);
+    __syncthreads();  // the last CTA-wide barrier: teams are independent from here on
 
-    PTShared& S = SS[active ? kin : 0];
-    uint32_t* words = wbase + (size_t)(active ? kin : 0) * n;
-    const uint32_t* Ub = Ubuf + (size_t)(active ? kin : 0) * kW * kUS;
-    uint64_t pass = a.p0;
-    int par = 0;
-    for (int s = 0; s < a.n_sweeps; ++s) {
-        const uint64_t t = a.t0 + (uint64_t)s;
-        par = (int)(t & 1);
-        for (int q = 0; q < nin; ++q) pt_stream_bases(a, SS[q], inst0 + q, 0, t);
-        // per-buffer threshold rows for the slots the buffers occupy this sweep
-        for (int e = tid; e < nin * kW * kUS; e += nt) {
-            const int q = e / (kW * kUS), r = e - q * kW * kUS, b = r / kUS, x = r - b * kUS;
-            Ubuf[e] = (b < nv && x < nidx) ? Uslot[SS[q].slot_of[b] * nidx + x] : 0u;
-        }
-        __syncthreads();
-        uint32_t C[kC3];
-#pragma unroll
-        for (int k = 0; k < kC3; ++k) C[k] = 0;
-        for (int c = 0; c < g.n_classes; ++c) {
-            const uint32_t c0 = g.class_ptr[c], c1 = g.class_ptr[c + 1];
-            for (uint32_t q = c0 + (uint32_t)ti; active && q < c1; q += (uint32_t)kTPI) {
-                const uint32_t i = cs[q];
-                const uint32_t mt = meta[i];
-                const int off = (int)(mt & 0xFFFFu) - 32768;
-                const uint32_t r0 = rp[i], r1 = rp[i + 1], nearly = (mt >> 16) & 0x7FFFu;
-                const bool heavy = (mt >> 31) != 0;
-                uint32_t P[6] = {0, 0, 0, 0, 0, 0};
-                for (uint32_t k = r0; k < r1; ++k) {
-                    const uint32_t e = adj[k];
-                    plane_add_edge<6>(P, words[adj_col(e)] ^ adj_sign(e), e);
-                }
-                uint32_t N[4], Nh[4];
-                {
-                    const uint32_t P4[4] = {P[0], P[1], P[2], P[3]};
-                    nibbles4(P4, N);
-                    const uint32_t H4[4] = {P[4], P[5], 0u, 0u};
-                    nibbles4(H4, Nh);
-                }
-                const uint64_t ph = (uint64_t)rk[i] * kPhi;
-                bool tie = false;
-                uint32_t nw = heavy ? k3_decide<true>(Ub, off, N, Nh, S, ph, a.mc, tie)
-                                    : k3_decide<false>(Ub, off, N, Nh, S, ph, a.mc, tie);
-                nw = ~nw & vmask;
-                if (tie) nw = heavy ? k3_decide_exact<true>(a, S, off, N, Nh, ph, nv)
-                                    : k3_decide_exact<false>(a, S, off, N, Nh, ph, nv);
-                words[i] = nw;
-                // energy: early edges (final on both ends now) and the field as weighted
-                // unsatisfied planes of this site (< 64), then folded into the counters
-                uint32_t U[6] = {0, 0, 0, 0, 0, 0};
-                for (uint32_t k = r0; k < r0 + nearly; ++k) {
-                    const uint32_t e = adj[k];
-                    plane_add_edge<6>(U, nw ^ words[adj_col(e)] ^ adj_sign(e), e);
-                }
-                const int hi = g3.h[i];
-                if (hi != 0) plane_addw<6>(U, hi > 0 ? ~nw : nw, (uint32_t)(hi > 0 ? hi : -hi));
-                planes_accumulate<kC3>(C, U);
-            }
-            __syncthreads();
-        }
-        // E_b = 2 U_b + Ek: reduce the per-thread planes of each instance's warps
+    const int unit = (int)blockIdx.x * ipb + kin;
+    int it0, it1;
+    if (BAL) {
+        if (unit >= a.sched_clusters) return;
+        it0 = a.sched_ptr[unit];
+        it1 = a.sched_ptr[unit + 1];
+    } else {
+        if (unit >= a.I) return;
+        it0 = 0;
+        it1 = 1;
+    }
+    const uint8_t* ub0 = reinterpret_cast<const uint8_t*>(Ubuf);
+    for (int it = it0; it < it1; ++it) {
+        const SchedItem item = BAL ? a.sched[it] : SchedItem{unit, 0, a.n_sweeps, -1, -1};
+        const int inst = item.inst;
+        if (BAL && item.wait >= 0) pt_wait_flag(a, item.wait, tm);
+        const uint64_t t0 = a.t0 + (uint64_t)item.s0;
         {
-            const uint32_t tot = warp_sliced_total<kC3>(C);
-            if (active && lane < nv) atomicAdd(&S.Ucnt[lane], tot);
-            __syncthreads();
-            for (int e = tid; e < nin * nv; e += nt) {
-                const int q = e / nv, b = e - q * nv;
-                SS[q].Eown[par][b] = 2 * (int32_t)SS[q].Ucnt[b] + Ek[inst0 + q];
-                SS[q].Ucnt[b] = 0;
+            const uint32_t* src = a.words + (size_t)inst * n;
+            for (int k = ti; k < n; k += kT3) {
+                const uint32_t v = src[k];
+                W2w[k] = v;
+                W2w[n + k] = ~v;
+            }
+            if (ti == 0) {
+                W2w[2 * n] = 0xFFFFFFFFu;
+                W2w[2 * n + 1] = 0u;
             }
         }
-        uint64_t pass_k = pass;
-        for (int q = 0; q < nin; ++q) {
-            pass_k = pass;
-            pt_epilogue<false>(a, SS[q], wbase + (size_t)q * n, inst0 + q, 0, t, pass_k);
+        pt_load_perm(a, S, inst, tm);
+        for (int r = ti; r < a.R; r += kT3) str_sh[kin][r] = a.streams[(size_t)inst * a.R + r];
+        for (int b = ti; b < nv; b += kT3) S.Eown[(t0 + 1) & 1][b] = a.E[(size_t)inst * a.B + b];
+        tm.sync();
+
+        uint64_t pass = a.p0;
+        if (a.swap_every > 0 && item.s0 > 0) pass += t0 / (uint64_t)a.swap_every - a.t0 / (uint64_t)a.swap_every;
+        int par = (int)((t0 + 1) & 1);
+        for (int s = item.s0; s < item.s1; ++s) {
+            const uint64_t t = a.t0 + (uint64_t)s;
+            const int prev = par;
+            par = (int)(t & 1);
+            {  // per-buffer stream bases for sweep t (pt_stream_bases with the staged stream states)
+                const uint64_t k0 = a.draw_base + t * (uint64_t)a.n_free + 1ull;
+                for (int b = ti; b < nv; b += kT3) S.sb[b] = str_sh[kin][S.slot_of[b]] + k0 * kPhi;
+            }
+            // per-buffer threshold rows for the slots the buffers occupy this sweep
+            for (int e = ti; e < kW * (kRow3 / 4); e += kT3) {
+                const int b = e / (kRow3 / 4), x4 = e - b * (kRow3 / 4);
+                if (b < nv && 4 * x4 < g.nidx4)
+                    reinterpret_cast<uint4*>(Ubuf)[e] =
+                        reinterpret_cast<const uint4*>(Uslot + (size_t)S.slot_of[b] * g.nidx4)[x4];
+            }
+            tm.sync();
+            uint32_t C[kC3];
+#pragma unroll
+            for (int k = 0; k < kC3; ++k) C[k] = 0;
+            int corr = 0;
+            for (int c = 0; c < g.n_classes; ++c) {
+                const int c0 = (int)cptr[c], c1 = (int)cptr[c + 1];
+                for (int base = c0; base < c1; base += kT3) {  // warp-uniform trip count
+                    const int q = base + ti;
+                    const bool on = q < c1;
+                    const uint4 md = on ? meta[q] : make_uint4(0, 0, 0, 0);
+                    const bool hw = __any_sync(0xFFFFFFFFu, on && ((md.w >> 16) & 15u) > 1u);
+                    if (on) {
+                        if (hw)
+                            k3_site<true>(a, S, md, W2, adj, ub0, n, vmask, nv, C, corr);
+                        else
+                            k3_site<false>(a, S, md, W2, adj, ub0, n, vmask, nv, C, corr);
+                    }
+                }
+                tm.sync();
+            }
+            // E_b += 2 (sum over threads of C_b - sum of the per-site constants)
+            {
+                const uint32_t tot = warp_sliced_total<kC3>(C);
+                if (lane < nv) atomicAdd(&S.Ucnt[lane], tot);
+                int cw = corr;
+#pragma unroll
+                for (int d = 16; d >= 1; d >>= 1) cw += __shfl_xor_sync(0xFFFFFFFFu, cw, d);
+                if (ti == 0) corr_sh[kin] = 0;
+                tm.sync();
+                if (lane == 0) atomicAdd(&corr_sh[kin], cw);
+                tm.sync();
+                for (int b = ti; b < nv; b += kT3) {
+                    S.Eown[par][b] = S.Eown[prev][b] + 2 * ((int32_t)S.Ucnt[b] - corr_sh[kin]);
+                    S.Ucnt[b] = 0;
+                }
+            }
+            pt_epilogue<false>(a, S, W2w, inst, 0, t, pass, tm);
         }
-        pass = pass_k;
+        {
+            uint32_t* dst = a.words + (size_t)inst * n;
+            for (int k = ti; k < n; k += kT3) dst[k] = W2w[k];
+        }
+        pt_finish<false>(a, S, inst, 0, par, tm);
+        if (BAL && item.signal >= 0) pt_signal_flag<false>(a, item.signal, 0, tm);
+        tm.sync();  // the team's shared memory is reused by the next item
     }
-    for (int q = 0; q < nin; ++q)
-        for (int k = tid; k < n; k += nt) a.words[(size_t)(inst0 + q) * n + k] = wbase[(size_t)q * n + k];
-    for (int q = 0; q < nin; ++q) pt_finish<false>(a, SS[q], inst0 + q, 0, par);
 }
 
-size_t k3_smem_bytes(int n, int R, int nidx, int nnz, int nfree) {
-    return ((size_t)R * nidx + (size_t)kIPB3 * kW * kUS + (size_t)kIPB3 * n + (n + 1) + nnz + 2 * (size_t)n + nfree) * 4;
+size_t k3_smem_bytes(int R, int nidx, int nadj, int nfree, int n, int ncls, int ipb) {
+    const size_t nidx4 = ((size_t)nidx + 3) & ~size_t(3), n2 = ((size_t)2 * n + 2 + 3) & ~size_t(3);
+    return ((size_t)R * nidx4 + (((size_t)nadj + 3) & ~size_t(3)) + 4 * (size_t)nfree +
+            (((size_t)ncls + 1 + 3) & ~size_t(3)) +
+            (size_t)ipb * ((size_t)kW * kRow3 + n2)) * 4;
 }
 
-cudaError_t launch_k3(const PTArgs& a, const CsrArgs& g, const uint32_t* rowptr3, const uint32_t* adj3,
-                      const uint32_t* meta3, const int32_t* h, const int32_t* Ek, cudaStream_t st) {
-    const size_t smem = k3_smem_bytes(a.n, a.R, a.nidx, g.nnz, (int)g.n_free);
-    cudaError_t e = cudaFuncSetAttribute(k3_bitcsr_pt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+int k3_row_stride() { return kRow3; }
+
+static cudaError_t k3_shape(const PTArgs& a, const Csr3& g, int ipb, size_t& smem) {
+    smem = k3_smem_bytes(a.R, a.nidx, g.nadj, (int)a.n_free, a.n, g.n_classes, ipb);
+    cudaError_t e = cudaFuncSetAttribute(k3_bitcsr_pt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k3_bitcsr_pt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return e;
+}
+
+// Co-resident instance teams of the K3 launch shape (balanced schedule): CTAs per SM x SMs x ipb.
+int k3_resident_units(const PTArgs& a, const Csr3& g, int ipb) {
+    size_t smem = 0;
+    if (k3_shape(a, g, ipb, smem) != cudaSuccess) return 0;
+    int per_sm = 0, dev = 0, nsm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_bitcsr_pt<true>, kT3 * ipb, smem) != cudaSuccess)
+        return 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
+    return per_sm * nsm * ipb;
+}
+
+cudaError_t launch_k3(const PTArgs& a, const Csr3& g, int ipb, cudaStream_t st) {
+    size_t smem = 0;
+    cudaError_t e = k3_shape(a, g, ipb, smem);
     if (e != cudaSuccess) return e;
-    const Csr3 g3{rowptr3, adj3, meta3, h, g.rank};
-    k3_bitcsr_pt<<<(a.I + kIPB3 - 1) / kIPB3, kTPI * kIPB3, smem, st>>>(a, g3, g, Ek);
+    const unsigned grid = a.sched ? (unsigned)((a.sched_clusters + ipb - 1) / ipb) : (unsigned)((a.I + ipb - 1) / ipb);
+    if (a.sched)
+        k3_bitcsr_pt<true><<<grid, kT3 * ipb, smem, st>>>(a, g);
+    else
+        k3_bitcsr_pt<false><<<grid, kT3 * ipb, smem, st>>>(a, g);
     return cudaGetLastError();
 }
 

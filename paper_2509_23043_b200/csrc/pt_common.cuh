@@ -5,11 +5,28 @@
 #pragma once
 #include <cooperative_groups.h>
 
+#include <type_traits>
+
 #include "kernels.h"
 
 namespace tapt_dev {
 
 namespace cg = cooperative_groups;
+
+// Thread teams.  CtaTeam: the whole CTA (K1, K2).  SubTeam: a warp-aligned group of threads
+// with its own named barrier, so several instances share one CTA (and its staged graph) while
+// progressing independently (K3).
+struct CtaTeam {
+    __device__ __forceinline__ int tid() const { return (int)threadIdx.x; }
+    __device__ __forceinline__ int nt() const { return (int)blockDim.x; }
+    __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+struct SubTeam {
+    int t, n, bar;  // thread index in the team, team size (multiple of 32), barrier id (>= 1)
+    __device__ __forceinline__ int tid() const { return t; }
+    __device__ __forceinline__ int nt() const { return n; }
+    __device__ __forceinline__ void sync() const { asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(n) : "memory"); }
+};
 
 struct PTShared {
     uint64_t sb[kW];        // stream base of each own buffer for the current sweep
@@ -54,26 +71,31 @@ __device__ __forceinline__ bool pt_swap_accept(const PTArgs& a, int r, int64_t d
 __device__ __forceinline__ int own_count(const PTArgs& a, int grp) { return min(a.W, a.B - grp * a.W); }
 
 // Load the permutation of instance `inst` into shared memory.
-__device__ __forceinline__ void pt_load_perm(const PTArgs& a, PTShared& S, int inst) {
-    for (int k = threadIdx.x; k < a.B; k += blockDim.x) S.slot_of[k] = a.slot_of[(size_t)inst * a.B + k];
+// (A SubTeam caller stages the swap metadata once per CTA itself: pt_stage_swap.)
+template <class TM = CtaTeam>
+__device__ __forceinline__ void pt_load_perm(const PTArgs& a, PTShared& S, int inst, const TM& tm = TM{}) {
+    const int t0 = tm.tid(), nt = tm.nt();
+    for (int k = t0; k < a.B; k += nt) S.slot_of[k] = a.slot_of[(size_t)inst * a.B + k];
     if (a.buf_of)
-        for (int k = threadIdx.x; k < a.R; k += blockDim.x) S.buf_of[k] = a.buf_of[(size_t)inst * a.R + k];
-    if (threadIdx.x == 0) {
+        for (int k = t0; k < a.R; k += nt) S.buf_of[k] = a.buf_of[(size_t)inst * a.R + k];
+    if (t0 == 0) {
         S.best = a.best ? a.best[inst] : 0x7FFFFFFF;
         S.tie = 0;
     }
-    for (int k = threadIdx.x; k < kW; k += blockDim.x) {
+    for (int k = t0; k < kW; k += nt) {
         S.Ucnt[k] = 0;
         S.Mcnt[k] = 0;
     }
-    for (int k = threadIdx.x; k < a.R; k += blockDim.x) S.sacc[k] = 0;
-    pt_stage_swap(a);
+    for (int k = t0; k < a.R; k += nt) S.sacc[k] = 0;
+    if constexpr (std::is_same_v<TM, CtaTeam>) pt_stage_swap(a);
 }
 
 // Per-buffer stream base for sweep t: S_slot + (draw_base + t*n_free + 1)*phi.
-__device__ __forceinline__ void pt_stream_bases(const PTArgs& a, PTShared& S, int inst, int grp, uint64_t t) {
+template <class TM = CtaTeam>
+__device__ __forceinline__ void pt_stream_bases(const PTArgs& a, PTShared& S, int inst, int grp, uint64_t t,
+                                                const TM& tm = TM{}) {
     const int nv = own_count(a, grp);
-    for (int b = threadIdx.x; b < nv; b += blockDim.x) {
+    for (int b = tm.tid(); b < nv; b += tm.nt()) {
         const int slot = S.slot_of[grp * a.W + b];
         const uint64_t k0 = a.draw_base + t * (uint64_t)a.n_free + 1ull;
         S.sb[b] = a.streams[(size_t)inst * a.R + slot] + k0 * kPhi;
@@ -82,10 +104,10 @@ __device__ __forceinline__ void pt_stream_bases(const PTArgs& a, PTShared& S, in
 
 // After Eown[par] is final for this CTA: gather, best, swap, measure.
 // `words` = this CTA's group spins in shared memory (n words).
-template <bool CLU>
+template <bool CLU, class TM = CtaTeam>
 __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words, int inst, int grp, uint64_t t,
-                            uint64_t& pass) {
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+                            uint64_t& pass, const TM& tm = TM{}) {
+    const int tid = tm.tid(), nt = tm.nt(), lane = tid & 31;
     const int par = (int)(t & 1);
     if constexpr (CLU) {
         cg::cluster_group cl = cg::this_cluster();
@@ -98,10 +120,10 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
     } else {
         // Without a cluster only this CTA's buffers are visible; the host never asks
         // for swaps or best-energy tracking when an instance spans several CTAs here.
-        __syncthreads();
+        tm.sync();
         for (int b = tid; b < own_count(a, grp); b += nt) S.Eall[grp * a.W + b] = S.Eown[par][b];
     }
-    __syncthreads();
+    tm.sync();
     const uint64_t T = t + 1;
     if (tid < 32 && a.best) {  // warp-wide min over the instance's energies
         int m = 0x7FFFFFFF;
@@ -128,7 +150,7 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
             }
         }
         ++pass;
-        __syncthreads();
+        tm.sync();
     }
     if (a.measure_every > 0 && T > a.measure_from && (T % (uint64_t)a.measure_every) == 0) {
         uint32_t C[kCnt];
@@ -137,7 +159,7 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
         for (int i = tid; i < a.n; i += nt) sliced_add1<kCnt>(C, words[i]);
         const uint32_t tot = warp_sliced_total<kCnt>(C);
         if (lane < own_count(a, grp)) atomicAdd(&S.Mcnt[lane], tot);
-        __syncthreads();
+        tm.sync();
         if (tid < own_count(a, grp)) {
             const int gb = grp * a.W + tid;
             const int slot = S.slot_of[gb];
@@ -156,14 +178,15 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
             }
             S.Mcnt[tid] = 0;
         }
-        __syncthreads();
+        tm.sync();
     }
 }
 
 // Balanced schedule (SchedItem): wait for / publish the state of a split job.  The wait is
 // bounded (~2 s of clock64 at 1.9 GHz); on timeout it flags an error instead of hanging.
-__device__ __forceinline__ void pt_wait_flag(const PTArgs& a, int f) {
-    if (threadIdx.x == 0) {
+template <class TM = CtaTeam>
+__device__ __forceinline__ void pt_wait_flag(const PTArgs& a, int f, const TM& tm = TM{}) {
+    if (tm.tid() == 0) {
         const long long t0 = clock64();
         while (atomicAdd(&a.flags[f], 0u) == 0u) {
             if (clock64() - t0 > 4000000000ll) {
@@ -174,31 +197,31 @@ __device__ __forceinline__ void pt_wait_flag(const PTArgs& a, int f) {
         }
         __threadfence();
     }
-    __syncthreads();
+    tm.sync();
 }
 
-template <bool CLU>
-__device__ __forceinline__ void pt_signal_flag(const PTArgs& a, int f, int grp) {
-    __threadfence();  // this CTA's stores (spins, permutation, energies) before the flag
-    __syncthreads();
+template <bool CLU, class TM = CtaTeam>
+__device__ __forceinline__ void pt_signal_flag(const PTArgs& a, int f, int grp, const TM& tm = TM{}) {
+    __threadfence();  // this team's stores (spins, permutation, energies) before the flag
+    tm.sync();
     if constexpr (CLU) cg::this_cluster().sync();
-    if (grp == 0 && threadIdx.x == 0) atomicExch(&a.flags[f], 1u);
+    if (grp == 0 && tm.tid() == 0) atomicExch(&a.flags[f], 1u);
 }
 
 // End of launch: persist permutation, energies of own buffers and best energy.
-template <bool CLU>
-__device__ void pt_finish(const PTArgs& a, PTShared& S, int inst, int grp, int last_par) {
-    const int tid = threadIdx.x;
-    __syncthreads();
+template <bool CLU, class TM = CtaTeam>
+__device__ void pt_finish(const PTArgs& a, PTShared& S, int inst, int grp, int last_par, const TM& tm = TM{}) {
+    const int tid = tm.tid(), nt = tm.nt();
+    tm.sync();
     if (a.E)
-        for (int b = tid; b < own_count(a, grp); b += blockDim.x)
+        for (int b = tid; b < own_count(a, grp); b += nt)
             a.E[(size_t)inst * a.B + grp * a.W + b] = S.Eown[last_par][b];
     if (grp == 0) {
-        for (int r = tid; r + 1 < a.R; r += blockDim.x)
+        for (int r = tid; r + 1 < a.R; r += nt)
             if (S.sacc[r]) a.swap_acc[(size_t)inst * (a.R - 1) + r] += S.sacc[r];
-        for (int k = tid; k < a.B; k += blockDim.x) a.slot_of[(size_t)inst * a.B + k] = S.slot_of[k];
+        for (int k = tid; k < a.B; k += nt) a.slot_of[(size_t)inst * a.B + k] = S.slot_of[k];
         if (a.buf_of)
-            for (int k = tid; k < a.R; k += blockDim.x) a.buf_of[(size_t)inst * a.R + k] = S.buf_of[k];
+            for (int k = tid; k < a.R; k += nt) a.buf_of[(size_t)inst * a.R + k] = S.buf_of[k];
         if (tid == 0 && a.best) atomicMin(&a.best[inst], S.best);
     }
     if constexpr (CLU) cg::this_cluster().sync();  // peers may still read our Eown

@@ -23,9 +23,9 @@ def _state(e):
     return (e.spins(), e.energies(), e.permutation(), e.acceptance(), e.observables(), e.histogram(), e.best())
 
 
-def _run(monkeypatch, balance, model, betas, I, ea=None, sweeps=(23, 41), clamps=None):
+def _run(monkeypatch, balance, model, betas, I, ea=None, sweeps=(23, 41), clamps=None, k3=False):
     monkeypatch.setenv("TAPT_BALANCE", "1" if balance else "0")
-    monkeypatch.setenv("TAPT_K3", "0")  # K3 runs unbalanced; these cases exercise K2's schedule
+    monkeypatch.setenv("TAPT_K3", "1" if k3 else "0")
     e = T.Ensemble(model, betas, n_instances=I, seed=17)
     if ea is not None:
         e.generate_ea_disorder(ea)
@@ -50,11 +50,13 @@ def _circuit(seed=3, n=60):
     return T.Model.graph(n, ci[keep], cj[keep], J, h, cl), rs
 
 
-@pytest.mark.parametrize("case", ["2d_no_cluster", "3d_ea_cluster", "k2_circuit_clamps", "k2_odd_ea"])
+@pytest.mark.parametrize("case", ["2d_no_cluster", "3d_ea_cluster", "k2_circuit_clamps", "k2_odd_ea",
+                                  "k3_circuit_clamps"])
 def test_balanced_schedule_equals_plain_launch(case, monkeypatch):
     # K1: 4096-site lattices (512-thread CTAs, one per SM); K2: 400 single-instance CTAs on
-    # ~296 co-resident -- I exceeds the co-resident count in every case
-    clamps, kern = None, "lattice"
+    # ~296 co-resident; K3: 700 instance teams on 148 x 4 -- I exceeds the co-resident count in
+    # every case
+    clamps, kern, k3 = None, "lattice", False
     if case == "2d_no_cluster":
         model, betas, I, ea = T.Model.lattice((64, 64)), H.geometric(0.2, 1.0, 32), 200, None
     elif case == "3d_ea_cluster":
@@ -64,10 +66,15 @@ def test_balanced_schedule_equals_plain_launch(case, monkeypatch):
         betas, I, ea, kern = H.geometric(0.1, 4.0, 32), 400, None, "csr"
         clamps = np.zeros((I, model.n_spins), np.int8)
         clamps[:, :6] = np.where(rs.random((I, 6)) < 0.5, 1, -1)
+    elif case == "k3_circuit_clamps":
+        model, rs = _circuit()
+        betas, I, ea, kern, k3 = H.geometric(0.1, 4.0, 32), 700, None, "bitcsr", True
+        clamps = np.zeros((I, model.n_spins), np.int8)
+        clamps[:, :6] = np.where(rs.random((I, 6)) < 0.5, 1, -1)
     else:  # odd periodic lattice: not bipartite -> K2, per-instance EA couplings
         model, betas, I, ea, kern = T.Model.lattice((5,)), H.linear(0.2, 3.0, 32), 400, 7, "csr"
-    a = _run(monkeypatch, True, model, betas, I, ea, clamps=clamps)
-    b = _run(monkeypatch, False, model, betas, I, ea, clamps=clamps)
+    a = _run(monkeypatch, True, model, betas, I, ea, clamps=clamps, k3=k3)
+    b = _run(monkeypatch, False, model, betas, I, ea, clamps=clamps, k3=k3)
     assert a.kernel == kern
     for x, y in zip(_state(a), _state(b)):
         if isinstance(x, tuple):
