@@ -354,7 +354,7 @@ def main():
     k_ev = []
 
     def step(timed):
-        ens.generate_proposals(targets, None, REFINE)
+        ens.generate_proposals(targets, None, REFINE, return_accepted=False)
         if timed:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
@@ -406,11 +406,17 @@ def main():
     hbm_bytes = I * (2 * 4 * N_SPINS * 2 + N_SPINS)  # spins in+out (2 groups) + bond bytes, per launch
     traffic, traffic_detail = None, None
     tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    issue = None
     if os.path.exists(tpath):  # dram bytes per instance-launch from the committed ncu --set full capture
         tr = json.load(open(tpath))
         traffic = tr["dram_bytes_per_instance_launch"] * I
         traffic_detail = {"dram_bytes_per_launch": traffic, "algorithmic_bytes_per_launch": hbm_bytes,
                           "source": tr["source"]}
+        if "thread_inst_per_update" in tr:  # issue slots the kernel actually uses (executed, not algorithmic)
+            ipu = tr["thread_inst_per_update"]
+            issue = {"thread_inst_per_update": ipu, "frac": achieved * ipu / (n_sm * 128 * f_sm),
+                     "what": "executed instructions per update (ncu) x updates/s / issue capacity n_SM*128*f_SM: "
+                             "the share of the SMs' issue slots the kernel fills", "source": tr["inst_source"]}
     roofline = {
         "bound": "alu", "unit": "Gupdates/s", "achieved": achieved / 1e9, "peak": peak / 1e9,
         "frac": achieved / peak, "traffic": traffic, "traffic_detail": traffic_detail,
@@ -419,6 +425,7 @@ def main():
         "probe_ceiling": {"value": probe / 1e9, "frac": achieved / probe,
                           "what": "k_decision_probe: the bare per-update work (splitmix64 high word + threshold "
                                   "lookup + compare + bit insert), no stencil or memory traffic, same unroll"},
+        "issue": issue,
         "kernel": "k1_lattice_pt<3,true,true>", "kernel_ms_per_launch": k_ms, "updates_per_launch": k_upd,
         "hbm": {"achieved_gbs": hbm_bytes / (k_ms * 1e-3) / 1e9, "peak_gbs": g_hbm,
                 "frac": hbm_bytes / (k_ms * 1e-3) / 1e9 / g_hbm,

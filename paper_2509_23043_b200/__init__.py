@@ -469,10 +469,12 @@ class Ensemble:
             _check(lib().tapt_inject_proposals_packed(self._h, p.ctypes.data, 0, _p(t, _u32p), len(t), _p(acc, _u8p)))
         return acc
 
-    def generate_proposals(self, targets, m_bias=None, refine=5):
+    def generate_proposals(self, targets, m_bias=None, refine=5, return_accepted=True):
+        """Synthetic TAPT round.  return_accepted=False keeps the round stream-ordered (no host
+        sync; the per-slot counters still record every decision)."""
         t = np.ascontiguousarray(targets, np.uint32)
         mb = None if m_bias is None else np.ascontiguousarray(m_bias, np.float64)
-        acc = np.zeros((self.I, len(t)), np.uint8)
+        acc = np.zeros((self.I, len(t)), np.uint8) if return_accepted else None
         _check(lib().tapt_generate_proposals(self._h, _p(t, _u32p), len(t), _p(mb, _f64p), int(refine),
                                              _p(acc, _u8p)))
         return acc

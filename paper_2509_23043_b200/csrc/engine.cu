@@ -68,6 +68,9 @@ __global__ void k_apply_proposals(uint32_t*, int, int, int, const uint8_t*, int,
                                   const uint32_t*, int, const uint8_t*);
 __global__ void k_gen_proposals(uint32_t*, int, int, int, int, const uint64_t*, const uint64_t*, const int8_t*, int);
 __global__ void k_ea_signs(int8_t*, int, int, const uint64_t*);
+__global__ void k_derive_round_streams(uint64_t, uint64_t, const uint32_t*, int, int, uint64_t, uint64_t*, uint64_t*,
+                                       uint64_t*);
+__global__ void k_best_from_E(const int32_t*, int, int, int*);
 __global__ void k_bond_bytes(const int8_t*, uint8_t*, LatDims, int);
 __global__ void k_csr_from_signs(const int8_t*, int, const uint32_t*, int, int, int8_t*);
 }  // namespace tapt_dev
@@ -706,7 +709,8 @@ struct tapt_ensemble_s {
     DevBuf<int32_t> pE;
     DevBuf<uint8_t> pslot, pacc, pforced, pbytes;
     DevBuf<int8_t> pint8;
-    DevBuf<uint64_t> pstreams, paccs, ptup;
+    DevBuf<uint64_t> pstreams, paccs, ptup, pfull;
+    std::vector<uint32_t> last_targets;  // prepare_targets: device copies are current for these
     DevBuf<uint32_t> ptargets;
 
     int n() const { return (int)m->n; }
@@ -777,7 +781,7 @@ struct tapt_ensemble_s {
         cudaError_t e;
         if (use_k1) {
             e = launch_k1(a, m->ld, k1_threads, cluster, stream);
-        } else if (!a.energy_only && k3_eligible()) {
+        } else if (!a.energy_only && a.G == 1 && k3_eligible()) {
             e = launch_k3(a, k3_args(), k3_ipb, stream);
         } else {
             e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster, stream);
@@ -805,13 +809,10 @@ struct tapt_ensemble_s {
         }
     }
 
-    void update_best_from_E() {
-        // best = min(best, min over buffers) -- done on the host side of small arrays
-        auto e = E.download(stream);
-        auto b = best.download(stream);
-        for (uint32_t i = 0; i < I; ++i)
-            for (int r = 0; r < R; ++r) b[i] = std::min(b[i], e[(size_t)i * R + r]);
-        best.upload(b, stream);
+    void update_best_from_E() {  // best = min(best, min over buffers), stream-ordered
+        ++g_launches;
+        k_best_from_E<<<(I + 127) / 128, 128, 0, stream>>>(E.p, (int)I, R, best.p);
+        CUDA_OK(cudaGetLastError());
     }
 
     // Heat-bath thresholds [R][nidx] and the swap (rows = pairs) / proposal (rows = slots)
@@ -1712,14 +1713,18 @@ void finish_proposals(tapt_ensemble_s* e, const uint32_t* targets, uint32_t T, b
         }
         CUDA_OK(cudaGetLastError());
     }
-    // accept streams for this round
-    std::vector<uint64_t> as(e->I);
-    for (uint32_t i = 0; i < e->I; ++i)
-        as[i] = tapt::RngStream::derive(e->seed, {tapt::stream::kCoordinator, e->gid0 + i, e->Q + 1}).state();
-    e->paccs.upload(as, e->stream);
+    // accept streams for this round (derived on the device: {kCoordinator, gid, round})
+    e->paccs.alloc(e->I);
+    ++g_launches;
+    k_derive_round_streams<<<e->I, 32, 0, e->stream>>>(e->seed, e->gid0, e->ptargets.p, 0, e->R, e->Q + 1, nullptr,
+                                                       nullptr, e->paccs.p);
+    CUDA_OK(cudaGetLastError());
     e->pacc.alloc((size_t)e->I * T);
     const uint8_t* forced = nullptr;
     if (lqc) {  // MH correction: decide on the host with libm exp (bit-exact with the oracle)
+        std::vector<uint64_t> as(e->I);
+        for (uint32_t i = 0; i < e->I; ++i)
+            as[i] = tapt::RngStream::derive(e->seed, {tapt::stream::kCoordinator, e->gid0 + i, e->Q + 1}).state();
         std::vector<int32_t> Ep = e->pE.download(e->stream);
         std::vector<int32_t> Eb = e->E.download(e->stream);
         std::vector<uint8_t> bo = e->buf_of.download(e->stream);
@@ -1748,12 +1753,11 @@ void finish_proposals(tapt_ensemble_s* e, const uint32_t* targets, uint32_t T, b
         e->words.p, n, e->G, e->W, e->buf_of.p, e->R, e->pwords.p, GT, WT, e->ptargets.p, (int)T, e->pacc.p);
     CUDA_OK(cudaGetLastError());
     e->update_best_from_E();
-    if (accepted) {
+    if (accepted) {  // synchronous copy into the caller's buffer; otherwise the round stays stream-ordered
         auto a = e->pacc.download(e->stream);
         std::copy(a.begin(), a.end(), accepted);
     }
     e->Q += 1;
-    sync_if(e->stream);
 }
 
 void prepare_targets(tapt_ensemble_s* e, const uint32_t* targets, uint32_t T) {
@@ -1769,6 +1773,8 @@ void prepare_targets(tapt_ensemble_s* e, const uint32_t* targets, uint32_t T) {
     e->pwords.alloc((size_t)e->I * GT * n);
     e->pE.alloc((size_t)e->I * T);
     std::vector<uint32_t> tg(targets, targets + T);
+    if (tg == e->last_targets && e->ptargets.n == T && e->pslot.n == (size_t)e->I * T) return;
+    e->last_targets = tg;
     e->ptargets.upload(tg, e->stream);
     std::vector<uint8_t> ps((size_t)e->I * T);
     for (uint32_t i = 0; i < e->I; ++i)
@@ -1798,6 +1804,7 @@ tapt_status tapt_inject_proposals(tapt_ensemble_t e, const int8_t* proposals, in
                                                                             (int)T, e->clamp_ptr(), e->clamp_count());
         CUDA_OK(cudaGetLastError());
         finish_proposals(e, targets, T, false, lqc, lqp, accepted);
+        if (!on_device) sync_if(e->stream);  // the caller's host buffer (possibly pinned) is free on return
     });
 }
 
@@ -1818,6 +1825,7 @@ tapt_status tapt_inject_proposals_packed(tapt_ensemble_t e, const uint8_t* propo
                                                                              e->clamp_ptr(), e->clamp_count());
         CUDA_OK(cudaGetLastError());
         finish_proposals(e, targets, T, false, nullptr, nullptr, accepted);
+        if (!on_device) sync_if(e->stream);  // the caller's host buffer (possibly pinned) is free on return
     });
 }
 
@@ -1828,22 +1836,23 @@ tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, 
         prepare_targets(e, targets, T);
         const int n = e->n();
         const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
-        // per (instance, target) proposal streams, per (target, sign) bias thresholds
-        std::vector<uint64_t> qs((size_t)e->I * T), full((size_t)e->I * e->R, 0), tup(2 * T);
-        for (uint32_t i = 0; i < e->I; ++i)
-            for (uint32_t t = 0; t < T; ++t) {
-                const uint64_t q = tapt::RngStream::derive(
-                                       e->seed, {tapt::stream::kReplica, e->gid0 + i, (uint64_t)targets[t], e->Q + 1})
-                                       .state();
-                qs[(size_t)i * T + t] = q;
-                full[(size_t)i * e->R + targets[t]] = q;
-            }
+        // per (instance, target) proposal streams {kReplica, gid, target, round}, derived on the device
+        // into [I][T] and slot-indexed [I][R] (the refinement sweeps); per (target, sign) bias thresholds
+        std::vector<uint64_t> tup(2 * T);
+        e->pstreams.alloc((size_t)e->I * T);
+        if (e->pfull.n != (size_t)e->I * e->R) {
+            e->pfull.alloc((size_t)e->I * e->R);
+            e->pfull.zero(e->stream);
+        }
+        ++g_launches;
+        k_derive_round_streams<<<e->I, 64, 0, e->stream>>>(e->seed, e->gid0, e->ptargets.p, (int)T, e->R, e->Q + 1,
+                                                           e->pstreams.p, e->pfull.p, nullptr);
+        CUDA_OK(cudaGetLastError());
         for (uint32_t t = 0; t < T; ++t) {
             const double mb = m_bias ? m_bias[t] : 0.0;
             tup[2 * t + 0] = threshold_of((1.0 + -1.0 * mb) / 2.0);
             tup[2 * t + 1] = threshold_of((1.0 + 1.0 * mb) / 2.0);
         }
-        e->pstreams.upload(qs, e->stream);
         e->ptup.upload(tup, e->stream);
         ++g_launches;
         k_gen_proposals<<<dim3((n + 255) / 256, GT, e->I), 256, 0, e->stream>>>(
@@ -1851,14 +1860,12 @@ tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, 
         CUDA_OK(cudaGetLastError());
         bool have_E = false;
         if (refine) {
-            DevBuf<uint64_t> fs;
-            fs.upload(full, e->stream);
             PTArgs a = e->base_args();
             a.words = e->pwords.p;
             a.G = GT;
             a.W = WT;
             a.B = (int)T;
-            a.streams = fs.p;
+            a.streams = e->pfull.p;
             a.slot_of = e->pslot.p;
             a.buf_of = nullptr;
             a.E = e->pE.p;
@@ -1877,7 +1884,6 @@ tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, 
             }
             e->launch(a, false);
             have_E = true;
-            sync_if(e->stream);
         }
         finish_proposals(e, targets, T, have_E, nullptr, nullptr, accepted);
     });

@@ -293,3 +293,42 @@ __global__ void k_csr_from_signs(const int8_t* signs, int nbonds, const uint32_t
 }
 
 }  // namespace tapt_dev
+
+namespace tapt_dev {
+
+// RngStream::derive (proj/include/tapt/rng.hpp:21-27; include/tapt/rng.hpp derive_n) on the device:
+// h = hash(root ^ phi), then h = hash(h ^ (p + phi)) for every path component, hash(v) = mix(v + phi).
+__device__ __forceinline__ uint64_t d_hash64(uint64_t v) { return mix_final(v + kPhi); }
+
+// Proposal-round streams: per (instance, target) {kReplica, gid, target, round} into qs [I][T] and
+// full [I][R] (slot-indexed, for the refinement sweeps), and per instance the accept stream
+// {kCoordinator, gid, round} into acc [I].  Grid: one block per instance.
+__global__ void k_derive_round_streams(uint64_t seed, uint64_t gid0, const uint32_t* targets, int T, int R,
+                                       uint64_t round, uint64_t* qs, uint64_t* full, uint64_t* acc) {
+    const int i = blockIdx.x;
+    const uint64_t h0 = d_hash64(seed ^ kPhi), gid = gid0 + (uint64_t)i;
+    for (int t = threadIdx.x; t < T; t += blockDim.x) {
+        uint64_t h = d_hash64(h0 ^ (0x22ull + kPhi));
+        h = d_hash64(h ^ (gid + kPhi));
+        h = d_hash64(h ^ ((uint64_t)targets[t] + kPhi));
+        h = d_hash64(h ^ (round + kPhi));
+        if (qs) qs[(size_t)i * T + t] = h;
+        if (full) full[(size_t)i * R + targets[t]] = h;
+    }
+    if (threadIdx.x == 0 && acc) {
+        uint64_t h = d_hash64(h0 ^ (0x33ull + kPhi));
+        h = d_hash64(h ^ (gid + kPhi));
+        acc[i] = d_hash64(h ^ (round + kPhi));
+    }
+}
+
+// best[i] = min(best[i], min_b E[i][b]) (one thread per instance)
+__global__ void k_best_from_E(const int32_t* E, int I, int B, int* best) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= I) return;
+    int m = best[i];
+    for (int b = 0; b < B; ++b) m = min(m, E[(size_t)i * B + b]);
+    best[i] = m;
+}
+
+}  // namespace tapt_dev

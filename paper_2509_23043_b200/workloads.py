@@ -55,7 +55,7 @@ def build(T, cfg, stream_ptr=None, instances=None):
         def step():
             for _ in range(1000 // every):
                 e.run(every, swap_every=1, measure_every=10)
-                e.generate_proposals(np.arange(nt), mb, refine=5)
+                e.generate_proposals(np.arange(nt), mb, refine=5, return_accepted=False)
         upd = I * (R * n * 1000 + (1000 // every) * nt * n * 5)
         desc = (f"config 2: 2D ferro L=64, 64 slots geometric [0.3,0.6], {I} chains, TAPT every 100 sweeps into "
                 "60 slots (Yang-biased i.i.d. + 5 sweeps + Eq. 2)")

@@ -23,7 +23,7 @@ for _ in range(10):
     a0.record(stream)
     e.run(100, swap_every=1, measure_every=10)
     a1.record(stream)
-    e.generate_proposals(np.arange(60), mb, refine=5)
+    e.generate_proposals(np.arange(60), mb, refine=5, return_accepted=False)
     a2.record(stream)
     torch.cuda.synchronize()
     tr += a0.elapsed_time(a1)
