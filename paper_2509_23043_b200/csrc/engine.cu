@@ -624,23 +624,34 @@ struct tapt_ensemble_s {
         if (m->k3_state != 1) return false;
         // energy counters: at most 2 x 127 per site and thread per sweep into 12 planes
         if (m->k3_max_per_thread * 254 > 4095) return false;
-        // instance teams per CTA: the most that fit the shared memory (graph staged once per CTA) and
-        // leave no more co-resident teams than instances, so that every SM gets work (the balanced
-        // schedule then spreads I > M instances evenly); fewer instances than one team per CTA can
-        // hold: one team per CTA
+        // Instance teams per CTA (the graph is staged once per CTA).  Modelled throughput, with the
+        // per-team rate r(k) for k teams on an SM measured on config 4 (tools/k3_ipb_shards.py:
+        // 1.64 / 1.32 / 1.00 / 0.83 G updates/s for k = 1..4):
+        //   balanced:   co-resident teams M(ipb) <= I, every SM busy  -> M x r(teams per SM)
+        //   one CTA/SM: ipb = ceil(I / SMs) <= 4                      -> I x r(ipb)
+        // (config 4 at 512 / 256 / 128 / 64 instances -> 3 / 2 / 1 / 1 teams per CTA)
         int fit = 0;
         for (int ipb = 4; ipb >= 1 && !fit; --ipb)
             if (k3_smem_bytes(R, nidx, m->k3_nadj, (int)m->free_sites.size(), n(), (int)m->col_ptr.size() - 1, ipb) <=
                 200 * 1024)
                 fit = ipb;
         if (!fit) return false;
-        k3_ipb = 1;
+        auto rate = [](int k) { return k <= 1 ? 1.64 : k == 2 ? 1.32 : k == 3 ? 1.0 : 0.83 * 4.0 / k; };
+        int dev = 0, nsm = 148;
+        CUDA_OK(cudaGetDevice(&dev));
+        CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         PTArgs a = base_args();
-        for (int ipb = fit; ipb >= 1; --ipb) {
+        double best = -1.0;
+        k3_ipb = 1;
+        for (int ipb = 1; ipb <= fit; ++ipb) {
             const int M = k3_resident_units(a, k3_args(), ipb);
-            if (M > 0 && M <= (int)I) {
+            double v = -1.0;
+            if (M > 0 && M <= (int)I) v = M * rate(M / nsm);
+            if (((int)I + ipb - 1) / ipb <= nsm)
+                v = std::max(v, (double)I * rate(ipb));
+            if (v > best) {
+                best = v;
                 k3_ipb = ipb;
-                break;
             }
         }
         if (const char* e = std::getenv("TAPT_K3_IPB"))
@@ -1211,6 +1222,35 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
         const int n = (int)m->n;
         e->use_k1 = m->k1 && d->order == TAPT_ORDER_COLOUR && !e->has_clamps();
         if (e->use_k1) {
+            // Replica-group width: with fewer instance-groups than SMs (e.g. configs 2/3 sharded over
+            // 8 GPUs), narrower groups (16 or 8 replicas per CTA, clusters of up to 8 CTAs) spread each
+            // instance over more SMs.  Results do not depend on the grouping (streams and tables are
+            // keyed by slot; tests/test_gpu_parity.py::test_k1_group_width_does_not_change_the_chain).
+            int dev = 0, nsm = 148;
+            CUDA_OK(cudaGetDevice(&dev));
+            CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+            // Model: throughput ~ eff(W) x min(1, CTAs / SMs) with one 512-thread CTA per SM; eff measured
+            // on config 3 (tools/narrow_groups.py: 32 / 16 / 8 replicas -> 782 / 550 / 355 G/s at 256
+            // instances).  Small lattices (several 128-thread CTAs per SM) keep 32-replica groups.
+            int w = e->W;
+            if (n / 4 >= TAPT_K1_DEFAULT_THREADS) {
+                auto score = [&](int cand) {
+                    const double eff = cand >= 32 ? 1.0 : (cand >= 16 ? 0.70 : 0.455);
+                    const double ctas = (double)e->I * ((e->R + cand - 1) / cand);
+                    return eff * std::min(1.0, ctas / nsm);
+                };
+                double best = score(w);
+                for (int cand : {16, 8})
+                    if (e->R > cand && (e->R + cand - 1) / cand <= 8 && score(cand) > 1.05 * best) {
+                        best = score(cand);
+                        w = cand;
+                    }
+            }
+            if (const char* env = std::getenv("TAPT_K1_W")) w = std::max(1, std::min(kW, std::atoi(env)));
+            w = std::min(w, e->R);
+            if ((e->R + w - 1) / w > 8) throw tapt::ConfigError("TAPT_K1_W: at most 8 replica groups per instance");
+            e->W = w;
+            e->G = (e->R + w - 1) / w;
             e->nidx = 2 * m->dim + 1;
             int nt = TAPT_K1_DEFAULT_THREADS;
             if (n / 4 < TAPT_K1_DEFAULT_THREADS) {

@@ -353,8 +353,14 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
                         nw[u] = 0;  // NOT(up) bits, replica b at bit b
                     }
                     bool tie = false;
+                    // full 32-, 16- and 8-replica groups unrolled (narrow groups spread an instance over
+                    // more CTAs when instances are few); partial groups take the rolled loop
                     if (nv == kW)
                         k1_decide<kW, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                    else if (nv == 16)
+                        k1_decide<16, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                    else if (nv == 8)
+                        k1_decide<8, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
                     else
                         k1_decide<0, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
                     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);

@@ -222,6 +222,37 @@ def test_k1_k2_k3_give_the_same_chain_on_a_lattice(monkeypatch):
         assert np.array_equal(a.energies(), e.energies())
 
 
+@pytest.mark.parametrize("dims,R", [((16,), 64), ((32, 32), 32), ((16, 16), 40)])
+def test_k1_group_width_does_not_change_the_chain(monkeypatch, dims, R):
+    """Narrow replica groups (16 or 8 replicas per CTA, clusters of up to 8 CTAs; chosen when the
+    instances are fewer than the SMs) give the same chain, counters, observables and histograms as
+    32-replica groups, and the oracle."""
+    betas = H.linear(0.2, 3.0, R)
+
+    def run(w):
+        monkeypatch.setenv("TAPT_K1_W", str(w))
+        e = T.Ensemble(T.Model.lattice(dims), betas, n_instances=3, seed=21)
+        assert e.kernel == "lattice"
+        if len(dims) == 1:
+            e.generate_ea_disorder(4)
+        e.init_random()
+        n = e.n
+        e.set_histogram(-3 * n, 16, 3 * n // 8)
+        e.run(17, swap_every=1, measure_every=3)
+        e.generate_proposals(np.arange(min(R, 20)), None, refine=2)
+        e.run(13, swap_every=2, measure_every=2)
+        return e
+    ref = run(32)
+    for w in (16, 8):
+        e = run(w)
+        for x, y in zip((ref.spins(), ref.energies(), ref.permutation(), ref.observables(), ref.histogram(), ref.best()),
+                        (e.spins(), e.energies(), e.permutation(), e.observables(), e.histogram(), e.best())):
+            assert np.array_equal(x, y)
+        for x, y in zip(ref.acceptance(), e.acceptance()):
+            assert np.array_equal(x, y)
+    monkeypatch.delenv("TAPT_K1_W")
+
+
 def test_k3_circuit_with_clamps_and_fields_matches_oracle(monkeypatch):
     monkeypatch.setenv("TAPT_K3", "1")
     g = _random_circuit(13)
