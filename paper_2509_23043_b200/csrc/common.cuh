@@ -158,6 +158,7 @@ struct MetroTable {
     const uint32_t* K;    // row length
     const int64_t* kz;    // largest -dE with nonzero probability (-1: none beyond table)
     const uint8_t* always;  // row accepts everything (c == 0)
+    const double* c;        // row coefficient: accept iff uniform < exp(-c k), k = -dE
 };
 
 __device__ __forceinline__ bool metro_accept(const MetroTable& t, int row, int64_t dE, uint64_t x) {

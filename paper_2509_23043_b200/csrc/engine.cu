@@ -48,7 +48,7 @@ int k3_row_stride();
 int k3_resident_units(const PTArgs& a, const Csr3& g, int ipb);
 cudaError_t launch_k3(const PTArgs& a, const Csr3& g, int ipb, cudaStream_t st);
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st);
-size_t k1_smem_bytes(int n, bool dis);
+size_t k1_smem_bytes(int n, bool dis, int R);
 size_t k2_smem_bytes(int n, int R, int nidx);
 size_t k2_smem_bytes_graph(int n, int R, int nidx, int nnz, int nfree);
 cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st,
@@ -213,7 +213,9 @@ struct HostMetro {
     std::vector<uint32_t> off, K;
     std::vector<int64_t> kz;
     std::vector<uint8_t> always;
+    std::vector<double> coef;
     void add_row(double c) {
+        coef.push_back(c > 0.0 ? c : 0.0);
         off.push_back(static_cast<uint32_t>(tab.size()));
         if (!(c > 0.0)) {  // c == 0: exp(0) = 1 > uniform always
             always.push_back(1);
@@ -261,14 +263,16 @@ struct DevMetro {
     DevBuf<uint32_t> off, K;
     DevBuf<int64_t> kz;
     DevBuf<uint8_t> always;
+    DevBuf<double> coef;
     void upload(const HostMetro& h, cudaStream_t st) {
+        coef.upload(h.coef, st);
         tab.upload(h.tab, st);
         off.upload(h.off, st);
         K.upload(h.K, st);
         kz.upload(h.kz, st);
         always.upload(h.always, st);
     }
-    MetroTable view() const { return MetroTable{tab.p, off.p, K.p, kz.p, always.p}; }
+    MetroTable view() const { return MetroTable{tab.p, off.p, K.p, kz.p, always.p, coef.p}; }
 };
 
 }  // namespace
@@ -1268,7 +1272,7 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
             // colour-1 sites (2*dim each) and up-spins of its share of all sites
             while (nt < 1024 && ((n / 2 + nt - 1) / nt * 2 * m->dim >= 256 || (n + nt - 1) / nt >= 256)) nt *= 2;
             e->k1_threads = nt;
-            if (k1_smem_bytes(n, true) > 227 * 1024) throw tapt::SizeError("lattice too large for shared memory");
+            if (k1_smem_bytes(n, true, e->R) > 227 * 1024) throw tapt::SizeError("lattice too large for shared memory");
         } else {
             if (m->max_sumabs > 255) throw tapt::SizeError("sum of |J| at a site exceeds 255 (byte-SWAR fields)");
             e->nidx = m->lmax - m->lmin + 1;

@@ -156,6 +156,9 @@ struct K1Smem {
 
 // Dynamic shared memory holds the spin words (and bond bytes); the control block is static.
 __host__ __device__ constexpr size_t k1_words_offset() { return 0; }
+__host__ __device__ constexpr size_t k1_stage_offset(int n, bool dis) {
+    return (k1_words_offset() + (size_t)n * 4 + (dis ? (size_t)n : 0) + 15) & ~size_t(15);
+}
 
 // Heat-bath decisions for one site word over the W replicas of this CTA.
 __device__ __forceinline__ uint32_t k1_decide_exact(const K1Smem& sm, int W, uint64_t phi_i, const uint32_t (&N)[4]) {
@@ -266,11 +269,19 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
     __shared__ K1Smem sm;  // static: table addresses fold into LDS immediates
     uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw);
     uint8_t* bonds = reinterpret_cast<uint8_t*>(words + a.n);
+    // staged once per launch / item: heat-bath thresholds of every slot and the instance's stream
+    // states, so that the per-sweep table and stream-base refresh reads no global memory
+    uint64_t* thrS = reinterpret_cast<uint64_t*>(smem_raw + k1_stage_offset(a.n, a.bonds != nullptr));
+    uint64_t* strS = thrS + (size_t)a.R * 8;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     const int cl = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
     const int half = n >> 1, nsub = half / SP;
     const int it0 = a.sched ? a.sched_ptr[cl] : 0, it1 = a.sched ? a.sched_ptr[cl + 1] : 1;
+    for (int e = tid; e < a.R * 8; e += nt) {
+        const int r = e >> 3, k = e & 7;
+        thrS[e] = k < a.nidx ? a.thr[(size_t)r * a.nidx + k] : 0ull;
+    }
     for (int it = it0; it < it1; ++it) {
     const SchedItem item = a.sched ? a.sched[it] : SchedItem{cl, 0, a.energy_only ? 1 : a.n_sweeps, -1, -1};
     const int inst = item.inst;
@@ -288,6 +299,7 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
         }
     }
     pt_load_perm(a, sm.S, inst);
+    for (int r = tid; r < a.R; r += nt) strS[r] = a.streams[(size_t)inst * a.R + r];
     __syncthreads();
 
     // swap passes before this item: sweeps T = t+1 in (t0, t0+s0] with swap_every | T
@@ -302,13 +314,16 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
         for (int e = tid; e < nv * 8; e += nt) {
             const int b = e >> 3, k = e & 7;
             const int slot = sm.S.slot_of[grp * W + b];
-            const uint64_t T = k < a.nidx ? a.thr[(size_t)slot * a.nidx + k] : 0ull;
+            const uint64_t T = thrS[slot * 8 + k];
             // UM1: store U - 1 (clamped at 0) so that h - (U - 1) is both the carry of the decision
             // and the tie band {0, 1, 2} (h = U - 1 falls in the band and is redone exactly)
             sm.Uhi[b][k] = TAPT_K1_UM1 ? max(thr_hi(T), 1u) - 1u : thr_hi(T);
             sm.T64[b][k] = T;
         }
-        pt_stream_bases(a, sm.S, inst, grp, t);
+        {  // pt_stream_bases with the staged stream states
+            const uint64_t k0 = a.draw_base + t * (uint64_t)a.n_free + 1ull;
+            for (int b = tid; b < nv; b += nt) sm.S.sb[b] = strS[sm.S.slot_of[grp * W + b]] + k0 * kPhi;
+        }
         __syncthreads();
 
         uint32_t C[kCnt];
@@ -425,16 +440,17 @@ __global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const L
     }
 }
 
-size_t k1_smem_bytes(int n, bool dis) {
-    // dynamic part only (the static K1Smem block is accounted by the compiler)
-    return k1_words_offset() + (size_t)n * 4 + (dis ? (size_t)n : 0);
+size_t k1_smem_bytes(int n, bool dis, int R) {
+    // dynamic part only (the static K1Smem block is accounted by the compiler): words, bond bytes,
+    // then the staged slot thresholds [R][8] and stream states [R]
+    return k1_stage_offset(n, dis) + (size_t)R * 9 * 8;
 }
 
 // resident != null: report how many clusters (or CTAs, without a cluster) of this launch shape
 // are co-resident on the device instead of launching.
 template <int DIM, bool DIS, bool CLU>
 static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st, int* resident) {
-    const size_t smem = k1_smem_bytes(a.n, DIS);
+    const size_t smem = k1_smem_bytes(a.n, DIS, a.R);
     // SP = 1 site word per thread-iteration at 1024 threads, else 2 interleaved at <= 512
     // launch shapes: 2 interleaved site words per thread-iteration at <= 512 threads (default),
     // 2 at 513..768 (<= 85 registers), 1 at > 768, 4 at <= 256

@@ -37,6 +37,7 @@ struct PTShared {
     uint8_t slot_of[kMaxR];
     uint8_t buf_of[kMaxR];
     uint32_t sacc[kMaxR];   // swap accepts of this launch by pair (flushed by pt_finish)
+    uint64_t coord;         // the instance's coordinator stream state (swap draws)
     int best;
     int tie;
 };
@@ -47,6 +48,7 @@ struct SwapMeta {
     uint32_t off, K;
     int64_t kz;
     uint32_t always;
+    double c;
 };
 constexpr int kSwm = 128;
 __shared__ SwapMeta g_swm[kSwm];
@@ -54,17 +56,27 @@ __shared__ SwapMeta g_swm[kSwm];
 __device__ __forceinline__ void pt_stage_swap(const PTArgs& a) {
     if (a.swap_every <= 0 || a.R - 1 > kSwm || !a.swap_tab.off) return;
     for (int r = threadIdx.x; r < a.R - 1; r += blockDim.x)
-        g_swm[r] = SwapMeta{a.swap_tab.off[r], a.swap_tab.K[r], a.swap_tab.kz[r], a.swap_tab.always[r]};
+        g_swm[r] = SwapMeta{a.swap_tab.off[r], a.swap_tab.K[r], a.swap_tab.kz[r], a.swap_tab.always[r],
+                            a.swap_tab.c ? a.swap_tab.c[r] : -1.0};
 }
 
-// metro_accept (common.cuh) for swap pair r with the staged metadata.
+// metro_accept (common.cuh) for swap pair r with the staged metadata.  Inside the table the
+// decision  uniform < p_host = exp(-c k)  (libm, tabulated as T = ceil(p 2^53)) is taken from the
+// device exp when the draw is outside a relative band of 1e-12 around it (device and host exp differ
+// by a few ulp, ~1e-16), so the table -- a dependent global load -- is read only inside the band.
 __device__ __forceinline__ bool pt_swap_accept(const PTArgs& a, int r, int64_t dE, uint64_t x) {
     if (a.R - 1 > kSwm) return metro_accept(a.swap_tab, r, dE, x);
     const SwapMeta m = g_swm[r];
     if (dE >= 0 || m.always) return true;
     const int64_t k = -dE;
-    const uint64_t T = k < (int64_t)m.K ? a.swap_tab.tab[m.off + k] : (k <= m.kz ? 1ull : 0ull);
-    return below(x, T);
+    if (k >= (int64_t)m.K) return below(x, k <= m.kz ? 1ull : 0ull);
+    if (m.c >= 0.0) {
+        const double p = exp(m.c * -(double)k);
+        const double u = (double)(x >> 11) * 0x1.0p-53;
+        if (u < p * (1.0 - 1e-12)) return true;
+        if (u > p * (1.0 + 1e-12)) return false;
+    }
+    return below(x, a.swap_tab.tab[m.off + k]);
 }
 
 // Number of valid buffers owned by group `grp` (the last group of an instance may be partial).
@@ -81,6 +93,7 @@ __device__ __forceinline__ void pt_load_perm(const PTArgs& a, PTShared& S, int i
     if (t0 == 0) {
         S.best = a.best ? a.best[inst] : 0x7FFFFFFF;
         S.tie = 0;
+        S.coord = a.coord ? a.coord[inst] : 0ull;
     }
     for (int k = t0; k < kW; k += nt) {
         S.Ucnt[k] = 0;
@@ -133,7 +146,7 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
     }
     if (a.swap_every > 0 && (T % (uint64_t)a.swap_every) == 0) {
         const int parity = (int)(pass & 1);
-        const uint64_t c0 = a.coord[inst];
+        const uint64_t c0 = S.coord;
         for (int r = parity + 2 * tid; r + 1 < a.R; r += 2 * nt) {
             const int b0 = S.buf_of[r], b1 = S.buf_of[r + 1];
             const int64_t dE = (int64_t)S.Eall[b1] - (int64_t)S.Eall[b0];
