@@ -345,16 +345,48 @@ __global__ void __launch_bounds__(kT3 * kIPB3, 1) k3_bitcsr_pt(const PTArgs a, c
                 }
                 tm.sync();
             }
-            // E_b += 2 (sum over threads of C_b - sum of the per-site constants)
+            // E_b += 2 (sum over threads of C_b - sum of the per-site constants).  The 4 warps' sliced
+            // counters are summed bit-sliced through shared memory (the threshold rows, rebuilt at the
+            // start of every sweep, serve as scratch), then each warp transposes a quarter of the planes.
             {
-                const uint32_t tot = warp_sliced_total<kC3>(C);
-                if (lane < nv) atomicAdd(&S.Ucnt[lane], tot);
+                constexpr int kP = kC3 + 2;  // planes of the 4-warp sum
+                const int wq = ti >> 5;      // warp in the team
+                uint32_t* scr = Ubuf;        // [3][kC3][32] counters of warps 1..3 | [kP][32] sum | [4] corr
+                uint32_t* sum = scr + 3 * kC3 * 32;
+                int* csc = reinterpret_cast<int*>(sum + kP * 32);
                 int cw = corr;
 #pragma unroll
                 for (int d = 16; d >= 1; d >>= 1) cw += __shfl_xor_sync(0xFFFFFFFFu, cw, d);
-                if (ti == 0) corr_sh[kin] = 0;
+                if (wq > 0) {
+#pragma unroll
+                    for (int k = 0; k < kC3; ++k) scr[((wq - 1) * kC3 + k) * 32 + lane] = C[k];
+                }
+                if (lane == 0) csc[wq] = cw;
                 tm.sync();
-                if (lane == 0) atomicAdd(&corr_sh[kin], cw);
+                if (wq == 0) {
+                    uint32_t A[kP];
+#pragma unroll
+                    for (int k = 0; k < kC3; ++k) A[k] = C[k];
+                    A[kC3] = A[kC3 + 1] = 0;
+#pragma unroll
+                    for (int q = 0; q < 3; ++q) {
+                        uint32_t c;
+                        ha(A[0], scr[(q * kC3) * 32 + lane], A[0], c);
+#pragma unroll
+                        for (int k = 1; k < kC3; ++k) fa(A[k], scr[(q * kC3 + k) * 32 + lane], c, A[k], c);
+                        ha(A[kC3], c, A[kC3], c);
+                        A[kC3 + 1] ^= c;
+                    }
+#pragma unroll
+                    for (int k = 0; k < kP; ++k) sum[k * 32 + lane] = A[k];
+                    if (lane == 0) corr_sh[kin] = csc[0] + csc[1] + csc[2] + csc[3];
+                }
+                tm.sync();
+                uint32_t tot = 0;
+#pragma unroll
+                for (int k = 0; k < kP; k += 4)
+                    if (k + wq < kP) tot += (uint32_t)__popc(warp_transpose32(sum[(k + wq) * 32 + lane])) << (k + wq);
+                if (lane < nv) atomicAdd(&S.Ucnt[lane], tot);
                 tm.sync();
                 for (int b = ti; b < nv; b += kT3) {
                     S.Eown[par][b] = S.Eown[prev][b] + 2 * ((int32_t)S.Ucnt[b] - corr_sh[kin]);
