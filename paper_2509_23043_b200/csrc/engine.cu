@@ -1259,12 +1259,13 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
             int nt = TAPT_K1_DEFAULT_THREADS;
             if (n / 4 < TAPT_K1_DEFAULT_THREADS) {
                 // small lattices: one whole-SM CTA per instance-group while they do not exceed the
-                // SMs, else 128-thread CTAs so that several share an SM (config 1, 1024 sites:
-                // 16 seeds 42 -> 51 G/s, 296 seeds 340 -> 627 G/s)
+                // SMs, else 256-thread CTAs (2 site words per thread, registers capped for 2 CTAs per
+                // SM) so that several share an SM (config 1, 1024 sites: 16 seeds 42 -> 51 G/s; 296
+                // seeds: 128-thread CTAs 627, 256-thread CTAs 674 G/s; tools/cfg1_shapes.sh)
                 int dev = 0, nsm = 148;
                 CUDA_OK(cudaGetDevice(&dev));
                 CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-                nt = (long long)e->I * e->G >= 2ll * nsm ? 128 : TAPT_K1_DEFAULT_THREADS;
+                nt = (long long)e->I * e->G >= 2ll * nsm ? 256 : TAPT_K1_DEFAULT_THREADS;
             }
             if (const char* env = std::getenv("TAPT_K1_THREADS")) nt = std::max(32, std::min(1024, std::atoi(env)));
             nt = (nt / 32) * 32;

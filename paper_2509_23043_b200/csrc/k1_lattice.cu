@@ -263,8 +263,9 @@ __device__ __forceinline__ void k1_decide2(const K1Smem& sm, int nv, uint64_t ph
     w1 = w[1];
 }
 
-template <int DIM, bool DIS, bool CLU, int SP, int MAXT>
-__global__ void __launch_bounds__(MAXT, 1) k1_lattice_pt(const PTArgs a, const LatDims d) {
+// MINB: CTAs per SM the register allocation must allow (2 for the 256-thread small-lattice shape)
+template <int DIM, bool DIS, bool CLU, int SP, int MAXT, int MINB = 1>
+__global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, const LatDims d) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ K1Smem sm;  // static: table addresses fold into LDS immediates
     uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw);
@@ -454,10 +455,11 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
     // SP = 1 site word per thread-iteration at 1024 threads, else 2 interleaved at <= 512
     // launch shapes: 2 interleaved site words per thread-iteration at <= 512 threads (default),
     // 2 at 513..768 (<= 85 registers), 1 at > 768, 4 at <= 256
-    auto fn = threads > 768   ? k1_lattice_pt<DIM, DIS, CLU, 1, 1024>
-              : threads > 512 ? k1_lattice_pt<DIM, DIS, CLU, 2, 768>
-              : threads > 256 ? k1_lattice_pt<DIM, DIS, CLU, 2, 512>
-                              : k1_lattice_pt<DIM, DIS, CLU, 4, 256>;
+    auto fn = threads > 768    ? k1_lattice_pt<DIM, DIS, CLU, 1, 1024>
+              : threads > 512  ? k1_lattice_pt<DIM, DIS, CLU, 2, 768>
+              : threads > 256  ? k1_lattice_pt<DIM, DIS, CLU, 2, 512>
+              : threads == 256 ? k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2>
+                               : k1_lattice_pt<DIM, DIS, CLU, 4, 256>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
