@@ -1266,6 +1266,14 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
                 CUDA_OK(cudaGetDevice(&dev));
                 CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
                 nt = (long long)e->I * e->G >= 2ll * nsm ? 256 : TAPT_K1_DEFAULT_THREADS;
+            } else if (k1_smem_bytes(n, true, e->R) <= 100 * 1024) {
+                // mid-size lattices with at least two instance-groups per SM: two independent 256-thread
+                // CTAs per SM (barriers decoupled) instead of one 512-thread CTA (config 3: 803 -> 840
+                // G/s; config 2's 256 groups on 296 slots lose 7 % and keep 512 threads)
+                int dev = 0, nsm = 148;
+                CUDA_OK(cudaGetDevice(&dev));
+                CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+                if ((long long)e->I * e->G >= 2ll * nsm) nt = 256;
             }
             if (const char* env = std::getenv("TAPT_K1_THREADS")) nt = std::max(32, std::min(1024, std::atoi(env)));
             nt = (nt / 32) * 32;
