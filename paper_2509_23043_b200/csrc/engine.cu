@@ -791,11 +791,11 @@ struct tapt_ensemble_s {
         return nt;
     }
 
-    void launch(const PTArgs& a, bool cluster) {
+    void launch(const PTArgs& a, bool cluster, int k1_nt = 0) {
         ++g_launches;
         cudaError_t e;
         if (use_k1) {
-            e = launch_k1(a, m->ld, k1_threads, cluster, stream);
+            e = launch_k1(a, m->ld, k1_nt > 0 ? k1_nt : k1_threads, cluster, stream);
         } else if (!a.energy_only && a.G == 1 && k3_eligible()) {
             e = launch_k3(a, k3_args(), k3_ipb, stream);
         } else {
@@ -1935,7 +1935,18 @@ tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, 
                                                                      g.J, g.nJ, g.nnz, g.h, e->pE.p);
                 CUDA_OK(cudaGetLastError());
             }
-            e->launch(a, false);
+            // refinement sweeps of the proposal groups: I x GT CTAs of their own; when they exceed the SMs
+            // but fit two 256-thread CTAs per SM, one wave of those beats two of 512-thread CTAs
+            // (config 2: 128 x 2 groups)
+            int nt = 0;
+            if (e->use_k1 && e->k1_threads == 512 && k1_smem_bytes(n, true, e->R) <= 100 * 1024) {
+                int dev = 0, nsm = 148;
+                CUDA_OK(cudaGetDevice(&dev));
+                CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+                const long long ctas = (long long)e->I * GT;
+                if (ctas > nsm && ctas <= 2ll * nsm) nt = 256;
+            }
+            e->launch(a, false, nt);
             have_E = true;
         }
         finish_proposals(e, targets, T, have_E, nullptr, nullptr, accepted);
