@@ -253,6 +253,51 @@ def test_k1_group_width_does_not_change_the_chain(monkeypatch, dims, R):
     monkeypatch.delenv("TAPT_K1_W")
 
 
+def test_k1_automatic_group_width_for_few_instances(monkeypatch):
+    """Few instances (4 x 64 slots on a 16^3 lattice: 8 groups of 32 < SMs) take narrower groups
+    automatically; the chain equals the 32-replica one."""
+    betas = H.linear(0.2, 3.0, 64)
+
+    def run(w):
+        if w is None:
+            monkeypatch.delenv("TAPT_K1_W", raising=False)
+        else:
+            monkeypatch.setenv("TAPT_K1_W", str(w))
+        e = T.Ensemble(T.Model.lattice((16,)), betas, n_instances=4, seed=33)
+        e.generate_ea_disorder(2)
+        e.init_random()
+        e.run(30, swap_every=1, measure_every=5)
+        return e
+    a, b = run(32), run(None)
+    for x, y in zip((a.spins(), a.energies(), a.permutation(), a.observables()),
+                    (b.spins(), b.energies(), b.permutation(), b.observables())):
+        assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("ipb", [1, 2, 3, 4])
+def test_k3_teams_per_cta_do_not_change_the_chain(monkeypatch, ipb):
+    """1-4 instance teams per CTA (named barriers, shared staged graph) give the same chain."""
+    M = T.Multiplier(8)
+    m = M.model()
+    I, R = 10, 32
+    prods = [T.random_semiprime(3, k, 8) for k in range(I)]
+    cl = np.stack([M.clamps(p * q) for p, q in prods])
+
+    def run(v):
+        monkeypatch.setenv("TAPT_K3_IPB", str(v))
+        e = T.Ensemble(m, H.geometric(0.1, 5.0, R), n_instances=I, seed=12)
+        assert e.kernel == "bitcsr"
+        e.set_clamps(cl)
+        e.init_random()
+        e.run(35, swap_every=1, measure_every=4)
+        return e
+    a, b = run(1), run(ipb)
+    for x, y in zip((a.spins(), a.energies(), a.permutation(), a.observables(), a.best()),
+                    (b.spins(), b.energies(), b.permutation(), b.observables(), b.best())):
+        assert np.array_equal(x, y)
+    monkeypatch.delenv("TAPT_K3_IPB")
+
+
 def test_k3_circuit_with_clamps_and_fields_matches_oracle(monkeypatch):
     monkeypatch.setenv("TAPT_K3", "1")
     g = _random_circuit(13)
