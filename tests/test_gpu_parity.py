@@ -620,6 +620,68 @@ def test_pt_stationarity_small_system():
     assert tv < 0.02, tv
 
 
+def _circuit_stationarity(model, clamp, betas, slot, k3):
+    """TV distance between the empirical distribution of slot `slot` (4096 independent ensembles,
+    40 samples each, 25 sweeps apart after 400) and Boltzmann(betas[slot]) over the free spins."""
+    import itertools
+    import os as _os
+    _os.environ["TAPT_K3"] = "1" if k3 else "0"
+    try:
+        e = T.Ensemble(model, betas, n_instances=4096, seed=8)
+        assert e.kernel == ("bitcsr" if k3 else "csr")
+        e.init_random()
+        e.run(400, swap_every=1)
+        free = np.where(clamp == 0)[0]
+        w = 1 << np.arange(len(free))
+        counts = np.zeros(1 << len(free))
+        for _ in range(40):
+            e.run(25, swap_every=1)
+            S = e.spins()[:, slot, :][:, free]
+            np.add.at(counts, ((S > 0) * w).sum(axis=1), 1)
+    finally:
+        _os.environ.pop("TAPT_K3", None)
+    p = np.zeros_like(counts)
+    base = clamp.astype(np.int8).copy()
+    for bits in itertools.product([-1, 1], repeat=len(free)):
+        st = base.copy()
+        st[free] = bits
+        p[((np.array(bits) > 0) * w).sum()] = -betas[slot] * model.energy(st)
+    p = np.exp(p - p.max())
+    p /= p.sum()
+    return 0.5 * np.abs(counts / counts.sum() - p).sum()
+
+
+@pytest.mark.parametrize("k3", [True, False])
+def test_pt_stationarity_clamped_circuits(k3):
+    """Colour-class PT on circuits with fields and clamps is stationary: the 2x2-bit multiplier with
+    its product clamped to 6 (8 free spins) and a 10-spin graph whose hub has S' = sum|J| + |h| = 20
+    (K3's heavy path), both within TV 0.02 of Boltzmann at two ladder slots.  Measured TV is
+    0.003-0.006; sampling the neighbouring slot's beta would give 0.08-0.15, a 5 % beta error ~0.03."""
+    M = T.Multiplier(2)
+    cl = M.clamps(6)
+    mm = T.Model.graph(M.n_spins, M.ci, M.cj, M.J, M.h, cl)
+    betas = np.linspace(0.1, 1.0, 8)
+    for slot in (4, 7):
+        tv = _circuit_stationarity(mm, cl, betas, slot, k3)
+        assert tv < 0.02, ("multiplier", slot, tv)
+    rs = np.random.default_rng(4)
+    n = 10
+    ci = [0] * 9 + list(rs.integers(1, n, 8))
+    cj = list(range(1, 10)) + list(rs.integers(1, n, 8))
+    keep = [i != j for i, j in zip(ci, cj)]
+    ci = np.array(ci)[keep]
+    cj = np.array(cj)[keep]
+    J = np.concatenate([np.where(np.arange(9) % 2 == 0, 2.0, -2.0), rs.choice([-1.0, 1.0], len(ci) - 9)])
+    h = rs.integers(-2, 3, n).astype(float)
+    h[0] = 2.0
+    cl0 = np.zeros(n, np.int8)
+    mh = T.Model.graph(n, ci, cj, J, h, cl0)
+    betas = np.linspace(0.1, 0.8, 8)
+    for slot in (3, 7):
+        tv = _circuit_stationarity(mh, cl0, betas, slot, k3)
+        assert tv < 0.02, ("hub graph", slot, tv)
+
+
 # ------------------------------------------------------- annealing (SPEC.md:564-570) --
 
 def test_estimate_ground_energy_ferromagnet_and_small_glass():
