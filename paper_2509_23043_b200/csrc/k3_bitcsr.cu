@@ -238,8 +238,10 @@ __device__ __forceinline__ void k3_site(const PTArgs& a, const PTShared& S, cons
     }
 }
 
-template <bool BAL>
-__global__ void __launch_bounds__(kT3 * kIPB3, 1) k3_bitcsr_pt(const PTArgs a, const Csr3 g) {
+// IPB: instance teams per CTA.  One instantiation per IPB so that each launch shape gets the whole
+// register file for its threads (3 teams: 167 registers, +2 % on config 4 over a 512-thread bound).
+template <bool BAL, int IPB>
+__global__ void __launch_bounds__(kT3 * IPB, 1) k3_bitcsr_pt(const PTArgs a, const Csr3 g) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ PTShared SS[kIPB3];
     __shared__ int corr_sh[kIPB3];
@@ -414,36 +416,52 @@ size_t k3_smem_bytes(int R, int nidx, int nadj, int nfree, int n, int ncls, int 
 
 int k3_row_stride() { return kRow3; }
 
-static cudaError_t k3_shape(const PTArgs& a, const Csr3& g, int ipb, size_t& smem) {
-    smem = k3_smem_bytes(a.R, a.nidx, g.nadj, (int)a.n_free, a.n, g.n_classes, ipb);
-    cudaError_t e = cudaFuncSetAttribute(k3_bitcsr_pt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int IPB>
+static cudaError_t k3_shape_t(const PTArgs& a, const Csr3& g, size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(k3_bitcsr_pt<false, IPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k3_bitcsr_pt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(k3_bitcsr_pt<true, IPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return e;
 }
 
-// Co-resident instance teams of the K3 launch shape (balanced schedule): CTAs per SM x SMs x ipb.
+template <int IPB>
+static cudaError_t k3_run_t(const PTArgs& a, const Csr3& g, cudaStream_t st, int* resident) {
+    const size_t smem = k3_smem_bytes(a.R, a.nidx, g.nadj, (int)a.n_free, a.n, g.n_classes, IPB);
+    cudaError_t e = k3_shape_t<IPB>(a, g, smem);
+    if (e != cudaSuccess) return e;
+    if (resident) {  // co-resident instance teams: CTAs per SM x SMs x IPB
+        int per_sm = 0, dev = 0, nsm = 0;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_bitcsr_pt<true, IPB>, kT3 * IPB, smem);
+        if (e == cudaSuccess) e = cudaGetDevice(&dev);
+        if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+        *resident = per_sm * nsm * IPB;
+        return e;
+    }
+    const unsigned grid = a.sched ? (unsigned)((a.sched_clusters + IPB - 1) / IPB) : (unsigned)((a.I + IPB - 1) / IPB);
+    if (a.sched)
+        k3_bitcsr_pt<true, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
+    else
+        k3_bitcsr_pt<false, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
+    return cudaGetLastError();
+}
+
+static cudaError_t k3_run(const PTArgs& a, const Csr3& g, int ipb, cudaStream_t st, int* resident) {
+    switch (ipb) {
+        case 1: return k3_run_t<1>(a, g, st, resident);
+        case 2: return k3_run_t<2>(a, g, st, resident);
+        case 3: return k3_run_t<3>(a, g, st, resident);
+        default: return k3_run_t<4>(a, g, st, resident);
+    }
+}
+
+// Co-resident instance teams of the K3 launch shape (balanced schedule).
 int k3_resident_units(const PTArgs& a, const Csr3& g, int ipb) {
-    size_t smem = 0;
-    if (k3_shape(a, g, ipb, smem) != cudaSuccess) return 0;
-    int per_sm = 0, dev = 0, nsm = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_bitcsr_pt<true>, kT3 * ipb, smem) != cudaSuccess)
-        return 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return 0;
-    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) return 0;
-    return per_sm * nsm * ipb;
+    int r = 0;
+    return k3_run(a, g, ipb, nullptr, &r) == cudaSuccess ? r : 0;
 }
 
 cudaError_t launch_k3(const PTArgs& a, const Csr3& g, int ipb, cudaStream_t st) {
-    size_t smem = 0;
-    cudaError_t e = k3_shape(a, g, ipb, smem);
-    if (e != cudaSuccess) return e;
-    const unsigned grid = a.sched ? (unsigned)((a.sched_clusters + ipb - 1) / ipb) : (unsigned)((a.I + ipb - 1) / ipb);
-    if (a.sched)
-        k3_bitcsr_pt<true><<<grid, kT3 * ipb, smem, st>>>(a, g);
-    else
-        k3_bitcsr_pt<false><<<grid, kT3 * ipb, smem, st>>>(a, g);
-    return cudaGetLastError();
+    return k3_run(a, g, ipb, st, nullptr);
 }
 
 }  // namespace tapt_dev
