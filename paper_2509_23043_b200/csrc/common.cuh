@@ -224,11 +224,14 @@ __device__ __forceinline__ uint32_t warp_transpose32(uint32_t w) {
 
 // Per-replica totals of a K-plane sliced counter summed over the warp: lane b
 // returns sum over lanes of the value held for replica (bit) b.
+// Planes that are zero in every lane (high planes of small per-thread counts) are skipped after
+// one warp vote.
 template <int K>
 __device__ __forceinline__ uint32_t warp_sliced_total(const uint32_t (&C)[K]) {
     uint32_t tot = 0;
 #pragma unroll
-    for (int k = 0; k < K; ++k) tot += static_cast<uint32_t>(__popc(warp_transpose32(C[k]))) << k;
+    for (int k = 0; k < K; ++k)
+        if (__any_sync(0xFFFFFFFFu, C[k] != 0u)) tot += static_cast<uint32_t>(__popc(warp_transpose32(C[k]))) << k;
     return tot;
 }
 
