@@ -1,5 +1,5 @@
-"""Share of the per-sweep epilogue (swap pass, measurement) in the fused run: config-3 and
-config-4 ensembles timed with swap_every = 1 / 0 and measure_every = 0 / 1."""
+"""Share of the per-sweep epilogue (swap pass, measurement) in the fused run: config-1, -3, -4 and
+-5 ensembles timed with swap_every = 1 / 0 and measure_every = 0 / 1."""
 import os
 import sys
 
@@ -11,7 +11,7 @@ import paper_2509_23043_b200 as T  # noqa: E402
 from paper_2509_23043_b200 import workloads as WL  # noqa: E402
 
 stream = torch.cuda.Stream()
-for c in (3, 4, 5):
+for c in (1, 3, 4, 5):
     if c == 5:
         m = T.Model.lattice((32,))
         import numpy as np
