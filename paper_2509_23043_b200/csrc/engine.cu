@@ -48,6 +48,10 @@ int k3_row_stride();
 int k3_resident_units(const PTArgs& a, const Csr3& g, int ipb);
 cudaError_t launch_k3(const PTArgs& a, const Csr3& g, int ipb, cudaStream_t st);
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st);
+size_t k4_smem_bytes(int n, int R, int nidx, int nnz, int nfree, int nlev, int ipb);
+int k4_max_ipb();
+int k4_resident_units(const PTArgs& a, const CsrArgs& g, int ipb);
+cudaError_t launch_k4(const PTArgs& a, const CsrArgs& g, int ipb, cudaStream_t st);
 size_t k1_smem_bytes(int n, bool dis, int R);
 size_t k2_smem_bytes(int n, int R, int nidx);
 size_t k2_smem_bytes_graph(int n, int R, int nidx, int nnz, int nfree);
@@ -663,6 +667,23 @@ struct tapt_ensemble_s {
         return k3_ipb > 0;
     }
 
+    // K4 (k4_levels.cu): the reference's index order on the dependency levels, one warp per site
+    // word; shared couplings, <= 32 slots.  TAPT_K4=0 selects K2.
+    int k4_ipb = -1;
+    bool k4_eligible() {
+        if (k4_ipb >= 0) return k4_ipb > 0;
+        k4_ipb = 0;
+        if (use_k1 || order != TAPT_ORDER_REFERENCE || G != 1 || csrJ.p || m->n >= (1u << 24)) return false;
+        if (const char* e = std::getenv("TAPT_K4"); e && std::atoi(e) == 0) return false;
+        const int nlev = (int)m->lev_ptr.size() - 1;
+        for (int ipb = std::min(k4_max_ipb(), (int)std::max(1u, I)); ipb >= 1; --ipb)
+            if (k4_smem_bytes(n(), R, nidx, (int)m->col.size(), (int)m->free_sites.size(), nlev, ipb) <= 200 * 1024) {
+                k4_ipb = ipb;
+                break;
+            }
+        return k4_ipb > 0;
+    }
+
     // balanced persistent K1 schedule (McNaughton), cached per launch length
     int k1_units = -1;  // co-resident clusters (or CTAs) of the sweep kernel's launch shape
     int sched_S = -1, sched_M = 0, sched_nflags = 0;
@@ -798,6 +819,8 @@ struct tapt_ensemble_s {
             e = launch_k1(a, m->ld, k1_nt > 0 ? k1_nt : k1_threads, cluster, stream);
         } else if (!a.energy_only && a.G == 1 && k3_eligible()) {
             e = launch_k3(a, k3_args(), k3_ipb, stream);
+        } else if (!a.energy_only && a.G == 1 && k4_eligible()) {
+            e = launch_k4(a, csr_args(true), k4_ipb, stream);
         } else {
             e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster, stream);
         }
@@ -859,6 +882,7 @@ struct tapt_ensemble_s {
         if (k1_units < 0)
             k1_units = use_k1           ? k1_resident_units(a, m->ld, k1_threads, cluster)
                        : k3_eligible() ? k3_resident_units(a, k3_args(), k3_ipb)
+                       : k4_eligible() ? k4_resident_units(a, csr_args(true), k4_ipb)
                                        : k2_resident_units(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster);
         const int M = k1_units;
         if (M <= 0 || (int)I <= M) return false;
@@ -1422,7 +1446,7 @@ const char* tapt_ensemble_kernel(tapt_ensemble_t e) {
     if (!e) return "csr";
     if (e->use_k1) return "lattice";
     try {
-        return e->k3_eligible() ? "bitcsr" : "csr";
+        return e->k3_eligible() ? "bitcsr" : e->k4_eligible() ? "levels" : "csr";
     } catch (...) {
         return "csr";
     }
@@ -1448,6 +1472,7 @@ tapt_status tapt_ensemble_set_bond_signs(tapt_ensemble_t e, const int8_t* signs,
             const int nnz = (int)m->col.size();
             e->csrJ.alloc((size_t)e->I * nnz);
             e->k3_ipb = -1;  // per-instance couplings: K2 only
+            e->k4_ipb = -1;
             e->k1_units = -1;
             ++g_launches;
             k_csr_from_signs<<<dim3((nnz + 255) / 256, e->I), 256, 0, e->stream>>>(

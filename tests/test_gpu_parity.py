@@ -127,14 +127,17 @@ def test_sweep_and_standalone_swap_compose():
 
 # ------------------------------------------------------------ K2 CSR --------
 
-def test_reference_order_pt_matches_reference_golden():
-    """Index-order PT on the device == the reference's own gibbs_sweep driven PT (golden)."""
+@pytest.mark.parametrize("kernel", ["levels", "csr"])
+def test_reference_order_pt_matches_reference_golden(kernel, monkeypatch):
+    """Index-order PT on the device == the reference's own gibbs_sweep driven PT (golden), with K4
+    (one warp per site word on the dependency levels) and with K2 (TAPT_K4=0)."""
+    monkeypatch.setenv("TAPT_K4", "1" if kernel == "levels" else "0")
     f = np.load(os.path.join(GOLD, "pt_cfg1_200.npz"))
     I, R, n = (int(x) for x in f["shape"])
     m = T.Model.lattice((32, 32))
     e = T.Ensemble(m, f["betas"], n_instances=I, seed=int(f["seed"]), instance_offset=int(f["gid0"]),
                    order="reference")
-    assert e.kernel == "csr"
+    assert e.kernel == kernel
     e.init_random()
     e.run(int(f["n_sweeps"]), swap_every=int(f["swap_every"]))
     spins = unpack(f["spins"], I * R * n).reshape(I, R, n)
@@ -188,6 +191,36 @@ def test_k2_colour_order_circuit_like_graph():
     e.run(150, swap_every=1)
     pts = H.run_oracle([g] * 3, betas, 5, 0, H.colour_order_for(colours), 150)
     compare(e, pts)
+
+
+def test_k4_reference_order_circuit_with_clamps_and_fields_equals_k2(monkeypatch):
+    """K4 (levels) == K2 in the reference's index order on a clamped circuit with fields (32 slots,
+    swaps, measurements, a TAPT round), and both == the oracle."""
+    g = _random_circuit(14, n=50)
+    m = T.Model.graph(g.n, g.ci, g.cj, g.J, g.h, g.clamp)
+    betas = H.geometric(0.2, 3.0, 32)
+
+    def run(k4):
+        monkeypatch.setenv("TAPT_K4", "1" if k4 else "0")
+        e = T.Ensemble(m, betas, n_instances=5, seed=13, order="reference")
+        assert e.kernel == ("levels" if k4 else "csr")
+        e.init_random()
+        e.set_histogram(-400, 8, 100)
+        e.run(60, swap_every=1, measure_every=3)
+        e.generate_proposals(np.arange(10), None, refine=2)
+        e.run(20, swap_every=1, measure_every=3)
+        return e
+    a, b = run(True), run(False)
+    for x, y in zip((a.spins(), a.energies(), a.permutation(), a.observables(), a.histogram(), a.best()),
+                    (b.spins(), b.energies(), b.permutation(), b.observables(), b.histogram(), b.best())):
+        assert np.array_equal(x, y)
+    for x, y in zip(a.acceptance(), b.acceptance()):
+        assert np.array_equal(x, y)
+    monkeypatch.setenv("TAPT_K4", "1")
+    e = T.Ensemble(m, betas, n_instances=2, seed=13, order="reference")
+    e.init_random()
+    e.run(40, swap_every=1)
+    compare(e, H.run_oracle([g] * 2, betas, 13, 0, H.index_order, 40))
 
 
 def test_k2_reference_order_with_clamps_and_fields():
