@@ -277,6 +277,11 @@ tapt_status tapt_former_get(tapt_former_t f, tapt_former_config* c, float* param
  * parameters.  Bad magic / truncation -> TAPT_ERR_FORMAT. */
 tapt_status tapt_former_save(tapt_former_t f, const char* path);
 tapt_status tapt_former_load(const char* path, tapt_former_t* out);
+/* K/V cache precision: 0 (default) fp32; 1 bf16 storage with fp32 attention math (half the bytes
+ * of the sampling-bound K/V stream; logits then agree with the fp32 path to ~1e-2, and sampling
+ * and log_prob stay mutually consistent).  No reference counterpart (the generator is a
+ * placeholder there). */
+tapt_status tapt_former_set_kv_bf16(tapt_former_t f, int bf16);
 /* forward_logits / log_prob: tokens [B][T] (0/1, host), betas [B]; log_q [B] sums the
  * Bernoulli log-probabilities of positions >= n_prefix; logits [B][T] (nullable). */
 tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_t B, uint32_t T, const double* betas,

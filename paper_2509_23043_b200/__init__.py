@@ -159,6 +159,7 @@ _SIGS = {
     "tapt_former_save": (C.c_int, [_vp, C.c_char_p]),
     "tapt_former_load": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
     "tapt_former_log_prob": (C.c_int, [_vp, _u8p, C.c_uint32, C.c_uint32, _f64p, C.c_uint32, _f64p, _f32p]),
+    "tapt_former_set_kv_bf16": (C.c_int, [_vp, C.c_int]),
     "tapt_former_sample": (C.c_int, [_vp, C.c_uint32, C.c_uint32, _f64p, _u8p, C.c_uint32, _u64p, _u8p, _f64p]),
 }
 
@@ -489,12 +490,19 @@ class Former:
 
     DEFAULT = dict(d_model=64, heads=2, ffn=128, layers=2, max_len=1024, beta_features=16)
 
-    def __init__(self, params=None, seed=0, scale=1.0, _handle=None, **cfg):
+    def __init__(self, params=None, seed=0, scale=1.0, _handle=None, kv="fp32", **cfg):
+        """kv: K/V cache precision, "fp32" (default) or "bf16" (half the bytes of the sampling-bound
+        K/V stream; fp32 attention math)."""
+        if kv not in ("fp32", "bf16"):
+            raise ConfigError("kv must be 'fp32' or 'bf16'")
+        self.kv = kv
         if _handle is not None:
             self._h = _handle
             c = FormerConfig()
             _check(lib().tapt_former_get(self._h, C.byref(c), None))
             self.config = {k: getattr(c, k) for k, _ in FormerConfig._fields_}
+            if kv == "bf16":
+                _check(lib().tapt_former_set_kv_bf16(self._h, 1))
             return
         conf = dict(self.DEFAULT)
         conf.update(cfg)
@@ -508,6 +516,8 @@ class Former:
         h = _vp()
         _check(lib().tapt_former_create(C.byref(c), _p(p, _f32p), C.byref(h)))
         self._h = h
+        if kv == "bf16":
+            _check(lib().tapt_former_set_kv_bf16(self._h, 1))
 
     @staticmethod
     def param_count(**cfg):

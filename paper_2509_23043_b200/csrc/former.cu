@@ -14,6 +14,7 @@
 // resident, 267 KB) with one column per lane and 8 rows per thread, so every weight load is
 // shared by 8 rows.  Sampling is bound by the K/V cache reads: sum over t of t x 2 layers x
 // (K + V) x 64 x 4 B per sequence.
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -50,7 +51,7 @@ struct FArgs {
     int L, fb;
     const float* pos;  // [max_len][D] sinusoidal positions
     int T, n_prefix, B;
-    float* cache;  // [slots][L][T][2][D]: K then V of every cached position
+    void* cache;   // [slots][L][T][2][D]: K then V of every cached position (float or bf16, KVT below)
     const uint8_t* tokens;     // forward: [B][T]; sample: prefix [B][n_prefix]
     const double* betas;       // [B]
     float* logits;             // forward: [B][T] (nullable)
@@ -155,8 +156,42 @@ __device__ void rows_gemm(const float* In, const float* W, const float* bias, fl
         }
 }
 
+// K/V cache element: float (default) or bf16 (opt-in: half the bytes of the sampling-bound stream;
+// the attention math stays fp32).  ld4 reads 4 consecutive elements as a float4.
+template <class KT>
+struct KVT;
+template <>
+struct KVT<float> {
+    static __device__ __forceinline__ float4 ld4(const void* base, size_t i) {
+        return *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(base) + i);
+    }
+    static __device__ __forceinline__ void st(void* base, size_t i, float v) { reinterpret_cast<float*>(base)[i] = v; }
+    static __device__ __forceinline__ void ld8(const void* base, size_t i, float4& a, float4& b) {
+        a = ld4(base, i);
+        b = ld4(base, i + 4);
+    }
+};
+template <>
+struct KVT<__nv_bfloat16> {
+    static __device__ __forceinline__ float4 ld4(const void* base, size_t i) {
+        const uint2 u = *reinterpret_cast<const uint2*>(reinterpret_cast<const __nv_bfloat16*>(base) + i);
+        return make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                           __uint_as_float(u.y & 0xFFFF0000u));
+    }
+    static __device__ __forceinline__ void st(void* base, size_t i, float v) {
+        reinterpret_cast<__nv_bfloat16*>(base)[i] = __float2bfloat16_rn(v);
+    }
+    static __device__ __forceinline__ void ld8(const void* base, size_t i, float4& a, float4& b) {  // one 16-B load
+        const uint4 u = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(base) + i);
+        a = make_float4(__uint_as_float(u.x << 16), __uint_as_float(u.x & 0xFFFF0000u), __uint_as_float(u.y << 16),
+                        __uint_as_float(u.y & 0xFFFF0000u));
+        b = make_float4(__uint_as_float(u.z << 16), __uint_as_float(u.z & 0xFFFF0000u), __uint_as_float(u.w << 16),
+                        __uint_as_float(u.w & 0xFFFF0000u));
+    }
+};
+
 // QKV projection: Q to shared memory, K and V appended to each valid row's cache.
-template <int RB>
+template <int RB, class KT>
 __device__ void rows_qkv(Smem<RB>& s, const FArgs& a, int l) {
     constexpr int NR = RB / 4;
     const LayerOff& o = a.lay[l];
@@ -192,9 +227,9 @@ __device__ void rows_qkv(Smem<RB>& s, const FArgs& a, int l) {
         const int r = rg + 4 * i;
         s.Q[r][c0] = acc[i][0] + __ldg(bias + c0);
         if (s.valid[r]) {
-            float* kv = a.cache + ((((size_t)s.slot[r] * a.L + l) * a.T + s.t[r]) * 2) * D;
-            kv[c0] = acc[i][1] + __ldg(bias + D + c0);
-            kv[D + c0] = acc[i][2] + __ldg(bias + 2 * D + c0);
+            const size_t kv = ((((size_t)s.slot[r] * a.L + l) * a.T + s.t[r]) * 2) * D;
+            KVT<KT>::st(a.cache, kv + c0, acc[i][1] + __ldg(bias + D + c0));
+            KVT<KT>::st(a.cache, kv + D + c0, acc[i][2] + __ldg(bias + 2 * D + c0));
         }
     }
 }
@@ -204,10 +239,14 @@ __device__ void rows_qkv(Smem<RB>& s, const FArgs& a, int l) {
 // its loads up front -- its key's K row (8 x float4) and a float4 slice of 8 V rows (keys
 // c + 4i + lane/8, dims 4*(lane%8)..+3) -- so a chunk costs one memory round trip; the lanes
 // sharing a dimension slice are reduced once per task.
-template <int RB>
+template <int RB, class KT>
 __device__ void rows_attention(Smem<RB>& s, const FArgs& a, int l, int H) {
+    // V slice per lane: fp32 4 dims of 8 keys (8 lanes per key); bf16 8 dims of 4 keys (4 lanes per
+    // key) so that every load is 16 bytes
+    constexpr bool W8 = sizeof(KT) == 2;
+    constexpr int VD = W8 ? 8 : 4, LPK = DH / VD, KPP = 32 / LPK, NP = 32 / KPP;  // dims, lanes/key, keys/pass, passes
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int kq = lane >> 3, dq = 4 * (lane & 7);
+    const int kq = lane / LPK, dq = VD * (lane % LPK);
     const float scale = rsqrtf((float)DH);
     for (int task = w; task < RB * H; task += NT / 32) {
         const int r = task / H, h = task - r * H;
@@ -216,21 +255,32 @@ __device__ void rows_attention(Smem<RB>& s, const FArgs& a, int l, int H) {
             continue;
         }
         const int tr = s.t[r];
-        const float* base = a.cache + (((size_t)s.slot[r] * a.L + l) * a.T) * 2 * D + h * DH;
+        const size_t base = (((size_t)s.slot[r] * a.L + l) * a.T) * 2 * D + h * DH;
         const float4* q4 = reinterpret_cast<const float4*>(&s.Q[r][h * DH]);
         float m = -INFINITY, lsum = 0.f;
-        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 o = make_float4(0.f, 0.f, 0.f, 0.f), o2 = o;
         for (int c = 0; c <= tr; c += 32) {
             const int j = c + lane;
-            float4 kk[DH / 4], vv[8];
+            float4 kk[DH / 4], vv[NP], vv2[NP];
 #pragma unroll
-            for (int q = 0; q < DH / 4; ++q)
-                kk[q] = j <= tr ? reinterpret_cast<const float4*>(base + (size_t)j * 2 * D)[q] : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < DH / 4; q += 2) {
+                if (j <= tr) {
+                    KVT<KT>::ld8(a.cache, base + (size_t)j * 2 * D + 4 * q, kk[q], kk[q + 1]);
+                } else {
+                    kk[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    kk[q + 1] = kk[q];
+                }
+            }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int key = c + 4 * i + kq;
-                vv[i] = key <= tr ? *reinterpret_cast<const float4*>(base + (size_t)key * 2 * D + D + dq)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int i = 0; i < NP; ++i) {
+                const int key = c + KPP * i + kq;
+                vv[i] = vv2[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+                if (key <= tr) {
+                    if constexpr (W8)
+                        KVT<KT>::ld8(a.cache, base + (size_t)key * 2 * D + D + dq, vv[i], vv2[i]);
+                    else
+                        vv[i] = KVT<KT>::ld4(a.cache, base + (size_t)key * 2 * D + D + dq);
+                }
             }
             float acc = 0.f;
 #pragma unroll
@@ -250,26 +300,47 @@ __device__ void rows_attention(Smem<RB>& s, const FArgs& a, int l, int H) {
             o.y *= corr;
             o.z *= corr;
             o.w *= corr;
+            if constexpr (W8) {
+                o2.x *= corr;
+                o2.y *= corr;
+                o2.z *= corr;
+                o2.w *= corr;
+            }
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const float pk = __shfl_sync(0xFFFFFFFFu, p, 4 * i + kq);
+            for (int i = 0; i < NP; ++i) {
+                const float pk = __shfl_sync(0xFFFFFFFFu, p, KPP * i + kq);
                 o.x = fmaf(pk, vv[i].x, o.x);
                 o.y = fmaf(pk, vv[i].y, o.y);
                 o.z = fmaf(pk, vv[i].z, o.z);
                 o.w = fmaf(pk, vv[i].w, o.w);
+                if constexpr (W8) {
+                    o2.x = fmaf(pk, vv2[i].x, o2.x);
+                    o2.y = fmaf(pk, vv2[i].y, o2.y);
+                    o2.z = fmaf(pk, vv2[i].z, o2.z);
+                    o2.w = fmaf(pk, vv2[i].w, o2.w);
+                }
             }
             m = mn;
         }
 #pragma unroll
-        for (int x = 8; x <= 16; x <<= 1) {
+        for (int x = LPK; x <= 16; x <<= 1) {  // lanes sharing a dimension slice
             o.x += __shfl_xor_sync(0xFFFFFFFFu, o.x, x);
             o.y += __shfl_xor_sync(0xFFFFFFFFu, o.y, x);
             o.z += __shfl_xor_sync(0xFFFFFFFFu, o.z, x);
             o.w += __shfl_xor_sync(0xFFFFFFFFu, o.w, x);
+            if constexpr (W8) {
+                o2.x += __shfl_xor_sync(0xFFFFFFFFu, o2.x, x);
+                o2.y += __shfl_xor_sync(0xFFFFFFFFu, o2.y, x);
+                o2.z += __shfl_xor_sync(0xFFFFFFFFu, o2.z, x);
+                o2.w += __shfl_xor_sync(0xFFFFFFFFu, o2.w, x);
+            }
         }
-        if (lane < 8) {
+        if (lane < LPK) {
             const float inv = 1.f / lsum;
             *reinterpret_cast<float4*>(&s.O[r][h * DH + dq]) = make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv);
+            if constexpr (W8)
+                *reinterpret_cast<float4*>(&s.O[r][h * DH + dq + 4]) =
+                    make_float4(o2.x * inv, o2.y * inv, o2.z * inv, o2.w * inv);
         }
     }
 }
@@ -278,12 +349,12 @@ __device__ void rows_attention(Smem<RB>& s, const FArgs& a, int l, int H) {
 // sequence: every 32-key chunk of the cache is staged in shared memory once per row block and
 // read by all (row, head) tasks (flash-attention style).  Warp w owns tasks w, w+8, ... and
 // keeps their online-softmax state in registers across chunks.
-template <int RB>
+template <int RB, class KT>
 __device__ void rows_attention_fwd(Smem<RB>& s, KVChunk& kv, const FArgs& a, int l) {
     constexpr int H = D / DH, NTASK = RB * H / (NT / 32);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const float scale = rsqrtf((float)DH);
-    const float* base = a.cache + (((size_t)s.slot[0] * a.L + l) * a.T) * 2 * D;
+    const size_t base = (((size_t)s.slot[0] * a.L + l) * a.T) * 2 * D;
     int tmax = -1;
     for (int r = 0; r < RB; ++r)
         if (s.valid[r]) tmax = max(tmax, s.t[r]);
@@ -299,7 +370,7 @@ __device__ void rows_attention_fwd(Smem<RB>& s, KVChunk& kv, const FArgs& a, int
         for (int e = threadIdx.x; e < 32 * 2 * D / 4; e += NT) {  // 32 keys x (K 64 | V 64), float4
             const int key = e / (2 * D / 4), q4 = e - key * (2 * D / 4);
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (c + key <= tmax) v = reinterpret_cast<const float4*>(base + (size_t)(c + key) * 2 * D)[q4];
+            if (c + key <= tmax) v = KVT<KT>::ld4(a.cache, base + (size_t)(c + key) * 2 * D + 4 * q4);
             float* dst = q4 < D / 4 ? &kv.K[key][4 * q4] : &kv.V[key][4 * q4 - D];
             dst[0] = v.x;
             dst[1] = v.y;
@@ -336,22 +407,22 @@ __device__ void rows_attention_fwd(Smem<RB>& s, KVChunk& kv, const FArgs& a, int
 }
 
 // All decoder layers + final LayerNorm + head for the current row block; logits in s.z.
-template <int RB>
+template <int RB, class KT>
 __device__ void rows_forward(Smem<RB>& s, const FArgs& a, KVChunk* kv = nullptr) {
     const int H = D / DH;
     for (int l = 0; l < a.L; ++l) {
         const LayerOff& o = a.lay[l];
         rows_ln(s.X, s.A, a.W + o.ln1_g, a.W + o.ln1_b);
         __syncthreads();
-        rows_qkv(s, a, l);
+        rows_qkv<RB, KT>(s, a, l);
         __syncthreads();
         if constexpr (RB == 32) {
             if (kv)
-                rows_attention_fwd<RB>(s, *kv, a, l);
+                rows_attention_fwd<RB, KT>(s, *kv, a, l);
             else
-                rows_attention(s, a, l, H);
+                rows_attention<RB, KT>(s, a, l, H);
         } else {
-            rows_attention(s, a, l, H);
+            rows_attention<RB, KT>(s, a, l, H);
         }
         __syncthreads();
         rows_gemm<RB, D, D, 1>(&s.O[0][0], a.W + o.w_o, a.W + o.b_o, &s.X[0][0]);
@@ -405,6 +476,7 @@ __device__ void rows_input(Smem<RB>& s, const FArgs& a) {
     }
 }
 
+template <class KT>
 __global__ void __launch_bounds__(NT) k_former_forward(const FArgs a) {
     constexpr int RB = 32;
     extern __shared__ __align__(16) unsigned char fsm[];
@@ -427,7 +499,7 @@ __global__ void __launch_bounds__(NT) k_former_forward(const FArgs a) {
             __syncthreads();
             rows_input(s, a);
             __syncthreads();
-            rows_forward(s, a, &kv);
+            rows_forward<RB, KT>(s, a, &kv);
             if (tid < RB && s.valid[tid]) {
                 const int t = s.t[tid];
                 const float z = s.z[tid];
@@ -445,7 +517,7 @@ __global__ void __launch_bounds__(NT) k_former_forward(const FArgs a) {
     }
 }
 
-template <int RB>
+template <int RB, class KT>
 __global__ void __launch_bounds__(NT) k_former_sample(const FArgs a) {
     extern __shared__ __align__(16) unsigned char fsm[];
     Smem<RB>& s = *reinterpret_cast<Smem<RB>*>(fsm);
@@ -469,7 +541,7 @@ __global__ void __launch_bounds__(NT) k_former_sample(const FArgs a) {
             __syncthreads();
             rows_input(s, a);
             __syncthreads();
-            rows_forward(s, a);
+            rows_forward<RB, KT>(s, a);
             if (tid < RB && s.valid[tid]) {
                 const int b = blk * RB + tid;
                 const double z = s.z[tid];
@@ -600,8 +672,9 @@ struct tapt_former_s {
     std::vector<float> params;
     float* dW = nullptr;
     float* dpos = nullptr;
-    float* cache = nullptr;
-    size_t cache_n = 0;
+    void* cache = nullptr;
+    size_t cache_n = 0;  // bytes
+    int kv16 = 0;        // K/V cache in bf16 (tapt_former_set_kv_bf16)
     void* tmp = nullptr;
     size_t tmp_n = 0;
     ~tapt_former_s() {
@@ -625,12 +698,13 @@ struct tapt_former_s {
         FCUDA(cudaMalloc(&dpos, P.size() * sizeof(float)));
         FCUDA(cudaMemcpy(dpos, P.data(), P.size() * sizeof(float), cudaMemcpyHostToDevice));
     }
-    float* need_cache(size_t n) {
-        if (n > cache_n) {
+    void* need_cache(size_t n) {  // n elements of the configured K/V type
+        const size_t bytes = n * (kv16 ? 2 : 4);
+        if (bytes > cache_n) {
             if (cache) cudaFree(cache);
             cache = nullptr;
-            FCUDA(cudaMalloc(&cache, n * sizeof(float)));
-            cache_n = n;
+            FCUDA(cudaMalloc(&cache, bytes));
+            cache_n = bytes;
         }
         return cache;
     }
@@ -794,6 +868,13 @@ tapt_status tapt_former_load(const char* path, tapt_former_t* out) {
     });
 }
 
+tapt_status tapt_former_set_kv_bf16(tapt_former_t f, int bf16) {
+    return fguard([&] {
+        check_former(f);
+        f->kv16 = bf16 ? 1 : 0;
+    });
+}
+
 tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_t B, uint32_t T, const double* betas,
                                  uint32_t n_prefix, double* log_q, float* logits) {
     return fguard([&] {
@@ -818,7 +899,10 @@ tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_
         a.betas = reinterpret_cast<const double*>(tmp + off_b);
         a.log_q = reinterpret_cast<double*>(tmp + off_q);
         a.logits = logits ? reinterpret_cast<float*>(tmp + off_z) : nullptr;
-        launch_rows<32>(k_former_forward, grid, a, sizeof(KVChunk));
+        if (f->kv16)
+            launch_rows<32>(k_former_forward<__nv_bfloat16>, grid, a, sizeof(KVChunk));
+        else
+            launch_rows<32>(k_former_forward<float>, grid, a, sizeof(KVChunk));
         FCUDA(cudaMemcpy(log_q, a.log_q, (size_t)B * 8, cudaMemcpyDeviceToHost));
         if (logits) FCUDA(cudaMemcpy(logits, a.logits, tb * 4, cudaMemcpyDeviceToHost));
     });
@@ -856,12 +940,21 @@ tapt_status tapt_former_sample(tapt_former_t f, uint32_t B, uint32_t T, const do
         a.streams = reinterpret_cast<const uint64_t*>(tmp + off_s);
         a.log_q = reinterpret_cast<double*>(tmp + off_q);
         a.tok_out = tmp + off_t;
-        if (RBs == 32)
-            launch_rows<32>(k_former_sample<32>, grid, a);
-        else if (RBs == 8)
-            launch_rows<8>(k_former_sample<8>, grid, a);
-        else
-            launch_rows<4>(k_former_sample<4>, grid, a);
+        if (f->kv16) {
+            if (RBs == 32)
+                launch_rows<32>(k_former_sample<32, __nv_bfloat16>, grid, a);
+            else if (RBs == 8)
+                launch_rows<8>(k_former_sample<8, __nv_bfloat16>, grid, a);
+            else
+                launch_rows<4>(k_former_sample<4, __nv_bfloat16>, grid, a);
+        } else {
+            if (RBs == 32)
+                launch_rows<32>(k_former_sample<32, float>, grid, a);
+            else if (RBs == 8)
+                launch_rows<8>(k_former_sample<8, float>, grid, a);
+            else
+                launch_rows<4>(k_former_sample<4, float>, grid, a);
+        }
         FCUDA(cudaMemcpy(tokens, a.tok_out, (size_t)B * T, cudaMemcpyDeviceToHost));
         FCUDA(cudaMemcpy(log_q, a.log_q, (size_t)B * 8, cudaMemcpyDeviceToHost));
     });

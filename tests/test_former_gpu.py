@@ -96,6 +96,30 @@ def test_sampling_matches_oracle_streams():
     assert same >= B - 2
 
 
+def test_bf16_kv_cache_logits_consistency_and_normalisation():
+    """bf16 K/V storage (fp32 math): logits within 3e-2 (relative to max |logit|) of the fp64 oracle,
+    sampling and log_prob consistent with each other, and the distribution still normalised."""
+    conf = dict(SMALL)
+    p = T.Former.init_params(seed=6, scale=2.0, **conf)
+    f = T.Former(p, kv="bf16", **conf)
+    rs = np.random.default_rng(4)
+    B, Tn = 4, 70
+    tok = rs.integers(0, 2, (B, Tn)).astype(np.uint8)
+    betas = np.array([0.2, 0.9, 1.7, 3.0])
+    _, z = f.log_prob(tok, betas, return_logits=True)
+    errs = []
+    for b in range(B):
+        zo = F.forward_logits(p, CFG, tok[b], betas[b])
+        errs.append(np.max(np.abs(z[b] - zo)) / max(1.0, np.max(np.abs(zo))))
+    assert max(errs) < 3e-2, errs
+    assert max(errs) > 0  # the bf16 path really runs (fp32 would be ~1e-5)
+    streams = np.array([T.derive_state(91, [0x44, b]) for b in range(32)], np.uint64)
+    tok2, lq = f.sample(32, 40, np.linspace(0.2, 3.0, 32), streams)
+    assert np.allclose(lq, f.log_prob(tok2, np.linspace(0.2, 3.0, 32)), atol=1e-4)
+    toks = np.array(list(itertools.product([0, 1], repeat=10)), np.uint8)
+    assert abs(np.exp(f.log_prob(toks, 1.1)).sum() - 1.0) < 1e-5
+
+
 def test_sample_token_statistics_follow_logits():
     """Many samples of a 3-token sequence: empirical frequencies vs exp(log_prob)."""
     f, _ = model(seed=6, scale=1.0)

@@ -6,7 +6,7 @@
   log_prob: tokens/s of the causal forward; FLOP/s (dense 2 x 65.5k MAC per token + causal
             attention) vs the fp32 CUDA-core peak (148 SMs x 128 FMA x 2 x f_SM).
 
-  python tools/bench_former.py [--cases mult8,lat16,mult16] [--batch B]
+  python tools/bench_former.py [--cases mult8,lat16,mult16] [--batch B] [--kv fp32|bf16]
 """
 import argparse
 import json
@@ -29,6 +29,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cases", default="mult8,lat16,mult16")
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--kv", default="fp32", choices=["fp32", "bf16"])
     args = ap.parse_args()
     import torch
 
@@ -36,7 +37,8 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
-    f = T.Former(seed=1, scale=1.0, max_len=1024)
+    f = T.Former(seed=1, scale=1.0, max_len=1024, kv=args.kv)
+    kvb = 2 if args.kv == "bf16" else 4
     L, D = f.config["layers"], f.config["d_model"]
     dense_mac = T.Former.param_count() - 2 * D - 16 * D - D  # every weight once per token (approx.)
     props = torch.cuda.get_device_properties(0)
@@ -62,13 +64,13 @@ def main():
         ev[3].record()
         torch.cuda.synchronize()
         ts, tf = ev[0].elapsed_time(ev[1]) * 1e-3, ev[2].elapsed_time(ev[3]) * 1e-3
-        kv = L * 2 * D * 4 * Tn * (Tn + 1) / 2 * B
+        kv = L * 2 * D * kvb * Tn * (Tn + 1) / 2 * B
         attn_flop = L * 2 * 2 * D * Tn * (Tn + 1) / 2 * B
         flop = 2.0 * dense_mac * Tn * B + attn_flop
         f_sm = props.clock_rate * 1e3 if hasattr(props, "clock_rate") else 1.965e9
         fp32_peak = props.multi_processor_count * 128 * 2 * 1.965e9
         print(json.dumps({
-            "case": name, "T": Tn, "prefix": npre, "batch": B,
+            "case": name, "T": Tn, "prefix": npre, "batch": B, "kv": args.kv,
             "sample": {"tokens_per_s": B * Tn / ts, "seconds": ts, "kv_gb": kv / 1e9,
                        "kv_gbs": kv / ts / 1e9, "hbm_frac": kv / ts / 1e9 / hbm},
             "log_prob": {"tokens_per_s": B * Tn / tf, "seconds": tf, "tflops": flop / tf / 1e12,
