@@ -48,6 +48,9 @@ class IsingFormer : public ProposalSource {
         return IsingFormer(g, f);
     }
     void save_checkpoint(const std::string& path) const { throw_status(tapt_former_save(f_.get(), path.c_str())); }
+    // K/V cache precision of the device model: bf16 storage halves the sampling-bound K/V stream
+    // (fp32 attention math).  Default fp32.
+    void set_kv_bf16(bool on) { throw_status(tapt_former_set_kv_bf16(f_.get(), on ? 1 : 0)); }
     static ParameterSet init_params(const GeneratorConfig& cfg, std::uint64_t seed, double scale = 1.0) {
         const auto c = cfg.c();
         ParameterSet p(cfg.parameter_count());
