@@ -81,6 +81,7 @@ struct Smem {
 struct KVChunk {
     float K[32][2 * 32 + 1];
     float V[32][2 * 32 + 1];
+    float4 P[NT / 32][8];  // per warp: the 32 key probabilities of the current task (float4-read)
 };
 
 __device__ __forceinline__ float warp_sum(float v) {
@@ -394,7 +395,17 @@ __device__ void rows_attention_fwd(Smem<RB>& s, KVChunk& kv, const FArgs& a, int
             lsum[k] = lsum[k] * corr + warp_sum(p);
             float oo = o[k] * corr;
 #pragma unroll 8
-            for (int jj = 0; jj < 32; ++jj) oo = fmaf(__shfl_sync(0xFFFFFFFFu, p, jj), kv.V[jj][h * DH + lane], oo);
+            reinterpret_cast<float*>(kv.P[w])[lane] = p;  // broadcast through shared memory, not 32 shuffles
+            __syncwarp();
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const float4 pq = kv.P[w][q];
+                oo = fmaf(pq.x, kv.V[4 * q + 0][h * DH + lane], oo);
+                oo = fmaf(pq.y, kv.V[4 * q + 1][h * DH + lane], oo);
+                oo = fmaf(pq.z, kv.V[4 * q + 2][h * DH + lane], oo);
+                oo = fmaf(pq.w, kv.V[4 * q + 3][h * DH + lane], oo);
+            }
+            __syncwarp();
             o[k] = oo;
             m[k] = mn;
         }
