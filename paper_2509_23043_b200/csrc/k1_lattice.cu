@@ -264,7 +264,8 @@ __device__ __forceinline__ void k1_decide2(const K1Smem& sm, int nv, uint64_t ph
 }
 
 // MINB: CTAs per SM the register allocation must allow (2 for the 256-thread small-lattice shape)
-template <int DIM, bool DIS, bool CLU, int SP, int MAXT, int MINB = 1>
+// BULK: per-item state loads as copy-engine bulk copies (large tiles; see the load below)
+template <int DIM, bool DIS, bool CLU, int SP, int MAXT, int MINB = 1, bool BULK = false>
 __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, const LatDims d) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ K1Smem sm;  // static: table addresses fold into LDS immediates
@@ -283,13 +284,34 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
         const int r = e >> 3, k = e & 7;
         thrS[e] = k < a.nidx ? a.thr[(size_t)r * a.nidx + k] : 0ull;
     }
+    // BULK (tiles of >= 16384 sites, config 5: +0.5 %): spin words and bond bytes of each item come
+    // in as bulk copies (copy engine, mbarrier).  Smaller tiles use uint4 loads, in an instantiation
+    // without this code (with it, config 2 measured 4.5 % slower even when the path was unused).
+    __shared__ uint64_t tile_bar;
+    constexpr bool bulk = BULK;
+    uint32_t tile_phase = 0;
+    if constexpr (BULK) {
+        if (tid == 0) mbar_init(&tile_bar);
+        __syncthreads();
+    }
     for (int it = it0; it < it1; ++it) {
     const SchedItem item = a.sched ? a.sched[it] : SchedItem{cl, 0, a.energy_only ? 1 : a.n_sweeps, -1, -1};
     const int inst = item.inst;
     if (item.wait >= 0) pt_wait_flag(a, item.wait);
 
     // ---- load this CTA's spins (and the instance's bond signs) into shared memory
-    {
+    if constexpr (bulk) {
+        fence_proxy_async_smem();  // the previous item's generic accesses before the copy engine writes
+        __syncthreads();
+        if (tid == 0) {
+            // a split job's words were written by another SM's generic stores (flag-ordered)
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            const uint32_t wb = (uint32_t)n * 4u, bb = DIS ? (uint32_t)n : 0u;
+            mbar_expect_tx(&tile_bar, wb + bb);
+            bulk_g2s(words, a.words + ((size_t)inst * a.G + grp) * n, wb, &tile_bar);
+            if constexpr (DIS) bulk_g2s(bonds, a.bonds + (size_t)inst * n, bb, &tile_bar);
+        }
+    } else {
         const uint4* src = reinterpret_cast<const uint4*>(a.words + ((size_t)inst * a.G + grp) * n);
         uint4* dst = reinterpret_cast<uint4*>(words);
         for (int k = tid; k < (n >> 2); k += nt) dst[k] = src[k];
@@ -301,6 +323,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
     }
     pt_load_perm(a, sm.S, inst);
     for (int r = tid; r < a.R; r += nt) strS[r] = a.streams[(size_t)inst * a.R + r];
+    if constexpr (bulk) {
+        mbar_wait(&tile_bar, tile_phase);
+        tile_phase ^= 1u;
+    }
     __syncthreads();
 
     // swap passes before this item: sweeps T = t+1 in (t0, t0+s0] with swap_every | T
@@ -455,11 +481,13 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
     // SP = 1 site word per thread-iteration at 1024 threads, else 2 interleaved at <= 512
     // launch shapes: 2 interleaved site words per thread-iteration at <= 512 threads (default),
     // 2 at 513..768 (<= 85 registers), 1 at > 768, 4 at <= 256
-    auto fn = threads > 768    ? k1_lattice_pt<DIM, DIS, CLU, 1, 1024>
-              : threads > 512  ? k1_lattice_pt<DIM, DIS, CLU, 2, 768>
-              : threads > 256  ? k1_lattice_pt<DIM, DIS, CLU, 2, 512>
-              : threads == 256 ? k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2>
-                               : k1_lattice_pt<DIM, DIS, CLU, 4, 256>;
+    const bool bulk = (a.n & 15) == 0 && a.n >= 16384;
+    auto fn = threads > 768             ? k1_lattice_pt<DIM, DIS, CLU, 1, 1024>
+              : threads > 512           ? k1_lattice_pt<DIM, DIS, CLU, 2, 768>
+              : threads > 256 && bulk   ? k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, true>
+              : threads > 256           ? k1_lattice_pt<DIM, DIS, CLU, 2, 512>
+              : threads == 256          ? k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2>
+                                        : k1_lattice_pt<DIM, DIS, CLU, 4, 256>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
