@@ -264,8 +264,12 @@ __device__ __forceinline__ void k1_decide2(const K1Smem& sm, int nv, uint64_t ph
 }
 
 // MINB: CTAs per SM the register allocation must allow (2 for the 256-thread small-lattice shape)
-// BULK: per-item state loads as copy-engine bulk copies (large tiles; see the load below)
-template <int DIM, bool DIS, bool CLU, int SP, int MAXT, int MINB = 1, bool BULK = false>
+// BULK: per-item state loads as copy-engine bulk copies (large tiles; see the load below).
+// NAR: unrolled decisions for 16- and 8-replica groups (narrow groups).  Both
+// are separate instantiations because the extra code shifts the hot loop's code generation: with the
+// narrow paths compiled in, 2D shapes measured up to 4 % faster and 3D shapes up to 1.2 % slower, so
+// 3D shapes carry them only when the launch uses narrow groups (tools/cfg_ab.sh, tools/k1_ab.sh).
+template <int DIM, bool DIS, bool CLU, int SP, int MAXT, int MINB = 1, bool BULK = false, bool NAR = true>
 __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, const LatDims d) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ K1Smem sm;  // static: table addresses fold into LDS immediates
@@ -399,9 +403,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
                     // more CTAs when instances are few); partial groups take the rolled loop
                     if (nv == kW)
                         k1_decide<kW, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
-                    else if (nv == 16)
+                    else if (NAR && nv == 16)
                         k1_decide<16, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
-                    else if (nv == 8)
+                    else if (NAR && nv == 8)
                         k1_decide<8, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
                     else
                         k1_decide<0, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
@@ -482,12 +486,16 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
     // launch shapes: 2 interleaved site words per thread-iteration at <= 512 threads (default),
     // 2 at 513..768 (<= 85 registers), 1 at > 768, 4 at <= 256
     const bool bulk = (a.n & 15) == 0 && a.n >= 16384;
-    auto fn = threads > 768             ? k1_lattice_pt<DIM, DIS, CLU, 1, 1024>
-              : threads > 512           ? k1_lattice_pt<DIM, DIS, CLU, 2, 768>
-              : threads > 256 && bulk   ? k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, true>
-              : threads > 256           ? k1_lattice_pt<DIM, DIS, CLU, 2, 512>
-              : threads == 256          ? k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2>
-                                        : k1_lattice_pt<DIM, DIS, CLU, 4, 256>;
+    constexpr bool NAR3 = DIM == 2;  // 3D: narrow decision paths only in the narrow-group instantiations
+    const bool narrow = a.W < kW;
+    auto fn = threads > 768                     ? k1_lattice_pt<DIM, DIS, CLU, 1, 1024>
+              : threads > 512                   ? k1_lattice_pt<DIM, DIS, CLU, 2, 768>
+              : threads > 256 && narrow         ? k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, true>
+              : threads > 256 && bulk           ? k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, true, NAR3>
+              : threads > 256                   ? k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, NAR3>
+              : threads == 256 && narrow        ? k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2, false, true>
+              : threads == 256                  ? k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2, false, NAR3>
+                                                : k1_lattice_pt<DIM, DIS, CLU, 4, 256>;
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
