@@ -280,6 +280,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
     uint64_t* thrS = reinterpret_cast<uint64_t*>(smem_raw + k1_stage_offset(a.n, a.bonds != nullptr));
     uint64_t* strS = thrS + (size_t)a.R * 8;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    constexpr int KV = DIM == 3 ? TAPT_K1_VARIANT3 : TAPT_K1_VARIANT;  // decision instruction mix
     const int cl = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
     const int half = n >> 1, nsub = half / SP;
@@ -402,13 +403,13 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
                     // full 32-, 16- and 8-replica groups unrolled (narrow groups spread an instance over
                     // more CTAs when instances are few); partial groups take the rolled loop
                     if (nv == kW)
-                        k1_decide<kW, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                        k1_decide<kW, KV, SP>(sm, nv, ph, N, a.mc, nw, tie);
                     else if (NAR && nv == 16)
-                        k1_decide<16, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                        k1_decide<16, KV, SP>(sm, nv, ph, N, a.mc, nw, tie);
                     else if (NAR && nv == 8)
-                        k1_decide<8, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                        k1_decide<8, KV, SP>(sm, nv, ph, N, a.mc, nw, tie);
                     else
-                        k1_decide<0, TAPT_K1_VARIANT, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                        k1_decide<0, KV, SP>(sm, nv, ph, N, a.mc, nw, tie);
                     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
 #pragma unroll
                     for (int u = 0; u < SP; ++u) nw[u] = ~nw[u] & vmask;
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(512) k_decision_probe(uint32_t iters, uint32_t
 cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint32_t* sink, cudaStream_t st,
                                   int variant) {
     const MixConsts mc = make_mix_consts();
-    switch (variant < 0 ? TAPT_K1_VARIANT : variant) {
+    switch (variant < 0 ? TAPT_K1_VARIANT3 : variant) {  // default: the config-5 (3D) kernel's variant
 #define TAPT_PROBE_CASE(v) \
     case v: k_decision_probe<v><<<blocks, threads, 0, st>>>(iters, sink, mc); break;
         TAPT_PROBE_CASE(0) TAPT_PROBE_CASE(1) TAPT_PROBE_CASE(2) TAPT_PROBE_CASE(3)
