@@ -255,18 +255,29 @@ def run_workload(args):
     clocks = clk.summary()
     f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
     n_sm = torch.cuda.get_device_properties(0).multi_processor_count
-    peak = n_sm * 128 * f_sm / WL.I_U[k]
     probe, _ = T.probe_decision_rate(1, 512, 20000)
+    ipath = os.path.join(ROOT, "profiles", "inst_per_update.json")
+    ie = json.load(open(ipath)).get(f"cfg{k}") if os.path.exists(ipath) else None
+    cap = n_sm * 128 * f_sm
+    alg = cap / WL.I_U[k]
+    roof = {"unit": "Gupdates/s", "achieved": value / 1e9,
+            "algorithmic": {"I_u": WL.I_U[k], "peak": alg / 1e9, "frac": value / alg,
+                            "what": "SURVEY.md 8(d) estimate of instructions per update (not a bound)"},
+            "probe_ceiling": {"value": probe / 1e9, "frac": value / probe}, "traffic": None}
+    if ie:
+        roof.update({"bound": "issue", "peak": cap / ie["I_exec"] / 1e9, "frac": value * ie["I_exec"] / cap,
+                     "peak_source": f"n_SM*128*f_SM/I_exec, I_exec={ie['I_exec']} executed thread-instructions per "
+                                    f"update ({ie['source']})"})
+    else:
+        roof.update({"bound": "alu", "peak": alg / 1e9, "frac": value / alg,
+                     "peak_source": f"SURVEY.md 8(d) n_SM*128*f_SM/I_u, I_u={WL.I_U[k]}"})
     out = {
         "metric": f"spin updates/sec, BASELINE config {k}", "value": value, "unit": UNIT, "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
         "scaling": "replicas only", "vs_baseline": None, "dtype": "u32 multi-spin words / u64 splitmix64",
         "data": "synthetic", "config": {"workload": w["desc"], "kernel": w["kernel"],
                                         "updates_per_step": w["updates_per_step"]},
-        "roofline": {"bound": "alu", "unit": "Gupdates/s", "achieved": value / 1e9, "peak": peak / 1e9,
-                     "frac": value / peak, "traffic": None,
-                     "peak_source": f"BASELINE.md section 4 ALU bound n_SM*128*f_SM/I_u, I_u={WL.I_U[k]}",
-                     "probe_ceiling": {"value": probe / 1e9, "frac": value / probe}},
+        "roofline": roof,
         "gpu_launches": T.launch_count() - l0, "clocks": clocks,
     }
     if not args.no_cpu_baseline:
@@ -315,10 +326,116 @@ def run_reference(args):
     }), flush=True)
 
 
+# --------------------------------------------------------------- multi-GPU --
+
+def launcher_cmd(argv, gpus, port=None):
+    """The torchrun command that re-executes this script with one rank per GPU (used when
+    `--gpus N` > 1 is given without a torch.distributed environment)."""
+    if port is None:
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+
+
+def check_world(args):
+    """--gpus N must equal the launcher's world size; without a launcher, N > 1 spawns the ranks."""
+    world = int(os.environ.get("WORLD_SIZE", "0"))
+    if world == 0:
+        if args.gpus > 1:
+            cmd = launcher_cmd(sys.argv[1:], args.gpus)
+            os.execv(cmd[0], cmd)  # does not return
+        return 1
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch one rank per GPU)")
+    return world
+
+
+def init_dist(world, local, backend="nccl"):
+    import torch
+    import torch.distributed as dist
+    if world > 1 and not dist.is_initialized():
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
+    return dist
+
+
+def sum_histograms(hist, world, stream=None):
+    """Per-beta energy histograms summed over the ranks -- with the timing max below, the only
+    collectives of the run (NCCL over NVLink on the B200 box, gloo in the CPU test).
+    Enqueued on `stream` (inside the timed region) when given."""
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        if stream is not None:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(hist)
+        else:
+            dist.all_reduce(hist)
+    return hist
+
+
+def max_over_ranks(ms, world, device):
+    """(max over ranks of a timed-region length, ranks in the communicator)."""
+    import torch
+    import torch.distributed as dist
+    if world <= 1:
+        return float(ms), 1
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item()), dist.get_world_size()
+
+
+# ---------------------------------------------------------------- roofline --
+
+def issue_roofline(achieved, n_sm, f_sm, probe, n_inst, hbm_bytes, k_ms, g_hbm, path=None):
+    """Roofline of the dominant kernel (K1, config 5).  Every spin update is shared-memory resident
+    integer work, so the bound is the SMs' instruction issue: n_SM x 128 thread-instructions/clk x
+    f_SM divided by the instructions the kernel executes per update (I_exec, from the committed ncu
+    --set full capture of the same kernel: smsp__inst_executed x 32 / updates).  frac is therefore
+    the share of issue slots the kernel fills (<= 1).  Secondary figures: SURVEY.md 8(d)'s
+    algorithmic bound (I_u = 42 estimated instructions per update), the measured decision-probe
+    ceiling, the ncu pipe utilisations, and HBM."""
+    path = path or os.path.join(ROOT, "profiles", "k1_traffic.json")
+    tr = json.load(open(path)) if os.path.exists(path) else {}
+    ipu = tr.get("thread_inst_per_update")
+    cap = n_sm * 128 * f_sm  # thread-instructions per second
+    alg = cap / I_U
+    out = {"unit": "Gupdates/s", "achieved": achieved / 1e9,
+           "algorithmic": {"I_u": I_U, "peak": alg / 1e9, "frac": achieved / alg,
+                           "what": "SURVEY.md 8(d) estimate (splitmix64 draw + threshold compare ~28, stencil ~14); "
+                                   "the compiled kernel executes fewer, so this is not a bound"},
+           "probe_ceiling": {"value": probe / 1e9, "frac": achieved / probe,
+                             "what": "k_decision_probe: the bare per-update work (splitmix64 high word + threshold "
+                                     "lookup + compare + bit insert), no stencil or memory traffic, same unroll"},
+           "hbm": {"achieved_gbs": hbm_bytes / (k_ms * 1e-3) / 1e9, "peak_gbs": g_hbm,
+                   "frac": hbm_bytes / (k_ms * 1e-3) / 1e9 / g_hbm,
+                   "note": "spins stay in shared memory for the whole 1000-sweep launch"}}
+    if ipu:
+        peak = cap / ipu
+        out.update({"bound": "issue", "peak": peak / 1e9, "frac": achieved / peak,
+                    "peak_source": f"n_SM*128*f_SM/I_exec: n_SM={n_sm}, f_SM = median SM clock sampled during the "
+                                   f"timed region ({f_sm / 1e6:.0f} MHz), I_exec={ipu:.2f} executed thread-"
+                                   f"instructions per update ({tr.get('inst_source')})",
+                    "traffic": tr["dram_bytes_per_instance_launch"] * n_inst,
+                    "traffic_detail": {"dram_bytes_per_launch": tr["dram_bytes_per_instance_launch"] * n_inst,
+                                       "algorithmic_bytes_per_launch": hbm_bytes, "source": tr["source"]},
+                    "pipes": tr.get("pipes")})
+    else:  # no committed capture: fall back to the algorithmic estimate
+        out.update({"bound": "alu", "peak": alg / 1e9, "frac": achieved / alg, "traffic": None,
+                    "peak_source": f"SURVEY.md 8(d) n_SM*128*f_SM/I_u, I_u={I_U} (no committed ncu capture)"})
+    return out
+
+
 # ------------------------------------------------------------------ B200 arm --
 
 def main():
     args = parse()
+    world_checked = check_world(args)
     if args.impl == "reference":
         run_reference(args)
         return
@@ -330,12 +447,11 @@ def main():
 
     import paper_2509_23043_b200 as T
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = world_checked
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    init_dist(world, local)
     from paper_2509_23043_b200 import sharding
     off, I = sharding.shard(args.instances, world, rank)  # contiguous global instance ids
     S = args.sweeps_per_step
@@ -376,19 +492,15 @@ def main():
         for _ in range(args.steps):
             step(True)
         ens.histogram(device_ptr=hist_t.data_ptr())
-        if world > 1:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(hist_t)
+        sum_histograms(hist_t, world, stream)  # inside the timed region
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     launches = T.launch_count() - l0
     ms = t_start.elapsed_time(t_end)
-    ms_t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(ms_t, op=dist.ReduceOp.MAX)
-    ms = float(ms_t.item())
+    ms, comm_ranks = max_over_ranks(ms, world, "cuda")
+    samples = int(hist_t.sum().item())
     upd_step = args.instances * (R * N_SPINS * S + N_TARGETS * N_SPINS * REFINE)
     value = upd_step * args.steps / (ms * 1e-3)
 
@@ -400,37 +512,13 @@ def main():
     clocks = clk.summary()
     f_sm = (clocks.get("sm_mhz") or 1965.0) * 1e6
     n_sm = torch.cuda.get_device_properties(local).multi_processor_count
-    peak = n_sm * 128 * f_sm / I_U
     g_hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))).get("hbm_gbs") if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else 6650.0
     hbm_bytes = I * (2 * 4 * N_SPINS * 2 + N_SPINS)  # spins in+out (2 groups) + bond bytes, per launch
-    traffic, traffic_detail = None, None
-    tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
-    issue = None
-    if os.path.exists(tpath):  # dram bytes per instance-launch from the committed ncu --set full capture
-        tr = json.load(open(tpath))
-        traffic = tr["dram_bytes_per_instance_launch"] * I
-        traffic_detail = {"dram_bytes_per_launch": traffic, "algorithmic_bytes_per_launch": hbm_bytes,
-                          "source": tr["source"]}
-        if "thread_inst_per_update" in tr:  # issue slots the kernel actually uses (executed, not algorithmic)
-            ipu = tr["thread_inst_per_update"]
-            issue = {"thread_inst_per_update": ipu, "frac": achieved * ipu / (n_sm * 128 * f_sm),
-                     "what": "executed instructions per update (ncu) x updates/s / issue capacity n_SM*128*f_SM: "
-                             "the share of the SMs' issue slots the kernel fills", "source": tr["inst_source"]}
-    roofline = {
-        "bound": "alu", "unit": "Gupdates/s", "achieved": achieved / 1e9, "peak": peak / 1e9,
-        "frac": achieved / peak, "traffic": traffic, "traffic_detail": traffic_detail,
-        "peak_source": f"BASELINE.md section 4 ALU/issue bound n_SM*128*f_SM/I_u with n_SM={n_sm}, f_SM = median "
-                       f"SM clock sampled during the timed region ({f_sm / 1e6:.0f} MHz), I_u={I_U} (cfg5)",
-        "probe_ceiling": {"value": probe / 1e9, "frac": achieved / probe,
-                          "what": "k_decision_probe: the bare per-update work (splitmix64 high word + threshold "
-                                  "lookup + compare + bit insert), no stencil or memory traffic, same unroll"},
-        "issue": issue,
-        "kernel": "k1_lattice_pt<3,true,true>", "kernel_ms_per_launch": k_ms, "updates_per_launch": k_upd,
-        "hbm": {"achieved_gbs": hbm_bytes / (k_ms * 1e-3) / 1e9, "peak_gbs": g_hbm,
-                "frac": hbm_bytes / (k_ms * 1e-3) / 1e9 / g_hbm,
-                "note": "spins stay in shared memory for the whole 1000-sweep launch"},
-    }
+    roofline = issue_roofline(achieved, n_sm, f_sm, probe, I, hbm_bytes, k_ms, g_hbm)
+    sweep_kernels = [x for x in ens.launch_log() if x.startswith("k1_lattice_pt<3,1,1,")]
+    roofline.update({"kernel": sweep_kernels[-1] if sweep_kernels else None, "kernel_ms_per_launch": k_ms,
+                     "updates_per_launch": k_upd})
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
@@ -440,7 +528,10 @@ def main():
                                "(swap every sweep, measure every 10) per step",
                    "instances_total": args.instances, "instances_per_gpu": I, "sweeps_per_step": S,
                    "updates_per_step": upd_step, "parallelism": f"instances sharded over {world} GPU(s)",
-                   "l2": "state 1 GiB/GPU at N=1 > 126 MB L2; spins are shared-memory resident within a launch"},
+                   "l2": "state 1 GiB/GPU at N=1 > 126 MB L2; spins are shared-memory resident within a launch",
+                   "histogram_samples_reduced": samples},
+        "comm": {"backend": "nccl" if world > 1 else None, "ranks": comm_ranks,
+                 "collectives": "all_reduce of the per-beta histograms (int64 [64][3072]) + max of the timed region"},
         "roofline": roofline, "gpu_launches": launches,
     }
     if not args.no_e2e:
@@ -462,41 +553,47 @@ def main():
 
 
 def e2e_leg(args, T, torch, ens, stream, I, S, world):
-    """Same metric through the public C-ABI call with HOST buffers: per step the externally
-    supplied proposals (bit-packed, pinned host memory) are copied H2D inside the timed
-    region, injected (energy + Eq. 2 on the device), 1000 PT sweeps run, and the per-slot
-    energies are read back D2H."""
+    """Same metric and the same step through the public C-ABI calls with HOST buffers: per step the
+    externally supplied proposals (the generator's output: bit-packed [I][56][4096 B] in pinned host
+    memory) are copied H2D inside the timed region and injected with their 5 refinement sweeps at the
+    target beta + Eq. 2 (tapt_inject_proposals_packed_refined), 1000 PT sweeps run with measurement
+    every 10 sweeps, and the step's outputs -- the per-beta energy histograms (config 5's output) and
+    the per-slot energies -- are read back D2H (histograms all-reduced over the ranks first)."""
     nbytes = (N_SPINS + 7) // 8
     rs = np.random.default_rng(7)
     host = torch.from_numpy(rs.integers(0, 256, size=(I, N_TARGETS, nbytes), dtype=np.uint8)).pin_memory()
     dev = torch.empty_like(host, device="cuda")
+    nb = 2 * 3 * N_SPINS // 64
+    hist_d = torch.zeros((R, nb), dtype=torch.int64, device="cuda")
+    hist_h = torch.zeros((R, nb), dtype=torch.int64).pin_memory()
     energies = torch.empty((I, R), dtype=torch.int64).pin_memory()
     targets = np.arange(N_TARGETS, dtype=np.uint32)
 
     def step():
         with torch.cuda.stream(stream):
             dev.copy_(host, non_blocking=True)
-        ens.inject_proposals_packed(None, targets, device_ptr=dev.data_ptr())
+        ens.inject_proposals_packed(None, targets, device_ptr=dev.data_ptr(), refine=REFINE, return_accepted=False)
         ens.run(S, swap_every=1, measure_every=args.measure_every)
+        ens.histogram(device_ptr=hist_d.data_ptr())
+        sum_histograms(hist_d, world, stream)
+        with torch.cuda.stream(stream):
+            hist_h.copy_(hist_d, non_blocking=True)
         energies.copy_(torch.from_numpy(ens.energies()))
 
-    for _ in range(1):
-        step()
+    step()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         step()
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
-    dt_t = torch.tensor([dt], dtype=torch.float64, device="cuda")
-    if world > 1:
-        import torch.distributed as dist
-        dist.all_reduce(dt_t, op=dist.ReduceOp.MAX)
-    dt = float(dt_t.item())
-    upd = args.instances * R * N_SPINS * S * args.steps
+    dt, _ = max_over_ranks(dt, world, "cuda")
+    upd = args.instances * (R * N_SPINS * S + N_TARGETS * N_SPINS * REFINE) * args.steps
     return {"value": upd / dt, "unit": UNIT, "h2d_bytes_per_step": int(host.numel()),
-            "d2h_bytes_per_step": int(I * R * 8),
-            "path": "tapt_inject_proposals_packed (host-supplied proposals) + tapt_run + tapt_ensemble_get_energies"}
+            "d2h_bytes_per_step": int(hist_h.numel() * 8 + I * R * 8),
+            "path": "tapt_inject_proposals_packed_refined (host-supplied proposals, 5 refinement sweeps, Eq. 2) + "
+                    "tapt_run + tapt_get_histogram (+ NCCL all_reduce) + tapt_ensemble_get_energies",
+            "timer": "host wall clock around K steps, synchronized on both sides, max over ranks"}
 
 
 if __name__ == "__main__":

@@ -258,17 +258,36 @@ inline RunTrace run_pt(const CouplingGraph& g, const BetaLadder& ladder, const T
     return run_tapt(g, ladder, c, nullptr, order);
 }
 
-// residual_energy: rho(t) = (coldest-replica energy after move t - E_gnd) / N.
-inline std::vector<double> residual_energy(const RunTrace& tr, double e_gnd, std::size_t n_spins) {
-    std::vector<double> rho;
-    for (const auto& E : tr.energies) rho.push_back((E.back() - e_gnd) / double(n_spins));
+// residual_energy: rho(t) = (<E_coldest(t)>_runs - E_gnd) / N, the
+// coldest replica's energy after global move t averaged over independent runs.  best_so_far: use each
+// run's best energy up to move t instead (the "best-so-far sense" of SPEC.md:456; non-increasing).
+// Runs must have the same number of moves (DimensionError otherwise).
+inline std::vector<double> residual_energy(const std::vector<RunTrace>& runs, double e_gnd, std::size_t n_spins,
+                                           bool best_so_far = false) {
+    if (runs.empty()) throw ConfigError("residual_energy needs at least one run");
+    if (n_spins == 0) throw ConfigError("n_spins must be > 0");
+    const std::size_t T = best_so_far ? runs[0].best_energy.size() : runs[0].energies.size();
+    std::vector<double> rho(T, 0.0);
+    for (const auto& tr : runs) {
+        const std::size_t Tk = best_so_far ? tr.best_energy.size() : tr.energies.size();
+        if (Tk != T) throw DimensionError("residual_energy: runs differ in their number of global moves");
+        for (std::size_t t = 0; t < T; ++t) {
+            if (!best_so_far && tr.energies[t].empty()) throw DimensionError("residual_energy: empty energy record");
+            rho[t] += best_so_far ? tr.best_energy[t] : tr.energies[t].back();
+        }
+    }
+    for (double& v : rho) v = (v / double(runs.size()) - e_gnd) / double(n_spins);
     return rho;
 }
 
-// adaptive_ladder: greedy from beta_min; a probe chain (device sweeps,
-// stream kProbe) estimates sigma_E at the current beta and the next beta is placed where the
-// Gaussian-approximated swap acceptance erfc(dbeta*sigma/2) equals the target; degenerate
-// variance falls back to geometric spacing.
+inline std::vector<double> residual_energy(const RunTrace& tr, double e_gnd, std::size_t n_spins) {
+    return residual_energy(std::vector<RunTrace>{tr}, e_gnd, n_spins);
+}
+
+// adaptive_ladder: greedy from beta_min; probe chains (device sweeps, stream
+// kProbe) estimate sigma_E, and the next beta is placed where the Gaussian-approximated swap
+// acceptance erfc(dbeta*sigma/2) equals the target, sigma being the mean of the probe estimates at
+// both ends of the gap (refined twice); degenerate variance falls back to geometric spacing.
 inline BetaLadder adaptive_ladder(const CouplingGraph& g, double beta_min, double beta_max, double target,
                                   std::uint64_t probe_budget, std::uint64_t seed) {
     if (!(target > 0.0 && target < 1.0)) throw ConfigError("target acceptance must be in (0, 1)");
@@ -285,14 +304,15 @@ inline BetaLadder adaptive_ladder(const CouplingGraph& g, double beta_min, doubl
     double b = beta_min;
     std::uint64_t k = 0;
     const std::uint64_t sweeps = std::max<std::uint64_t>(probe_budget, 8);
-    while (b < beta_max && out.betas.size() < 256) {
-        out.betas.push_back(b);
+    // sigma_E at beta from a fresh probe chain (own streams {kProbe, k, 0|1}, second half of the run)
+    auto sigma = [&](double beta) {
         RngStream init = RngStream::derive(seed, {stream::kProbe, k, 0});
         RngStream dyn = RngStream::derive(seed, {stream::kProbe, k, 1});
+        ++k;
         SpinConfiguration s = random_configuration(g, init);
         std::vector<double> dE;
         const double e0 = energy(g, s);
-        gibbs_sweeps(g, s, b, dyn, static_cast<std::uint32_t>(sweeps), &dE);
+        gibbs_sweeps(g, s, beta, dyn, static_cast<std::uint32_t>(sweeps), &dE);
         std::vector<double> E;
         double cur = e0;
         for (double d : dE) E.push_back(cur += d);
@@ -302,15 +322,33 @@ inline BetaLadder adaptive_ladder(const CouplingGraph& g, double beta_min, doubl
         mu /= double(E.size() - from);
         for (std::size_t t = from; t < E.size(); ++t) var += (E[t] - mu) * (E[t] - mu);
         var /= double(E.size() - from);
+        return std::sqrt(var);
+    };
+    const double x = 2.0 * erfcinv(target);  // erfc(dbeta * sigma / 2) = target  <=>  dbeta * sigma = x
+    // at most 255 probe points + beta_max (the engine's 256-slot limit)
+    while (b < beta_max && out.betas.size() < 255) {
+        out.betas.push_back(b);
+        const double s0 = sigma(b);
         double step;
-        if (var <= 0.0)
+        if (s0 <= 0.0) {
             step = b * (std::pow(beta_max / std::max(beta_min, 1e-3), 1.0 / 15.0) - 1.0) + 1e-3;
-        else
-            step = 2.0 * erfcinv(target) / std::sqrt(var);
+        } else {
+            // sigma_E changes across the gap: place the next beta with the mean of sigma at both ends
+            // (two fixed-point refinements, each probing the candidate), not sigma at b alone
+            step = x / s0;
+            for (int it = 0; it < 2 && b + step < beta_max; ++it) {
+                const double s1 = sigma(b + step);
+                step = x / (0.5 * (s0 + s1) > 0.0 ? 0.5 * (s0 + s1) : s0);
+            }
+        }
         b += std::max(step, 1e-4);
-        ++k;
     }
-    if (out.betas.back() < beta_max) out.betas.push_back(beta_max);
+    // close at beta_max; a last gap below the minimum step would make the swap tables oversize
+    // ("beta spacing too fine"), so beta_max then replaces the last probe point instead
+    if (out.betas.size() > 1 && beta_max - out.betas.back() < 1e-4)
+        out.betas.back() = beta_max;
+    else if (out.betas.back() < beta_max)
+        out.betas.push_back(beta_max);
     return out;
 }
 

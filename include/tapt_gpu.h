@@ -138,8 +138,12 @@ tapt_status tapt_ensemble_destroy(tapt_ensemble_t e);
 /* cudaStream_t to enqueue on (NULL: the handle's own non-blocking stream). */
 tapt_status tapt_ensemble_set_stream(tapt_ensemble_t e, void* cuda_stream);
 tapt_status tapt_ensemble_synchronize(tapt_ensemble_t e);
-/* Kernel that serves sweeps of this ensemble: "lattice" (K1) or "csr" (K2). */
+/* Kernel that serves sweeps of this ensemble: "lattice" (K1), "bitcsr" (K3), "levels" (K4) or "csr" (K2). */
 const char* tapt_ensemble_kernel(tapt_ensemble_t e);
+/* Distinct sweep-kernel instantiations this ensemble has launched, one per line, in first-launch
+ * order ("k1_lattice_pt<3,1,1,2,512,1,1,0> balanced M=74" = template arguments, plus the persistent
+ * grid's co-resident units when the balanced schedule ran).  Test evidence of which path ran. */
+tapt_status tapt_ensemble_launch_log(tapt_ensemble_t e, char* buf, size_t cap);
 
 /* Edwards-Anderson +-J disorder for lattice models, one sign per bond:
  * signs [n_instances][n_bonds] (+-1, bond order of LatticeSpec::graph), or generate
@@ -212,6 +216,14 @@ tapt_status tapt_inject_proposals(tapt_ensemble_t e, const int8_t* proposals, in
 /* Same, bit-packed proposals [I][n_targets][ceil(n/8)] (ISFD1 bit order). */
 tapt_status tapt_inject_proposals_packed(tapt_ensemble_t e, const uint8_t* proposals, int on_device,
                                          const uint32_t* targets, uint32_t n_targets, uint8_t* accepted);
+/* Same, with `refine` heat-bath sweeps of each proposal at its target slot's beta before Eq. 2
+ * (BASELINE.json configs[4]: "i.i.d. +-1 spins, then 5 Gibbs sweeps at the target beta").  The
+ * refinement of slot r in round q draws from derive(seed, {kReplica, gid, r, q+1}) starting at
+ * draw n+2, exactly as tapt_generate_proposals does after its own n+1 generator draws, so
+ * host-generated proposals equal to the synthetic generator's give identical results. */
+tapt_status tapt_inject_proposals_packed_refined(tapt_ensemble_t e, const uint8_t* proposals, int on_device,
+                                                 const uint32_t* targets, uint32_t n_targets, uint32_t refine,
+                                                 uint8_t* accepted);
 
 /* Synthetic stand-in generator + Eq. 2 in one call (BASELINE configs 2 and 5): for each
  * target slot r, i.i.d. spins with P(+1) = (1 + sign*m_bias[r])/2 (sign: coin), clamps,

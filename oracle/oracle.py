@@ -46,6 +46,11 @@ class OcGraph(C.Structure):
                 ("J", _i32p), ("h", _i32p), ("clamp", _i8p), ("rank", _u32p)]
 
 
+class OcRGraph(C.Structure):
+    _fields_ = [("n", C.c_uint32), ("n_free", C.c_uint32), ("rowptr", _u32p), ("col", _u32p),
+                ("J", _f64p), ("h", _f64p), ("clamp", _i8p), ("rank", _u32p)]
+
+
 _lib = None
 _ref = None
 
@@ -93,6 +98,24 @@ def lib():
                                                 C.c_uint64, C.c_uint64, _u8p, C.c_int, _i8p, _i64p]
         L.oc_pt_measure.argtypes = [_i8p, C.c_size_t, C.c_int, _i64p, _i64p, _i64p, _i64p, _i64p, _i64p,
                                     C.c_int64, C.c_int64, C.c_int, _i64p]
+        # real-valued couplings (tapt_oracle.c "real couplings")
+        G = C.POINTER(OcRGraph)
+        L.oc_renergy.restype = C.c_double
+        L.oc_renergy.argtypes = [G, _i8p]
+        L.oc_rlocal_field.restype = C.c_double
+        L.oc_rlocal_field.argtypes = [G, _i8p, C.c_uint32]
+        L.oc_rsweep.restype = C.c_double
+        L.oc_rsweep.argtypes = [G, _u32p, _i8p, C.c_double, C.c_uint64, C.c_uint64]
+        L.oc_rupdate.restype = C.c_int8
+        L.oc_rupdate.argtypes = [G, _i8p, C.c_uint32, C.c_double, C.c_uint64]
+        L.oc_rpt_init.argtypes = [G, C.c_int, C.c_uint64, C.c_uint64, _i8p, _f64p]
+        L.oc_rpt_sweep_all.argtypes = [G, _u32p, C.c_int, _f64p, C.c_uint64, C.c_uint64, C.c_uint64, _i8p, _f64p]
+        L.oc_rpt_swap_pass.argtypes = [C.c_int, _f64p, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, _i8p,
+                                       C.c_size_t, _f64p, _u64p, _u64p, _u8p]
+        L.oc_rpt_inject.argtypes = [C.c_int, _f64p, C.c_uint64, C.c_uint64, C.c_uint64, _u8p, _i8p, _f64p,
+                                    _i8p, C.c_size_t, _f64p, _u64p, _u64p, _u8p]
+        L.oc_rpt_synthetic_proposals.argtypes = [G, _u32p, C.c_int, _f64p, _f64p, C.c_uint64, C.c_uint64,
+                                                 C.c_uint64, _u8p, C.c_int, _i8p, _f64p]
         _lib = L
     return _lib
 
@@ -224,6 +247,16 @@ class Graph:
                     _p(self._hi, _i32p), _p(self.clamp, _i8p), _p(self.rank, _u32p))
         self._oc = g
         return g
+
+    def roc(self):
+        """ctypes view with real-valued couplings and fields (cached)."""
+        if getattr(self, "_roc", None) is not None:
+            return self._roc
+        self._Jf = np.ascontiguousarray(self.adjJ, np.float64)
+        self._hf = np.ascontiguousarray(self.h, np.float64)
+        self._roc = OcRGraph(self.n, len(self.free), _p(self.rowptr, _u32p), _p(self.col, _u32p),
+                             _p(self._Jf, _f64p), _p(self._hf, _f64p), _p(self.clamp, _i8p), _p(self.rank, _u32p))
+        return self._roc
 
     def colour_order(self, colours: np.ndarray) -> np.ndarray:
         """Free sites grouped by colour class (stable: ascending index inside a class)."""
@@ -441,6 +474,76 @@ class PT:
             if measure_every and T > measure_from and T % measure_every == 0:
                 self.measure(e_lo, width, nbins)
             if prop_every and T % prop_every == 0:
+                props, Ep = self.synthetic_proposals(mask, mb, refine)
+                self.inject(mask, props, Ep)
+
+
+class RPT:
+    """PT with real-valued couplings (FP64 energies): the restated driver of tapt_oracle.c's
+    "real couplings" section, one instance, state stored by slot.  Same schedule as PT.run."""
+
+    def __init__(self, g: Graph, betas, seed: int, gid: int, order: np.ndarray):
+        self.g, self.gc = g, g.roc()
+        self.R = len(betas)
+        self.beta = np.ascontiguousarray(betas, dtype=np.float64)
+        self.seed, self.gid = seed, gid
+        self.order = np.ascontiguousarray(order, dtype=np.uint32)
+        self.spins = np.zeros((self.R, g.n), np.int8)
+        self.E = np.zeros(self.R, np.float64)
+        self.T = self.P = self.Q = 0
+        self.swap_att = np.zeros(max(self.R - 1, 1), np.uint64)
+        self.swap_acc = np.zeros(max(self.R - 1, 1), np.uint64)
+        self.prop_att = np.zeros(self.R, np.uint64)
+        self.prop_acc = np.zeros(self.R, np.uint64)
+        lib().oc_rpt_init(C.byref(self.gc), self.R, seed, gid, _p(self.spins, _i8p), _p(self.E, _f64p))
+        self.best = float(self.E.min())
+
+    def sweep(self):
+        lib().oc_rpt_sweep_all(C.byref(self.gc), _p(self.order, _u32p), self.R, _p(self.beta, _f64p), self.seed,
+                               self.gid, self.T, _p(self.spins, _i8p), _p(self.E, _f64p))
+        self.T += 1
+        self.best = min(self.best, float(self.E.min()))
+
+    def swap(self, parity=None):
+        parity = (self.P & 1) if parity is None else parity
+        dec = np.zeros(max(self.R - 1, 1), np.uint8)
+        lib().oc_rpt_swap_pass(self.R, _p(self.beta, _f64p), self.seed, self.gid, self.P, parity,
+                               _p(self.spins, _i8p), self.g.n, _p(self.E, _f64p), _p(self.swap_att, _u64p),
+                               _p(self.swap_acc, _u64p), _p(dec, _u8p))
+        self.P += 1
+        return dec
+
+    def synthetic_proposals(self, mask, m_bias, refine):
+        mask = np.ascontiguousarray(mask, dtype=np.uint8)
+        mb = np.ascontiguousarray(m_bias, dtype=np.float64)
+        props = np.zeros_like(self.spins)
+        Ep = np.zeros(self.R, np.float64)
+        lib().oc_rpt_synthetic_proposals(C.byref(self.gc), _p(self.order, _u32p), self.R, _p(self.beta, _f64p),
+                                         _p(mb, _f64p), self.seed, self.gid, self.Q, _p(mask, _u8p), refine,
+                                         _p(props, _i8p), _p(Ep, _f64p))
+        return props, Ep
+
+    def inject(self, mask, props, Ep):
+        mask = np.ascontiguousarray(mask, dtype=np.uint8)
+        props = np.ascontiguousarray(props, dtype=np.int8)
+        Ep = np.ascontiguousarray(Ep, dtype=np.float64)
+        dec = np.zeros(self.R, np.uint8)
+        lib().oc_rpt_inject(self.R, _p(self.beta, _f64p), self.seed, self.gid, self.Q, _p(mask, _u8p),
+                            _p(props, _i8p), _p(Ep, _f64p), _p(self.spins, _i8p), self.g.n, _p(self.E, _f64p),
+                            _p(self.prop_att, _u64p), _p(self.prop_acc, _u64p), _p(dec, _u8p))
+        self.Q += 1
+        self.best = min(self.best, float(self.E.min()))
+        return dec
+
+    def run(self, n_sweeps, swap_every=1, prop_every=0, n_targets=0, m_bias=None, refine=0):
+        mask = np.zeros(self.R, np.uint8)
+        mask[:n_targets] = 1
+        mb = np.zeros(self.R) if m_bias is None else np.asarray(m_bias, np.float64)
+        for _ in range(n_sweeps):
+            self.sweep()
+            if swap_every and self.T % swap_every == 0:
+                self.swap()
+            if prop_every and self.T % prop_every == 0:
                 props, Ep = self.synthetic_proposals(mask, mb, refine)
                 self.inject(mask, props, Ep)
 

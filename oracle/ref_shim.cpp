@@ -71,6 +71,27 @@ void* ref_graph_lattice(int kind, int ly, int lx, int l, double J, int periodic)
     return new CouplingGraph(s.graph());
 }
 
+// The reference tests' random graph (proj/tests/test_spin_model.cpp:24-32): for each i, an edge
+// (i, j > i) with probability edge_prob and a standard-normal coupling (RngStream::normal), then a
+// normal field if `fields`; draws from RngStream(seed) in that order.  Writes the Builder input
+// (ci, cj, J: up to n(n-1)/2 entries; h: n) and returns the coupling count.
+std::uint32_t ref_random_graph(std::uint32_t n, double edge_prob, int fields, std::uint64_t seed, std::uint32_t* ci,
+                               std::uint32_t* cj, double* J, double* h) {
+    RngStream rng(seed);
+    std::uint32_t m = 0;
+    for (std::uint32_t i = 0; i < n; ++i) {
+        for (std::uint32_t j = i + 1; j < n; ++j)
+            if (rng.uniform() < edge_prob) {
+                ci[m] = i;
+                cj[m] = j;
+                J[m] = rng.normal();
+                ++m;
+            }
+        h[i] = fields ? rng.normal() : 0.0;
+    }
+    return m;
+}
+
 void ref_graph_free(void* g) { delete static_cast<CouplingGraph*>(g); }
 
 std::uint32_t ref_graph_n(void* g) { return static_cast<std::uint32_t>(static_cast<CouplingGraph*>(g)->n_spins()); }
@@ -102,6 +123,23 @@ void ref_random_configuration(void* g, std::uint64_t root, const std::uint64_t* 
     RngStream r = derive_path(root, path, n);
     SpinConfiguration s = random_configuration(*G, r);
     std::memcpy(out, s.data(), s.size());
+}
+
+// gibbs_update (mcmc.cpp:24-28) at site i with stream derive(root, path); *clamped = 1 when the
+// reference throws ClampedSiteError.  Returns the stream state afterwards.
+std::uint64_t ref_gibbs_update(void* g, std::int8_t* spins, std::uint32_t i, double beta, std::uint64_t root,
+                               const std::uint64_t* path, int n, int* clamped) {
+    auto* G = static_cast<CouplingGraph*>(g);
+    RngStream r = derive_path(root, path, n);
+    SpinConfiguration s(spins, spins + G->n_spins());
+    *clamped = 0;
+    try {
+        gibbs_update(*G, s, i, beta, r);
+    } catch (const ClampedSiteError&) {
+        *clamped = 1;
+    }
+    std::memcpy(spins, s.data(), s.size());
+    return r.state();
 }
 
 // n_sweeps consecutive reference gibbs_sweep calls on one stream; dE per sweep.

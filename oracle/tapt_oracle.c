@@ -295,3 +295,144 @@ void oc_pt_measure(const int8_t* spins, size_t n, int R, const int64_t* E, int64
         }
     }
 }
+
+/* ======================================================= real couplings ==== */
+/* The same path for real-valued couplings and fields (the reference's CouplingGraph
+ * takes any double J, spin_model.cpp:18-24, and gibbs_sweep works in FP64,
+ * mcmc.cpp:30-45).  Energies are doubles: the initial energy is energy()
+ * (spin_model.cpp:79-89: couplings in (i<j) order, then fields), after a sweep
+ * E += the sweep's return value (the sum, in visiting order, of 2*s_old*l over the
+ * flipped sites, mcmc.cpp:38-42), and a proposal's energy is energy() of it.  Swap and
+ * proposal decisions are the expressions of ref_shim.cpp's restated driver (Eq. 1, 2)
+ * on these doubles.  Index order reproduces the reference bit for bit (pinned by
+ * tests/golden/pt_real*.npz from oracle/_ref). */
+
+typedef struct {
+    uint32_t n;
+    uint32_t n_free;
+    const uint32_t* rowptr;
+    const uint32_t* col;
+    const double* J;      /* rowptr[n], merged coupling value per CSR entry */
+    const double* h;      /* n */
+    const int8_t* clamp;
+    const uint32_t* rank;
+} oc_rgraph;
+
+double oc_renergy(const oc_rgraph* g, const int8_t* s) {
+    double e = 0.0;
+    for (uint32_t i = 0; i < g->n; ++i)
+        for (uint32_t k = g->rowptr[i]; k < g->rowptr[i + 1]; ++k) {
+            uint32_t j = g->col[k];
+            if (j > i) e -= g->J[k] * (double)(s[i] * s[j]);
+        }
+    for (uint32_t i = 0; i < g->n; ++i) e -= g->h[i] * (double)s[i];
+    return e;
+}
+
+double oc_rlocal_field(const oc_rgraph* g, const int8_t* s, uint32_t i) {
+    double l = g->h[i];
+    for (uint32_t k = g->rowptr[i]; k < g->rowptr[i + 1]; ++k) l += g->J[k] * (double)s[g->col[k]];
+    return l;
+}
+
+/* One sweep over `order` (n_free sites); site i takes draw draw_base + rank[i] + 1. */
+double oc_rsweep(const oc_rgraph* g, const uint32_t* order, int8_t* s, double beta, uint64_t s0, uint64_t draw_base) {
+    double delta = 0.0;
+    for (uint32_t q = 0; q < g->n_free; ++q) {
+        uint32_t i = order[q];
+        double l = oc_rlocal_field(g, s, i);
+        uint64_t x = oc_draw(s0, draw_base + g->rank[i] + 1);
+        int8_t next = oc_uniform(x) < oc_conditional_up(beta, l) ? 1 : -1;
+        if (next != s[i]) {
+            delta += 2.0 * (double)s[i] * l;
+            s[i] = next;
+        }
+    }
+    return delta;
+}
+
+/* gibbs_update (mcmc.cpp:24-28): one site, the stream's next draw (draw 1 of s0). */
+int8_t oc_rupdate(const oc_rgraph* g, const int8_t* s, uint32_t i, double beta, uint64_t s0) {
+    double l = oc_rlocal_field(g, s, i);
+    return oc_uniform(oc_draw(s0, 1)) < oc_conditional_up(beta, l) ? 1 : -1;
+}
+
+void oc_rpt_init(const oc_rgraph* g, int R, uint64_t seed, uint64_t gid, int8_t* spins, double* E) {
+    for (int r = 0; r < R; ++r) {
+        int8_t* s = spins + (size_t)r * g->n;
+        uint64_t s0 = oc_stream_init(seed, gid, (uint64_t)r);
+        for (uint32_t i = 0; i < g->n; ++i) s[i] = (oc_draw(s0, (uint64_t)i + 1) >> 63) ? 1 : -1;
+        for (uint32_t i = 0; i < g->n; ++i)
+            if (g->clamp[i]) s[i] = g->clamp[i];
+        E[r] = oc_renergy(g, s);
+    }
+}
+
+void oc_rpt_sweep_all(const oc_rgraph* g, const uint32_t* order, int R, const double* beta, uint64_t seed,
+                      uint64_t gid, uint64_t t, int8_t* spins, double* E) {
+    for (int r = 0; r < R; ++r) {
+        uint64_t s0 = oc_stream_replica(seed, gid, (uint64_t)r);
+        E[r] += oc_rsweep(g, order, spins + (size_t)r * g->n, beta[r], s0, t * (uint64_t)g->n_free);
+    }
+}
+
+void oc_rpt_swap_pass(int R, const double* beta, uint64_t seed, uint64_t gid, uint64_t p, int parity, int8_t* spins,
+                      size_t n, double* E, uint64_t* att, uint64_t* acc, uint8_t* dec) {
+    uint64_t c0 = oc_stream_coord(seed, gid);
+    int8_t* tmp = (int8_t*)malloc(n ? n : 1);
+    if (dec)
+        for (int r = 0; r + 1 < R; ++r) dec[r] = 0;
+    for (int r = parity; r + 1 < R; r += 2) {
+        uint64_t x = oc_draw(c0, p * (uint64_t)R + (uint64_t)r + 1);
+        int accept = oc_uniform(x) < exp((beta[r + 1] - beta[r]) * (E[r + 1] - E[r]));
+        if (att) att[r] += 1;
+        if (accept) {
+            if (acc) acc[r] += 1;
+            memcpy(tmp, spins + (size_t)r * n, n);
+            memcpy(spins + (size_t)r * n, spins + (size_t)(r + 1) * n, n);
+            memcpy(spins + (size_t)(r + 1) * n, tmp, n);
+            double e = E[r];
+            E[r] = E[r + 1];
+            E[r + 1] = e;
+        }
+        if (dec) dec[r] = (uint8_t)(accept ? 1 : 2);
+    }
+    free(tmp);
+}
+
+void oc_rpt_inject(int R, const double* beta, uint64_t seed, uint64_t gid, uint64_t round, const uint8_t* mask,
+                   const int8_t* props, const double* Eprop, int8_t* spins, size_t n, double* E, uint64_t* att,
+                   uint64_t* acc, uint8_t* dec) {
+    uint64_t a0 = oc_stream_accept(seed, gid, round);
+    for (int r = 0; r < R; ++r) {
+        if (dec) dec[r] = 0;
+        if (!mask[r]) continue;
+        uint64_t x = oc_draw(a0, (uint64_t)r + 1);
+        int accept = oc_uniform(x) < exp(beta[r] * (E[r] - Eprop[r]));
+        if (att) att[r] += 1;
+        if (accept) {
+            if (acc) acc[r] += 1;
+            memcpy(spins + (size_t)r * n, props + (size_t)r * n, n);
+            E[r] = Eprop[r];
+        }
+        if (dec) dec[r] = (uint8_t)(accept ? 1 : 2);
+    }
+}
+
+void oc_rpt_synthetic_proposals(const oc_rgraph* g, const uint32_t* order, int R, const double* beta,
+                                const double* m_bias, uint64_t seed, uint64_t gid, uint64_t round,
+                                const uint8_t* mask, int refine, int8_t* props, double* Eprop) {
+    for (int r = 0; r < R; ++r) {
+        if (!mask[r]) continue;
+        int8_t* s = props + (size_t)r * g->n;
+        uint64_t q = oc_stream_proposal(seed, gid, (uint64_t)r, round);
+        double sign = (oc_draw(q, 1) >> 63) ? 1.0 : -1.0;
+        double p_up = (1.0 + sign * m_bias[r]) / 2.0;
+        for (uint32_t i = 0; i < g->n; ++i) s[i] = oc_uniform(oc_draw(q, (uint64_t)i + 2)) < p_up ? 1 : -1;
+        for (uint32_t i = 0; i < g->n; ++i)
+            if (g->clamp[i]) s[i] = g->clamp[i];
+        for (int m = 0; m < refine; ++m)
+            oc_rsweep(g, order, s, beta[r], q, (uint64_t)g->n + 1 + (uint64_t)m * g->n_free);
+        Eprop[r] = oc_renergy(g, s);
+    }
+}

@@ -117,6 +117,7 @@ _SIGS = {
     "tapt_ensemble_set_stream": (C.c_int, [_vp, _vp]),
     "tapt_ensemble_synchronize": (C.c_int, [_vp]),
     "tapt_ensemble_kernel": (C.c_char_p, [_vp]),
+    "tapt_ensemble_launch_log": (C.c_int, [_vp, C.c_char_p, C.c_size_t]),
     "tapt_ensemble_set_bond_signs": (C.c_int, [_vp, _i8p, C.c_size_t]),
     "tapt_ensemble_generate_ea_disorder": (C.c_int, [_vp, C.c_uint64]),
     "tapt_ensemble_get_bond_signs": (C.c_int, [_vp, _i8p, C.c_size_t]),
@@ -142,6 +143,7 @@ _SIGS = {
     "tapt_run": (C.c_int, [_vp, C.POINTER(Schedule)]),
     "tapt_inject_proposals": (C.c_int, [_vp, _vp, C.c_int, _u32p, C.c_uint32, _f64p, _f64p, _u8p]),
     "tapt_inject_proposals_packed": (C.c_int, [_vp, _vp, C.c_int, _u32p, C.c_uint32, _u8p]),
+    "tapt_inject_proposals_packed_refined": (C.c_int, [_vp, _vp, C.c_int, _u32p, C.c_uint32, C.c_uint32, _u8p]),
     "tapt_generate_proposals": (C.c_int, [_vp, _u32p, C.c_uint32, _f64p, C.c_uint32, _u8p]),
     "tapt_problem_last_error": (C.c_char_p, []),
     "tapt_multiplier_spins": (C.c_uint32, [C.c_uint32]),
@@ -334,6 +336,13 @@ class Ensemble:
         self.close()
 
     # -- setup
+    def launch_log(self):
+        """Distinct sweep-kernel instantiations launched so far (template arguments; ' balanced M=k'
+        when the persistent McNaughton grid ran)."""
+        buf = C.create_string_buffer(8192)
+        _check(lib().tapt_ensemble_launch_log(self._h, buf, len(buf)))
+        return [x for x in buf.value.decode().split("\n") if x]
+
     def set_stream(self, cuda_stream_ptr):
         _check(lib().tapt_ensemble_set_stream(self._h, cuda_stream_ptr))
 
@@ -449,8 +458,17 @@ class Ensemble:
     def inject_proposals(self, proposals, targets, log_q_cur=None, log_q_prop=None, device_ptr=None):
         t = np.ascontiguousarray(targets, np.uint32)
         acc = np.zeros((self.I, len(t)), np.uint8)
-        lqc = None if log_q_cur is None else np.ascontiguousarray(log_q_cur, np.float64)
-        lqp = None if log_q_prop is None else np.ascontiguousarray(log_q_prop, np.float64)
+        if (log_q_cur is None) != (log_q_prop is None):
+            raise ConfigError("log_q_cur and log_q_prop must be given together (mh_corrected_move)")
+        lqc = lqp = None
+        if log_q_cur is not None:  # the C ABI reads I x len(targets) doubles from each
+            lqc = np.ascontiguousarray(log_q_cur, np.float64)
+            lqp = np.ascontiguousarray(log_q_prop, np.float64)
+            for name, v in (("log_q_cur", lqc), ("log_q_prop", lqp)):
+                if v.size != self.I * len(t):
+                    raise DimensionError(f"{name} has {v.size} entries, expected n_instances x n_targets = "
+                                         f"{self.I} x {len(t)}")
+            lqc, lqp = lqc.reshape(self.I, len(t)), lqp.reshape(self.I, len(t))
         if device_ptr is not None:
             _check(lib().tapt_inject_proposals(self._h, device_ptr, 1, _p(t, _u32p), len(t), _p(lqc, _f64p),
                                                _p(lqp, _f64p), _p(acc, _u8p)))
@@ -460,14 +478,23 @@ class Ensemble:
                                                _p(lqp, _f64p), _p(acc, _u8p)))
         return acc
 
-    def inject_proposals_packed(self, packed, targets, device_ptr=None):
+    def inject_proposals_packed(self, packed, targets, device_ptr=None, refine=0, return_accepted=True):
+        """Bit-packed proposals [I][n_targets][ceil(n/8)] (host array, or device_ptr); refine > 0 runs
+        that many heat-bath sweeps of each proposal at its target's beta before Eq. 2."""
         t = np.ascontiguousarray(targets, np.uint32)
-        acc = np.zeros((self.I, len(t)), np.uint8)
+        acc = np.zeros((self.I, len(t)), np.uint8) if return_accepted else None
         if device_ptr is not None:
-            _check(lib().tapt_inject_proposals_packed(self._h, device_ptr, 1, _p(t, _u32p), len(t), _p(acc, _u8p)))
+            src, on_dev = device_ptr, 1
         else:
             p = np.ascontiguousarray(packed, np.uint8)
-            _check(lib().tapt_inject_proposals_packed(self._h, p.ctypes.data, 0, _p(t, _u32p), len(t), _p(acc, _u8p)))
+            if p.size != self.I * len(t) * ((self.n + 7) // 8):
+                raise DimensionError("packed proposals must be [n_instances][n_targets][ceil(n/8)]")
+            src, on_dev = p.ctypes.data, 0
+        if refine:
+            _check(lib().tapt_inject_proposals_packed_refined(self._h, src, on_dev, _p(t, _u32p), len(t), int(refine),
+                                                              _p(acc, _u8p)))
+        else:
+            _check(lib().tapt_inject_proposals_packed(self._h, src, on_dev, _p(t, _u32p), len(t), _p(acc, _u8p)))
         return acc
 
     def generate_proposals(self, targets, m_bias=None, refine=5, return_accepted=True):

@@ -33,6 +33,7 @@
 namespace tapt_dev {
 cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st);
 int k1_resident_units(const PTArgs& a, const LatDims& d, int threads, bool cluster);
+void k1_variant_name(const PTArgs& a, const LatDims& d, int threads, bool cluster, char* out);
 int k2_resident_units(const PTArgs& a, const CsrArgs& g, int threads, bool cluster);
 struct Csr3 {
     const uint4* meta;
@@ -726,6 +727,7 @@ struct tapt_ensemble_s {
     bool have_disorder = false;
     uint32_t launch_chunk = 2000;
     bool swap_oversize = false, prop_oversize = false;  // exact tables too large for this ladder
+    bool ladder_unordered = false;  // set_betas accepted a decreasing neighbour pair: swaps refused
 
     DevBuf<uint32_t> words;
     DevBuf<int32_t> E;
@@ -812,18 +814,37 @@ struct tapt_ensemble_s {
         return nt;
     }
 
+    // Distinct sweep-kernel instantiations this ensemble launched ("name" or "name balanced M=<units>"),
+    // in first-launch order: test evidence of which code path ran (tapt_ensemble_launch_log).
+    std::vector<std::string> launch_log;
+    void log_launch(std::string name, const PTArgs& a) {
+        if (a.sched) name += " balanced M=" + std::to_string(a.sched_clusters);
+        if (std::find(launch_log.begin(), launch_log.end(), name) == launch_log.end() && launch_log.size() < 64)
+            launch_log.push_back(std::move(name));
+    }
+
     void launch(const PTArgs& a, bool cluster, int k1_nt = 0) {
         ++g_launches;
         cudaError_t e;
         if (use_k1) {
-            e = launch_k1(a, m->ld, k1_nt > 0 ? k1_nt : k1_threads, cluster, stream);
+            const int nt = k1_nt > 0 ? k1_nt : k1_threads;
+            char name[96];
+            k1_variant_name(a, m->ld, nt, cluster, name);
+            log_launch(name, a);
+            e = launch_k1(a, m->ld, nt, cluster, stream);
         } else if (!a.energy_only && a.G == 1 && k3_eligible()) {
+            log_launch("k3_bitcsr_pt<" + std::string(a.sched ? "1," : "0,") + std::to_string(k3_ipb) + ">", a);
             e = launch_k3(a, k3_args(), k3_ipb, stream);
         } else if (!a.energy_only && a.G == 1 && k4_eligible()) {
+            log_launch(std::string("k4_levels_pt<") + (a.sched ? "1>" : "0>"), a);
             e = launch_k4(a, csr_args(true), k4_ipb, stream);
         } else {
+            log_launch(std::string("k2_csr_pt") + (cluster ? "<cluster>" : ""), a);
             e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster, stream);
         }
+        if (e == cudaErrorCooperativeLaunchTooLarge)
+            throw tapt::CudaError("balanced sweep schedule: the persistent grid cannot be co-resident on this "
+                                  "device (cooperative launch refused); set TAPT_BALANCE=0");
         if (e != cudaSuccess) throw tapt::CudaError(std::string("sweep kernel launch: ") + cudaGetErrorString(e));
         CUDA_OK(cudaGetLastError());
     }
@@ -918,6 +939,9 @@ struct tapt_ensemble_s {
         if (swap_every && R < 2) swap_every = 0;
         if (swap_every && swap_oversize)
             throw tapt::ConfigError("beta spacing too fine for exact swap tables (adjacent betas closer than ~1e-5)");
+        if (swap_every && ladder_unordered)
+            throw tapt::ConfigError("replica swaps need a non-decreasing beta ladder (SPEC.md:388); the "
+                                    "current ladder (set with allow_flat=2) has a decreasing neighbour pair");
         const bool cluster = G > 1;
         uint32_t done = 0;
         while (done < n_sweeps) {
@@ -1372,8 +1396,13 @@ tapt_status tapt_ensemble_set_betas(tapt_ensemble_t e, const double* betas, int 
             if (r && !(betas[r] > betas[r - 1]) && !(allow_flat == 1 && betas[r] >= betas[r - 1]) && allow_flat != 2)
                 throw tapt::ConfigError("beta ladder must be strictly increasing (SPEC.md:388)");
         }
+        // Eq. 1 with equal neighbours accepts every swap (exp(0) = 1), which the c = 0 rows do; a
+        // decreasing pair would need exp(c dE) with c < 0, which the tables clamp to "always"
+        bool decreasing = false;
+        for (int r = 1; r < e->R; ++r) decreasing = decreasing || betas[r] < betas[r - 1];
         CUDA_OK(cudaStreamSynchronize(e->stream));
         e->betas.assign(betas, betas + e->R);
+        e->ladder_unordered = decreasing;
         e->build_tables();
         sync_if(e->stream);
     });
@@ -1439,6 +1468,17 @@ tapt_status tapt_ensemble_synchronize(tapt_ensemble_t e) {
         check_ens(e);
         e->poll_sched(true);
         CUDA_OK(cudaStreamSynchronize(e->stream));
+    });
+}
+
+tapt_status tapt_ensemble_launch_log(tapt_ensemble_t e, char* buf, size_t cap) {
+    return guard([&] {
+        check_ens(e);
+        if (!buf || cap == 0) throw tapt::ConfigError("null buffer");
+        std::string all;
+        for (const auto& s : e->launch_log) all += s + "\n";
+        if (all.size() + 1 > cap) throw tapt::SizeError("launch log buffer too small");
+        std::memcpy(buf, all.c_str(), all.size() + 1);
     });
 }
 
@@ -1732,6 +1772,9 @@ tapt_status tapt_swap_pass(tapt_ensemble_t e, int parity) {
         check_ens(e);
         if (parity != 0 && parity != 1) throw tapt::ConfigError("parity must be 0 or 1");
         if (e->swap_oversize) throw tapt::ConfigError("beta spacing too fine for exact swap tables");
+        if (e->ladder_unordered)
+            throw tapt::ConfigError("replica swaps need a non-decreasing beta ladder (SPEC.md:388); the "
+                                    "current ladder (set with allow_flat=2) has a decreasing neighbour pair");
         if (e->R >= 2) {
             ++g_launches;
             k_swap_pass<<<e->I, std::max(32, (e->R / 2 + 31) / 32 * 32), 0, e->stream>>>(
@@ -1886,26 +1929,93 @@ tapt_status tapt_inject_proposals(tapt_ensemble_t e, const int8_t* proposals, in
     });
 }
 
-tapt_status tapt_inject_proposals_packed(tapt_ensemble_t e, const uint8_t* proposals, int on_device,
-                                         const uint32_t* targets, uint32_t T, uint8_t* accepted) {
-    return guard([&] {
-        check_ens(e);
-        prepare_targets(e, targets, T);
-        const int n = e->n(), nb = (n + 7) / 8;
-        const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
-        const uint8_t* src = proposals;
-        if (!on_device) {
-            e->pbytes.upload(proposals, (size_t)e->I * T * nb, e->stream);
-            src = e->pbytes.p;
+// The refinement sweeps of a proposal round (BASELINE.json configs[1], configs[4]: M Gibbs sweeps of each
+// proposal at its target's beta before Eq. 2): the proposal groups [I][GT][n] are swept by the sweep
+// kernel with the round's slot streams derive(seed,{kReplica,g,r,q+1}) (e->pfull), draws offset past the
+// n + 1 generator draws.  Leaves exact proposal energies in e->pE.  Returns whether it ran.
+static bool refine_proposals(tapt_ensemble_s* e, uint32_t T, uint32_t refine) {
+    if (!refine) return false;
+    const int n = e->n();
+    const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
+    PTArgs a = e->base_args();
+    a.words = e->pwords.p;
+    a.G = GT;
+    a.W = WT;
+    a.B = (int)T;
+    a.streams = e->pfull.p;
+    a.slot_of = e->pslot.p;
+    a.buf_of = nullptr;
+    a.E = e->pE.p;
+    a.draw_base = (uint64_t)n + 1;
+    a.t0 = 0;
+    a.n_sweeps = (int)refine;
+    a.swap_every = 0;
+    a.measure_every = 0;
+    a.best = nullptr;
+    if (!e->use_k1) {  // K2 tracks energies incrementally: seed them
+        CsrArgs g = e->csr_args(false);
+        ++g_launches;
+        k_energy_csr<<<dim3(GT, e->I), 256, 0, e->stream>>>(e->pwords.p, n, GT, WT, (int)T, g.rowptr, g.col, g.J,
+                                                             g.nJ, g.nnz, g.h, e->pE.p);
+        CUDA_OK(cudaGetLastError());
+    }
+    // refinement sweeps of the proposal groups: I x GT CTAs of their own; when they exceed the SMs
+    // but fit two 256-thread CTAs per SM, one wave of those beats two of 512-thread CTAs
+    // (config 2: 128 x 2 groups)
+    int nt = 0;
+    if (e->use_k1 && e->k1_threads == 512 && k1_smem_bytes(n, true, e->R) <= 100 * 1024) {
+        int dev = 0, nsm = 148;
+        CUDA_OK(cudaGetDevice(&dev));
+        CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        const long long ctas = (long long)e->I * GT;
+        if (ctas > nsm && ctas <= 2ll * nsm) nt = 256;
+    }
+    e->launch(a, false, nt);
+    return true;
+}
+
+static void inject_packed(tapt_ensemble_t e, const uint8_t* proposals, int on_device, const uint32_t* targets,
+                          uint32_t T, uint32_t refine, uint8_t* accepted) {
+    check_ens(e);
+    prepare_targets(e, targets, T);
+    const int n = e->n(), nb = (n + 7) / 8;
+    const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
+    const uint8_t* src = proposals;
+    if (!on_device) {
+        e->pbytes.upload(proposals, (size_t)e->I * T * nb, e->stream);
+        src = e->pbytes.p;
+    }
+    ++g_launches;
+    k_set_packed<<<dim3((n + 255) / 256, GT, e->I), 256, 0, e->stream>>>(e->pwords.p, n, GT, WT, (int)T, src, (int)T,
+                                                                         e->clamp_ptr(), e->clamp_count());
+    CUDA_OK(cudaGetLastError());
+    if (refine) {  // the round's slot streams for the refinement sweeps
+        e->pstreams.alloc((size_t)e->I * T);
+        if (e->pfull.n != (size_t)e->I * e->R) {
+            e->pfull.alloc((size_t)e->I * e->R);
+            e->pfull.zero(e->stream);
         }
         ++g_launches;
-        k_set_packed<<<dim3((n + 255) / 256, GT, e->I), 256, 0, e->stream>>>(e->pwords.p, n, GT, WT, (int)T, src, (int)T,
-                                                                             e->clamp_ptr(), e->clamp_count());
+        k_derive_round_streams<<<e->I, 64, 0, e->stream>>>(e->seed, e->gid0, e->ptargets.p, (int)T, e->R, e->Q + 1,
+                                                           e->pstreams.p, e->pfull.p, nullptr);
         CUDA_OK(cudaGetLastError());
-        finish_proposals(e, targets, T, false, nullptr, nullptr, accepted);
-        if (!on_device) sync_if(e->stream);  // the caller's host buffer (possibly pinned) is free on return
-    });
+    }
+    const bool have_E = refine_proposals(e, T, refine);
+    finish_proposals(e, targets, T, have_E, nullptr, nullptr, accepted);
+    if (!on_device) sync_if(e->stream);  // the caller's host buffer (possibly pinned) is free on return
 }
+
+tapt_status tapt_inject_proposals_packed(tapt_ensemble_t e, const uint8_t* proposals, int on_device,
+                                         const uint32_t* targets, uint32_t T, uint8_t* accepted) {
+    return guard([&] { inject_packed(e, proposals, on_device, targets, T, 0, accepted); });
+}
+
+tapt_status tapt_inject_proposals_packed_refined(tapt_ensemble_t e, const uint8_t* proposals, int on_device,
+                                                 const uint32_t* targets, uint32_t T, uint32_t refine,
+                                                 uint8_t* accepted) {
+    return guard([&] { inject_packed(e, proposals, on_device, targets, T, refine, accepted); });
+}
+
 
 tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, uint32_t T, const double* m_bias,
                                     uint32_t refine, uint8_t* accepted) {
@@ -1936,44 +2046,7 @@ tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, 
         k_gen_proposals<<<dim3((n + 255) / 256, GT, e->I), 256, 0, e->stream>>>(
             e->pwords.p, n, GT, WT, (int)T, e->pstreams.p, e->ptup.p, e->clamp_ptr(), e->clamp_count());
         CUDA_OK(cudaGetLastError());
-        bool have_E = false;
-        if (refine) {
-            PTArgs a = e->base_args();
-            a.words = e->pwords.p;
-            a.G = GT;
-            a.W = WT;
-            a.B = (int)T;
-            a.streams = e->pfull.p;
-            a.slot_of = e->pslot.p;
-            a.buf_of = nullptr;
-            a.E = e->pE.p;
-            a.draw_base = (uint64_t)n + 1;
-            a.t0 = 0;
-            a.n_sweeps = (int)refine;
-            a.swap_every = 0;
-            a.measure_every = 0;
-            a.best = nullptr;
-            if (!e->use_k1) {  // K2 tracks energies incrementally: seed them
-                CsrArgs g = e->csr_args(false);
-                ++g_launches;
-                k_energy_csr<<<dim3(GT, e->I), 256, 0, e->stream>>>(e->pwords.p, n, GT, WT, (int)T, g.rowptr, g.col,
-                                                                     g.J, g.nJ, g.nnz, g.h, e->pE.p);
-                CUDA_OK(cudaGetLastError());
-            }
-            // refinement sweeps of the proposal groups: I x GT CTAs of their own; when they exceed the SMs
-            // but fit two 256-thread CTAs per SM, one wave of those beats two of 512-thread CTAs
-            // (config 2: 128 x 2 groups)
-            int nt = 0;
-            if (e->use_k1 && e->k1_threads == 512 && k1_smem_bytes(n, true, e->R) <= 100 * 1024) {
-                int dev = 0, nsm = 148;
-                CUDA_OK(cudaGetDevice(&dev));
-                CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
-                const long long ctas = (long long)e->I * GT;
-                if (ctas > nsm && ctas <= 2ll * nsm) nt = 256;
-            }
-            e->launch(a, false, nt);
-            have_E = true;
-        }
+        const bool have_E = refine_proposals(e, T, refine);
         finish_proposals(e, targets, T, have_E, nullptr, nullptr, accepted);
     });
 }

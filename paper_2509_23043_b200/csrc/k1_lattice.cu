@@ -481,7 +481,8 @@ size_t k1_smem_bytes(int n, bool dis, int R) {
 // resident != null: report how many clusters (or CTAs, without a cluster) of this launch shape
 // are co-resident on the device instead of launching.
 template <int DIM, bool DIS, bool CLU>
-static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st, int* resident) {
+static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st, int* resident,
+                               char* name) {
     const size_t smem = k1_smem_bytes(a.n, DIS, a.R);
     // SP = 1 site word per thread-iteration at 1024 threads, else 2 interleaved at <= 512
     // launch shapes: 2 interleaved site words per thread-iteration at <= 512 threads (default),
@@ -489,14 +490,29 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
     const bool bulk = (a.n & 15) == 0 && a.n >= 16384;
     constexpr bool NAR3 = DIM == 2;  // 3D: narrow decision paths only in the narrow-group instantiations
     const bool narrow = a.W < kW;
-    auto fn = threads > 768                     ? k1_lattice_pt<DIM, DIS, CLU, 1, 1024>
-              : threads > 512                   ? k1_lattice_pt<DIM, DIS, CLU, 2, 768>
-              : threads > 256 && narrow         ? k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, true>
-              : threads > 256 && bulk           ? k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, true, NAR3>
-              : threads > 256                   ? k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, NAR3>
-              : threads == 256 && narrow        ? k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2, false, true>
-              : threads == 256                  ? k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2, false, NAR3>
-                                                : k1_lattice_pt<DIM, DIS, CLU, 4, 256>;
+    // (SP, MAXT, MINB, BULK, NAR) of the instantiation this launch shape selects
+    const int pick = threads > 768                ? 0
+                     : threads > 512              ? 1
+                     : threads > 256 && narrow    ? 2
+                     : threads > 256 && bulk      ? 3
+                     : threads > 256              ? 4
+                     : threads == 256 && narrow   ? 5
+                     : threads == 256             ? 6
+                                                  : 7;
+    static const int shape[8][5] = {{1, 1024, 1, 0, 1}, {2, 768, 1, 0, 1},   {2, 512, 1, 0, 1}, {2, 512, 1, 1, NAR3},
+                                    {2, 512, 1, 0, NAR3}, {2, 256, 2, 0, 1}, {2, 256, 2, 0, NAR3}, {4, 256, 1, 0, 1}};
+    static void (*const table[8])(const PTArgs, const LatDims) = {
+        k1_lattice_pt<DIM, DIS, CLU, 1, 1024>,          k1_lattice_pt<DIM, DIS, CLU, 2, 768>,
+        k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, true>, k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, true, NAR3>,
+        k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, NAR3>, k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2, false, true>,
+        k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2, false, NAR3>, k1_lattice_pt<DIM, DIS, CLU, 4, 256>};
+    auto fn = table[pick];
+    if (name) {
+        const int* v = shape[pick];
+        snprintf(name, 96, "k1_lattice_pt<%d,%d,%d,%d,%d,%d,%d,%d>", DIM, (int)DIS, (int)CLU, v[0], v[1], v[2], v[3],
+                 v[4]);
+        return cudaSuccess;
+    }
     cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     cudaLaunchConfig_t cfg = {};
@@ -522,28 +538,34 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
         *resident = per_sm * nsm;
         return q;
     }
-    return cudaLaunchKernelEx(&cfg, fn, a, d);
+    return pt_launch(fn, cfg.gridDim.x, (unsigned)threads, smem, st, CLU ? (unsigned)a.G : 1u, a.sched != nullptr, a, d);
 }
 
 static cudaError_t k1_dispatch(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st,
-                               int* resident) {
+                               int* resident, char* name = nullptr) {
     const bool dis = a.bonds != nullptr;
     if (d.dim == 2) {
         if (dis)
-            return cluster ? launch_k1_t<2, true, true>(a, d, threads, st, resident)
-                           : launch_k1_t<2, true, false>(a, d, threads, st, resident);
-        return cluster ? launch_k1_t<2, false, true>(a, d, threads, st, resident)
-                       : launch_k1_t<2, false, false>(a, d, threads, st, resident);
+            return cluster ? launch_k1_t<2, true, true>(a, d, threads, st, resident, name)
+                           : launch_k1_t<2, true, false>(a, d, threads, st, resident, name);
+        return cluster ? launch_k1_t<2, false, true>(a, d, threads, st, resident, name)
+                       : launch_k1_t<2, false, false>(a, d, threads, st, resident, name);
     }
     if (dis)
-        return cluster ? launch_k1_t<3, true, true>(a, d, threads, st, resident)
-                       : launch_k1_t<3, true, false>(a, d, threads, st, resident);
-    return cluster ? launch_k1_t<3, false, true>(a, d, threads, st, resident)
-                   : launch_k1_t<3, false, false>(a, d, threads, st, resident);
+        return cluster ? launch_k1_t<3, true, true>(a, d, threads, st, resident, name)
+                       : launch_k1_t<3, true, false>(a, d, threads, st, resident, name);
+    return cluster ? launch_k1_t<3, false, true>(a, d, threads, st, resident, name)
+                   : launch_k1_t<3, false, false>(a, d, threads, st, resident, name);
 }
 
 cudaError_t launch_k1(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st) {
     return k1_dispatch(a, d, threads, cluster, st, nullptr);
+}
+
+// Name of the instantiation (template arguments) a launch with these arguments selects.
+void k1_variant_name(const PTArgs& a, const LatDims& d, int threads, bool cluster, char* out) {
+    out[0] = 0;
+    k1_dispatch(a, d, threads, cluster, nullptr, nullptr, out);
 }
 
 // Co-resident clusters (cluster launches) or CTAs of the K1 launch shape (balanced schedule).

@@ -338,7 +338,8 @@ static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, i
         *resident = per_sm * nsm;
         return q;
     }
-    return cudaLaunchKernelEx(&cfg, fn, a, g, ipb);
+    return pt_launch(fn, cfg.gridDim.x, (unsigned)threads, smem, st, CLU ? (unsigned)a.G : 1u, a.sched != nullptr, a, g,
+                     ipb);
 }
 
 // Instances per CTA when one CTA holds a whole instance (G == 1, no cluster): 2 measured best

@@ -438,10 +438,8 @@ static cudaError_t k3_run_t(const PTArgs& a, const Csr3& g, cudaStream_t st, int
         return e;
     }
     const unsigned grid = a.sched ? (unsigned)((a.sched_clusters + IPB - 1) / IPB) : (unsigned)((a.I + IPB - 1) / IPB);
-    if (a.sched)
-        k3_bitcsr_pt<true, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
-    else
-        k3_bitcsr_pt<false, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
+    if (a.sched) return pt_launch(k3_bitcsr_pt<true, IPB>, grid, kT3 * IPB, smem, st, 1u, true, a, g);
+    k3_bitcsr_pt<false, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
     return cudaGetLastError();
 }
 

@@ -159,10 +159,8 @@ static cudaError_t k4_run(const PTArgs& a, const CsrArgs& g, int ipb, cudaStream
         return e;
     }
     const unsigned grid = a.sched ? (unsigned)((a.sched_clusters + ipb - 1) / ipb) : (unsigned)((a.I + ipb - 1) / ipb);
-    if (a.sched)
-        k4_levels_pt<true><<<grid, kT4 * ipb, smem, st>>>(a, g);
-    else
-        k4_levels_pt<false><<<grid, kT4 * ipb, smem, st>>>(a, g);
+    if (a.sched) return pt_launch(k4_levels_pt<true>, grid, kT4 * ipb, smem, st, 1u, true, a, g);
+    k4_levels_pt<false><<<grid, kT4 * ipb, smem, st>>>(a, g);
     return cudaGetLastError();
 }
 

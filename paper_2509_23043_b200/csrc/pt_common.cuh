@@ -6,6 +6,7 @@
 #include <cooperative_groups.h>
 
 #include <type_traits>
+#include <utility>
 
 #include "kernels.h"
 
@@ -193,6 +194,37 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
         }
         tm.sync();
     }
+}
+
+// Launch a fused PT kernel: optional thread-block cluster of `cluster_x` CTAs; balanced persistent
+// grids (`coop`) launch with the cooperative attribute, so the runtime either makes every CTA of the
+// grid co-resident (gang scheduling, whatever else holds SMs) or refuses the launch
+// (cudaErrorCooperativeLaunchTooLarge) -- a split job's flag wait can therefore never starve.
+template <class... KArgs, class... Args>
+__host__ cudaError_t pt_launch(void (*fn)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
+                               unsigned cluster_x, bool coop, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (cluster_x > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = cluster_x;
+        attr[na].val.clusterDim.y = 1;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (coop) {
+        attr[na].id = cudaLaunchAttributeCooperative;
+        attr[na].val.cooperative = 1;
+        ++na;
+    }
+    cfg.attrs = na ? attr : nullptr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
 }
 
 // Balanced schedule (SchedItem): wait for / publish the state of a split job.  The wait is

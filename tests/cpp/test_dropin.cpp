@@ -127,6 +127,28 @@ static int cpu_tests() {
         CHECK(f2.config().max_sequence_length == gc.max_sequence_length && f2.prefix_length() == 0);
         CHECK(throws<DimensionError>([&] { IsingFormer(gl, gc, ParameterSet(10)); }));
     }
+    // residual_energy: mean over runs of the coldest replica's energy, minus E_gnd, / N
+    {
+        auto chain = [](double e_cold, double e_best) {
+            RunTrace t;
+            t.energies = {{0.0, 5.0, e_cold}, {1.0, e_cold}};
+            t.best_energy = {e_best, e_best};
+            return t;
+        };
+        const double eg = -9.0;  // open ferromagnetic chain, N = 10 spins, J = 1: E_gnd = -9
+        auto r0 = residual_energy(chain(eg, eg), eg, 10);
+        CHECK(r0.size() == 2 && r0[0] == 0.0 && r0[1] == 0.0);                 // trace at the ground state
+        auto r1 = residual_energy(chain(eg + 2.0, eg + 2.0), eg, 10);          // one excited bond, dE = 2J
+        CHECK(std::fabs(r1[0] - 0.2) < 1e-15 && std::fabs(r1[1] - 0.2) < 1e-15);
+        auto r2 = residual_energy(std::vector<RunTrace>{chain(eg, eg), chain(eg + 4.0, eg + 4.0)}, eg, 10);
+        CHECK(std::fabs(r2[0] - 0.2) < 1e-15);                                 // mean over runs
+        auto r3 = residual_energy(std::vector<RunTrace>{chain(eg + 4.0, eg)}, eg, 10, true);
+        CHECK(r3[0] == 0.0);                                                   // best-so-far variant
+        RunTrace shorter = chain(eg, eg);
+        shorter.energies.pop_back();
+        CHECK(throws<DimensionError>([&] { residual_energy(std::vector<RunTrace>{chain(eg, eg), shorter}, eg, 10); }));
+        CHECK(throws<ConfigError>([&] { residual_energy(std::vector<RunTrace>{}, eg, 10); }));
+    }
     std::printf("cpu ok\n");
     return 0;
 }
@@ -235,6 +257,57 @@ static int gpu_tests() {
     auto al = adaptive_ladder(g, 0.2, 1.0, 0.5, 50, 1);
     for (std::size_t r = 1; r < al.betas.size(); ++r) CHECK(al.betas[r] > al.betas[r - 1]);
     CHECK(al.betas.front() == 0.2 && al.betas.back() == 1.0);
+    // adaptive_ladder's SPEC.md:447-449 examples, measured with run_pt on the ladder it returns
+    auto pair_acceptance = [](const CouplingGraph& gg, const BetaLadder& lad, std::uint64_t moves) {
+        TAPTConfig c;
+        c.n_swap = moves;
+        c.M = 1;
+        c.seed = 21;
+        auto t = run_pt(gg, lad, c);
+        std::vector<double> acc;
+        for (std::size_t r = 0; r + 1 < lad.betas.size(); ++r)
+            acc.push_back(double(t.swap_accepts[r]) / double(std::max<std::uint64_t>(t.swap_attempts[r], 1)));
+        return acc;
+    };
+    {  // zero-coupling graph (E constant): geometric fallback, still strictly increasing to beta_max
+        CouplingGraph::Builder bz(4);
+        auto z = adaptive_ladder(bz.build(), 0.1, 2.0, 0.5, 20, 3);
+        CHECK(z.betas.size() >= 3 && z.betas.front() == 0.1 && z.betas.back() == 2.0);
+        for (std::size_t r = 1; r < z.betas.size(); ++r) CHECK(z.betas[r] > z.betas[r - 1]);
+        CHECK(throws<ConfigError>([&] { adaptive_ladder(bz.build(), 0.1, 2.0, 1.0, 20, 3); }));
+        CHECK(throws<ConfigError>([&] { adaptive_ladder(bz.build(), 0.1, 2.0, 0.0, 20, 3); }));
+    }
+    {  // target 0.99 on a 3x3 ferromagnet -> dense ladder, every neighbour pair accepts >= 0.8
+        auto g3 = LatticeSpec::grid2d(3, 3).graph();
+        auto lad = adaptive_ladder(g3, 0.1, 1.0, 0.99, 4000, 5);
+        CHECK(lad.betas.size() > 10 && lad.betas.size() <= 256);
+        auto acc = pair_acceptance(g3, lad, 6000);
+        for (double a : acc) CHECK(a >= 0.8);
+    }
+    {  // target 0.3 on a 3D EA instance, L = 4 -> >= 80 % of pairs accept within [0.1, 0.6]
+        auto spec = LatticeSpec::grid3d(4, 1.0, LatticeSpec::Boundary::periodic);
+        auto base = spec.graph();
+        CouplingGraph::Builder be(base.n_spins());
+        RngStream dr(77);
+        for (const auto& c : base.couplings()) be.add_coupling(c.i, c.j, dr.coin() ? 1.0 : -1.0);
+        auto ea = be.build();
+        auto lad = adaptive_ladder(ea, 0.2, 3.0, 0.3, 4000, 6);
+        auto acc = pair_acceptance(ea, lad, 6000);
+        std::size_t ok = 0;
+        for (double a : acc) ok += (a >= 0.1 && a <= 0.6);
+        std::printf("adaptive ladder EA L=4: %zu betas, %zu/%zu pairs in [0.1,0.6]\n", lad.betas.size(), ok, acc.size());
+        CHECK(ok * 5 >= acc.size() * 4);
+        // residual energy in the best-so-far sense is non-increasing
+        TAPTConfig c;
+        c.n_swap = 300;
+        c.M = 2;
+        c.seed = 4;
+        std::vector<RunTrace> runs{run_pt(ea, lad, c)};
+        c.seed = 5;
+        runs.push_back(run_pt(ea, lad, c));
+        auto rho = residual_energy(runs, -200.0, ea.n_spins(), true);
+        for (std::size_t t = 1; t < rho.size(); ++t) CHECK(rho[t] <= rho[t - 1]);
+    }
     std::printf("gpu ok\n");
     return 0;
 }

@@ -99,3 +99,38 @@ def test_balanced_schedule_matches_oracle_on_a_split_instance():
         pt = O.PT(g, betas, 19, k, g.colour_order(O.checkerboard_colours(dims)))
         pt.run(57, 1)
         assert np.array_equal(S[k], pt.spins) and np.array_equal(E[k], pt.E)
+
+
+def test_balanced_schedule_with_a_competing_kernel(monkeypatch):
+    """Forward progress: the persistent grid launches cooperatively, so while another stream keeps
+    the SMs busy it either runs with every CTA co-resident (and stays bit-exact) or the launch is
+    refused -- it never starts half-resident and waits on a split job's flag."""
+    import torch
+    dims, betas, I = (64, 64), H.geometric(0.2, 1.0, 32), 200
+    ref = _run(monkeypatch, False, T.Model.lattice(dims), betas, I)
+    monkeypatch.setenv("TAPT_BALANCE", "1")
+    e = T.Ensemble(T.Model.lattice(dims), betas, n_instances=I, seed=17)
+    side = torch.cuda.Stream()
+    a = torch.randn(4096, 4096, device="cuda")
+    with torch.cuda.stream(side):
+        for _ in range(40):  # ~100 ms of SM work on another stream, racing the sweeps below
+            a = torch.tanh(a @ a * 1e-3)
+    e.init_random()
+    e.set_histogram(-4 * 4096, 8, 64)
+    try:
+        e.run(23, swap_every=1, measure_every=3)
+        e.generate_proposals(np.arange(8), None, refine=2)
+        e.run(41, swap_every=2, measure_every=5, measure_from=10)
+        st = _state(e)
+    except T.CudaError as err:  # refused at launch: acceptable, but it must say so
+        assert "cooperative" in str(err)
+        return
+    finally:
+        torch.cuda.synchronize()
+    assert any("balanced" in x for x in e.launch_log())
+    for x, y in zip(st, _state(ref)):
+        if isinstance(x, tuple):
+            for u, v in zip(x, y):
+                assert np.array_equal(u, v)
+        else:
+            assert np.array_equal(x, y)

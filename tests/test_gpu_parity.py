@@ -842,3 +842,113 @@ def test_tapt_rounds_with_two_proposal_groups(kernel):
     order = H.checkerboard_order((L,)) if kernel == "lattice" else H.colour_order_for(m.schedule()[0])
     pts = H.run_oracle(graphs, betas, 12, 3, order, 45, props=dict(every=15, targets=56, m_bias=np.zeros(R), refine=5))
     compare(e, pts)
+
+
+# ---------------------------------------------- the headline kernel, exact --
+
+def mcnaughton_split(I, S, M):
+    """Jobs McNaughton's wrap-around rule (engine.cu mcnaughton()) cuts between two clusters."""
+    total = I * S
+    C = -(-total // M)
+    return sorted({(k * C) // S for k in range(1, M) if k * C < total and (k * C) % S})
+
+
+def _cfg5_oracle(gids, n1, n2, seed=20250923, disorder=43):
+    betas = H.linear(0.2, 3.0, 64)
+    out = []
+    for gid in gids:
+        g = O.ea_graph((32,), disorder, gid)
+        pt = O.PT(g, betas, seed, gid, H.checkerboard_order((32,))(g))
+        pt.run(n1, 1, n1, 56, None, 5)  # n1 sweeps (swap every sweep), then one TAPT round
+        pt.run(n2, 1)
+        out.append(pt)
+    return out
+
+
+def test_cfg5_headline_kernel_bit_exact_with_oracle():
+    """bench.py's exact config-5 path at a size where every one of its code paths engages:
+    3D EA L=32 (32768 sites -> cp.async.bulk state loads), 64 slots as a 2-CTA cluster of
+    32-replica groups, more instances than co-resident clusters (-> the balanced McNaughton grid
+    with split jobs), and a TAPT round (56 fair i.i.d. proposals, 5 refinement sweeps on the
+    non-cluster bulk instantiation, Eq. 2).  Spins, energies, swap and proposal counters of the
+    first instance, a split instance and the last instance equal the oracle."""
+    L, R, I, S1, S2 = 32, 64, 160, 20, 20
+    e = T.Ensemble(T.Model.lattice((L,)), H.linear(0.2, 3.0, R), n_instances=I, seed=20250923)
+    e.generate_ea_disorder(43)
+    e.init_random()
+    e.run(S1, swap_every=1)
+    e.generate_proposals(np.arange(56, dtype=np.uint32), None, refine=5, return_accepted=False)
+    e.run(S2, swap_every=1)
+    log = e.launch_log()
+    head = [x for x in log if x.startswith("k1_lattice_pt<3,1,1,2,512,1,1,0> balanced M=")]
+    assert head, log  # the bench's instantiation (3D, disorder, cluster, bulk) on the balanced grid
+    assert any(x.startswith("k1_lattice_pt<3,1,0,2,512,1,1,0>") for x in log), log  # bulk refinement sweeps
+    M = int(head[0].split("M=")[1])
+    split = mcnaughton_split(I, S1, M)
+    assert split, (I, S1, M)
+    gids = [0, split[0], I - 1]
+    pts = _cfg5_oracle(gids, S1, S2)
+    S, E = e.spins(), e.energies()
+    sa, sc, pa, pc = e.acceptance()
+    for gid, pt in zip(gids, pts):
+        assert np.array_equal(E[gid], pt.E), gid
+        assert np.array_equal(S[gid], pt.spins), gid
+        assert np.array_equal(sc[gid], pt.swap_acc[: R - 1]), gid
+        assert np.array_equal(pc[gid], pt.prop_acc), gid
+
+
+def test_cfg5_bulk_kernel_with_forced_full_groups(monkeypatch):
+    """Few instances: the group-width model would narrow the replica groups; TAPT_K1_W=32 forces
+    the 32-replica bulk instantiation (plain grid, no balancing) and it must match the oracle."""
+    monkeypatch.setenv("TAPT_K1_W", "32")
+    L, R, I = 32, 64, 2
+    e = T.Ensemble(T.Model.lattice((L,)), H.linear(0.2, 3.0, R), n_instances=I, seed=20250923, instance_offset=7)
+    e.generate_ea_disorder(43)
+    e.init_random()
+    e.run(12, swap_every=1)
+    e.generate_proposals(np.arange(56, dtype=np.uint32), None, refine=5, return_accepted=False)
+    e.run(12, swap_every=1)
+    assert "k1_lattice_pt<3,1,1,2,512,1,1,0>" in e.launch_log(), e.launch_log()
+    pts = _cfg5_oracle([7, 8], 12, 12)
+    compare(e, pts)
+
+
+def _fair_proposals_host(seed, gids, targets, rnd, n):
+    """The synthetic generator's fair i.i.d. proposals computed on the host (slot r of
+    round q draws from derive(seed, {kReplica, gid, r, q+1}); site i: draw i+2, +1 iff the top bit
+    is 0), packed LSB-first [I][T][ceil(n/8)]."""
+    out = np.zeros((len(gids), len(targets), (n + 7) // 8), np.uint8)
+    k = np.arange(2, n + 2, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        for a, gid in enumerate(gids):
+            for b, r in enumerate(targets):
+                z = np.uint64(O.derive(seed, [0x22, gid, int(r), rnd + 1])) + k * np.uint64(O.PHI)
+                z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+                z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+                z = z ^ (z >> np.uint64(31))
+                up = ((z >> np.uint64(63)) == 0).astype(np.uint8)
+                out[a, b] = np.packbits(up, bitorder="little")
+    return out
+
+
+def test_host_supplied_proposals_with_refinement_equal_the_synthetic_round():
+    """tapt_inject_proposals_packed_refined (bench.py's e2e path: proposals from host memory, 5
+    refinement sweeps at the target beta, Eq. 2) equals the on-device synthetic round when fed the
+    same proposals -- spins, energies, acceptance decisions."""
+    L, R, I, seed = 16, 64, 3, 5
+    betas = H.linear(0.2, 3.0, R)
+    targets = np.arange(40, dtype=np.uint32)
+    a = T.Ensemble(T.Model.lattice((L,)), betas, n_instances=I, seed=seed, instance_offset=11)
+    b = T.Ensemble(T.Model.lattice((L,)), betas, n_instances=I, seed=seed, instance_offset=11)
+    for e in (a, b):
+        e.generate_ea_disorder(3)
+        e.init_random()
+        e.run(7, swap_every=1)
+    acc_a = a.generate_proposals(targets, None, refine=5)
+    host = _fair_proposals_host(seed, [11, 12, 13], targets, 0, L ** 3)
+    acc_b = b.inject_proposals_packed(host, targets, refine=5)
+    assert np.array_equal(acc_a, acc_b)
+    for e in (a, b):
+        e.run(5, swap_every=1)
+    assert np.array_equal(a.spins(), b.spins()) and np.array_equal(a.energies(), b.energies())
+    assert acc_a.sum() > 0
