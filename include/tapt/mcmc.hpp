@@ -104,10 +104,12 @@ inline double gibbs_sweep(const CouplingGraph& g, SpinConfiguration& s, double b
     return gibbs_sweeps(g, s, beta, rng, 1);
 }
 
-// Single-site heat-bath update (mcmc.cpp:24-28): one draw of rng.
+// Single-site heat-bath update (mcmc.cpp:24-28) on the device (tapt_gibbs_update: K5 with a one-site
+// visit list): one draw of rng; ClampedSiteError for a clamped i, DimensionError on a length mismatch.
 inline void gibbs_update(const CouplingGraph& g, SpinConfiguration& s, std::uint32_t i, double beta, RngStream& rng) {
-    const double l = local_field(g, s, i);  // throws ClampedSiteError
-    s[i] = rng.uniform() < 1.0 / (1.0 + std::exp(-2.0 * beta * l)) ? 1 : -1;
+    std::uint64_t st = rng.state();
+    throw_status(tapt_gibbs_update(g.device(), s.data(), s.size(), i, beta, &st));
+    rng = RngStream::from_state(st);
 }
 
 inline void check_chain_config(const ChainConfig& c) {

@@ -146,10 +146,10 @@ class Replicas {
         return acc;
     }
 
-    std::vector<double> energies() const {
-        std::vector<std::int64_t> e(size());
-        throw_status(tapt_ensemble_get_energies(e_.get(), e.data()));
-        return std::vector<double>(e.begin(), e.end());
+    std::vector<double> energies() const {  // doubles: exact for integer and real-valued couplings
+        std::vector<double> e(size());
+        throw_status(tapt_ensemble_get_energies_f64(e_.get(), e.data()));
+        return e;
     }
     std::vector<SpinConfiguration> states() const {
         const std::size_t n = g_->n_spins();

@@ -9,6 +9,7 @@
  *   tapt_model_create_lattice   LatticeSpec::grid2d / grid3d + graph()      proj/include/tapt/lattice.hpp:25-35, proj/src/lattice.cpp:5-24,55-87
  *   tapt_model_create_graph     CouplingGraph::Builder(...).build()          proj/include/tapt/spin_model.hpp:32-48, proj/src/spin_model.cpp:15-77
  *   tapt_gibbs_sweep            gibbs_sweep(g, s, beta, rng)                 proj/include/tapt/mcmc.hpp:43-45, proj/src/mcmc.cpp:30-45
+ *   tapt_gibbs_update           gibbs_update(g, s, i, beta, rng)             proj/include/tapt/mcmc.hpp:40-41, proj/src/mcmc.cpp:24-28
  *   tapt_ensemble_create        BetaLadder / TAPTConfig / replica state
  *   tapt_ensemble_init_random   random_configuration per replica             proj/src/spin_model.cpp:116-121, PAPER.md:89-90 (Alg. 1 l.1-2)
  *   tapt_sweep                  M x gibbs_sweep of every replica             PAPER.md:107-111 (Alg. 1)
@@ -87,12 +88,18 @@ tapt_status tapt_probe_decision_rate(int blocks_per_sm, int threads, uint32_t it
 /* ----------------------------------------------------------------- models -- */
 
 /* LatticeSpec::grid2d(ly, lx, J, boundary) for dim == 2 (lz ignored),
- * LatticeSpec::grid3d(l = lx, J, boundary) for dim == 3.  J must be integer-valued. */
+ * LatticeSpec::grid3d(l = lx, J, boundary) for dim == 3.  Any double J, as the reference:
+ * integer-valued couplings take the exact-table kernels (K1-K4), real-valued ones K5 (see below). */
 tapt_status tapt_model_create_lattice(int dim, int ly, int lx, int lz, double J, int boundary, tapt_model_t* out);
 
 /* CouplingGraph::Builder: n spins, n_couplings (i, j, J) triples (duplicates summed,
  * i != j), per-spin fields h (nullable), clamp values (nullable; 0 free, +-1 clamped).
- * Couplings and fields must be integer-valued (device thresholds are exact tables). */
+ * Any double J and h, as CouplingGraph::Builder (spin_model.cpp:18-24).  Integer-valued couplings
+ * (|J| <= 127) and fields run on the exact-table kernels K1-K4.  Real-valued ones run on K5: FP64 local
+ * fields in the reference's order, device exp, and every decision whose draw falls within a relative
+ * 1e-12 of the probability (a near tie) re-evaluated with the host's glibc exp -- with a state replay
+ * if the device's provisional decision differed -- so results stay bit-identical to the reference.
+ * Such ensembles report energies and observables as doubles (the *_f64 getters). */
 tapt_status tapt_model_create_graph(uint32_t n, uint32_t n_couplings, const uint32_t* ci, const uint32_t* cj,
                                     const double* J, const double* h, const int8_t* clamp, tapt_model_t* out);
 tapt_status tapt_model_destroy(tapt_model_t m);
@@ -113,6 +120,11 @@ tapt_status tapt_model_digest(tapt_model_t m, uint64_t* digest);
 tapt_status tapt_model_energy(tapt_model_t m, const int8_t* s, size_t len, double* out);
 
 /* -------------------------------------------------------- drop-in sweeps -- */
+
+/* gibbs_update(g, s, i, beta, rng) (mcmc.cpp:24-28) on the device: s[i] <- heat-bath draw with the
+ * stream's next draw; *rng_state advances by one draw.  Clamped i -> TAPT_ERR_CLAMPED_SITE,
+ * len != n_spins -> TAPT_ERR_DIMENSION, as the reference throws. */
+tapt_status tapt_gibbs_update(tapt_model_t m, int8_t* s, size_t len, uint32_t site, double beta, uint64_t* rng_state);
 
 /* gibbs_sweep(g, s, beta, rng) on the device: updates s (host, n_spins entries) in
  * place with n_sweeps consecutive index-ascending heat-bath sweeps starting at
@@ -231,6 +243,16 @@ tapt_status tapt_inject_proposals_packed_refined(tapt_ensemble_t e, const uint8_
  * (nullable = fair coin). */
 tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, uint32_t n_targets,
                                     const double* m_bias, uint32_t refine, uint8_t* accepted);
+
+/* ------------------------------------------------------- real couplings -- */
+/* Energies by slot [I][R] as doubles (every model; required for real-valued couplings, where
+ * tapt_ensemble_get_energies returns TAPT_ERR_NUMERIC). */
+tapt_status tapt_ensemble_get_energies_f64(tapt_ensemble_t e, double* out);
+/* Observables [I][R][5] (count, sum E, sum E^2, sum |M|, sum M^2) and best energies [I] as doubles. */
+tapt_status tapt_get_observables_f64(tapt_ensemble_t e, double* obs);
+tapt_status tapt_get_best_f64(tapt_ensemble_t e, double* best);
+/* Near-tie decisions K5 re-evaluated with glibc exp so far, and the state replays they caused. */
+tapt_status tapt_ensemble_near_ties(tapt_ensemble_t e, uint64_t* ties, uint64_t* replays);
 
 /* ------------------------------------------------------ problem suite -- */
 /* Instance construction for BASELINE config 4 (proj/src/problems.cpp:1 is a

@@ -135,6 +135,11 @@ _SIGS = {
     "tapt_get_histogram": (C.c_int, [_vp, _vp, C.c_int]),
     "tapt_get_best": (C.c_int, [_vp, _i64p]),
     "tapt_reset_observables": (C.c_int, [_vp]),
+    "tapt_ensemble_get_energies_f64": (C.c_int, [_vp, _f64p]),
+    "tapt_get_observables_f64": (C.c_int, [_vp, _f64p]),
+    "tapt_get_best_f64": (C.c_int, [_vp, _f64p]),
+    "tapt_ensemble_near_ties": (C.c_int, [_vp, _u64p, _u64p]),
+    "tapt_gibbs_update": (C.c_int, [_vp, _i8p, C.c_size_t, C.c_uint32, C.c_double, _u64p]),
     "tapt_ensemble_set_betas": (C.c_int, [_vp, _f64p, C.c_int]),
     "tapt_ensemble_set_streams": (C.c_int, [_vp, _u64p]),
     "tapt_ensemble_init_from_streams": (C.c_int, [_vp, _u64p]),
@@ -309,6 +314,16 @@ def gibbs_sweep(model: Model, s: np.ndarray, beta: float, rng_state: int, n_swee
     return st.value, dE[:n_sweeps]
 
 
+def gibbs_update(model: Model, s: np.ndarray, site: int, beta: float, rng_state: int):
+    """Drop-in for tapt::gibbs_update (mcmc.cpp:24-28), on the device: s[site] resampled in place
+    with the stream's next draw; returns the new rng_state.  ClampedSiteError for a clamped site."""
+    if s.dtype != np.int8 or not s.flags.c_contiguous:
+        raise DimensionError("spins must be a contiguous int8 array")
+    st = C.c_uint64(rng_state)
+    _check(lib().tapt_gibbs_update(model._h, _p(s, _i8p), len(s), int(site), float(beta), C.byref(st)))
+    return st.value
+
+
 # ---------------------------------------------------------------- ensembles --
 
 class Ensemble:
@@ -383,10 +398,26 @@ class Ensemble:
         _check(lib().tapt_ensemble_get_spins_packed(self._h, _p(out, _u8p)))
         return out
 
+    @property
+    def real(self):
+        """Real-valued couplings: K5 (FP64 energies and observables)."""
+        return self.kernel == "real"
+
     def energies(self):
+        """Per-slot energies: int64 for integer couplings, float64 for real-valued ones."""
+        if self.real:
+            out = np.zeros((self.I, self.R), np.float64)
+            _check(lib().tapt_ensemble_get_energies_f64(self._h, _p(out, _f64p)))
+            return out
         out = np.zeros((self.I, self.R), np.int64)
         _check(lib().tapt_ensemble_get_energies(self._h, _p(out, _i64p)))
         return out
+
+    def near_ties(self):
+        """(near-tie decisions re-evaluated with glibc exp, state replays) -- K5 only."""
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(lib().tapt_ensemble_near_ties(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def permutation(self):
         out = np.zeros((self.I, self.R), np.uint8)
@@ -406,6 +437,10 @@ class Ensemble:
         return sa[:, : self.R - 1], sc[:, : self.R - 1], pa, pc
 
     def observables(self):
+        if self.real:
+            out = np.zeros((self.I, self.R, 5), np.float64)
+            _check(lib().tapt_get_observables_f64(self._h, _p(out, _f64p)))
+            return out
         out = np.zeros((self.I, self.R, 5), np.int64)
         _check(lib().tapt_get_observables(self._h, _p(out, _i64p)))
         return out
@@ -423,6 +458,10 @@ class Ensemble:
         return out
 
     def best(self):
+        if self.real:
+            out = np.zeros(self.I, np.float64)
+            _check(lib().tapt_get_best_f64(self._h, _p(out, _f64p)))
+            return out
         out = np.zeros(self.I, np.int64)
         _check(lib().tapt_get_best(self._h, _p(out, _i64p)))
         return out

@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "real.h"
 #include "tapt/spin_model.hpp"
 
 #ifndef TAPT_K1_DEFAULT_THREADS
@@ -288,6 +289,32 @@ struct tapt_model_s {
     // single-replica ensemble reused by the drop-in tapt_gibbs_sweep (created lazily)
     tapt_ensemble_t dropin = nullptr;
     std::mutex dropin_mu;
+    // real-valued couplings or fields (or |J| > 127): every ensemble of the model runs on K5 (real.h)
+    bool real = false;
+    std::vector<double> Jcsr;  // merged coupling value of every CSR entry
+    // single-replica K5 engine of the drop-in gibbs_sweep (per-sweep dE) / gibbs_update (created lazily)
+    std::unique_ptr<tapt_real::RealEngine> dropin_real;
+    cudaStream_t dropin_stream = nullptr;
+
+    tapt_real::RealGraph real_graph() const {
+        tapt_real::RealGraph g;
+        g.n = n;
+        g.rowptr = rowptr;
+        g.col = col;
+        g.ci = ci;
+        g.cj = cj;
+        g.free_sites = free_sites;
+        g.rank = rank;
+        g.J = Jcsr;
+        g.h = h;
+        g.cJ = J;
+        g.clamp = clamp;
+        g.colour_order = col_sites;
+        g.integral = !real;
+        g.lmin = lmin;
+        g.lmax = lmax;
+        return g;
+    }
     ~tapt_model_s();
     uint32_t n = 0;
     std::vector<uint32_t> ci, cj;  // merged, sorted (i<j)
@@ -463,6 +490,7 @@ void build_model(tapt_model_s& m, uint32_t n, const std::vector<uint32_t>& ai, c
         for (auto& [j, k] : adj[i]) {
             m.col.push_back(j);
             const double v = m.J[k];
+            m.Jcsr.push_back(v);
             if (!is_integer(v) || std::fabs(v) > 127) integral = false;
             m.adjJ.push_back(static_cast<int8_t>(integral ? v : 0));
             m.adj_bond.push_back(m.bond_of[k]);
@@ -470,9 +498,13 @@ void build_model(tapt_model_s& m, uint32_t n, const std::vector<uint32_t>& ai, c
         if (!is_integer(m.h[i])) integral = false;
         m.hi[i] = integral ? static_cast<int32_t>(m.h[i]) : 0;
     }
-    if (!integral)
-        throw tapt::NumericError(
-            "the device path needs integer-valued couplings (|J| <= 127) and fields: thresholds are exact tables");
+    // Real-valued (or large) couplings and fields: no exact threshold tables exist; such models run on
+    // K5 (real.h: FP64 fields in the reference's order, device exp with near ties resolved by glibc).
+    m.real = !integral;
+    if (m.real) {
+        std::fill(m.adjJ.begin(), m.adjJ.end(), (int8_t)0);
+        std::fill(m.hi.begin(), m.hi.end(), 0);
+    }
     for (uint32_t i = 0; i < n; ++i)
         if (!m.clamp[i]) m.free_sites.push_back(i);
     m.rank.assign(n, 0);
@@ -600,6 +632,8 @@ HostSched mcnaughton(int I, int S, int M) {
 
 struct tapt_ensemble_s {
     tapt_model_s* m = nullptr;
+    // real-valued models: the whole ensemble lives in K5's engine (real.h); the fields below are unused
+    std::unique_ptr<tapt_real::RealEngine> rx;
     uint32_t I = 0;
     uint64_t gid0 = 0;
     int R = 0, W = 0, G = 0, order = 0;
@@ -1099,7 +1133,6 @@ tapt_status tapt_model_create_lattice(int dim, int ly, int lx, int lz, double J,
         if (dim == 2 && (ly < 1 || lx < 1)) throw tapt::ConfigError("grid2d dimensions must be >= 1");
         if (dim == 3 && lx < 1) throw tapt::ConfigError("grid3d size must be >= 1");
         (void)lz;
-        if (!is_integer(J)) throw tapt::NumericError("lattice coupling must be integer-valued on the device path");
         auto m = std::make_unique<tapt_model_s>();
         std::vector<uint32_t> ci, cj;
         const bool per = boundary == TAPT_BOUNDARY_PERIODIC;
@@ -1118,7 +1151,7 @@ tapt_status tapt_model_create_lattice(int dim, int ly, int lx, int lz, double J,
         m->Jsign = J < 0 ? -1 : 1;
         m->nbonds = (uint32_t)ci.size();
         const int a = ilog2_exact(lx), b = ilog2_exact(m->ly);
-        m->k1 = per && a >= 2 && b >= 2 && (dim == 2 || a == b) && n <= 40000 && m->J0 <= 127;
+        m->k1 = !m->real && per && a >= 2 && b >= 2 && (dim == 2 || a == b) && n <= 40000 && m->J0 <= 127;
         m->ld.dim = dim;
         m->ld.log2Lx = a;
         m->ld.log2Ly = b;
@@ -1183,6 +1216,8 @@ tapt_status tapt_model_destroy(tapt_model_t m) {
 
 tapt_model_s::~tapt_model_s() {
     if (dropin) tapt_ensemble_destroy(dropin);
+    dropin_real.reset();
+    if (dropin_stream) cudaStreamDestroy(dropin_stream);
 }
 
 extern "C" {
@@ -1270,6 +1305,12 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
         e->G = (e->R + kW - 1) / kW;
         CUDA_OK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
         e->own_stream = true;
+        if (m->real) {
+            e->rx = std::make_unique<tapt_real::RealEngine>(m->real_graph(), e->I, e->gid0, e->betas, e->seed, e->order,
+                                                            e->stream);
+            *out = e.release();
+            return;
+        }
         m->ensure_device(e->stream);
         const int n = (int)m->n;
         e->use_k1 = m->k1 && d->order == TAPT_ORDER_COLOUR && !e->has_clamps();
@@ -1373,7 +1414,7 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
         e->best.upload(b, e->stream);
         sync_if(e->stream);
         *out = e.release();
-        if (m->lattice && m->Jsign < 0 && m->J0 != 0) {  // antiferromagnet: every bond negative
+        if (m->lattice && !m->real && m->Jsign < 0 && m->J0 != 0) {  // antiferromagnet: every bond negative
             std::vector<int8_t> sg((size_t)(*out)->I * m->nbonds, -1);
             if (tapt_ensemble_set_bond_signs(*out, sg.data(), m->nbonds) != TAPT_OK) {
                 const std::string msg = g_last_error;
@@ -1391,6 +1432,20 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
 tapt_status tapt_ensemble_set_betas(tapt_ensemble_t e, const double* betas, int allow_flat) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->set_betas(std::vector<double>(betas, betas + e->R), [&] {
+                for (int r = 0; r < e->R; ++r) {
+                    if (!(betas[r] >= 0.0) || !std::isfinite(betas[r])) throw tapt::ConfigError("beta must be >= 0");
+                    if (r && !(betas[r] > betas[r - 1]) && !(allow_flat == 1 && betas[r] >= betas[r - 1]) && allow_flat != 2)
+                        throw tapt::ConfigError("beta ladder must be strictly increasing (SPEC.md:388)");
+                }
+                bool dec = false;
+                for (int r = 1; r < e->R; ++r) dec = dec || betas[r] < betas[r - 1];
+                return dec;
+            }());
+            e->betas.assign(betas, betas + e->R);
+            return;
+        }
         for (int r = 0; r < e->R; ++r) {
             if (!(betas[r] >= 0.0) || !std::isfinite(betas[r])) throw tapt::ConfigError("beta must be >= 0");
             if (r && !(betas[r] > betas[r - 1]) && !(allow_flat == 1 && betas[r] >= betas[r - 1]) && allow_flat != 2)
@@ -1411,6 +1466,12 @@ tapt_status tapt_ensemble_set_betas(tapt_ensemble_t e, const double* betas, int 
 tapt_status tapt_ensemble_set_streams(tapt_ensemble_t e, const uint64_t* states) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            if (!states) throw tapt::ConfigError("null stream states");
+            e->rx->set_streams(states);
+            sync_if(e->stream);
+            return;
+        }
         if (!states) throw tapt::ConfigError("null stream states");
         e->streams.upload(states, (size_t)e->I * e->R, e->stream);
         sync_if(e->stream);
@@ -1420,6 +1481,11 @@ tapt_status tapt_ensemble_set_streams(tapt_ensemble_t e, const uint64_t* states)
 tapt_status tapt_ensemble_init_from_streams(tapt_ensemble_t e, const uint64_t* init_states) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            if (!init_states) throw tapt::ConfigError("null stream states");
+            e->rx->init_from_streams(init_states);
+            return;
+        }
         if (!init_states) throw tapt::ConfigError("null stream states");
         DevBuf<uint64_t> ds;
         ds.upload(init_states, (size_t)e->I * e->R, e->stream);
@@ -1460,6 +1526,7 @@ tapt_status tapt_ensemble_set_stream(tapt_ensemble_t e, void* s) {
             CUDA_OK(cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking));
             e->own_stream = true;
         }
+        if (e->rx) e->rx->set_stream(e->stream);
     });
 }
 
@@ -1477,6 +1544,7 @@ tapt_status tapt_ensemble_launch_log(tapt_ensemble_t e, char* buf, size_t cap) {
         if (!buf || cap == 0) throw tapt::ConfigError("null buffer");
         std::string all;
         for (const auto& s : e->launch_log) all += s + "\n";
+        if (e->rx) all += std::string(e->rx->kernel_name()) + "\n";
         if (all.size() + 1 > cap) throw tapt::SizeError("launch log buffer too small");
         std::memcpy(buf, all.c_str(), all.size() + 1);
     });
@@ -1484,6 +1552,7 @@ tapt_status tapt_ensemble_launch_log(tapt_ensemble_t e, char* buf, size_t cap) {
 
 const char* tapt_ensemble_kernel(tapt_ensemble_t e) {
     if (!e) return "csr";
+    if (e->rx) return "real";
     if (e->use_k1) return "lattice";
     try {
         return e->k3_eligible() ? "bitcsr" : e->k4_eligible() ? "levels" : "csr";
@@ -1495,6 +1564,7 @@ const char* tapt_ensemble_kernel(tapt_ensemble_t e) {
 tapt_status tapt_ensemble_set_bond_signs(tapt_ensemble_t e, const int8_t* signs, size_t n_bonds) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) throw tapt::ConfigError("bond signs apply to integer lattice models (this model has real-valued couplings)");
         tapt_model_s* m = e->m;
         if (!m->lattice) throw tapt::ConfigError("bond signs apply to lattice models only");
         if (n_bonds != m->nbonds) throw tapt::DimensionError("bond count mismatch");
@@ -1527,6 +1597,7 @@ tapt_status tapt_ensemble_set_bond_signs(tapt_ensemble_t e, const int8_t* signs,
 tapt_status tapt_ensemble_generate_ea_disorder(tapt_ensemble_t e, uint64_t disorder_seed) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) throw tapt::ConfigError("EA disorder applies to integer lattice models (this model has real-valued couplings)");
         tapt_model_s* m = e->m;
         if (!m->lattice || m->boundary != TAPT_BOUNDARY_PERIODIC || m->lx <= 2 || m->ly <= 2)
             throw tapt::ConfigError("EA disorder generation needs a periodic lattice with L > 2");
@@ -1553,6 +1624,7 @@ tapt_status tapt_ensemble_generate_ea_disorder(tapt_ensemble_t e, uint64_t disor
 tapt_status tapt_ensemble_get_bond_signs(tapt_ensemble_t e, int8_t* signs, size_t n_bonds) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) throw tapt::ConfigError("bond signs apply to integer lattice models");
         if (n_bonds != e->m->nbonds) throw tapt::DimensionError("bond count mismatch");
         if (!e->signs.p) {
             std::fill(signs, signs + (size_t)e->I * n_bonds, (int8_t)1);
@@ -1566,6 +1638,7 @@ tapt_status tapt_ensemble_get_bond_signs(tapt_ensemble_t e, int8_t* signs, size_
 tapt_status tapt_ensemble_set_clamps(tapt_ensemble_t e, const int8_t* clamps) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) throw tapt::ConfigError("per-instance clamps need integer couplings; clamp the model instead");
         const uint32_t n = e->m->n;
         for (uint32_t i = 0; i < e->I; ++i)
             for (uint32_t s = 0; s < n; ++s) {
@@ -1582,6 +1655,10 @@ tapt_status tapt_ensemble_set_clamps(tapt_ensemble_t e, const int8_t* clamps) {
 tapt_status tapt_ensemble_init_random(tapt_ensemble_t e) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->init_random();
+            return;
+        }
         std::vector<uint64_t> st((size_t)e->I * e->R);
         for (uint32_t i = 0; i < e->I; ++i)
             for (int r = 0; r < e->R; ++r)
@@ -1622,6 +1699,10 @@ static void set_spins_impl(tapt_ensemble_t e, const int8_t* spins, bool force_cl
 tapt_status tapt_ensemble_set_spins(tapt_ensemble_t e, const int8_t* spins) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->set_spins(spins, true);
+            return;
+        }
         set_spins_impl(e, spins, true);
     });
 }
@@ -1629,6 +1710,10 @@ tapt_status tapt_ensemble_set_spins(tapt_ensemble_t e, const int8_t* spins) {
 tapt_status tapt_ensemble_get_spins(tapt_ensemble_t e, int8_t* spins) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->get_spins(spins);
+            return;
+        }
         e->poll_sched(true);
         const int n = e->n();
         DevBuf<int8_t> d;
@@ -1645,6 +1730,10 @@ tapt_status tapt_ensemble_get_spins(tapt_ensemble_t e, int8_t* spins) {
 tapt_status tapt_ensemble_get_spins_packed(tapt_ensemble_t e, uint8_t* packed) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->get_spins_packed(packed);
+            return;
+        }
         e->poll_sched(true);
         const int n = e->n(), nb = (n + 7) / 8;
         DevBuf<uint8_t> d;
@@ -1661,6 +1750,7 @@ tapt_status tapt_ensemble_get_spins_packed(tapt_ensemble_t e, uint8_t* packed) {
 tapt_status tapt_ensemble_get_energies(tapt_ensemble_t e, int64_t* out) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) throw tapt::NumericError("energies are real-valued for this model: use tapt_ensemble_get_energies_f64");
         e->poll_sched(true);
         auto E = e->E.download(e->stream);
         auto bo = e->buf_of.download(e->stream);
@@ -1673,6 +1763,10 @@ tapt_status tapt_ensemble_get_energies(tapt_ensemble_t e, int64_t* out) {
 tapt_status tapt_ensemble_get_permutation(tapt_ensemble_t e, uint8_t* out) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->get_permutation(out);
+            return;
+        }
         e->poll_sched(true);
         auto bo = e->buf_of.download(e->stream);
         std::copy(bo.begin(), bo.end(), out);
@@ -1682,6 +1776,10 @@ tapt_status tapt_ensemble_get_permutation(tapt_ensemble_t e, uint8_t* out) {
 tapt_status tapt_ensemble_counters(tapt_ensemble_t e, uint64_t* sweeps, uint64_t* passes, uint64_t* rounds) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->counters(sweeps, passes, rounds);
+            return;
+        }
         if (sweeps) *sweeps = e->T;
         if (passes) *passes = e->P;
         if (rounds) *rounds = e->Q;
@@ -1691,6 +1789,10 @@ tapt_status tapt_ensemble_counters(tapt_ensemble_t e, uint64_t* sweeps, uint64_t
 tapt_status tapt_get_acceptance(tapt_ensemble_t e, uint64_t* sa, uint64_t* sc, uint64_t* pa, uint64_t* pc) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->acceptance(sa, sc, pa, pc);
+            return;
+        }
         e->poll_sched(true);
         const size_t np = (size_t)e->I * (e->R - 1);
         if (sa && np) {
@@ -1712,6 +1814,7 @@ tapt_status tapt_get_acceptance(tapt_ensemble_t e, uint64_t* sa, uint64_t* sc, u
 tapt_status tapt_get_observables(tapt_ensemble_t e, int64_t* obs) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) throw tapt::NumericError("observables are real-valued for this model: use tapt_get_observables_f64");
         e->poll_sched(true);
         auto v = e->obs.download(e->stream);
         std::copy(v.begin(), v.end(), obs);
@@ -1721,6 +1824,11 @@ tapt_status tapt_get_observables(tapt_ensemble_t e, int64_t* obs) {
 tapt_status tapt_set_histogram(tapt_ensemble_t e, int64_t e_lo, int64_t width, uint32_t nbins) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            if (width < 1) throw tapt::ConfigError("histogram bin width must be >= 1");
+            e->rx->set_histogram((double)e_lo, (double)width, nbins);
+            return;
+        }
         if (width < 1) throw tapt::ConfigError("histogram bin width must be >= 1");
         e->e_lo = e_lo;
         e->width = width;
@@ -1734,6 +1842,10 @@ tapt_status tapt_set_histogram(tapt_ensemble_t e, int64_t e_lo, int64_t width, u
 tapt_status tapt_get_histogram(tapt_ensemble_t e, uint64_t* dst, int on_device) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->get_histogram(dst, on_device != 0);
+            return;
+        }
         e->poll_sched(true);
         if (!e->nbins) throw tapt::ConfigError("no histogram configured");
         CUDA_OK(cudaMemcpyAsync(dst, e->hist.p, e->hist.n * sizeof(uint64_t),
@@ -1745,6 +1857,7 @@ tapt_status tapt_get_histogram(tapt_ensemble_t e, uint64_t* dst, int on_device) 
 tapt_status tapt_get_best(tapt_ensemble_t e, int64_t* best) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) throw tapt::NumericError("energies are real-valued for this model: use tapt_get_best_f64");
         e->poll_sched(true);
         auto v = e->best.download(e->stream);
         for (uint32_t i = 0; i < e->I; ++i) best[i] = v[i];
@@ -1754,15 +1867,70 @@ tapt_status tapt_get_best(tapt_ensemble_t e, int64_t* best) {
 tapt_status tapt_reset_observables(tapt_ensemble_t e) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->reset_observables();
+            return;
+        }
         e->obs.zero(e->stream);
         e->hist.zero(e->stream);
         sync_if(e->stream);
     });
 }
 
+tapt_status tapt_ensemble_get_energies_f64(tapt_ensemble_t e, double* out) {
+    return guard([&] {
+        check_ens(e);
+        if (e->rx) {
+            e->rx->get_energies(out);
+            return;
+        }
+        std::vector<int64_t> v((size_t)e->I * e->R);
+        if (tapt_ensemble_get_energies(e, v.data()) != TAPT_OK) throw tapt::CudaError(g_last_error);
+        for (size_t k = 0; k < v.size(); ++k) out[k] = (double)v[k];
+    });
+}
+
+tapt_status tapt_get_observables_f64(tapt_ensemble_t e, double* obs) {
+    return guard([&] {
+        check_ens(e);
+        if (e->rx) {
+            e->rx->observables(obs);
+            return;
+        }
+        e->poll_sched(true);
+        auto v = e->obs.download(e->stream);
+        for (size_t k = 0; k < v.size(); ++k) obs[k] = (double)v[k];
+    });
+}
+
+tapt_status tapt_get_best_f64(tapt_ensemble_t e, double* best) {
+    return guard([&] {
+        check_ens(e);
+        if (e->rx) {
+            e->rx->best(best);
+            return;
+        }
+        e->poll_sched(true);
+        auto v = e->best.download(e->stream);
+        for (uint32_t i = 0; i < e->I; ++i) best[i] = v[i];
+    });
+}
+
+tapt_status tapt_ensemble_near_ties(tapt_ensemble_t e, uint64_t* ties, uint64_t* replays) {
+    return guard([&] {
+        check_ens(e);
+        if (ties) *ties = e->rx ? e->rx->ties_seen() : 0;
+        if (replays) *replays = e->rx ? e->rx->replays() : 0;
+    });
+}
+
 tapt_status tapt_sweep(tapt_ensemble_t e, uint32_t n_sweeps) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->run(n_sweeps, 0, 0, 0);
+            return;
+        }
         e->run(n_sweeps, 0, 0, 0);
     });
 }
@@ -1770,6 +1938,11 @@ tapt_status tapt_sweep(tapt_ensemble_t e, uint32_t n_sweeps) {
 tapt_status tapt_swap_pass(tapt_ensemble_t e, int parity) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            if (parity != 0 && parity != 1) throw tapt::ConfigError("parity must be 0 or 1");
+            e->rx->swap_pass(parity);
+            return;
+        }
         if (parity != 0 && parity != 1) throw tapt::ConfigError("parity must be 0 or 1");
         if (e->swap_oversize) throw tapt::ConfigError("beta spacing too fine for exact swap tables");
         if (e->ladder_unordered)
@@ -1789,6 +1962,11 @@ tapt_status tapt_swap_pass(tapt_ensemble_t e, int parity) {
 tapt_status tapt_run(tapt_ensemble_t e, const tapt_schedule* s) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            if (!s) throw tapt::ConfigError("null schedule");
+            e->rx->run(s->n_sweeps, s->swap_every, s->measure_every, s->measure_from);
+            return;
+        }
         if (!s) throw tapt::ConfigError("null schedule");
         if (s->measure_every && !e->obs.p) throw tapt::ConfigError("observables not allocated");
         e->run(s->n_sweeps, s->swap_every, s->measure_every, s->measure_from);
@@ -1911,6 +2089,10 @@ tapt_status tapt_inject_proposals(tapt_ensemble_t e, const int8_t* proposals, in
                                   uint32_t T, const double* lqc, const double* lqp, uint8_t* accepted) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->inject(proposals, on_device != 0, targets, T, lqc, lqp, accepted);
+            return;
+        }
         if ((lqc == nullptr) != (lqp == nullptr)) throw tapt::ConfigError("log_q_cur and log_q_prop go together");
         prepare_targets(e, targets, T);
         const int n = e->n();
@@ -1977,6 +2159,10 @@ static bool refine_proposals(tapt_ensemble_s* e, uint32_t T, uint32_t refine) {
 static void inject_packed(tapt_ensemble_t e, const uint8_t* proposals, int on_device, const uint32_t* targets,
                           uint32_t T, uint32_t refine, uint8_t* accepted) {
     check_ens(e);
+    if (e->rx) {
+        e->rx->inject_packed(proposals, on_device != 0, targets, T, refine, accepted);
+        return;
+    }
     prepare_targets(e, targets, T);
     const int n = e->n(), nb = (n + 7) / 8;
     const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
@@ -2021,6 +2207,10 @@ tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, 
                                     uint32_t refine, uint8_t* accepted) {
     return guard([&] {
         check_ens(e);
+        if (e->rx) {
+            e->rx->generate(targets, T, m_bias, refine, accepted);
+            return;
+        }
         prepare_targets(e, targets, T);
         const int n = e->n();
         const int WT = std::min<int>((int)T, kW), GT = ((int)T + kW - 1) / kW;
@@ -2053,6 +2243,35 @@ tapt_status tapt_generate_proposals(tapt_ensemble_t e, const uint32_t* targets, 
 
 // ------------------------------------------------------------ drop-in sweep
 
+static tapt_real::RealEngine& dropin_real(tapt_model_t m, double beta) {
+    if (!m->dropin_real) {
+        cudaStream_t st = nullptr;
+        CUDA_OK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        m->dropin_stream = st;
+        m->dropin_real = std::make_unique<tapt_real::RealEngine>(m->real_graph(), 1, 0, std::vector<double>{beta}, 0,
+                                                                 TAPT_ORDER_REFERENCE, st);
+    }
+    return *m->dropin_real;
+}
+
+// gibbs_update (mcmc.cpp:24-28): one heat-bath update of site i with the stream's next draw, on the
+// device (K5 with a one-site visit list).  Clamped site -> ClampedSiteError (local_field,
+// spin_model.cpp:93), length mismatch -> DimensionError.
+tapt_status tapt_gibbs_update(tapt_model_t m, int8_t* s, size_t len, uint32_t site, double beta, uint64_t* rng_state) {
+    return guard([&] {
+        check_model(m);
+        if (len != m->n) throw tapt::DimensionError("configuration length mismatch");
+        if (site >= m->n) throw tapt::ConfigError("site index out of range");
+        if (m->clamp[site]) throw tapt::ClampedSiteError("spin " + std::to_string(site) + " is clamped");
+        if (!(beta >= 0.0)) throw tapt::ConfigError("beta must be >= 0");
+        if (!rng_state) throw tapt::ConfigError("null rng state");
+        if (tapt_device_count() == 0) throw tapt::CudaError("no CUDA device: the TAPT engine has no CPU fallback");
+        std::lock_guard<std::mutex> lock(m->dropin_mu);
+        dropin_real(m, beta).dropin_update(s, site, beta, *rng_state, nullptr, 0, 0);
+        *rng_state += tapt_dev::kPhi;
+    });
+}
+
 tapt_status tapt_gibbs_sweep(tapt_model_t m, int8_t* s, size_t len, double beta, uint64_t* rng_state,
                              uint32_t n_sweeps, double* dE) {
     return guard([&] {
@@ -2066,6 +2285,13 @@ tapt_status tapt_gibbs_sweep(tapt_model_t m, int8_t* s, size_t len, double beta,
             return;
         }
         std::lock_guard<std::mutex> lock(m->dropin_mu);
+        if (m->real || dE) {
+            // K5: the reference's sequential index order in FP64 with every sweep's dE, one launch
+            // (real-valued couplings; integer ones decide by their exact tables)
+            dropin_real(m, beta).dropin_sweeps(s, beta, *rng_state, n_sweeps, dE, nullptr, 0, 0);
+            *rng_state += (uint64_t)n_sweeps * (uint64_t)m->free_sites.size() * tapt_dev::kPhi;
+            return;
+        }
         if (!m->dropin) {
             tapt_ensemble_desc d{};
             d.n_instances = 1;

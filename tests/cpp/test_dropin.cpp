@@ -183,6 +183,53 @@ static int gpu_tests() {
         }
         CHECK(d == dh && s == h && r1.state() == r2.state());
     }
+    // real-valued couplings (the reference tests' Gaussian random graphs, test_spin_model.cpp:24-32):
+    // the drop-in gibbs_sweep / gibbs_update run on K5 and equal the host restatement bit for bit
+    {
+        RngStream gr(4242);
+        CouplingGraph::Builder b(30);
+        for (std::uint32_t i = 0; i < 30; ++i) {
+            for (std::uint32_t j = i + 1; j < 30; ++j)
+                if (gr.uniform() < 0.2) b.add_coupling(i, j, gr.normal());
+            b.add_field(i, gr.normal());
+        }
+        b.set_clamp(7, -1);
+        auto gg = b.build();
+        RngStream ri(5);
+        auto sd = random_configuration(gg, ri), sh = sd;
+        RngStream d1 = RngStream::derive(3, {stream::kChain}), d2 = d1;
+        for (int k = 0; k < 10; ++k) {
+            const double dd = gibbs_sweep(gg, sd, 0.9, d1);
+            double dh = 0.0;
+            for (std::uint32_t i : gg.free_sites()) {
+                const double l = local_field(gg, sh, i);
+                const std::int8_t nx = d2.uniform() < 1.0 / (1.0 + std::exp(-2.0 * 0.9 * l)) ? 1 : -1;
+                if (nx != sh[i]) {
+                    dh += 2.0 * sh[i] * l;
+                    sh[i] = nx;
+                }
+            }
+            CHECK(dd == dh && sd == sh && d1.state() == d2.state());
+        }
+        for (std::uint32_t i = 0; i < 30; ++i) {
+            if (i == 7) {
+                CHECK(throws<ClampedSiteError>([&] { gibbs_update(gg, sd, i, 1.1, d1); }));
+                continue;
+            }
+            const double l = local_field(gg, sh, i);
+            sh[i] = d2.uniform() < 1.0 / (1.0 + std::exp(-2.0 * 1.1 * l)) ? 1 : -1;
+            gibbs_update(gg, sd, i, 1.1, d1);
+            CHECK(sd == sh && d1.state() == d2.state());
+        }
+        // PT on it: energies stay the reference's doubles (E += gibbs_sweep's return)
+        auto lad = BetaLadder::geometric(0.3, 2.0, 6);
+        TAPTConfig c;
+        c.n_swap = 20;
+        c.M = 2;
+        c.seed = 6;
+        auto tr = run_pt(gg, lad, c);
+        CHECK(std::fabs(energy(gg, tr.final_state) - tr.final_energy) < 1e-9);
+    }
     // run_chain: deterministic per seed, records distinct
     ChainConfig cc;
     cc.beta = 0.4;

@@ -98,6 +98,67 @@ def corpus_fixture(tag, g: O.Graph, betas, per_beta, mixing, thinning, seed):
                         spins=pack(out.reshape(-1)), shape=np.array(out.shape))
 
 
+def ref_random_graph(n, p, fields, seed):
+    """The reference tests' random_graph (proj/tests/test_spin_model.cpp:24-32): Gaussian couplings
+    and fields from the reference's RngStream::normal."""
+    m = n * (n - 1) // 2
+    ci, cj = np.zeros(m, np.uint32), np.zeros(m, np.uint32)
+    J, h = np.zeros(m, np.float64), np.zeros(n, np.float64)
+    R().ref_random_graph.restype = C.c_uint32
+    R().ref_random_graph.argtypes = [C.c_uint32, C.c_double, C.c_int, C.c_uint64, O._u32p, O._u32p, O._f64p,
+                                     O._f64p]
+    k = R().ref_random_graph(n, p, int(fields), seed, O._p(ci, O._u32p), O._p(cj, O._u32p), O._p(J, O._f64p),
+                             O._p(h, O._f64p))
+    return ci[:k], cj[:k], J[:k], h
+
+
+def real_fixtures():
+    """Real-valued (Gaussian) couplings and fields: the reference's own random test graphs run
+    through the reference gibbs_sweep / gibbs_update and the restated PT/TAPT driver (FP64 energies)."""
+    graphs = []
+    for k, (n, p, fields, seed) in enumerate(((24, 0.3, True, 101), (40, 0.15, True, 202), (32, 0.25, False, 303))):
+        ci, cj, J, h = ref_random_graph(n, p, fields, seed)
+        cl = np.zeros(n, np.int8)
+        if k == 1:
+            cl[[3, 17, 30]] = [1, -1, 1]
+        graphs.append(O.Graph.from_couplings(n, ci, cj, J, h, cl))
+    out = {}
+    for k, g in enumerate(graphs):
+        out[f"g{k}_n"] = np.int64(g.n)
+        out[f"g{k}_ci"], out[f"g{k}_cj"], out[f"g{k}_J"] = g.ci, g.cj, g.J
+        out[f"g{k}_h"], out[f"g{k}_clamp"] = g.h, g.clamp
+    # single-chain gibbs_sweep trajectories (drop-in tapt::gibbs_sweep)
+    for k, g in enumerate(graphs):
+        rg = ref_graph(g)
+        s = np.zeros(g.n, np.int8)
+        pth = np.array([0x11, 0, k], np.uint64)
+        R().ref_random_configuration(rg, 9, O._p(pth, O._u64p), 3, O._p(s, O._i8p))
+        out[f"sweep{k}_init"] = s.copy()
+        d = np.zeros(25, np.float64)
+        pth = np.array([0x22, 0, k], np.uint64)
+        R().ref_gibbs_sweeps(rg, O._p(s, O._i8p), 0.7, 9, O._p(pth, O._u64p), 3, 25, O._p(d, O._f64p))
+        out[f"sweep{k}_final"], out[f"sweep{k}_dE"] = s, d
+        # gibbs_update at every site in turn (ClampedSiteError at clamped sites), stream {kChain, k}
+        R().ref_gibbs_update.restype = C.c_uint64
+        R().ref_gibbs_update.argtypes = [C.c_void_p, O._i8p, C.c_uint32, C.c_double, C.c_uint64, O._u64p, C.c_int,
+                                         C.POINTER(C.c_int)]
+        upd, err = np.zeros((g.n, g.n), np.int8), np.zeros(g.n, np.int8)
+        for i in range(g.n):
+            s2 = out[f"sweep{k}_init"].copy()
+            flag = C.c_int(0)
+            pth = np.array([0x44, k, i], np.uint64)
+            R().ref_gibbs_update(rg, O._p(s2, O._i8p), i, 1.3, 5, O._p(pth, O._u64p), 3, C.byref(flag))
+            upd[i], err[i] = s2, flag.value
+        out[f"update{k}_spins"], out[f"update{k}_clamped"] = upd, err
+        R().ref_graph_free(rg)
+    np.savez_compressed(os.path.join(HERE, "real_graphs.npz"), **out)
+    # PT + TAPT rounds on them (index order), two instances of graph 0 and one each of graphs 1, 2
+    betas = np.linspace(0.1, 2.5, 8)
+    pt_fixture("real_g0", [graphs[0], graphs[0]], betas, 41, 3, 60, 1, 20, 4, np.zeros(8), 2)
+    pt_fixture("real_g1", [graphs[1]], betas, 42, 0, 60, 1, 30, 6, np.full(8, 0.3), 3)
+    pt_fixture("real_g2", [graphs[2]], betas, 43, 0, 80, 2, 0, 0, np.zeros(8), 0)
+
+
 def main():
     if not O.have_ref():
         raise SystemExit("build oracle/_ref first: make -C oracle all")
@@ -129,6 +190,7 @@ def main():
     cl = np.zeros(64, np.int8)
     cl[:8] = [1, 1, -1, -1, 1, -1, 1, -1]
     corpus_fixture("2d8clamped", O.lattice_graph((8, 8), 1.0, False, cl), [0.2, 0.44, 0.7, 1.5], 3, 20, 5, 99)
+    real_fixtures()
     print("golden fixtures written to", HERE)
 
 

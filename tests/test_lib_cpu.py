@@ -106,8 +106,8 @@ def test_error_taxonomy():
         T.Model.graph(3, [0], [5], [1.0])                     # out of range (spin_model.cpp:21)
     with pytest.raises(T.ConfigError):
         T.Model.graph(3, [0], [1], [1.0], None, [2, 0, 0])    # clamp value (spin_model.cpp:35)
-    with pytest.raises(T.NumericError):
-        T.Model.graph(3, [0], [1], [0.5])                     # device path is integer-exact
+    half = T.Model.graph(3, [0], [1], [0.5], [0.25, 0.0, -1.5])  # real-valued: accepted (spin_model.cpp:18-24)
+    assert half.energy(np.array([1, -1, 1], np.int8)) == 0.5 - 0.25 + 1.5
     m = T.Model.lattice((4, 4))
     with pytest.raises(T.DimensionError):
         m.energy(np.ones(3, np.int8))                         # spin_model.cpp:80-82

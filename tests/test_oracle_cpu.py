@@ -227,3 +227,60 @@ def test_checkerboard_is_a_different_valid_order():
         gc = g.oc()
         for r in range(2):
             assert pt.E[r] == O.lib().oc_energy(gc, pt.spins[r].ctypes.data_as(O._i8p))
+
+
+# ------------------------------------------- real-valued (Gaussian) couplings --
+
+def real_graphs():
+    f = load("real_graphs.npz")
+    gs = [O.Graph.from_couplings(int(f[f"g{k}_n"]), f[f"g{k}_ci"], f[f"g{k}_cj"], f[f"g{k}_J"], f[f"g{k}_h"],
+                                 f[f"g{k}_clamp"]) for k in range(3)]
+    return f, gs
+
+
+def test_real_graphs_are_not_integer_valued():
+    f, gs = real_graphs()
+    for g in gs:
+        assert np.any(g.J != np.rint(g.J))
+    assert np.any(gs[0].h != 0) and np.all(gs[2].h == 0) and np.count_nonzero(gs[1].clamp) == 3
+
+
+def test_real_sweeps_and_updates_match_reference_golden():
+    """oc_rsweep / oc_rupdate (FP64 local fields, libm exp) against the reference's gibbs_sweep and
+    gibbs_update on its own Gaussian random graphs (test_spin_model.cpp:24-32)."""
+    f, gs = real_graphs()
+    for k, g in enumerate(gs):
+        gc = g.roc()
+        s = f[f"sweep{k}_init"].copy()
+        order = g.index_order()
+        s0 = O.derive(9, [0x22, 0, k])
+        for t in range(25):
+            d = O.lib().oc_rsweep(gc, order.ctypes.data_as(O._u32p), s.ctypes.data_as(O._i8p), 0.7, s0,
+                                  t * len(g.free))
+            assert d == f[f"sweep{k}_dE"][t]
+        assert np.array_equal(s, f[f"sweep{k}_final"])
+        for i in range(g.n):
+            if f[f"update{k}_clamped"][i]:
+                assert g.clamp[i] != 0
+                continue
+            s2 = f[f"sweep{k}_init"].copy()
+            s2[i] = O.lib().oc_rupdate(gc, s2.ctypes.data_as(O._i8p), i, 1.3, O.derive(5, [0x44, k, i]))
+            assert np.array_equal(s2, f[f"update{k}_spins"][i])
+
+
+@pytest.mark.parametrize("tag,which", [("real_g0", [0, 0]), ("real_g1", [1]), ("real_g2", [2])])
+def test_real_pt_matches_reference_golden(tag, which):
+    _, gs = real_graphs()
+    f = load(f"pt_{tag}.npz")
+    I, R, n = (int(x) for x in f["shape"])
+    spins = unpack(f["spins"], I * R * n).reshape(I, R, n)
+    for k, w in enumerate(which):
+        g = gs[w]
+        pt = O.RPT(g, f["betas"], int(f["seed"]), int(f["gid0"]) + k, g.index_order())
+        pt.run(int(f["n_sweeps"]), int(f["swap_every"]), int(f["prop_every"]), int(f["n_targets"]),
+               f["m_bias"], int(f["refine"]))
+        assert np.array_equal(pt.spins, spins[k])
+        assert np.array_equal(pt.E, f["E"][k])  # FP64 energies, bit for bit
+        assert np.array_equal(pt.swap_acc[: R - 1], f["swap_acc"][k][: R - 1])
+        assert np.array_equal(pt.prop_acc, f["prop_acc"][k])
+    assert f["swap_acc"].sum() > 0
