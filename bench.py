@@ -280,6 +280,24 @@ def run_workload(args):
         "roofline": roof,
         "gpu_launches": T.launch_count() - l0, "clocks": clocks,
     }
+    if k == 1:  # BASELINE config 1 itself is ONE instance: its whole 10^4-sweep run, on the device
+        e1 = T.Ensemble(T.Model.lattice((32, 32)), WL.geometric(0.2, 1.0, 32), n_instances=1, seed=1)
+        e1.set_stream(stream.cuda_stream)
+        e1.init_random()
+        e1.run(100, swap_every=1, measure_every=1)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        e1.run(10000, swap_every=1, measure_every=1, measure_from=5000)
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms1 = a.elapsed_time(b)
+        out["single_instance"] = {
+            "what": "BASELINE configs[0] as specified: 1 instance x 32 slots x 10^4 sweeps (swap every sweep, "
+                    "observables over the last half); the headline line above fills the GPU with 296 "
+                    "independent seeds of the same run (replicas only)",
+            "seconds": ms1 / 1e3, "value": 32 * 1024 * 10000 / (ms1 * 1e-3), "unit": UNIT,
+            "kernel": e1.launch_log()}
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         rate, dt, used, sample = cpu_workload_rate(k, threads)
@@ -364,19 +382,22 @@ def init_dist(world, local, backend="nccl"):
     return dist
 
 
-def sum_histograms(hist, world, stream=None):
-    """Per-beta energy histograms summed over the ranks -- with the timing max below, the only
-    collectives of the run (NCCL over NVLink on the B200 box, gloo in the CPU test).
-    Enqueued on `stream` (inside the timed region) when given."""
-    import torch
+def share_unique_id(make_uid, rank):
+    """Rank 0 makes the NCCL unique id (128 bytes); every rank receives it (torch.distributed
+    broadcast -- the plumbing; the reduction itself is the library's NCCL call)."""
     import torch.distributed as dist
-    if world > 1:
-        if stream is not None:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(hist)
-        else:
-            dist.all_reduce(hist)
-    return hist
+    obj = [make_uid() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def reduce_observables(T, ens, comm):
+    """The run's collectives: per-beta energy histograms, per-slot observables and the
+    best energy over every rank's instances -- tapt_allreduce_observables, NCCL over NVLink on the
+    ensemble's stream (one process per GPU); rank-local at N = 1."""
+    if comm is None:
+        return {"hist": ens.histogram(), "obs": None, "best": int(ens.best().min())}
+    return T.allreduce_observables(ens, comm)
 
 
 def max_over_ranks(ms, world, device):
@@ -452,6 +473,7 @@ def main():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     init_dist(world, local)
+    comm = T.NcclComm(share_unique_id(T.NcclComm.unique_id, rank), world, rank) if world > 1 else None
     from paper_2509_23043_b200 import sharding
     off, I = sharding.shard(args.instances, world, rank)  # contiguous global instance ids
     S = args.sweeps_per_step
@@ -465,7 +487,6 @@ def main():
     nb = 2 * 3 * N_SPINS // 64
     ens.set_histogram(-3 * N_SPINS, 64, nb)
     targets = np.arange(N_TARGETS, dtype=np.uint32)
-    hist_t = torch.zeros((R, nb), dtype=torch.int64, device="cuda")
 
     k_ev = []
 
@@ -491,8 +512,7 @@ def main():
         t_start.record(stream)
         for _ in range(args.steps):
             step(True)
-        ens.histogram(device_ptr=hist_t.data_ptr())
-        sum_histograms(hist_t, world, stream)  # inside the timed region
+        red = reduce_observables(T, ens, comm)  # inside the timed region
         t_end.record(stream)
         torch.cuda.synchronize()
     if world > 1:
@@ -500,7 +520,7 @@ def main():
     launches = T.launch_count() - l0
     ms = t_start.elapsed_time(t_end)
     ms, comm_ranks = max_over_ranks(ms, world, "cuda")
-    samples = int(hist_t.sum().item())
+    samples = int(np.asarray(red["hist"]).sum())
     upd_step = args.instances * (R * N_SPINS * S + N_TARGETS * N_SPINS * REFINE)
     value = upd_step * args.steps / (ms * 1e-3)
 
@@ -530,12 +550,14 @@ def main():
                    "updates_per_step": upd_step, "parallelism": f"instances sharded over {world} GPU(s)",
                    "l2": "state 1 GiB/GPU at N=1 > 126 MB L2; spins are shared-memory resident within a launch",
                    "histogram_samples_reduced": samples},
-        "comm": {"backend": "nccl" if world > 1 else None, "ranks": comm_ranks,
-                 "collectives": "all_reduce of the per-beta histograms (int64 [64][3072]) + max of the timed region"},
+        "comm": {"backend": "nccl (tapt_allreduce_observables)" if world > 1 else None, "ranks": comm_ranks,
+                 "nccl_ranks": comm.size() if comm is not None else 1,
+                 "collectives": "all_reduce of the per-beta histograms (u64 [64][3072]), per-slot observables and "
+                                "best energy (library NCCL call) + max of the timed region"},
         "roofline": roofline, "gpu_launches": launches,
     }
     if not args.no_e2e:
-        out["e2e"] = e2e_leg(args, T, torch, ens, stream, I, S, world)
+        out["e2e"] = e2e_leg(args, T, torch, ens, stream, I, S, world, comm)
     out["clocks"] = clocks
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
@@ -552,7 +574,7 @@ def main():
         dist.destroy_process_group()
 
 
-def e2e_leg(args, T, torch, ens, stream, I, S, world):
+def e2e_leg(args, T, torch, ens, stream, I, S, world, comm):
     """Same metric and the same step through the public C-ABI calls with HOST buffers: per step the
     externally supplied proposals (the generator's output: bit-packed [I][56][4096 B] in pinned host
     memory) are copied H2D inside the timed region and injected with their 5 refinement sweeps at the
@@ -564,8 +586,6 @@ def e2e_leg(args, T, torch, ens, stream, I, S, world):
     host = torch.from_numpy(rs.integers(0, 256, size=(I, N_TARGETS, nbytes), dtype=np.uint8)).pin_memory()
     dev = torch.empty_like(host, device="cuda")
     nb = 2 * 3 * N_SPINS // 64
-    hist_d = torch.zeros((R, nb), dtype=torch.int64, device="cuda")
-    hist_h = torch.zeros((R, nb), dtype=torch.int64).pin_memory()
     energies = torch.empty((I, R), dtype=torch.int64).pin_memory()
     targets = np.arange(N_TARGETS, dtype=np.uint32)
 
@@ -574,10 +594,7 @@ def e2e_leg(args, T, torch, ens, stream, I, S, world):
             dev.copy_(host, non_blocking=True)
         ens.inject_proposals_packed(None, targets, device_ptr=dev.data_ptr(), refine=REFINE, return_accepted=False)
         ens.run(S, swap_every=1, measure_every=args.measure_every)
-        ens.histogram(device_ptr=hist_d.data_ptr())
-        sum_histograms(hist_d, world, stream)
-        with torch.cuda.stream(stream):
-            hist_h.copy_(hist_d, non_blocking=True)
+        reduce_observables(T, ens, comm)  # per-beta histograms to the host (all-reduced over the ranks)
         energies.copy_(torch.from_numpy(ens.energies()))
 
     step()
@@ -590,9 +607,10 @@ def e2e_leg(args, T, torch, ens, stream, I, S, world):
     dt, _ = max_over_ranks(dt, world, "cuda")
     upd = args.instances * (R * N_SPINS * S + N_TARGETS * N_SPINS * REFINE) * args.steps
     return {"value": upd / dt, "unit": UNIT, "h2d_bytes_per_step": int(host.numel()),
-            "d2h_bytes_per_step": int(hist_h.numel() * 8 + I * R * 8),
+            "d2h_bytes_per_step": int(R * nb * 8 + I * R * 8 + (R * 5 * 8 + 8 if comm is not None else I * 8)),
             "path": "tapt_inject_proposals_packed_refined (host-supplied proposals, 5 refinement sweeps, Eq. 2) + "
-                    "tapt_run + tapt_get_histogram (+ NCCL all_reduce) + tapt_ensemble_get_energies",
+                    "tapt_run + tapt_get_histogram / tapt_allreduce_observables (NCCL at N > 1) + "
+                    "tapt_ensemble_get_energies",
             "timer": "host wall clock around K steps, synchronized on both sides, max over ranks"}
 
 

@@ -254,6 +254,23 @@ tapt_status tapt_get_best_f64(tapt_ensemble_t e, double* best);
 /* Near-tie decisions K5 re-evaluated with glibc exp so far, and the state replays they caused. */
 tapt_status tapt_ensemble_near_ties(tapt_ensemble_t e, uint64_t* ties, uint64_t* replays);
 
+/* ------------------------------------------------------------ multi-GPU -- */
+/* One process per GPU; rank g owns a contiguous block of global instance ids (instance_offset), so a
+ * sharded run equals the single-GPU run instance by instance.  Replicas never span GPUs: the only
+ * collectives are these end-of-run reductions over NCCL (SPEC.md:472-473 concurrency contract,
+ * proj/include/tapt/threading.hpp:14-35 parallel_for over instances).  NCCL is loaded at run time;
+ * its failures return TAPT_ERR_NCCL.  comm is an ncclComm_t (created here or by the caller). */
+tapt_status tapt_nccl_unique_id(uint8_t* id, size_t len); /* rank 0 creates, broadcasts 128 bytes */
+tapt_status tapt_nccl_comm_create(const uint8_t* id, int n_ranks, int rank, void** comm);
+tapt_status tapt_nccl_comm_destroy(void* comm);
+tapt_status tapt_nccl_comm_size(void* comm, int* n_ranks);
+/* All-reduce over the communicator (every rank receives the result; each nullable):
+ *   obs  [R][5]      per-slot count, sum E, sum E^2, sum |M|, sum M^2 over all ranks' instances
+ *   hist [R][nbins]  per-slot energy histograms summed over ranks (the ensemble's own stays local)
+ *   best [1]         lowest energy seen by any instance on any rank
+ * Integer-coupling ensembles. */
+tapt_status tapt_allreduce_observables(tapt_ensemble_t e, void* comm, int64_t* obs, uint64_t* hist, int64_t* best);
+
 /* ------------------------------------------------------ problem suite -- */
 /* Instance construction for BASELINE config 4 (proj/src/problems.cpp:1 is a
  * placeholder).  Host-only, never on the timed path.  Spin +1 = logical 1. */

@@ -140,6 +140,11 @@ _SIGS = {
     "tapt_get_best_f64": (C.c_int, [_vp, _f64p]),
     "tapt_ensemble_near_ties": (C.c_int, [_vp, _u64p, _u64p]),
     "tapt_gibbs_update": (C.c_int, [_vp, _i8p, C.c_size_t, C.c_uint32, C.c_double, _u64p]),
+    "tapt_nccl_unique_id": (C.c_int, [_u8p, C.c_size_t]),
+    "tapt_nccl_comm_create": (C.c_int, [_u8p, C.c_int, C.c_int, C.POINTER(_vp)]),
+    "tapt_nccl_comm_destroy": (C.c_int, [_vp]),
+    "tapt_nccl_comm_size": (C.c_int, [_vp, C.POINTER(C.c_int)]),
+    "tapt_allreduce_observables": (C.c_int, [_vp, _vp, _i64p, _u64p, _i64p]),
     "tapt_ensemble_set_betas": (C.c_int, [_vp, _f64p, C.c_int]),
     "tapt_ensemble_set_streams": (C.c_int, [_vp, _u64p]),
     "tapt_ensemble_init_from_streams": (C.c_int, [_vp, _u64p]),
@@ -322,6 +327,47 @@ def gibbs_update(model: Model, s: np.ndarray, site: int, beta: float, rng_state:
     st = C.c_uint64(rng_state)
     _check(lib().tapt_gibbs_update(model._h, _p(s, _i8p), len(s), int(site), float(beta), C.byref(st)))
     return st.value
+
+
+class NcclComm:
+    """An NCCL communicator owned by the native library (tapt_nccl_*): rank 0 makes the 128-byte
+    unique id (`NcclComm.unique_id()`), every rank passes it in (broadcast it out of band, e.g. with
+    torch.distributed).  Used by `allreduce_observables` -- the end-of-run reductions of a sharded run."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = np.zeros(128, np.uint8)
+        _check(lib().tapt_nccl_unique_id(_p(buf, _u8p), 128))
+        return buf.tobytes()
+
+    def __init__(self, uid: bytes, n_ranks: int, rank: int):
+        buf = np.frombuffer(bytes(uid), np.uint8).copy()
+        self._h = _vp()
+        _check(lib().tapt_nccl_comm_create(_p(buf, _u8p), int(n_ranks), int(rank), C.byref(self._h)))
+
+    def size(self) -> int:
+        v = C.c_int()
+        _check(lib().tapt_nccl_comm_size(self._h, C.byref(v)))
+        return v.value
+
+    def close(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.tapt_nccl_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+
+def allreduce_observables(ens, comm: NcclComm):
+    """Per-slot observables [R][5], per-slot histograms [R][nbins] (if configured) and the best energy,
+    summed / minimised over every rank's instances with NCCL (tapt_allreduce_observables)."""
+    obs = np.zeros((ens.R, 5), np.int64)
+    best = np.zeros(1, np.int64)
+    nb = getattr(ens, "_nbins", 0)
+    hist = np.zeros((ens.R, nb), np.uint64) if nb else None
+    _check(lib().tapt_allreduce_observables(ens._h, comm._h, _p(obs, _i64p), _p(hist, _u64p), _p(best, _i64p)))
+    return {"obs": obs, "hist": hist, "best": int(best[0])}
 
 
 # ---------------------------------------------------------------- ensembles --

@@ -7,6 +7,8 @@
 // stream states (rng.hpp:21-27), choose the kernel (K1 lattice / K2 CSR), and keep the
 // global sweep / pass / round counters that address every random draw.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <atomic>
@@ -123,6 +125,9 @@ tapt_status guard(F&& f) {
     } catch (const tapt::CudaError& e) {
         g_last_error = e.what();
         return TAPT_ERR_CUDA;
+    } catch (const tapt::NcclError& e) {
+        g_last_error = e.what();
+        return TAPT_ERR_NCCL;
     } catch (const std::bad_alloc&) {
         g_last_error = "host allocation failed";
         return TAPT_ERR_INTERNAL;
@@ -390,6 +395,68 @@ struct tapt_model_s {
                 meta.push_back(make_uint4(i, rank[i], (uint32_t)start,
                                           (uint32_t)(off_of[i] + 32768) | ((uint32_t)nch_of[i] << 16) |
                                               ((uint32_t)sp_of[i] << 20)));
+            }
+        }
+        // Bank-aware entry order.  A warp gathers entry k of 32 rows (32 lanes = 32 consecutive class
+        // positions) in one LDS per k; lanes reading different words of one bank serialise.  Each row's
+        // entries are a multiset that the carry-save count sums in any order, so per warp, chunk and
+        // entry column a greedy pick (most-constrained lane first) takes a word already chosen in the
+        // column (broadcast) or one in an unused bank.  Config 4: 1616 -> 886 wavefronts per sweep for
+        // 576 gathers; the counts, and so every result, are unchanged.
+        if (std::getenv("TAPT_K3_BANKS") == nullptr || std::atoi(std::getenv("TAPT_K3_BANKS")) != 0) {
+            for (size_t c = 0; c + 1 < col_ptr.size(); ++c) {
+                const uint32_t p0 = col_ptr[c], p1 = col_ptr[c + 1];
+                for (uint32_t w0 = p0; w0 < p1; w0 += 32) {
+                    const uint32_t w1 = std::min(p1, w0 + 32);
+                    int maxch = 0;
+                    for (uint32_t q = w0; q < w1; ++q) maxch = std::max(maxch, (int)((meta[q].w >> 16) & 15u));
+                    for (int ch = 0; ch < maxch; ++ch) {
+                        std::vector<uint32_t> lanes;
+                        for (uint32_t q = w0; q < w1; ++q)
+                            if ((int)((meta[q].w >> 16) & 15u) > ch) lanes.push_back(q);
+                        std::vector<std::vector<uint32_t>> rem(lanes.size()), out(lanes.size());
+                        for (size_t l = 0; l < lanes.size(); ++l) {
+                            const uint32_t st = meta[lanes[l]].z + 16u * ch;
+                            rem[l].assign(adj.begin() + st, adj.begin() + st + 16);
+                        }
+                        for (int k = 0; k < 16; ++k) {
+                            std::vector<size_t> order(lanes.size());
+                            std::iota(order.begin(), order.end(), 0);
+                            auto distinct = [](const std::vector<uint32_t>& v) {
+                                std::vector<uint32_t> u(v);
+                                std::sort(u.begin(), u.end());
+                                return (size_t)(std::unique(u.begin(), u.end()) - u.begin());
+                            };
+                            std::vector<size_t> nd(lanes.size());
+                            for (size_t l = 0; l < lanes.size(); ++l) nd[l] = distinct(rem[l]);
+                            std::stable_sort(order.begin(), order.end(), [&](size_t x, size_t y) { return nd[x] < nd[y]; });
+                            std::vector<std::vector<uint32_t>> bank(32);
+                            for (size_t l : order) {
+                                size_t bi = 0;
+                                int bc0 = 1 << 30, bc1 = 0;
+                                for (size_t e = 0; e < rem[l].size(); ++e) {
+                                    const uint32_t wd = rem[l][e] / 4;
+                                    const auto& bk = bank[wd % 32];
+                                    const bool shared = std::find(bk.begin(), bk.end(), wd) != bk.end();
+                                    const int c0 = shared ? 0 : (int)bk.size();
+                                    const int c1 = (int)std::count(rem[l].begin(), rem[l].end(), rem[l][e]);
+                                    if (c0 < bc0 || (c0 == bc0 && c1 > bc1)) {
+                                        bi = e;
+                                        bc0 = c0;
+                                        bc1 = c1;
+                                    }
+                                }
+                                const uint32_t pick = rem[l][bi];
+                                rem[l].erase(rem[l].begin() + bi);
+                                out[l].push_back(pick);
+                                auto& bk = bank[(pick / 4) % 32];
+                                if (std::find(bk.begin(), bk.end(), pick / 4) == bk.end()) bk.push_back(pick / 4);
+                            }
+                        }
+                        for (size_t l = 0; l < lanes.size(); ++l)
+                            std::copy(out[l].begin(), out[l].end(), adj.begin() + meta[lanes[l]].z + 16u * ch);
+                    }
+                }
             }
         }
         k3_nadj = (int)adj.size();
@@ -2325,6 +2392,149 @@ tapt_status tapt_gibbs_sweep(tapt_model_t m, int8_t* s, size_t len, double beta,
         }
         if (tapt_ensemble_get_spins(e, s) != TAPT_OK) throw tapt::CudaError(g_last_error);
         *rng_state = st + (uint64_t)n_sweeps * (uint64_t)m->free_sites.size() * tapt_dev::kPhi;
+    });
+}
+
+}  // extern "C"
+
+// ============================================================== multi-GPU ===
+// Instances are sharded across ranks (one process per GPU); replicas of an instance never span
+// GPUs, so the only collectives are the end-of-run observable reductions: per-slot
+// sums over every rank's instances, the per-slot energy histograms, and the global best energy --
+// ncclAllReduce on the ensemble's stream over NVLink / NVSwitch.  NCCL is loaded at run time
+// (dlopen "libnccl.so.2": the copy torch already mapped, else the system one), so the library has no
+// link-time NCCL dependency and a missing NCCL is a TAPT_ERR_NCCL at the call.
+
+namespace {
+
+struct NcclApi {
+    ncclResult_t (*get_unique_id)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_count)(const ncclComm_t, int*) = nullptr;
+    const char* (*error_string)(ncclResult_t) = nullptr;
+};
+
+const NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    static std::string err;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            err = std::string("NCCL not available: ") + dlerror();
+            return;
+        }
+        api.get_unique_id = reinterpret_cast<decltype(api.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        api.comm_init_rank = reinterpret_cast<decltype(api.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        api.comm_count = reinterpret_cast<decltype(api.comm_count)>(dlsym(h, "ncclCommCount"));
+        api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
+        if (!api.get_unique_id || !api.comm_init_rank || !api.comm_destroy || !api.all_reduce || !api.comm_count)
+            err = "NCCL library lacks the expected symbols";
+    });
+    if (!err.empty()) throw tapt::NcclError(err);
+    return api;
+}
+
+void nccl_ok(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess)
+        throw tapt::NcclError(std::string(what) + ": " + (nccl().error_string ? nccl().error_string(r) : "error"));
+}
+
+// per-slot sums over the instances: obs [I][R][5] -> out [R][5]
+__global__ void k_obs_slot_sums(const long long* obs, int I, int R, long long* out) {
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= R * 5) return;
+    long long v = 0;
+    for (int i = 0; i < I; ++i) v += obs[(size_t)i * R * 5 + k];
+    out[k] = v;
+}
+__global__ void k_best_min(const int* best, int I, long long* out) {
+    long long m = 0x7FFFFFFFll;
+    for (int i = threadIdx.x; i < I; i += blockDim.x) m = min(m, (long long)best[i]);
+    for (int o = 16; o; o >>= 1) m = min(m, __shfl_xor_sync(0xFFFFFFFFu, m, o));
+    if (threadIdx.x == 0) *out = m;
+}
+
+}  // namespace
+
+extern "C" {
+
+tapt_status tapt_nccl_unique_id(uint8_t* id, size_t len) {
+    return guard([&] {
+        if (!id || len < NCCL_UNIQUE_ID_BYTES) throw tapt::ConfigError("unique id buffer must hold 128 bytes");
+        ncclUniqueId u;
+        nccl_ok(nccl().get_unique_id(&u), "ncclGetUniqueId");
+        std::memcpy(id, &u, NCCL_UNIQUE_ID_BYTES);
+    });
+}
+
+tapt_status tapt_nccl_comm_create(const uint8_t* id, int n_ranks, int rank, void** comm) {
+    return guard([&] {
+        if (!id || !comm) throw tapt::ConfigError("null unique id / output");
+        if (n_ranks < 1 || rank < 0 || rank >= n_ranks) throw tapt::ConfigError("bad rank / world size");
+        if (tapt_device_count() == 0) throw tapt::CudaError("no CUDA device");
+        ncclUniqueId u;
+        std::memcpy(&u, id, NCCL_UNIQUE_ID_BYTES);
+        ncclComm_t c = nullptr;
+        nccl_ok(nccl().comm_init_rank(&c, n_ranks, u, rank), "ncclCommInitRank");
+        *comm = c;
+    });
+}
+
+tapt_status tapt_nccl_comm_destroy(void* comm) {
+    return guard([&] {
+        if (comm) nccl_ok(nccl().comm_destroy(static_cast<ncclComm_t>(comm)), "ncclCommDestroy");
+    });
+}
+
+tapt_status tapt_nccl_comm_size(void* comm, int* n_ranks) {
+    return guard([&] {
+        if (!comm || !n_ranks) throw tapt::ConfigError("null communicator / output");
+        nccl_ok(nccl().comm_count(static_cast<ncclComm_t>(comm), n_ranks), "ncclCommCount");
+    });
+}
+
+tapt_status tapt_allreduce_observables(tapt_ensemble_t e, void* comm, int64_t* obs, uint64_t* hist, int64_t* best) {
+    return guard([&] {
+        check_ens(e);
+        if (!comm) throw tapt::NcclError("null NCCL communicator");
+        if (e->rx) throw tapt::ConfigError("observable reductions of real-valued models: use the f64 getters per rank");
+        e->poll_sched(true);
+        const auto& api = nccl();
+        ncclComm_t c = static_cast<ncclComm_t>(comm);
+        const int R = e->R;
+        DevBuf<long long> o, b;
+        if (obs) {
+            o.alloc((size_t)R * 5);
+            ++g_launches;
+            k_obs_slot_sums<<<(R * 5 + 127) / 128, 128, 0, e->stream>>>(e->obs.p, (int)e->I, R, o.p);
+            CUDA_OK(cudaGetLastError());
+            nccl_ok(api.all_reduce(o.p, o.p, o.n, ncclInt64, ncclSum, c, e->stream), "ncclAllReduce(observables)");
+        }
+        DevBuf<unsigned long long> h;  // the ensemble keeps its own (rank-local) histogram
+        if (hist) {
+            if (!e->nbins) throw tapt::ConfigError("no histogram configured");
+            h.alloc(e->hist.n);
+            nccl_ok(api.all_reduce(e->hist.p, h.p, h.n, ncclUint64, ncclSum, c, e->stream), "ncclAllReduce(histograms)");
+        }
+        if (best) {
+            b.alloc(1);
+            ++g_launches;
+            k_best_min<<<1, 32, 0, e->stream>>>(e->best.p, (int)e->I, b.p);
+            CUDA_OK(cudaGetLastError());
+            nccl_ok(api.all_reduce(b.p, b.p, 1, ncclInt64, ncclMin, c, e->stream), "ncclAllReduce(best)");
+        }
+        if (obs) CUDA_OK(cudaMemcpyAsync(obs, o.p, o.n * sizeof(long long), cudaMemcpyDeviceToHost, e->stream));
+        if (hist)
+            CUDA_OK(cudaMemcpyAsync(hist, h.p, h.n * sizeof(uint64_t), cudaMemcpyDeviceToHost, e->stream));
+        if (best) CUDA_OK(cudaMemcpyAsync(best, b.p, sizeof(long long), cudaMemcpyDeviceToHost, e->stream));
+        CUDA_OK(cudaStreamSynchronize(e->stream));
     });
 }
 

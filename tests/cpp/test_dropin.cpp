@@ -7,6 +7,7 @@
 #include <iostream>
 #include <sstream>
 
+#include "tapt/distributed.hpp"
 #include "tapt/generator.hpp"
 #include "tapt/lattice.hpp"
 #include "tapt/mcmc.hpp"
@@ -354,6 +355,32 @@ static int gpu_tests() {
         runs.push_back(run_pt(ea, lad, c));
         auto rho = residual_energy(runs, -200.0, ea.n_spins(), true);
         for (std::size_t t = 1; t < rho.size(); ++t) CHECK(rho[t] <= rho[t - 1]);
+    }
+    // multi-GPU plumbing from C++: shards cover every instance once; a one-rank NCCL communicator's
+    // reductions equal the local sums (the only collectives of a sharded run)
+    {
+        for (int world : {1, 2, 3, 8}) {
+            std::uint64_t next = 0;
+            for (int r = 0; r < world; ++r) {
+                auto sh = Shard::of(4096, world, r);
+                CHECK(sh.offset == next);
+                next += sh.count;
+            }
+            CHECK(next == 4096);
+        }
+        Communicator comm(Communicator::unique_id(), 1, 0);
+        CHECK(comm.size() == 1);
+        Replicas reps(g, BetaLadder::geometric(0.2, 1.0, 6), 5);
+        throw_status(tapt_set_histogram(reps.handle(), -600, 8, 160));
+        tapt_schedule sc{40, 1, 4, 0};
+        throw_status(tapt_run(reps.handle(), &sc));
+        auto red = comm.allreduce_observables(reps.handle(), 6, 160);
+        std::vector<std::int64_t> local(6 * 5);
+        throw_status(tapt_get_observables(reps.handle(), local.data()));
+        CHECK(red.obs == local && red.obs[0] == 10);
+        std::uint64_t tot = 0;
+        for (auto v : red.hist) tot += v;
+        CHECK(tot == 6 * 10);
     }
     std::printf("gpu ok\n");
     return 0;

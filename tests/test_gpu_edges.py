@@ -215,3 +215,25 @@ def test_empty_model_dropin_sweep():
     s = np.array([1, -1, 1], np.int8)
     st, dE = T.gibbs_sweep(c, s, 2.0, 99, n_sweeps=2)
     assert st == 99 and np.all(dE == 0) and list(s) == [1, -1, 1]
+
+
+def test_nccl_reductions_one_rank_equal_local_sums():
+    """tapt_allreduce_observables over a one-rank NCCL communicator (the GPU box has one GPU; the
+    N > 1 host logic is covered by the gloo tests): per-slot observables, histograms and best energy
+    equal the local reductions, and the ensemble's own histogram stays rank-local."""
+    m = T.Model.lattice((16, 16))
+    e = T.Ensemble(m, np.linspace(0.2, 1.0, 8), n_instances=5, seed=3)
+    e.init_random()
+    e.set_histogram(-512, 8, 128)
+    e.run(50, swap_every=1, measure_every=5)
+    comm = T.NcclComm(T.NcclComm.unique_id(), 1, 0)
+    assert comm.size() == 1
+    r = T.allreduce_observables(e, comm)
+    assert np.array_equal(r["obs"], e.observables().sum(axis=0))
+    h = e.histogram()
+    assert np.array_equal(r["hist"], h) and h.sum() == 5 * 8 * 10
+    assert r["best"] == e.best().min()
+    comm.close()
+    with pytest.raises(T.NcclError):
+        T.lib().tapt_allreduce_observables  # noqa: B018 (symbol exists)
+        T._check(T.lib().tapt_allreduce_observables(e._h, None, None, None, None))
