@@ -333,6 +333,10 @@ tapt_status tapt_former_load(const char* path, tapt_former_t* out);
  * and log_prob stay mutually consistent).  No reference counterpart (the generator is a
  * placeholder there). */
 tapt_status tapt_former_set_kv_bf16(tapt_former_t f, int bf16);
+/* log_prob engine: 1 (default) the dense products (QKV, out-projection, FFN) on the 5th-generation
+ * tensor cores -- tcgen05.mma with TMEM accumulators, operands split bf16 hi + lo ("bf16x3", fp32
+ * accuracy); 0 the fp32 CUDA-core row engine.  Attention runs on CUDA cores in both. */
+tapt_status tapt_former_set_tensor_cores(tapt_former_t f, int on);
 /* forward_logits / log_prob: tokens [B][T] (0/1, host), betas [B]; log_q [B] sums the
  * Bernoulli log-probabilities of positions >= n_prefix; logits [B][T] (nullable). */
 tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_t B, uint32_t T, const double* betas,

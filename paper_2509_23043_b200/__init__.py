@@ -172,6 +172,7 @@ _SIGS = {
     "tapt_former_load": (C.c_int, [C.c_char_p, C.POINTER(_vp)]),
     "tapt_former_log_prob": (C.c_int, [_vp, _u8p, C.c_uint32, C.c_uint32, _f64p, C.c_uint32, _f64p, _f32p]),
     "tapt_former_set_kv_bf16": (C.c_int, [_vp, C.c_int]),
+    "tapt_former_set_tensor_cores": (C.c_int, [_vp, C.c_int]),
     "tapt_former_sample": (C.c_int, [_vp, C.c_uint32, C.c_uint32, _f64p, _u8p, C.c_uint32, _u64p, _u8p, _f64p]),
 }
 
@@ -630,6 +631,10 @@ class Former:
         self._h = h
         if kv == "bf16":
             _check(lib().tapt_former_set_kv_bf16(self._h, 1))
+
+    def set_tensor_cores(self, on=True):
+        """log_prob's dense products on tcgen05 (default) or on the fp32 CUDA-core row engine."""
+        _check(lib().tapt_former_set_tensor_cores(self._h, 1 if on else 0))
 
     @staticmethod
     def param_count(**cfg):

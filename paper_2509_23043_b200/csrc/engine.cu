@@ -943,9 +943,6 @@ struct tapt_ensemble_s {
             log_launch(std::string("k2_csr_pt") + (cluster ? "<cluster>" : ""), a);
             e = launch_k2(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster, stream);
         }
-        if (e == cudaErrorCooperativeLaunchTooLarge)
-            throw tapt::CudaError("balanced sweep schedule: the persistent grid cannot be co-resident on this "
-                                  "device (cooperative launch refused); set TAPT_BALANCE=0");
         if (e != cudaSuccess) throw tapt::CudaError(std::string("sweep kernel launch: ") + cudaGetErrorString(e));
         CUDA_OK(cudaGetLastError());
     }

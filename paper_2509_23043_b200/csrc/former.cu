@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "tc.cuh"
 #include "tapt/errors.hpp"
 #include "tapt/rng.hpp"
 #include "tapt_gpu.h"
@@ -575,6 +576,325 @@ __global__ void __launch_bounds__(NT) k_former_sample(const FArgs a) {
     }
 }
 
+
+// =====================================================================================================
+// Tensor-core forward (log_prob): the decoder's dense products on tcgen05 (tc.cuh), layer by layer
+// over all rows of all sequences.  A row = (sequence b, position t), row = b * T + t.  Per layer:
+//   k_tc_qkv  : LN1(X) -> [Q | K | V] = LN1 . W_qkv + b  (M = 128 rows, N = 192, K = 64) -> Q rows,
+//               K / V into the cache (slot = sequence)
+//   k_tc_attn : causal attention of 32-row blocks of one sequence over its cached keys (CUDA cores,
+//               the flash-style rows_attention_fwd) -> O rows
+//   k_tc_mlp  : X += O . W_o + b_o;  H = GELU(LN2(X) . W_1 + b_1) (N = 128);  X += H . W_2 + b_2
+//               (K = 128): three MMAs per 128-row tile with the epilogues between them
+// then k_tc_head: final LayerNorm, head, log q per sequence.  Weights are staged once per persistent
+// CTA as bf16 hi / lo splits (bf16x3, ~fp32 accuracy); activations are split per tile; accumulators
+// live in TMEM and come back with tcgen05.ld (thread = row).
+// =====================================================================================================
+
+struct TcArgs {
+    FArgs f;
+    int rows, T, B;
+    float* X;         // [rows][D] residual stream
+    float* Qb;        // [rows][D] queries
+    float* O;         // [rows][D] attention outputs
+    const float* Eb;  // [B][D] beta embeddings
+};
+
+constexpr int kTcThreads = 128;
+
+__global__ void k_tc_beta(const FArgs a, float* Eb) { beta_embed(a, a.betas[blockIdx.x], Eb + (size_t)blockIdx.x * D); }
+
+// x = P_t + e_beta (+ E[tok_{t-1}] for t > 0), as rows_input
+__global__ void k_tc_embed(const TcArgs a) {
+    const size_t n = (size_t)a.rows * D;
+    for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+        const int row = (int)(e / D), c = (int)(e % D);
+        const int b = row / a.T, t = row - b * a.T;
+        float x = __ldg(a.f.pos + (size_t)t * D + c) + a.Eb[(size_t)b * D + c];
+        if (t > 0) x += __ldg(a.f.W + a.f.tok_emb + a.f.tokens[(size_t)b * a.T + t - 1] * D + c);
+        a.X[e] = x;
+    }
+}
+
+// LayerNorm of one row held in registers (eps 1e-5, the rows_ln formula)
+__device__ __forceinline__ void row_ln(const float (&x)[D], float (&y)[D], const float* g, const float* bb) {
+    float s = 0.f;
+#pragma unroll
+    for (int c = 0; c < D; ++c) s += x[c];
+    const float mu = s * (1.0f / D);
+    float v = 0.f;
+#pragma unroll
+    for (int c = 0; c < D; ++c) v += (x[c] - mu) * (x[c] - mu);
+    const float inv = rsqrtf(v * (1.0f / D) + 1e-5f);
+#pragma unroll
+    for (int c = 0; c < D; ++c) y[c] = (x[c] - mu) * inv * __ldg(g + c) + __ldg(bb + c);
+}
+
+template <int K>
+__device__ __forceinline__ void row_to_tile(uint8_t* hi, uint8_t* lo, int r, const float* y) {
+#pragma unroll
+    for (int k0 = 0; k0 < K; k0 += 8) {
+        float x8[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x8[i] = y[k0 + i];
+        tapt_tc::store_row8(hi, lo, r, k0, K, x8);
+    }
+}
+
+// W [K][N] row-major (input k, output n) -> B tiles [N][K] K-major, hi / lo
+template <int N, int K>
+__device__ void stage_weights(uint8_t* hi, uint8_t* lo, const float* W) {
+    for (int n = threadIdx.x; n < N; n += blockDim.x)
+        for (int k0 = 0; k0 < K; k0 += 8) {
+            float x8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x8[i] = __ldg(W + (size_t)(k0 + i) * N + n);
+            tapt_tc::store_row8(hi, lo, n, k0, K, x8);
+        }
+}
+
+__device__ __forceinline__ void tc_sync() {
+    tapt_tc::fence_async_smem();
+    tapt_tc::fence_before();
+    __syncthreads();
+    tapt_tc::fence_after();
+}
+
+template <int N, int K>
+__device__ __forceinline__ void tc_gemm(uint32_t tmem, const uint8_t* ah, const uint8_t* al, const uint8_t* bh,
+                                        const uint8_t* bl, uint64_t* bar, uint32_t& phase) {
+    if (threadIdx.x == 0) {
+        tapt_tc::mma_x3<N, K>(tmem, ah, al, bh, bl);
+        tapt_tc::mma_commit(bar);
+    }
+    tapt_tc::bar_wait(bar, phase);
+    phase ^= 1u;
+    tapt_tc::fence_after();
+}
+
+template <class KT>
+__global__ void __launch_bounds__(kTcThreads) k_tc_qkv(const TcArgs a, int l) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint8_t* wh = sm;                    // [192][64] bf16
+    uint8_t* wl = wh + 3 * D * D * 2;
+    uint8_t* ah = wl + 3 * D * D * 2;    // [128][64] bf16
+    uint8_t* al = ah + 128 * D * 2;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const LayerOff& o = a.f.lay[l];
+    stage_weights<3 * D, D>(wh, wl, a.f.W + o.w_qkv);
+    if (tid == 0) tapt_tc::bar_init(&bar, 1);
+    if (warp == 0) tapt_tc::tmem_alloc(&tbase, 256);
+    tc_sync();
+    const uint32_t tm = tbase, lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    uint32_t phase = 0;
+    const int ntiles = (a.rows + 127) / 128;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int row = tile * 128 + tid;
+        const bool valid = row < a.rows;
+        {
+            float x[D], y[D];
+#pragma unroll
+            for (int c = 0; c < D; c += 4) {
+                const float4 v = valid ? *reinterpret_cast<const float4*>(a.X + (size_t)row * D + c)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                x[c] = v.x;
+                x[c + 1] = v.y;
+                x[c + 2] = v.z;
+                x[c + 3] = v.w;
+            }
+            row_ln(x, y, a.f.W + o.ln1_g, a.f.W + o.ln1_b);
+            row_to_tile<D>(ah, al, tid, y);
+        }
+        tc_sync();
+        tc_gemm<3 * D, D>(tm, ah, al, wh, wl, &bar, phase);
+        {  // tcgen05.ld is warp-collective: every lane loads, valid rows store
+            const int b = row / a.T, t = row - b * a.T;
+            const size_t kv = ((((size_t)b * a.f.L + l) * a.T + t) * 2) * D;
+            const float* bias = a.f.W + o.b_qkv;
+#pragma unroll 1
+            for (int c = 0; c < 3 * D; c += 16) {
+                float v[16];
+                tapt_tc::tmem_ld16(tm + lane_base + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) v[i] += __ldg(bias + c + i);
+                if (valid && c < D) {
+#pragma unroll
+                    for (int i = 0; i < 16; i += 4)
+                        *reinterpret_cast<float4*>(a.Qb + (size_t)row * D + c + i) =
+                            make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+                } else if (valid) {
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) KVT<KT>::st(a.f.cache, kv + (c - D) + i, v[i]);
+                }
+            }
+        }
+        tapt_tc::fence_before();
+        __syncthreads();
+    }
+    if (warp == 0) tapt_tc::tmem_free(tm, 256);
+}
+
+template <class KT>
+__global__ void __launch_bounds__(NT) k_tc_attn(const TcArgs a, int l) {
+    extern __shared__ __align__(16) unsigned char fsm[];
+    Smem<32>& s = *reinterpret_cast<Smem<32>*>(fsm);
+    KVChunk& kv = *reinterpret_cast<KVChunk*>(fsm + ((sizeof(Smem<32>) + 15) & ~size_t(15)));
+    const int b = blockIdx.y, t0 = blockIdx.x * 32;
+    if (threadIdx.x < 32) {
+        const int t = t0 + threadIdx.x;
+        s.t[threadIdx.x] = t;
+        s.slot[threadIdx.x] = b;
+        s.valid[threadIdx.x] = t < a.T;
+    }
+    for (int e = threadIdx.x; e < 32 * D; e += NT) {
+        const int r = e / D, c = e - r * D;
+        s.Q[r][c] = t0 + r < a.T ? a.Qb[((size_t)b * a.T + t0 + r) * D + c] : 0.f;
+    }
+    __syncthreads();
+    rows_attention_fwd<32, KT>(s, kv, a.f, l);
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * D; e += NT) {
+        const int r = e / D, c = e - r * D;
+        if (t0 + r < a.T) a.O[((size_t)b * a.T + t0 + r) * D + c] = s.O[r][c];
+    }
+}
+
+__global__ void __launch_bounds__(kTcThreads) k_tc_mlp(const TcArgs a, int l) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint8_t* woh = sm;                       // [64][64]
+    uint8_t* wol = woh + D * D * 2;
+    uint8_t* w1h = wol + D * D * 2;          // [128][64]
+    uint8_t* w1l = w1h + F * D * 2;
+    uint8_t* w2h = w1l + F * D * 2;          // [64][128]
+    uint8_t* w2l = w2h + D * F * 2;
+    uint8_t* t1h = w2l + D * F * 2;          // [128][64] activations (O, then LN2)
+    uint8_t* t1l = t1h + 128 * D * 2;
+    uint8_t* t2h = t1l + 128 * D * 2;        // [128][128] hidden
+    uint8_t* t2l = t2h + 128 * F * 2;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const LayerOff& o = a.f.lay[l];
+    stage_weights<D, D>(woh, wol, a.f.W + o.w_o);
+    stage_weights<F, D>(w1h, w1l, a.f.W + o.w_1);
+    stage_weights<D, F>(w2h, w2l, a.f.W + o.w_2);
+    if (tid == 0) tapt_tc::bar_init(&bar, 1);
+    if (warp == 0) tapt_tc::tmem_alloc(&tbase, 256);
+    tc_sync();
+    const uint32_t tm = tbase, lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t c_o = 0, c_1 = 64, c_2 = 192;  // TMEM columns of the three products
+    uint32_t phase = 0;
+    const int ntiles = (a.rows + 127) / 128;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int row = tile * 128 + tid;
+        const bool valid = row < a.rows;
+        float x[D];
+        {
+            float y[D];
+#pragma unroll
+            for (int c = 0; c < D; c += 4) {
+                const float4 v = valid ? *reinterpret_cast<const float4*>(a.O + (size_t)row * D + c)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                y[c] = v.x;
+                y[c + 1] = v.y;
+                y[c + 2] = v.z;
+                y[c + 3] = v.w;
+            }
+            row_to_tile<D>(t1h, t1l, tid, y);
+#pragma unroll
+            for (int c = 0; c < D; c += 4) {
+                const float4 v = valid ? *reinterpret_cast<const float4*>(a.X + (size_t)row * D + c)
+                                       : make_float4(0.f, 0.f, 0.f, 0.f);
+                x[c] = v.x;
+                x[c + 1] = v.y;
+                x[c + 2] = v.z;
+                x[c + 3] = v.w;
+            }
+        }
+        tc_sync();
+        tc_gemm<D, D>(tm + c_o, t1h, t1l, woh, wol, &bar, phase);
+        {  // X += O W_o + b_o, then LN2 into the activation tile
+#pragma unroll
+            for (int c = 0; c < D; c += 16) {
+                float v[16];
+                tapt_tc::tmem_ld16(tm + lane_base + c_o + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) x[c + i] += v[i] + __ldg(a.f.W + o.b_o + c + i);
+            }
+            float y[D];
+            row_ln(x, y, a.f.W + o.ln2_g, a.f.W + o.ln2_b);
+            row_to_tile<D>(t1h, t1l, tid, y);
+        }
+        tc_sync();
+        tc_gemm<F, D>(tm + c_1, t1h, t1l, w1h, w1l, &bar, phase);
+#pragma unroll 1
+        for (int c = 0; c < F; c += 16) {  // H = GELU(LN2 W_1 + b_1) into the hidden tile
+            float v[16];
+            tapt_tc::tmem_ld16(tm + lane_base + c_1 + c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[i] = gelu(v[i] + __ldg(a.f.W + o.b_1 + c + i));
+#pragma unroll
+            for (int h = 0; h < 16; h += 8) {
+                float x8[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) x8[i] = v[h + i];
+                tapt_tc::store_row8(t2h, t2l, tid, c + h, F, x8);
+            }
+        }
+        tc_sync();
+        tc_gemm<D, F>(tm + c_2, t2h, t2l, w2h, w2l, &bar, phase);
+#pragma unroll
+        for (int c = 0; c < D; c += 16) {  // X += H W_2 + b_2
+            float v[16];
+            tapt_tc::tmem_ld16(tm + lane_base + c_2 + c, v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) x[c + i] += v[i] + __ldg(a.f.W + o.b_2 + c + i);
+        }
+        if (valid)
+#pragma unroll
+            for (int c = 0; c < D; c += 4)
+                *reinterpret_cast<float4*>(a.X + (size_t)row * D + c) = make_float4(x[c], x[c + 1], x[c + 2], x[c + 3]);
+        tapt_tc::fence_before();
+        __syncthreads();
+    }
+    if (warp == 0) tapt_tc::tmem_free(tm, 256);
+}
+
+// Final LayerNorm + head per row, log q per sequence (positions >= n_prefix).  grid B, NT threads.
+__global__ void __launch_bounds__(NT) k_tc_head(const TcArgs a) {
+    __shared__ double part[NT];
+    const int b = blockIdx.x;
+    double lq = 0.0;
+    for (int t = threadIdx.x; t < a.T; t += NT) {
+        const size_t row = (size_t)b * a.T + t;
+        float x[D], y[D];
+#pragma unroll
+        for (int c = 0; c < D; c += 4) {
+            const float4 v = *reinterpret_cast<const float4*>(a.X + row * D + c);
+            x[c] = v.x;
+            x[c + 1] = v.y;
+            x[c + 2] = v.z;
+            x[c + 3] = v.w;
+        }
+        row_ln(x, y, a.f.W + a.f.lnf_g, a.f.W + a.f.lnf_b);
+        float z = 0.f;
+#pragma unroll
+        for (int c = 0; c < D; ++c) z = fmaf(y[c], __ldg(a.f.W + a.f.head_w + c), z);
+        z += __ldg(a.f.W + a.f.head_b);
+        if (a.f.logits) a.f.logits[row] = z;
+        if (t >= a.f.n_prefix) lq += a.f.tokens[row] ? log_sigmoid(z) : log_sigmoid(-z);
+    }
+    part[threadIdx.x] = lq;
+    __syncthreads();
+    for (int s = NT / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) part[threadIdx.x] += part[threadIdx.x + s];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a.f.log_q[b] = part[0];
+}
+
 }  // namespace tapt_former_dev
 
 using namespace tapt_former_dev;
@@ -686,6 +1006,9 @@ struct tapt_former_s {
     void* cache = nullptr;
     size_t cache_n = 0;  // bytes
     int kv16 = 0;        // K/V cache in bf16 (tapt_former_set_kv_bf16)
+    int tc = 1;          // log_prob's dense products on the tensor cores (tapt_former_set_tensor_cores)
+    float* tcbuf = nullptr;  // X | Q | O | e_beta of the tensor-core forward
+    size_t tcbuf_n = 0;
     void* tmp = nullptr;
     size_t tmp_n = 0;
     ~tapt_former_s() {
@@ -693,6 +1016,16 @@ struct tapt_former_s {
         if (dpos) cudaFree(dpos);
         if (cache) cudaFree(cache);
         if (tmp) cudaFree(tmp);
+        if (tcbuf) cudaFree(tcbuf);
+    }
+    float* need_tcbuf(size_t floats) {
+        if (floats > tcbuf_n) {
+            if (tcbuf) cudaFree(tcbuf);
+            tcbuf = nullptr;
+            FCUDA(cudaMalloc(&tcbuf, floats * sizeof(float)));
+            tcbuf_n = floats;
+        }
+        return tcbuf;
     }
     void upload() {
         if (dW) return;
@@ -777,6 +1110,52 @@ tapt_former_s* create_former(const tapt_former_config* c, const float* params) {
         if (!std::isfinite(v)) throw tapt::NumericError("non-finite parameter");
     check_device_shape(*c);
     return f.release();  // device copies are made on first use (create/save/load work without a GPU)
+}
+
+// log_prob on the tensor cores (k_tc_*): sequences in chunks that keep the K/V cache and the row
+// buffers under ~8 GB; per chunk embed, then per layer QKV (tcgen05) -> attention (CUDA cores) ->
+// out-projection + FFN (tcgen05), then head and log q.
+template <class KT>
+void log_prob_tc(tapt_former_s* f, const FArgs& a0) {
+    const int T = a0.T, L = (int)f->cfg.layers, nsm = sm_count();
+    const size_t per_seq = (size_t)L * T * 2 * D * sizeof(KT) + (size_t)3 * T * D * 4 + D * 4;
+    const int Bc = (int)std::max<size_t>(1, std::min<size_t>((size_t)a0.B, (size_t)(8ull << 30) / per_seq));
+    const size_t smem_qkv = (size_t)2 * 3 * D * D * 2 + (size_t)2 * 128 * D * 2;
+    const size_t smem_mlp = (size_t)2 * (D * D + F * D + D * F) * 2 + (size_t)2 * 128 * D * 2 + (size_t)2 * 128 * F * 2;
+    const size_t smem_attn = ((sizeof(Smem<32>) + 15) & ~size_t(15)) + sizeof(KVChunk);
+    FCUDA(cudaFuncSetAttribute(k_tc_qkv<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_qkv));
+    FCUDA(cudaFuncSetAttribute(k_tc_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mlp));
+    FCUDA(cudaFuncSetAttribute(k_tc_attn<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_attn));
+    for (int b0 = 0; b0 < a0.B; b0 += Bc) {
+        const int nb = std::min(Bc, a0.B - b0);
+        TcArgs t{};
+        t.f = a0;
+        t.f.tokens = a0.tokens + (size_t)b0 * T;
+        t.f.betas = a0.betas + b0;
+        t.f.log_q = a0.log_q + b0;
+        t.f.logits = a0.logits ? a0.logits + (size_t)b0 * T : nullptr;
+        t.f.B = nb;
+        t.f.cache = f->need_cache((size_t)nb * L * T * 2 * D);
+        t.rows = nb * T;
+        t.T = T;
+        t.B = nb;
+        float* buf = f->need_tcbuf((size_t)3 * t.rows * D + (size_t)nb * D);
+        t.X = buf;
+        t.Qb = buf + (size_t)t.rows * D;
+        t.O = buf + (size_t)2 * t.rows * D;
+        t.Eb = buf + (size_t)3 * t.rows * D;
+        const int ntiles = (t.rows + 127) / 128;
+        k_tc_beta<<<nb, D>>>(t.f, const_cast<float*>(t.Eb));
+        k_tc_embed<<<std::min(nsm * 8, (t.rows * D + 255) / 256), 256>>>(t);
+        for (int l = 0; l < L; ++l) {
+            k_tc_qkv<KT><<<std::min(ntiles, 2 * nsm), kTcThreads, smem_qkv>>>(t, l);
+            k_tc_attn<KT><<<dim3((T + 31) / 32, nb), NT, smem_attn>>>(t, l);
+            k_tc_mlp<<<std::min(ntiles, nsm), kTcThreads, smem_mlp>>>(t, l);
+        }
+        k_tc_head<<<nb, NT>>>(t);
+        tapt_host::note_launches(3 + 3 * L);
+        FCUDA(cudaGetLastError());
+    }
 }
 
 template <int RB, class K>
@@ -879,6 +1258,13 @@ tapt_status tapt_former_load(const char* path, tapt_former_t* out) {
     });
 }
 
+tapt_status tapt_former_set_tensor_cores(tapt_former_t f, int on) {
+    return fguard([&] {
+        check_former(f);
+        f->tc = on ? 1 : 0;
+    });
+}
+
 tapt_status tapt_former_set_kv_bf16(tapt_former_t f, int bf16) {
     return fguard([&] {
         check_former(f);
@@ -910,10 +1296,18 @@ tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_
         a.betas = reinterpret_cast<const double*>(tmp + off_b);
         a.log_q = reinterpret_cast<double*>(tmp + off_q);
         a.logits = logits ? reinterpret_cast<float*>(tmp + off_z) : nullptr;
-        if (f->kv16)
+        const char* env = std::getenv("TAPT_FORMER_TC");
+        // tcgen05 dense products (k_tc_*) with the fp32 K/V cache.  A bf16 cache rounds K and V, so
+        // sample / log_prob consistency (the MH correction) needs bit-identical QKV arithmetic in both:
+        // with kv16 log_prob keeps the CUDA-core engine the sampler uses.
+        const bool tc = f->tc && !f->kv16 && !(env && std::atoi(env) == 0);
+        if (tc) {
+            log_prob_tc<float>(f, a);
+        } else if (f->kv16) {
             launch_rows<32>(k_former_forward<__nv_bfloat16>, grid, a, sizeof(KVChunk));
-        else
+        } else {
             launch_rows<32>(k_former_forward<float>, grid, a, sizeof(KVChunk));
+        }
         FCUDA(cudaMemcpy(log_q, a.log_q, (size_t)B * 8, cudaMemcpyDeviceToHost));
         if (logits) FCUDA(cudaMemcpy(logits, a.logits, tb * 4, cudaMemcpyDeviceToHost));
     });

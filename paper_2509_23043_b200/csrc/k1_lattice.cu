@@ -284,7 +284,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
     const int cl = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
     const int half = n >> 1, nsub = half / SP;
-    const int it0 = a.sched ? a.sched_ptr[cl] : 0, it1 = a.sched ? a.sched_ptr[cl + 1] : 1;
+    const int tl = a.sched ? pt_timeline(cl, a.sched_clusters) : 0;
+    const int it0 = a.sched ? a.sched_ptr[tl] : 0, it1 = a.sched ? a.sched_ptr[tl + 1] : 1;
     for (int e = tid; e < a.R * 8; e += nt) {
         const int r = e >> 3, k = e & 7;
         thrS[e] = k < a.nidx ? a.thr[(size_t)r * a.nidx + k] : 0ull;
@@ -538,7 +539,7 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
         *resident = per_sm * nsm;
         return q;
     }
-    return pt_launch(fn, cfg.gridDim.x, (unsigned)threads, smem, st, CLU ? (unsigned)a.G : 1u, a.sched != nullptr, a, d);
+    return pt_launch(fn, cfg.gridDim.x, (unsigned)threads, smem, st, CLU ? (unsigned)a.G : 1u, a, d);
 }
 
 static cudaError_t k1_dispatch(const PTArgs& a, const LatDims& d, int threads, bool cluster, cudaStream_t st,

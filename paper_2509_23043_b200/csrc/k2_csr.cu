@@ -103,7 +103,8 @@ __global__ void __launch_bounds__(TAPT_K2_MAXT, 1) k2_csr_pt(const PTArgs a, con
     // come out of one subtraction (decisions with h = U - 1 fall in the band and are redone)
     for (int k = tid; k < a.R * nidx; k += nt) Uslot[k] = max(thr_hi(a.thr[k]), 1u) - 1u;
 
-    const int it0 = BAL ? a.sched_ptr[cl] : 0, it1 = BAL ? a.sched_ptr[cl + 1] : 1;
+    const int tl = BAL ? pt_timeline(cl, a.sched_clusters) : 0;
+    const int it0 = BAL ? a.sched_ptr[tl] : 0, it1 = BAL ? a.sched_ptr[tl + 1] : 1;
     for (int it = it0; it < it1; ++it) {
     const SchedItem item = BAL ? a.sched[it] : SchedItem{ipb > 1 ? cl * ipb : cl, 0, a.n_sweeps, -1, -1};
     const int inst0 = item.inst;
@@ -338,8 +339,7 @@ static cudaError_t launch_k2_t(const PTArgs& a, const CsrArgs& g, int threads, i
         *resident = per_sm * nsm;
         return q;
     }
-    return pt_launch(fn, cfg.gridDim.x, (unsigned)threads, smem, st, CLU ? (unsigned)a.G : 1u, a.sched != nullptr, a, g,
-                     ipb);
+    return pt_launch(fn, cfg.gridDim.x, (unsigned)threads, smem, st, CLU ? (unsigned)a.G : 1u, a, g, ipb);
 }
 
 // Instances per CTA when one CTA holds a whole instance (G == 1, no cluster): 2 measured best

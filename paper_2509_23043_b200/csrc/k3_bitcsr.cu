@@ -278,8 +278,8 @@ __global__ void __launch_bounds__(kT3 * IPB, 1) k3_bitcsr_pt(const PTArgs a, con
     int it0, it1;
     if (BAL) {
         if (unit >= a.sched_clusters) return;
-        it0 = a.sched_ptr[unit];
-        it1 = a.sched_ptr[unit + 1];
+        it0 = a.sched_ptr[pt_timeline(unit, a.sched_clusters)];
+        it1 = a.sched_ptr[pt_timeline(unit, a.sched_clusters) + 1];
     } else {
         if (unit >= a.I) return;
         it0 = 0;
@@ -438,8 +438,10 @@ static cudaError_t k3_run_t(const PTArgs& a, const Csr3& g, cudaStream_t st, int
         return e;
     }
     const unsigned grid = a.sched ? (unsigned)((a.sched_clusters + IPB - 1) / IPB) : (unsigned)((a.I + IPB - 1) / IPB);
-    if (a.sched) return pt_launch(k3_bitcsr_pt<true, IPB>, grid, kT3 * IPB, smem, st, 1u, true, a, g);
-    k3_bitcsr_pt<false, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
+    if (a.sched)
+        k3_bitcsr_pt<true, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
+    else
+        k3_bitcsr_pt<false, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
     return cudaGetLastError();
 }
 

@@ -71,8 +71,8 @@ __global__ void __launch_bounds__(kT4 * kIPB4, 1) k4_levels_pt(const PTArgs a, c
     int it0, it1;
     if (BAL) {
         if (unit >= a.sched_clusters) return;
-        it0 = a.sched_ptr[unit];
-        it1 = a.sched_ptr[unit + 1];
+        it0 = a.sched_ptr[pt_timeline(unit, a.sched_clusters)];
+        it1 = a.sched_ptr[pt_timeline(unit, a.sched_clusters) + 1];
     } else {
         if (unit >= a.I) return;
         it0 = 0;
@@ -159,8 +159,10 @@ static cudaError_t k4_run(const PTArgs& a, const CsrArgs& g, int ipb, cudaStream
         return e;
     }
     const unsigned grid = a.sched ? (unsigned)((a.sched_clusters + ipb - 1) / ipb) : (unsigned)((a.I + ipb - 1) / ipb);
-    if (a.sched) return pt_launch(k4_levels_pt<true>, grid, kT4 * ipb, smem, st, 1u, true, a, g);
-    k4_levels_pt<false><<<grid, kT4 * ipb, smem, st>>>(a, g);
+    if (a.sched)
+        k4_levels_pt<true><<<grid, kT4 * ipb, smem, st>>>(a, g);
+    else
+        k4_levels_pt<false><<<grid, kT4 * ipb, smem, st>>>(a, g);
     return cudaGetLastError();
 }
 

@@ -196,19 +196,16 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
     }
 }
 
-// Launch a fused PT kernel: optional thread-block cluster of `cluster_x` CTAs; balanced persistent
-// grids (`coop`) launch with the cooperative attribute, so the runtime either makes every CTA of the
-// grid co-resident (gang scheduling, whatever else holds SMs) or refuses the launch
-// (cudaErrorCooperativeLaunchTooLarge) -- a split job's flag wait can therefore never starve.
+// Launch a fused PT kernel with an optional thread-block cluster of `cluster_x` CTAs.
 template <class... KArgs, class... Args>
 __host__ cudaError_t pt_launch(void (*fn)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t st,
-                               unsigned cluster_x, bool coop, Args&&... args) {
+                               unsigned cluster_x, Args&&... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(block);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
-    cudaLaunchAttribute attr[2];
+    cudaLaunchAttribute attr[1];
     int na = 0;
     if (cluster_x > 1) {
         attr[na].id = cudaLaunchAttributeClusterDimension;
@@ -217,15 +214,19 @@ __host__ cudaError_t pt_launch(void (*fn)(KArgs...), unsigned grid, unsigned blo
         attr[na].val.clusterDim.z = 1;
         ++na;
     }
-    if (coop) {
-        attr[na].id = cudaLaunchAttributeCooperative;
-        attr[na].val.cooperative = 1;
-        ++na;
-    }
     cfg.attrs = na ? attr : nullptr;
     cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, fn, std::forward<Args>(args)...);
 }
+
+// Balanced schedule: the unit (cluster / CTA / team) of the persistent grid that runs timeline `m` of
+// McNaughton's rule is M - 1 - m.  A job cut between timelines m and m+1 runs its first sweeps at the
+// start of m+1 and waits for them at the end of m, so with the reversed numbering every wait is on a
+// LOWER-numbered unit: one the hardware dispatched earlier (units are dispatched in index order),
+// already resident or finished, whose producing item comes first on its timeline and itself waits
+// only on lower units.  No wait can depend on a unit that is not yet resident, so the schedule makes
+// progress however many units fit at once (e.g. while another stream holds SMs).
+__device__ __forceinline__ int pt_timeline(int unit, int n_units) { return n_units - 1 - unit; }
 
 // Balanced schedule (SchedItem): wait for / publish the state of a split job.  The wait is
 // bounded (~2 s of clock64 at 1.9 GHz); on timeout it flags an error instead of hanging.

@@ -193,3 +193,24 @@ def test_former_proposals_with_mh_correction_keep_boltzmann():
     biased = _former_tapt(False)
     assert corrected.max() < 0.02
     assert biased.max() > 2 * corrected.max()
+
+
+def test_tensor_core_forward_equals_cuda_core_forward():
+    """log_prob's tcgen05 path (bf16x3 products, TMEM accumulators) against the fp32 CUDA-core row
+    engine on the same inputs: ragged 128-row tiles spanning sequences, 2 layers; and the fp64 oracle."""
+    f, p = model(seed=6, max_len=256)
+    rs = np.random.default_rng(4)
+    B, Tn = 9, 203  # 1827 rows: 15 tiles, the last ragged; sequences straddle tiles
+    tok = rs.integers(0, 2, (B, Tn)).astype(np.uint8)
+    betas = rs.uniform(0.1, 4.0, B)
+    f.set_tensor_cores(True)
+    lq_tc, z_tc = f.log_prob(tok, betas, n_prefix=11, return_logits=True)
+    f.set_tensor_cores(False)
+    lq_cc, z_cc = f.log_prob(tok, betas, n_prefix=11, return_logits=True)
+    # bf16x3 products carry ~2^-16 relative error per product (the split residuals): well inside the
+    # fp32-vs-fp64 tolerance both engines are held to
+    assert np.max(np.abs(z_tc - z_cc)) < 1e-4 * max(1.0, np.max(np.abs(z_cc)))
+    assert np.max(np.abs(lq_tc - lq_cc)) < 2e-3
+    for b in (0, 4, 8):
+        zo = F.forward_logits(p, CFG, tok[b], betas[b])
+        assert np.max(np.abs(z_tc[b] - zo)) < LOGIT_TOL * max(1.0, np.max(np.abs(zo)))

@@ -102,9 +102,10 @@ def test_balanced_schedule_matches_oracle_on_a_split_instance():
 
 
 def test_balanced_schedule_with_a_competing_kernel(monkeypatch):
-    """Forward progress: the persistent grid launches cooperatively, so while another stream keeps
-    the SMs busy it either runs with every CTA co-resident (and stays bit-exact) or the launch is
-    refused -- it never starts half-resident and waits on a split job's flag."""
+    """Forward progress: the persistent grid numbers McNaughton's timelines in reverse (pt_timeline),
+    so every split-job wait is on a lower-numbered, earlier-dispatched unit.  While another stream
+    keeps the SMs busy and only part of the grid is resident, the run must still finish (no 2 s
+    wait-timeout error) and stay bit-identical to the plain launch."""
     import torch
     dims, betas, I = (64, 64), H.geometric(0.2, 1.0, 32), 200
     ref = _run(monkeypatch, False, T.Model.lattice(dims), betas, I)
@@ -122,9 +123,6 @@ def test_balanced_schedule_with_a_competing_kernel(monkeypatch):
         e.generate_proposals(np.arange(8), None, refine=2)
         e.run(41, swap_every=2, measure_every=5, measure_from=10)
         st = _state(e)
-    except T.CudaError as err:  # refused at launch: acceptable, but it must say so
-        assert "cooperative" in str(err)
-        return
     finally:
         torch.cuda.synchronize()
     assert any("balanced" in x for x in e.launch_log())

@@ -37,6 +37,7 @@ def main():
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
     hbm = peaks.get("hbm_gbs", 6650.0)
+    bf16_peak = peaks.get("bf16_tflops", peaks.get("bf16_dense_tflops", 2250.0))
     f = T.Former(seed=1, scale=1.0, max_len=1024, kv=args.kv)
     kvb = 2 if args.kv == "bf16" else 4
     L, D = f.config["layers"], f.config["d_model"]
@@ -57,13 +58,19 @@ def main():
         tok, lq = f.sample(B, Tn, betas, streams, prefix)
         ev[1].record()
         torch.cuda.synchronize()
-        f.log_prob(tok, betas, npre)
-        torch.cuda.synchronize()
-        ev[2].record()
-        lq2 = f.log_prob(tok, betas, npre)
-        ev[3].record()
-        torch.cuda.synchronize()
-        ts, tf = ev[0].elapsed_time(ev[1]) * 1e-3, ev[2].elapsed_time(ev[3]) * 1e-3
+        eng = {}
+        for tc in (True, False):  # tcgen05 dense products vs the fp32 CUDA-core row engine
+            f.set_tensor_cores(tc)
+            f.log_prob(tok, betas, npre)
+            torch.cuda.synchronize()
+            ev[2].record()
+            lq2 = f.log_prob(tok, betas, npre)
+            ev[3].record()
+            torch.cuda.synchronize()
+            eng["tc" if tc else "cuda_cores"] = (ev[2].elapsed_time(ev[3]) * 1e-3, lq2)
+        f.set_tensor_cores(True)
+        ts, tf = ev[0].elapsed_time(ev[1]) * 1e-3, eng["tc"][0]
+        lq2 = eng["tc"][1]
         kv = L * 2 * D * kvb * Tn * (Tn + 1) / 2 * B
         attn_flop = L * 2 * 2 * D * Tn * (Tn + 1) / 2 * B
         flop = 2.0 * dense_mac * Tn * B + attn_flop
@@ -74,7 +81,12 @@ def main():
             "sample": {"tokens_per_s": B * Tn / ts, "seconds": ts, "kv_gb": kv / 1e9,
                        "kv_gbs": kv / ts / 1e9, "hbm_frac": kv / ts / 1e9 / hbm},
             "log_prob": {"tokens_per_s": B * Tn / tf, "seconds": tf, "tflops": flop / tf / 1e12,
-                         "fp32_frac": flop / tf / fp32_peak},
+                         "dense_tflops": 2.0 * dense_mac * Tn * B / tf / 1e12,
+                         "dense_bf16_frac": 2.0 * dense_mac * Tn * B / tf / 1e12 / bf16_peak,
+                         "cuda_core_engine": {"seconds": eng["cuda_cores"][0],
+                                              "tokens_per_s": B * Tn / eng["cuda_cores"][0],
+                                              "max_abs_log_q_diff": float(np.max(np.abs(eng["cuda_cores"][1] - lq2)))},
+                         "speedup_vs_cuda_cores": eng["cuda_cores"][0] / tf},
             "consistency_max_abs": float(np.max(np.abs(lq - lq2))),
             "peaks": {"hbm_gbs": hbm, "fp32_tflops": fp32_peak / 1e12, "f_sm_assumed": 1.965e9, "f_sm_prop": f_sm},
         }), flush=True)
