@@ -862,6 +862,151 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_mlp(const TcArgs a, int l) {
     if (warp == 0) tapt_tc::tmem_free(tm, 256);
 }
 
+// Causal attention of one 128-position query block of one sequence on the tensor cores (flash
+// style).  Per 64-key chunk: K and V of both heads are staged as bf16 hi / lo tiles (V transposed:
+// [dim][key], K-major for the PV product); per head S = Q K^T (M 128, N 64, K 32) lands in TMEM,
+// each thread (= query row) reads its 64 scores, applies the causal mask and the online softmax,
+// writes P as a hi / lo tile, and P V (M 128, N 32, K 64) comes back from TMEM into the row's fp32
+// output accumulator.  grid (ceil(T / 128), B), 128 threads.
+constexpr int kAttnKeys = 64;
+
+__global__ void __launch_bounds__(kTcThreads) k_tc_attn_mma(const TcArgs a, int l) {
+    extern __shared__ __align__(128) uint8_t sm[];
+    uint8_t* qh = sm;                                  // [2 heads][128][32] hi
+    uint8_t* ql = qh + 2 * 128 * DH * 2;               //                    lo
+    uint8_t* kh = ql + 2 * 128 * DH * 2;               // [2][64 keys][32] hi
+    uint8_t* kl = kh + 2 * kAttnKeys * DH * 2;
+    uint8_t* vh = kl + 2 * kAttnKeys * DH * 2;         // [2][32 dims][64 keys] hi
+    uint8_t* vl = vh + 2 * DH * kAttnKeys * 2;
+    uint8_t* ph = vl + 2 * DH * kAttnKeys * 2;         // [128][64 keys] hi
+    uint8_t* pl = ph + 128 * kAttnKeys * 2;
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tbase;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const int b = blockIdx.y, q0 = blockIdx.x * 128, t = q0 + tid;
+    const int tq = min(t, a.T - 1);  // rows past the sequence end attend like its last row (not stored)
+    const size_t base = (((size_t)b * a.f.L + l) * a.T) * 2 * D;
+    constexpr int QT = 128 * DH * 2, KT = kAttnKeys * DH * 2, VT = DH * kAttnKeys * 2;
+    {  // Q of this row, both heads
+        const float* q = a.Qb + ((size_t)b * a.T + tq) * D;
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+            for (int k0 = 0; k0 < DH; k0 += 8) {
+                float x8[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) x8[i] = q[h * DH + k0 + i];
+                tapt_tc::store_row8(qh + h * QT, ql + h * QT, tid, k0, DH, x8);
+            }
+    }
+    if (tid == 0) tapt_tc::bar_init(&bar, 1);
+    if (warp == 0) tapt_tc::tmem_alloc(&tbase, 128);
+    tc_sync();
+    const uint32_t tm = tbase, lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t cS = 0, cO = 64;  // TMEM columns: scores [0, 64), P V [64, 96)
+    const float scale = rsqrtf((float)DH);
+    float m[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f}, o[2][DH];
+#pragma unroll
+    for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int d = 0; d < DH; ++d) o[h][d] = 0.f;
+    uint32_t phase = 0;
+    const int kmax = min(q0 + 127, a.T - 1);
+    for (int c0 = 0; c0 <= kmax; c0 += kAttnKeys) {
+        // stage K (rows = keys) and V^T (rows = dims) of both heads for keys c0 .. c0 + 63
+        {
+            const int j = tid >> 1;
+            if ((tid & 1) == 0) {  // K of key c0 + j
+                const bool ok = c0 + j <= kmax;
+                const float* kr = a.f.cache ? reinterpret_cast<const float*>(a.f.cache) + base + (size_t)(c0 + j) * 2 * D
+                                            : nullptr;
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int k0 = 0; k0 < DH; k0 += 8) {
+                        float x8[8];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) x8[i] = ok ? kr[h * DH + k0 + i] : 0.f;
+                        tapt_tc::store_row8(kh + h * KT, kl + h * KT, j, k0, DH, x8);
+                    }
+            }
+        }
+        for (int task = tid; task < 2 * DH * (kAttnKeys / 8); task += kTcThreads) {  // V^T: (dim, 8-key group)
+            const int dim = task % (2 * DH), g = task / (2 * DH), h = dim / DH, d = dim - h * DH;
+            float x8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int key = c0 + 8 * g + i;
+                x8[i] = key <= kmax ? reinterpret_cast<const float*>(a.f.cache)[base + (size_t)key * 2 * D + D + dim]
+                                    : 0.f;
+            }
+            tapt_tc::store_row8(vh + h * VT, vl + h * VT, d, 8 * g, kAttnKeys, x8);
+        }
+        tc_sync();
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // unrolled: o[h] stays in registers
+            tc_gemm<kAttnKeys, DH>(tm + cS, qh + h * QT, ql + h * QT, kh + h * KT, kl + h * KT, &bar, phase);
+            // two passes over the TMEM scores (row max, then exp / sum / P), keeping 16 in registers
+            float mx = m[h];
+#pragma unroll
+            for (int c = 0; c < kAttnKeys; c += 16) {
+                float v[16];
+                tapt_tc::tmem_ld16(tm + lane_base + cS + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i)
+                    if (c0 + c + i <= tq) mx = fmaxf(mx, v[i] * scale);
+            }
+            const float corr = __expf(m[h] - mx);
+            float ps = 0.f;
+#pragma unroll
+            for (int c = 0; c < kAttnKeys; c += 16) {
+                float v[16];
+                tapt_tc::tmem_ld16(tm + lane_base + cS + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) {
+                    v[i] = c0 + c + i <= tq ? __expf(v[i] * scale - mx) : 0.f;
+                    ps += v[i];
+                }
+#pragma unroll
+                for (int k0 = 0; k0 < 16; k0 += 8) {
+                    float x8[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) x8[i] = v[k0 + i];
+                    tapt_tc::store_row8(ph, pl, tid, c + k0, kAttnKeys, x8);
+                }
+            }
+            lsum[h] = lsum[h] * corr + ps;
+            m[h] = mx;
+            tc_sync();
+            tc_gemm<DH, kAttnKeys>(tm + cO, ph, pl, vh + h * VT, vl + h * VT, &bar, phase);
+#pragma unroll
+            for (int c = 0; c < DH; c += 16) {
+                float v[16];
+                tapt_tc::tmem_ld16(tm + lane_base + cO + c, v);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o[h][c + i] = o[h][c + i] * corr + v[i];
+            }
+            tapt_tc::fence_before();
+            __syncthreads();  // P and the TMEM columns are rewritten by the next head / chunk
+            tapt_tc::fence_after();
+        }
+    }
+    if (t < a.T) {
+        float* dst = a.O + ((size_t)b * a.T + t) * D;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const float inv = 1.f / lsum[h];
+#pragma unroll
+            for (int d = 0; d < DH; d += 4)
+                *reinterpret_cast<float4*>(dst + h * DH + d) =
+                    make_float4(o[h][d] * inv, o[h][d + 1] * inv, o[h][d + 2] * inv, o[h][d + 3] * inv);
+        }
+    }
+    tapt_tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tapt_tc::tmem_free(tm, 128);
+}
+
 // Final LayerNorm + head per row, log q per sequence (positions >= n_prefix).  grid B, NT threads.
 __global__ void __launch_bounds__(NT) k_tc_head(const TcArgs a) {
     __shared__ double part[NT];
@@ -1126,6 +1271,12 @@ void log_prob_tc(tapt_former_s* f, const FArgs& a0) {
     FCUDA(cudaFuncSetAttribute(k_tc_qkv<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_qkv));
     FCUDA(cudaFuncSetAttribute(k_tc_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mlp));
     FCUDA(cudaFuncSetAttribute(k_tc_attn<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_attn));
+    // attention products on the tensor cores too (fp32 cache only); TAPT_FORMER_ATTN_TC=0: CUDA cores
+    const char* ae = std::getenv("TAPT_FORMER_ATTN_TC");
+    const bool attn_tc = sizeof(KT) == 4 && !(ae && std::atoi(ae) == 0);
+    const size_t smem_amma = (size_t)2 * (2 * 128 * DH * 2) + (size_t)2 * (2 * kAttnKeys * DH * 2) +
+                             (size_t)2 * (2 * DH * kAttnKeys * 2) + (size_t)2 * (128 * kAttnKeys * 2);
+    FCUDA(cudaFuncSetAttribute(k_tc_attn_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_amma));
     for (int b0 = 0; b0 < a0.B; b0 += Bc) {
         const int nb = std::min(Bc, a0.B - b0);
         TcArgs t{};
@@ -1149,7 +1300,10 @@ void log_prob_tc(tapt_former_s* f, const FArgs& a0) {
         k_tc_embed<<<std::min(nsm * 8, (t.rows * D + 255) / 256), 256>>>(t);
         for (int l = 0; l < L; ++l) {
             k_tc_qkv<KT><<<std::min(ntiles, 2 * nsm), kTcThreads, smem_qkv>>>(t, l);
-            k_tc_attn<KT><<<dim3((T + 31) / 32, nb), NT, smem_attn>>>(t, l);
+            if (attn_tc)
+                k_tc_attn_mma<<<dim3((T + 127) / 128, nb), kTcThreads, smem_amma>>>(t, l);
+            else
+                k_tc_attn<KT><<<dim3((T + 31) / 32, nb), NT, smem_attn>>>(t, l);
             k_tc_mlp<<<std::min(ntiles, nsm), kTcThreads, smem_mlp>>>(t, l);
         }
         k_tc_head<<<nb, NT>>>(t);
