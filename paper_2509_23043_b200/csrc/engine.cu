@@ -358,43 +358,82 @@ struct tapt_model_s {
         k3_state = -1;
         const uint32_t nf = (uint32_t)free_sites.size();
         if (nf == 0 || (size_t)(2 * n + 2) * 4 >= (1u << 31)) return;
-        std::vector<uint32_t> pos_site;
-        std::vector<int> nch_of(n, 0), off_of(n, 0), sp_of(n, 0);
+        // Rows with S' <= 15 ("light"): unit entries (a coupling |J| times, a field |h| times, zeros
+        // padding) in one 16-entry chunk, counted into 4 planes.  Heavier rows: the field is the constant
+        // hc = max(h, 0) (its entries would all read ONES or ZEROS), and each coupling is split into
+        // |J| = 2q + r: q entries in weight-2 chunks (their count enters one plane up) and r in weight-1
+        // chunks, counted into 7 planes.  Multiplier inputs (16 x J=1, 16 x J=2, h=16): 2 chunks, not 4.
+        std::vector<int> nch_of(n, 0), off_of(n, 0), sp_of(n, 0), key_of(n, 0);
+        std::vector<std::vector<uint32_t>> rows_of(n);
+        std::vector<uint32_t> w2_of(n, 0), hc_of(n, 0);
+        const uint32_t ONES = 2 * n, ZEROS = 2 * n + 1;
+        if (nf >= (1u << 24)) return;
         for (uint32_t i = 0; i < n; ++i) {
             if (clamp[i]) continue;
             int sp = std::abs(hi[i]);
             for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) sp += std::abs((int)adjJ[k]);
             if (sp > 127) return;
             sp_of[i] = sp;
-            // one 16-entry chunk holds S' <= 15 (4 planes); heavier rows take 2..8 chunks (7 planes)
-            nch_of[i] = sp <= 15 ? 1 : std::max(2, (sp + 15) / 16);
             off_of[i] = -sp - lmin;
+            auto& e = rows_of[i];
+            if (sp <= 15) {
+                for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+                    const int Jk = adjJ[k];
+                    for (int r = 0; r < std::abs(Jk); ++r) e.push_back(4u * (Jk > 0 ? col[k] : n + col[k]));
+                }
+                for (int r = 0; r < std::abs(hi[i]); ++r) e.push_back(4u * (hi[i] > 0 ? ONES : ZEROS));
+                while (e.size() < 16) e.push_back(4u * ZEROS);
+                nch_of[i] = 1;
+                key_of[i] = 1;
+                continue;
+            }
+            std::vector<uint32_t> l1, l2;
+            for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+                const int Jk = adjJ[k];
+                const uint32_t ent = 4u * (Jk > 0 ? col[k] : n + col[k]);
+                for (int r = 0; r < std::abs(Jk) / 2; ++r) l2.push_back(ent);
+                if (std::abs(Jk) & 1) l1.push_back(ent);
+            }
+            const int c1 = (int)((l1.size() + 15) / 16), c2 = (int)((l2.size() + 15) / 16);
+            if (c1 + c2 <= 4) {
+                e = l1;
+                e.resize(16 * (size_t)c1, 4u * ZEROS);
+                e.insert(e.end(), l2.begin(), l2.end());
+                e.resize(16 * (size_t)(c1 + c2), 4u * ZEROS);
+                nch_of[i] = c1 + c2;
+                for (int ch = c1; ch < c1 + c2; ++ch) w2_of[i] |= 1u << ch;
+            } else {  // unit weights
+                for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+                    const int Jk = adjJ[k];
+                    for (int r = 0; r < std::abs(Jk); ++r) e.push_back(4u * (Jk > 0 ? col[k] : n + col[k]));
+                }
+                nch_of[i] = (int)((e.size() + 15) / 16);
+                e.resize(16 * (size_t)nch_of[i], 4u * ZEROS);
+            }
+            hc_of[i] = hi[i] > 0 ? (uint32_t)hi[i] : 0u;
+            key_of[i] = 16 + nch_of[i];  // heavy rows first, then by chunk count
         }
         std::vector<uint32_t> adj;
         std::vector<uint4> meta;
-        const uint32_t ONES = 2 * n, ZEROS = 2 * n + 1;
         int per_thread = 0;
         for (size_t c = 0; c + 1 < col_ptr.size(); ++c) {
             std::vector<uint32_t> v(col_sites.begin() + col_ptr[c], col_sites.begin() + col_ptr[c + 1]);
             std::stable_sort(v.begin(), v.end(), [&](uint32_t x, uint32_t y) {
-                if (nch_of[x] != nch_of[y]) return nch_of[x] > nch_of[y];
+                if (key_of[x] != key_of[y]) return key_of[x] > key_of[y];
                 if (off_of[x] != off_of[y]) return off_of[x] < off_of[y];
                 return x < y;
             });
             per_thread += (int)((v.size() + 127) / 128);
             for (uint32_t i : v) {
                 const size_t start = adj.size();
-                for (uint32_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
-                    const int Jk = adjJ[k];
-                    const uint32_t e = 4u * (Jk > 0 ? col[k] : n + col[k]);
-                    for (int r = 0; r < std::abs(Jk); ++r) adj.push_back(e);
-                }
-                for (int r = 0; r < std::abs(hi[i]); ++r) adj.push_back(4u * (hi[i] > 0 ? ONES : ZEROS));
-                while (adj.size() < start + 16 * (size_t)nch_of[i]) adj.push_back(4u * ZEROS);
+                adj.insert(adj.end(), rows_of[i].begin(), rows_of[i].end());
                 if (off_of[i] + 32768 < 0 || off_of[i] + 32768 > 0xFFFF) return;
-                meta.push_back(make_uint4(i, rank[i], (uint32_t)start,
+                // x: site; y: rank | hc << 24; z: first entry; w: off+32768 | nch << 16 | S' << 20 |
+                // heavy << 27 | weight-2 chunk flags << 28
+                meta.push_back(make_uint4(i, rank[i] | (hc_of[i] << 24), (uint32_t)start,
                                           (uint32_t)(off_of[i] + 32768) | ((uint32_t)nch_of[i] << 16) |
-                                              ((uint32_t)sp_of[i] << 20)));
+                                              ((uint32_t)sp_of[i] << 20) | ((uint32_t)(sp_of[i] > 15) << 27) |
+                                              (w2_of[i] << 28)));
             }
         }
         // Bank-aware entry order.  A warp gathers entry k of 32 rows (32 lanes = 32 consecutive class

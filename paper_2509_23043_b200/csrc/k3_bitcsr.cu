@@ -189,30 +189,40 @@ __device__ __forceinline__ void k3_site(const PTArgs& a, const PTShared& S, cons
                                         const uint32_t* adj, const uint8_t* ub0, int n, uint32_t vmask, int nv,
                                         uint32_t (&C)[kC3], int& corr) {
     const uint32_t i = md.x;
-    const uint64_t ph = (uint64_t)md.y * kPhi;
+    const uint64_t ph = (uint64_t)(md.y & 0xFFFFFFu) * kPhi;
     const int off = (int)(md.w & 0xFFFFu) - 32768;
     const int nch = (int)((md.w >> 16) & 15u);
     const uint32_t sp = (md.w >> 20) & 127u;
+    const bool heavy = HW && ((md.w >> 27) & 1u);
     const uint32_t* ap = adj + md.z;
     uint32_t A[7];
-    {
+    if (heavy) {  // A = hc + sum over chunks of (count << weight), 7 planes
+        const uint32_t hc = md.y >> 24;
+#pragma unroll
+        for (int p = 0; p < 7; ++p) A[p] = ((hc >> p) & 1u) ? 0xFFFFFFFFu : 0u;
+        for (int ch = 0; ch < nch; ++ch) {
+            uint32_t P[5];
+            chunk_count(W2, ap + 16 * ch, P);
+            uint32_t c;
+            if ((md.w >> (28 + ch)) & 1u) {  // weight 2: planes 1..5
+                ha(A[1], P[0], A[1], c);
+#pragma unroll
+                for (int p = 2; p < 6; ++p) fa(A[p], P[p - 1], c, A[p], c);
+                A[6] ^= c;
+            } else {
+                ha(A[0], P[0], A[0], c);
+#pragma unroll
+                for (int p = 1; p < 5; ++p) fa(A[p], P[p], c, A[p], c);
+                ha(A[5], c, A[5], c);
+                A[6] ^= c;
+            }
+        }
+    } else {
         uint32_t P[5];
         chunk_count(W2, ap, P);
 #pragma unroll
         for (int p = 0; p < 5; ++p) A[p] = P[p];
         A[5] = A[6] = 0;
-    }
-    if constexpr (HW) {
-        for (int ch = 1; ch < nch; ++ch) {  // heavy rows: 7-plane ripple of each chunk's count
-            uint32_t P[5];
-            chunk_count(W2, ap + 16 * ch, P);
-            uint32_t c;
-            ha(A[0], P[0], A[0], c);
-#pragma unroll
-            for (int p = 1; p < 5; ++p) fa(A[p], P[p], c, A[p], c);
-            ha(A[5], c, A[5], c);
-            A[6] ^= c;
-        }
     }
     uint32_t N[4], Nh[4];
     nibbles4(A[0], A[1], A[2], A[3], N);
@@ -229,7 +239,7 @@ __device__ __forceinline__ void k3_site(const PTArgs& a, const PTShared& S, cons
     nw |= old & ~vmask;
     *reinterpret_cast<uint32_t*>(W2 + 4 * i) = nw;
     *reinterpret_cast<uint32_t*>(W2 + 4 * (n + i)) = ~nw;
-    if (HW && nch > 1) {
+    if (heavy) {
         k3_energy<7>(C, A, sp, nw, old);
         corr += 127;
     } else {
@@ -337,7 +347,7 @@ __global__ void __launch_bounds__(kT3 * IPB, 1) k3_bitcsr_pt(const PTArgs a, con
                     const int q = base + ti;
                     const bool on = q < c1;
                     const uint4 md = on ? meta[q] : make_uint4(0, 0, 0, 0);
-                    const bool hw = __any_sync(0xFFFFFFFFu, on && ((md.w >> 16) & 15u) > 1u);
+                    const bool hw = __any_sync(0xFFFFFFFFu, on && ((md.w >> 27) & 1u));
                     if (on) {
                         if (hw)
                             k3_site<true>(a, S, md, W2, adj, ub0, n, vmask, nv, C, corr);
