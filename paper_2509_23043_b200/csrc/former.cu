@@ -598,7 +598,15 @@ struct TcArgs {
     float* Qb;        // [rows][D] queries
     float* O;         // [rows][D] attention outputs
     const float* Eb;  // [B][D] beta embeddings
+    // K/V as tensor-core operand tiles for k_tc_attn_mma (null: the fp32 cache for k_tc_attn):
+    // [B][L][ceil(T/32)] chunks of 32 keys x [2 heads][K hi | K lo | V^T hi | V^T lo] (2 KB each)
+    uint8_t* kvt;
+    int nchunk;
 };
+
+constexpr int kChunkKeys = 32;                                     // keys per attention chunk
+constexpr int kChunkTile = kChunkKeys * 32 * 2;                    // one 32 x 32 bf16 tile (2 KB)
+constexpr int kChunkBytes = 2 * 4 * kChunkTile;                    // both heads, K / V, hi / lo: 16 KB
 
 constexpr int kTcThreads = 128;
 
@@ -724,9 +732,31 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_qkv(const TcArgs a, int l) {
                     for (int i = 0; i < 16; i += 4)
                         *reinterpret_cast<float4*>(a.Qb + (size_t)row * D + c + i) =
                             make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-                } else if (valid) {
+                } else if (valid && !a.kvt) {
 #pragma unroll
                     for (int i = 0; i < 16; ++i) KVT<KT>::st(a.f.cache, kv + (c - D) + i, v[i]);
+                } else if (valid) {  // operand tiles of this key's chunk: K row j; V^T column j
+                    const int j = t % kChunkKeys, isv = c >= 2 * D, hh = ((c - D) % D) / DH, d0 = (c - D) % DH;
+                    uint8_t* blk = a.kvt + (((size_t)b * a.f.L + l) * a.nchunk + t / kChunkKeys) * kChunkBytes +
+                                   (size_t)hh * 4 * kChunkTile;
+                    if (!isv) {
+#pragma unroll
+                        for (int k0 = 0; k0 < 16; k0 += 8) {
+                            float x8[8];
+#pragma unroll
+                            for (int i = 0; i < 8; ++i) x8[i] = v[k0 + i];
+                            tapt_tc::store_row8(blk, blk + kChunkTile, j, d0 + k0, 32, x8);
+                        }
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < 16; ++i) {
+                            __nv_bfloat16 hi, lo;
+                            tapt_tc::split_bf16(v[i], hi, lo);
+                            const uint32_t off = tapt_tc::kmajor_off(d0 + i, j, kChunkKeys);
+                            *reinterpret_cast<__nv_bfloat16*>(blk + 2 * kChunkTile + off) = hi;
+                            *reinterpret_cast<__nv_bfloat16*>(blk + 3 * kChunkTile + off) = lo;
+                        }
+                    }
                 }
             }
         }
@@ -863,148 +893,134 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_mlp(const TcArgs a, int l) {
 }
 
 // Causal attention of one 128-position query block of one sequence on the tensor cores (flash
-// style).  Per 64-key chunk: K and V of both heads are staged as bf16 hi / lo tiles (V transposed:
-// [dim][key], K-major for the PV product); per head S = Q K^T (M 128, N 64, K 32) lands in TMEM,
-// each thread (= query row) reads its 64 scores, applies the causal mask and the online softmax,
-// writes P as a hi / lo tile, and P V (M 128, N 32, K 64) comes back from TMEM into the row's fp32
-// output accumulator.  grid (ceil(T / 128), B), 128 threads.
-constexpr int kAttnKeys = 64;
+// style).  256 threads: warpgroup h (warps 4h .. 4h+3) owns head h, thread = query row (TMEM lane).
+// K and V arrive as ready-made operand tiles (k_tc_qkv writes them: per 32-key chunk, K [key][dim]
+// and V^T [dim][key], bf16 hi / lo, both heads, 16 KB), copied into shared memory by cp.async.bulk,
+// double-buffered so the next chunk lands while this one computes.  Per chunk one thread issues
+// S_h = Q_h K_h^T for both heads (M 128, N 32, K 32) into TMEM; each warpgroup applies the causal
+// mask and the online softmax to its rows and writes P_h as a hi / lo tile; one thread issues P_h V_h
+// (M 128, N 32, K 32); each row folds the result into its fp32 accumulator.  grid (ceil(T/128), B).
+constexpr int kAttnThreads = 256;
 
-__global__ void __launch_bounds__(kTcThreads) k_tc_attn_mma(const TcArgs a, int l) {
+__global__ void __launch_bounds__(kAttnThreads) k_tc_attn_mma(const TcArgs a, int l) {
     extern __shared__ __align__(128) uint8_t sm[];
-    uint8_t* qh = sm;                                  // [2 heads][128][32] hi
-    uint8_t* ql = qh + 2 * 128 * DH * 2;               //                    lo
-    uint8_t* kh = ql + 2 * 128 * DH * 2;               // [2][64 keys][32] hi
-    uint8_t* kl = kh + 2 * kAttnKeys * DH * 2;
-    uint8_t* vh = kl + 2 * kAttnKeys * DH * 2;         // [2][32 dims][64 keys] hi
-    uint8_t* vl = vh + 2 * DH * kAttnKeys * 2;
-    uint8_t* ph = vl + 2 * DH * kAttnKeys * 2;         // [128][64 keys] hi
-    uint8_t* pl = ph + 128 * kAttnKeys * 2;
-    __shared__ uint64_t bar;
+    constexpr int QT = 128 * DH * 2, PT = 128 * kChunkKeys * 2;
+    uint8_t* qh = sm;                 // [2 heads][128][32] hi
+    uint8_t* ql = qh + 2 * QT;        //                    lo
+    uint8_t* kv = ql + 2 * QT;        // [2 buffers][16 KB chunk]
+    uint8_t* ph = kv + 2 * kChunkBytes;  // [2 heads][128][32 keys]
+    uint8_t* pl = ph + 2 * PT;
+    __shared__ uint64_t bar, kvbar[2];
     __shared__ uint32_t tbase;
-    const int tid = threadIdx.x, warp = tid >> 5;
-    const int b = blockIdx.y, q0 = blockIdx.x * 128, t = q0 + tid;
+    const int tid = threadIdx.x, warp = tid >> 5, h = tid >> 7, r = tid & 127;
+    const int b = blockIdx.y, q0 = blockIdx.x * 128, t = q0 + r;
     const int tq = min(t, a.T - 1);  // rows past the sequence end attend like its last row (not stored)
-    const size_t base = (((size_t)b * a.f.L + l) * a.T) * 2 * D;
-    constexpr int QT = 128 * DH * 2, KT = kAttnKeys * DH * 2, VT = DH * kAttnKeys * 2;
-    {  // Q of this row, both heads
-        const float* q = a.Qb + ((size_t)b * a.T + tq) * D;
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-#pragma unroll
-            for (int k0 = 0; k0 < DH; k0 += 8) {
-                float x8[8];
-#pragma unroll
-                for (int i = 0; i < 8; ++i) x8[i] = q[h * DH + k0 + i];
-                tapt_tc::store_row8(qh + h * QT, ql + h * QT, tid, k0, DH, x8);
-            }
+    const int kmax = min(q0 + 127, a.T - 1), nch = kmax / kChunkKeys + 1;
+    const uint8_t* src = a.kvt + (((size_t)b * a.f.L + l) * a.nchunk) * kChunkBytes;
+    if (tid == 0) {
+        tapt_tc::bar_init(&bar, 1);
+        tapt_tc::bar_init(&kvbar[0], 1);
+        tapt_tc::bar_init(&kvbar[1], 1);
+        tapt_dev::mbar_expect_tx(&kvbar[0], kChunkBytes);  // chunk 0
+        tapt_dev::bulk_g2s(kv, src, kChunkBytes, &kvbar[0]);
     }
-    if (tid == 0) tapt_tc::bar_init(&bar, 1);
-    if (warp == 0) tapt_tc::tmem_alloc(&tbase, 128);
-    tc_sync();
-    const uint32_t tm = tbase, lane_base = (uint32_t)(32 * (warp & 3)) << 16;
-    const uint32_t cS = 0, cO = 64;  // TMEM columns: scores [0, 64), P V [64, 96)
-    const float scale = rsqrtf((float)DH);
-    float m[2] = {-INFINITY, -INFINITY}, lsum[2] = {0.f, 0.f}, o[2][DH];
+    {  // Q of this row, this head
+        const float* q = a.Qb + ((size_t)b * a.T + tq) * D + h * DH;
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int d = 0; d < DH; ++d) o[h][d] = 0.f;
-    uint32_t phase = 0;
-    const int kmax = min(q0 + 127, a.T - 1);
-    for (int c0 = 0; c0 <= kmax; c0 += kAttnKeys) {
-        // stage K (rows = keys) and V^T (rows = dims) of both heads for keys c0 .. c0 + 63
-        {
-            const int j = tid >> 1;
-            if ((tid & 1) == 0) {  // K of key c0 + j
-                const bool ok = c0 + j <= kmax;
-                const float* kr = a.f.cache ? reinterpret_cast<const float*>(a.f.cache) + base + (size_t)(c0 + j) * 2 * D
-                                            : nullptr;
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int k0 = 0; k0 < DH; k0 += 8) {
-                        float x8[8];
-#pragma unroll
-                        for (int i = 0; i < 8; ++i) x8[i] = ok ? kr[h * DH + k0 + i] : 0.f;
-                        tapt_tc::store_row8(kh + h * KT, kl + h * KT, j, k0, DH, x8);
-                    }
-            }
-        }
-        for (int task = tid; task < 2 * DH * (kAttnKeys / 8); task += kTcThreads) {  // V^T: (dim, 8-key group)
-            const int dim = task % (2 * DH), g = task / (2 * DH), h = dim / DH, d = dim - h * DH;
+        for (int k0 = 0; k0 < DH; k0 += 8) {
             float x8[8];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int key = c0 + 8 * g + i;
-                x8[i] = key <= kmax ? reinterpret_cast<const float*>(a.f.cache)[base + (size_t)key * 2 * D + D + dim]
-                                    : 0.f;
-            }
-            tapt_tc::store_row8(vh + h * VT, vl + h * VT, d, 8 * g, kAttnKeys, x8);
-        }
-        tc_sync();
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {  // unrolled: o[h] stays in registers
-            tc_gemm<kAttnKeys, DH>(tm + cS, qh + h * QT, ql + h * QT, kh + h * KT, kl + h * KT, &bar, phase);
-            // two passes over the TMEM scores (row max, then exp / sum / P), keeping 16 in registers
-            float mx = m[h];
-#pragma unroll
-            for (int c = 0; c < kAttnKeys; c += 16) {
-                float v[16];
-                tapt_tc::tmem_ld16(tm + lane_base + cS + c, v);
-#pragma unroll
-                for (int i = 0; i < 16; ++i)
-                    if (c0 + c + i <= tq) mx = fmaxf(mx, v[i] * scale);
-            }
-            const float corr = __expf(m[h] - mx);
-            float ps = 0.f;
-#pragma unroll
-            for (int c = 0; c < kAttnKeys; c += 16) {
-                float v[16];
-                tapt_tc::tmem_ld16(tm + lane_base + cS + c, v);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) {
-                    v[i] = c0 + c + i <= tq ? __expf(v[i] * scale - mx) : 0.f;
-                    ps += v[i];
-                }
-#pragma unroll
-                for (int k0 = 0; k0 < 16; k0 += 8) {
-                    float x8[8];
-#pragma unroll
-                    for (int i = 0; i < 8; ++i) x8[i] = v[k0 + i];
-                    tapt_tc::store_row8(ph, pl, tid, c + k0, kAttnKeys, x8);
-                }
-            }
-            lsum[h] = lsum[h] * corr + ps;
-            m[h] = mx;
-            tc_sync();
-            tc_gemm<DH, kAttnKeys>(tm + cO, ph, pl, vh + h * VT, vl + h * VT, &bar, phase);
-#pragma unroll
-            for (int c = 0; c < DH; c += 16) {
-                float v[16];
-                tapt_tc::tmem_ld16(tm + lane_base + cO + c, v);
-#pragma unroll
-                for (int i = 0; i < 16; ++i) o[h][c + i] = o[h][c + i] * corr + v[i];
-            }
-            tapt_tc::fence_before();
-            __syncthreads();  // P and the TMEM columns are rewritten by the next head / chunk
-            tapt_tc::fence_after();
+            for (int i = 0; i < 8; ++i) x8[i] = q[k0 + i];
+            tapt_tc::store_row8(qh + h * QT, ql + h * QT, r, k0, DH, x8);
         }
     }
-    if (t < a.T) {
-        float* dst = a.O + ((size_t)b * a.T + t) * D;
+    if (warp == 0) tapt_tc::tmem_alloc(&tbase, 256);
+    tc_sync();
+    const uint32_t tm = tbase, lane_base = (uint32_t)(32 * (warp & 3)) << 16;
+    const uint32_t cS = (uint32_t)kChunkKeys * h, cO = 128u + 32u * h;  // TMEM: scores [0, 64), P V [128, 192)
+    const float scale = rsqrtf((float)DH);
+    float m = -INFINITY, lsum = 0.f, o[DH];
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const float inv = 1.f / lsum[h];
-#pragma unroll
-            for (int d = 0; d < DH; d += 4)
-                *reinterpret_cast<float4*>(dst + h * DH + d) =
-                    make_float4(o[h][d] * inv, o[h][d + 1] * inv, o[h][d + 2] * inv, o[h][d + 3] * inv);
+    for (int d = 0; d < DH; ++d) o[d] = 0.f;
+    uint32_t phase = 0, kvphase = 0;  // kvphase bit s: parity of buffer s
+    for (int ci = 0; ci < nch; ++ci) {
+        const int c0 = ci * kChunkKeys, s = ci & 1;
+        const uint8_t* kb = kv + s * kChunkBytes;
+        if (tid == 0) {
+            if (ci + 1 < nch) {  // prefetch the next chunk into the other buffer (its MMAs have retired)
+                tapt_dev::mbar_expect_tx(&kvbar[s ^ 1], kChunkBytes);
+                tapt_dev::bulk_g2s(kv + (s ^ 1) * kChunkBytes, src + (size_t)(ci + 1) * kChunkBytes, kChunkBytes, &kvbar[s ^ 1]);
+            }
+            tapt_tc::bar_wait(&kvbar[s], (kvphase >> s) & 1u);
+            tapt_tc::fence_after();
+            // S_h = Q_h K_h^T, both heads
+            tapt_tc::mma_x3<kChunkKeys, DH>(tm + 0, qh, ql, kb, kb + kChunkTile);
+            tapt_tc::mma_x3<kChunkKeys, DH>(tm + kChunkKeys, qh + QT, ql + QT, kb + 4 * kChunkTile,
+                                            kb + 5 * kChunkTile);
+            tapt_tc::mma_commit(&bar);
         }
+        kvphase ^= 1u << s;
+        tapt_tc::bar_wait(&bar, phase);
+        phase ^= 1u;
+        tapt_tc::fence_after();
+        // online softmax of this row / head over the chunk
+        float v[kChunkKeys];
+#pragma unroll
+        for (int c = 0; c < kChunkKeys; c += 16) {
+            float w16[16];
+            tapt_tc::tmem_ld16(tm + lane_base + cS + c, w16);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) v[c + i] = c0 + c + i <= tq ? w16[i] * scale : -INFINITY;
+        }
+        float mx = m;
+#pragma unroll
+        for (int i = 0; i < kChunkKeys; ++i) mx = fmaxf(mx, v[i]);
+        const float corr = __expf(m - mx);
+        float ps = 0.f;
+#pragma unroll
+        for (int i = 0; i < kChunkKeys; ++i) {
+            v[i] = c0 + i <= tq ? __expf(v[i] - mx) : 0.f;
+            ps += v[i];
+        }
+#pragma unroll
+        for (int k0 = 0; k0 < kChunkKeys; k0 += 8) {
+            float x8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) x8[i] = v[k0 + i];
+            tapt_tc::store_row8(ph + h * PT, pl + h * PT, r, k0, kChunkKeys, x8);
+        }
+        lsum = lsum * corr + ps;
+        m = mx;
+        tc_sync();
+        if (tid == 0) {  // P_h V_h, both heads
+            tapt_tc::mma_x3<DH, kChunkKeys>(tm + 128, ph, pl, kb + 2 * kChunkTile, kb + 3 * kChunkTile);
+            tapt_tc::mma_x3<DH, kChunkKeys>(tm + 128 + DH, ph + PT, pl + PT, kb + 6 * kChunkTile, kb + 7 * kChunkTile);
+            tapt_tc::mma_commit(&bar);
+        }
+        tapt_tc::bar_wait(&bar, phase);
+        phase ^= 1u;
+        tapt_tc::fence_after();
+#pragma unroll
+        for (int c = 0; c < DH; c += 16) {
+            float w16[16];
+            tapt_tc::tmem_ld16(tm + lane_base + cO + c, w16);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[c + i] = o[c + i] * corr + w16[i];
+        }
+        tapt_tc::fence_before();
+        __syncthreads();  // P tiles and the TMEM columns are rewritten by the next chunk
+        tapt_tc::fence_after();
+    }
+    if (t < a.T) {
+        float* dst = a.O + ((size_t)b * a.T + t) * D + h * DH;
+        const float inv = 1.f / lsum;
+#pragma unroll
+        for (int d = 0; d < DH; d += 4)
+            *reinterpret_cast<float4*>(dst + d) = make_float4(o[d] * inv, o[d + 1] * inv, o[d + 2] * inv, o[d + 3] * inv);
     }
     tapt_tc::fence_before();
     __syncthreads();
-    if (warp == 0) tapt_tc::tmem_free(tm, 128);
+    if (warp == 0) tapt_tc::tmem_free(tm, 256);
 }
 
 // Final LayerNorm + head per row, log q per sequence (positions >= n_prefix).  grid B, NT threads.
@@ -1263,7 +1279,9 @@ tapt_former_s* create_former(const tapt_former_config* c, const float* params) {
 template <class KT>
 void log_prob_tc(tapt_former_s* f, const FArgs& a0) {
     const int T = a0.T, L = (int)f->cfg.layers, nsm = sm_count();
-    const size_t per_seq = (size_t)L * T * 2 * D * sizeof(KT) + (size_t)3 * T * D * 4 + D * 4;
+    const int nchunk = (T + kChunkKeys - 1) / kChunkKeys;
+    const size_t per_seq = (size_t)L * T * 2 * D * sizeof(KT) + (size_t)3 * T * D * 4 + D * 4 +
+                           (size_t)L * nchunk * kChunkBytes;
     const int Bc = (int)std::max<size_t>(1, std::min<size_t>((size_t)a0.B, (size_t)(8ull << 30) / per_seq));
     const size_t smem_qkv = (size_t)2 * 3 * D * D * 2 + (size_t)2 * 128 * D * 2;
     const size_t smem_mlp = (size_t)2 * (D * D + F * D + D * F) * 2 + (size_t)2 * 128 * D * 2 + (size_t)2 * 128 * F * 2;
@@ -1274,8 +1292,7 @@ void log_prob_tc(tapt_former_s* f, const FArgs& a0) {
     // attention products on the tensor cores too (fp32 cache only); TAPT_FORMER_ATTN_TC=0: CUDA cores
     const char* ae = std::getenv("TAPT_FORMER_ATTN_TC");
     const bool attn_tc = sizeof(KT) == 4 && !(ae && std::atoi(ae) == 0);
-    const size_t smem_amma = (size_t)2 * (2 * 128 * DH * 2) + (size_t)2 * (2 * kAttnKeys * DH * 2) +
-                             (size_t)2 * (2 * DH * kAttnKeys * 2) + (size_t)2 * (128 * kAttnKeys * 2);
+    const size_t smem_amma = (size_t)2 * (2 * 128 * DH * 2) + (size_t)2 * kChunkBytes + (size_t)2 * (2 * 128 * kChunkKeys * 2);
     FCUDA(cudaFuncSetAttribute(k_tc_attn_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_amma));
     for (int b0 = 0; b0 < a0.B; b0 += Bc) {
         const int nb = std::min(Bc, a0.B - b0);
@@ -1290,18 +1307,25 @@ void log_prob_tc(tapt_former_s* f, const FArgs& a0) {
         t.rows = nb * T;
         t.T = T;
         t.B = nb;
-        float* buf = f->need_tcbuf((size_t)3 * t.rows * D + (size_t)nb * D);
+        const size_t kvt_floats = attn_tc ? ((size_t)nb * L * nchunk * kChunkBytes + 3) / 4 : 0;
+        float* buf = f->need_tcbuf((size_t)3 * t.rows * D + (size_t)nb * D + kvt_floats);
         t.X = buf;
         t.Qb = buf + (size_t)t.rows * D;
         t.O = buf + (size_t)2 * t.rows * D;
         t.Eb = buf + (size_t)3 * t.rows * D;
+        t.nchunk = nchunk;
+        t.kvt = nullptr;
+        if (attn_tc) {  // chunk tiles; keys past T stay zero (finite operands for the masked products)
+            t.kvt = reinterpret_cast<uint8_t*>(buf + (size_t)3 * t.rows * D + (size_t)nb * D);
+            FCUDA(cudaMemsetAsync(t.kvt, 0, (size_t)nb * L * nchunk * kChunkBytes));
+        }
         const int ntiles = (t.rows + 127) / 128;
         k_tc_beta<<<nb, D>>>(t.f, const_cast<float*>(t.Eb));
         k_tc_embed<<<std::min(nsm * 8, (t.rows * D + 255) / 256), 256>>>(t);
         for (int l = 0; l < L; ++l) {
             k_tc_qkv<KT><<<std::min(ntiles, 2 * nsm), kTcThreads, smem_qkv>>>(t, l);
             if (attn_tc)
-                k_tc_attn_mma<<<dim3((T + 127) / 128, nb), kTcThreads, smem_amma>>>(t, l);
+                k_tc_attn_mma<<<dim3((T + 127) / 128, nb), kAttnThreads, smem_amma>>>(t, l);
             else
                 k_tc_attn<KT><<<dim3((T + 31) / 32, nb), NT, smem_attn>>>(t, l);
             k_tc_mlp<<<std::min(ntiles, nsm), kTcThreads, smem_mlp>>>(t, l);
