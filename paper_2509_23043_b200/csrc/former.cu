@@ -895,34 +895,46 @@ __global__ void __launch_bounds__(kTcThreads) k_tc_mlp(const TcArgs a, int l) {
 // Causal attention of one 128-position query block of one sequence on the tensor cores (flash
 // style).  256 threads: warpgroup h (warps 4h .. 4h+3) owns head h, thread = query row (TMEM lane).
 // K and V arrive as ready-made operand tiles (k_tc_qkv writes them: per 32-key chunk, K [key][dim]
-// and V^T [dim][key], bf16 hi / lo, both heads, 16 KB), copied into shared memory by cp.async.bulk,
-// double-buffered so the next chunk lands while this one computes.  Per chunk one thread issues
-// S_h = Q_h K_h^T for both heads (M 128, N 32, K 32) into TMEM; each warpgroup applies the causal
-// mask and the online softmax to its rows and writes P_h as a hi / lo tile; one thread issues P_h V_h
-// (M 128, N 32, K 32); each row folds the result into its fp32 accumulator.  grid (ceil(T/128), B).
-constexpr int kAttnThreads = 256;
+// and V^T [dim][key], bf16 hi / lo, both heads, 16 KB), copied into shared memory by cp.async.bulk
+// into a ring of 3 buffers, two chunks ahead.  Software-pipelined so each chunk costs ONE MMA round
+// trip: after the softmax of chunk c (scores from TMEM, causal mask, online max / sum, P as a hi / lo
+// tile) one thread issues P_c V_c and S_{c+1} = Q K_{c+1}^T for both heads under a single commit; the
+// next iteration folds P_c V_c into the row's fp32 accumulator and starts the softmax of c + 1.
+// grid (ceil(T / 128), B).
+constexpr int kAttnThreads = 256, kKvBufs = 3;
 
 __global__ void __launch_bounds__(kAttnThreads) k_tc_attn_mma(const TcArgs a, int l) {
     extern __shared__ __align__(128) uint8_t sm[];
     constexpr int QT = 128 * DH * 2, PT = 128 * kChunkKeys * 2;
-    uint8_t* qh = sm;                 // [2 heads][128][32] hi
-    uint8_t* ql = qh + 2 * QT;        //                    lo
-    uint8_t* kv = ql + 2 * QT;        // [2 buffers][16 KB chunk]
-    uint8_t* ph = kv + 2 * kChunkBytes;  // [2 heads][128][32 keys]
+    uint8_t* qh = sm;                          // [2 heads][128][32] hi
+    uint8_t* ql = qh + 2 * QT;                 //                    lo
+    uint8_t* kv = ql + 2 * QT;                 // [3 buffers][16 KB chunk]
+    uint8_t* ph = kv + kKvBufs * kChunkBytes;  // [2 heads][128][32 keys]
     uint8_t* pl = ph + 2 * PT;
-    __shared__ uint64_t bar, kvbar[2];
+    __shared__ uint64_t bar, kvbar[kKvBufs];
     __shared__ uint32_t tbase;
     const int tid = threadIdx.x, warp = tid >> 5, h = tid >> 7, r = tid & 127;
     const int b = blockIdx.y, q0 = blockIdx.x * 128, t = q0 + r;
     const int tq = min(t, a.T - 1);  // rows past the sequence end attend like its last row (not stored)
     const int kmax = min(q0 + 127, a.T - 1), nch = kmax / kChunkKeys + 1;
     const uint8_t* src = a.kvt + (((size_t)b * a.f.L + l) * a.nchunk) * kChunkBytes;
+    auto fetch = [&](int ci) {  // thread 0
+        uint64_t* kb = &kvbar[ci % kKvBufs];
+        tapt_dev::mbar_expect_tx(kb, kChunkBytes);
+        tapt_dev::bulk_g2s(kv + (ci % kKvBufs) * kChunkBytes, src + (size_t)ci * kChunkBytes, kChunkBytes, kb);
+    };
+    auto issue_qk = [&](int ci) {  // thread 0: S_h = Q_h K_h^T of chunk ci, both heads
+        const uint8_t* kb = kv + (ci % kKvBufs) * kChunkBytes;
+        tapt_tc::bar_wait(&kvbar[ci % kKvBufs], (uint32_t)(ci / kKvBufs) & 1u);
+        tapt_tc::fence_after();
+        tapt_tc::mma_x3<kChunkKeys, DH>(tbase + 0, qh, ql, kb, kb + kChunkTile);
+        tapt_tc::mma_x3<kChunkKeys, DH>(tbase + kChunkKeys, qh + QT, ql + QT, kb + 4 * kChunkTile, kb + 5 * kChunkTile);
+    };
     if (tid == 0) {
         tapt_tc::bar_init(&bar, 1);
-        tapt_tc::bar_init(&kvbar[0], 1);
-        tapt_tc::bar_init(&kvbar[1], 1);
-        tapt_dev::mbar_expect_tx(&kvbar[0], kChunkBytes);  // chunk 0
-        tapt_dev::bulk_g2s(kv, src, kChunkBytes, &kvbar[0]);
+        for (int i = 0; i < kKvBufs; ++i) tapt_tc::bar_init(&kvbar[i], 1);
+        fetch(0);
+        if (nch > 1) fetch(1);
     }
     {  // Q of this row, this head
         const float* q = a.Qb + ((size_t)b * a.T + tq) * D + h * DH;
@@ -939,31 +951,30 @@ __global__ void __launch_bounds__(kAttnThreads) k_tc_attn_mma(const TcArgs a, in
     const uint32_t tm = tbase, lane_base = (uint32_t)(32 * (warp & 3)) << 16;
     const uint32_t cS = (uint32_t)kChunkKeys * h, cO = 128u + 32u * h;  // TMEM: scores [0, 64), P V [128, 192)
     const float scale = rsqrtf((float)DH);
-    float m = -INFINITY, lsum = 0.f, o[DH];
+    float m = -INFINITY, lsum = 0.f, corr = 1.f, o[DH];
 #pragma unroll
     for (int d = 0; d < DH; ++d) o[d] = 0.f;
-    uint32_t phase = 0, kvphase = 0;  // kvphase bit s: parity of buffer s
-    for (int ci = 0; ci < nch; ++ci) {
-        const int c0 = ci * kChunkKeys, s = ci & 1;
-        const uint8_t* kb = kv + s * kChunkBytes;
-        if (tid == 0) {
-            if (ci + 1 < nch) {  // prefetch the next chunk into the other buffer (its MMAs have retired)
-                tapt_dev::mbar_expect_tx(&kvbar[s ^ 1], kChunkBytes);
-                tapt_dev::bulk_g2s(kv + (s ^ 1) * kChunkBytes, src + (size_t)(ci + 1) * kChunkBytes, kChunkBytes, &kvbar[s ^ 1]);
-            }
-            tapt_tc::bar_wait(&kvbar[s], (kvphase >> s) & 1u);
-            tapt_tc::fence_after();
-            // S_h = Q_h K_h^T, both heads
-            tapt_tc::mma_x3<kChunkKeys, DH>(tm + 0, qh, ql, kb, kb + kChunkTile);
-            tapt_tc::mma_x3<kChunkKeys, DH>(tm + kChunkKeys, qh + QT, ql + QT, kb + 4 * kChunkTile,
-                                            kb + 5 * kChunkTile);
-            tapt_tc::mma_commit(&bar);
-        }
-        kvphase ^= 1u << s;
-        tapt_tc::bar_wait(&bar, phase);
+    uint32_t phase = 0;
+    if (tid == 0) {
+        issue_qk(0);
+        tapt_tc::mma_commit(&bar);
+    }
+    for (int ci = 0; ci <= nch; ++ci) {
+        tapt_tc::bar_wait(&bar, phase);  // S_ci and P_{ci-1} V_{ci-1} have landed
         phase ^= 1u;
         tapt_tc::fence_after();
-        // online softmax of this row / head over the chunk
+        if (ci > 0) {  // fold P V of the previous chunk in, with that chunk's rescale
+#pragma unroll
+            for (int c = 0; c < DH; c += 16) {
+                float w16[16];
+                tapt_tc::tmem_ld16(tm + lane_base + cO + c, w16);
+#pragma unroll
+                for (int i = 0; i < 16; ++i) o[c + i] = o[c + i] * corr + w16[i];
+            }
+        }
+        if (ci == nch) break;
+        if (tid == 0 && ci + 2 < nch) fetch(ci + 2);  // its buffer held chunk ci - 1, whose MMAs have retired
+        const int c0 = ci * kChunkKeys;
         float v[kChunkKeys];
 #pragma unroll
         for (int c = 0; c < kChunkKeys; c += 16) {
@@ -975,7 +986,7 @@ __global__ void __launch_bounds__(kAttnThreads) k_tc_attn_mma(const TcArgs a, in
         float mx = m;
 #pragma unroll
         for (int i = 0; i < kChunkKeys; ++i) mx = fmaxf(mx, v[i]);
-        const float corr = __expf(m - mx);
+        corr = __expf(m - mx);
         float ps = 0.f;
 #pragma unroll
         for (int i = 0; i < kChunkKeys; ++i) {
@@ -991,25 +1002,14 @@ __global__ void __launch_bounds__(kAttnThreads) k_tc_attn_mma(const TcArgs a, in
         }
         lsum = lsum * corr + ps;
         m = mx;
-        tc_sync();
-        if (tid == 0) {  // P_h V_h, both heads
+        tc_sync();  // P written; the scores and the P V columns have been read
+        if (tid == 0) {
+            const uint8_t* kb = kv + (ci % kKvBufs) * kChunkBytes;
             tapt_tc::mma_x3<DH, kChunkKeys>(tm + 128, ph, pl, kb + 2 * kChunkTile, kb + 3 * kChunkTile);
             tapt_tc::mma_x3<DH, kChunkKeys>(tm + 128 + DH, ph + PT, pl + PT, kb + 6 * kChunkTile, kb + 7 * kChunkTile);
+            if (ci + 1 < nch) issue_qk(ci + 1);
             tapt_tc::mma_commit(&bar);
         }
-        tapt_tc::bar_wait(&bar, phase);
-        phase ^= 1u;
-        tapt_tc::fence_after();
-#pragma unroll
-        for (int c = 0; c < DH; c += 16) {
-            float w16[16];
-            tapt_tc::tmem_ld16(tm + lane_base + cO + c, w16);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) o[c + i] = o[c + i] * corr + w16[i];
-        }
-        tapt_tc::fence_before();
-        __syncthreads();  // P tiles and the TMEM columns are rewritten by the next chunk
-        tapt_tc::fence_after();
     }
     if (t < a.T) {
         float* dst = a.O + ((size_t)b * a.T + t) * D + h * DH;
@@ -1280,19 +1280,20 @@ template <class KT>
 void log_prob_tc(tapt_former_s* f, const FArgs& a0) {
     const int T = a0.T, L = (int)f->cfg.layers, nsm = sm_count();
     const int nchunk = (T + kChunkKeys - 1) / kChunkKeys;
-    const size_t per_seq = (size_t)L * T * 2 * D * sizeof(KT) + (size_t)3 * T * D * 4 + D * 4 +
-                           (size_t)L * nchunk * kChunkBytes;
-    const int Bc = (int)std::max<size_t>(1, std::min<size_t>((size_t)a0.B, (size_t)(8ull << 30) / per_seq));
+    // attention products on the tensor cores too (fp32 cache only); TAPT_FORMER_ATTN_TC=0: CUDA cores
+    const char* ae = std::getenv("TAPT_FORMER_ATTN_TC");
+    const bool attn_tc = sizeof(KT) == 4 && !(ae && std::atoi(ae) == 0);
+    const size_t per_seq = (size_t)3 * T * D * 4 + D * 4 +
+                           (attn_tc ? (size_t)L * nchunk * kChunkBytes : (size_t)L * T * 2 * D * sizeof(KT));
+    const int Bc = (int)std::max<size_t>(1, std::min<size_t>((size_t)a0.B, (size_t)(16ull << 30) / per_seq));
     const size_t smem_qkv = (size_t)2 * 3 * D * D * 2 + (size_t)2 * 128 * D * 2;
     const size_t smem_mlp = (size_t)2 * (D * D + F * D + D * F) * 2 + (size_t)2 * 128 * D * 2 + (size_t)2 * 128 * F * 2;
     const size_t smem_attn = ((sizeof(Smem<32>) + 15) & ~size_t(15)) + sizeof(KVChunk);
     FCUDA(cudaFuncSetAttribute(k_tc_qkv<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_qkv));
     FCUDA(cudaFuncSetAttribute(k_tc_mlp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_mlp));
     FCUDA(cudaFuncSetAttribute(k_tc_attn<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_attn));
-    // attention products on the tensor cores too (fp32 cache only); TAPT_FORMER_ATTN_TC=0: CUDA cores
-    const char* ae = std::getenv("TAPT_FORMER_ATTN_TC");
-    const bool attn_tc = sizeof(KT) == 4 && !(ae && std::atoi(ae) == 0);
-    const size_t smem_amma = (size_t)2 * (2 * 128 * DH * 2) + (size_t)2 * kChunkBytes + (size_t)2 * (2 * 128 * kChunkKeys * 2);
+    const size_t smem_amma =
+        (size_t)2 * (2 * 128 * DH * 2) + (size_t)kKvBufs * kChunkBytes + (size_t)2 * (2 * 128 * kChunkKeys * 2);
     FCUDA(cudaFuncSetAttribute(k_tc_attn_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_amma));
     for (int b0 = 0; b0 < a0.B; b0 += Bc) {
         const int nb = std::min(Bc, a0.B - b0);
@@ -1303,7 +1304,7 @@ void log_prob_tc(tapt_former_s* f, const FArgs& a0) {
         t.f.log_q = a0.log_q + b0;
         t.f.logits = a0.logits ? a0.logits + (size_t)b0 * T : nullptr;
         t.f.B = nb;
-        t.f.cache = f->need_cache((size_t)nb * L * T * 2 * D);
+        t.f.cache = attn_tc ? nullptr : f->need_cache((size_t)nb * L * T * 2 * D);
         t.rows = nb * T;
         t.T = T;
         t.B = nb;
@@ -1317,7 +1318,9 @@ void log_prob_tc(tapt_former_s* f, const FArgs& a0) {
         t.kvt = nullptr;
         if (attn_tc) {  // chunk tiles; keys past T stay zero (finite operands for the masked products)
             t.kvt = reinterpret_cast<uint8_t*>(buf + (size_t)3 * t.rows * D + (size_t)nb * D);
-            FCUDA(cudaMemsetAsync(t.kvt, 0, (size_t)nb * L * nchunk * kChunkBytes));
+            if (T % kChunkKeys)  // only the last chunk of each (sequence, layer) has keys past T
+                FCUDA(cudaMemset2DAsync(t.kvt + (size_t)(nchunk - 1) * kChunkBytes, (size_t)nchunk * kChunkBytes, 0,
+                                        kChunkBytes, (size_t)nb * L));
         }
         const int ntiles = (t.rows + 127) / 128;
         k_tc_beta<<<nb, D>>>(t.f, const_cast<float*>(t.Eb));
@@ -1464,7 +1467,6 @@ tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_
         a.T = (int)T;
         a.n_prefix = (int)n_prefix;
         a.B = (int)B;
-        a.cache = f->need_cache((size_t)grid * f->cfg.layers * T * 2 * D);
         const size_t tb = (size_t)B * T, off_b = (tb + 255) & ~size_t(255), off_q = off_b + (size_t)B * 8,
                      off_z = off_q + (size_t)B * 8;
         uint8_t* tmp = f->need_tmp(off_z + (logits ? tb * 4 : 0));
@@ -1479,6 +1481,7 @@ tapt_status tapt_former_log_prob(tapt_former_t f, const uint8_t* tokens, uint32_
         // sample / log_prob consistency (the MH correction) needs bit-identical QKV arithmetic in both:
         // with kv16 log_prob keeps the CUDA-core engine the sampler uses.
         const bool tc = f->tc && !f->kv16 && !(env && std::atoi(env) == 0);
+        if (!tc) a.cache = f->need_cache((size_t)grid * f->cfg.layers * T * 2 * D);
         if (tc) {
             log_prob_tc<float>(f, a);
         } else if (f->kv16) {
