@@ -116,6 +116,8 @@ def lib():
                                     _i8p, C.c_size_t, _f64p, _u64p, _u64p, _u8p]
         L.oc_rpt_synthetic_proposals.argtypes = [G, _u32p, C.c_int, _f64p, _f64p, C.c_uint64, C.c_uint64,
                                                  C.c_uint64, _u8p, C.c_int, _i8p, _f64p]
+        L.oc_rpt_inject_mh.argtypes = [C.c_int, _f64p, C.c_uint64, C.c_uint64, C.c_uint64, _u8p, _i8p, _f64p, _f64p,
+                                       _f64p, _i8p, C.c_size_t, _f64p, _u64p, _u64p, _u8p]
         _lib = L
     return _lib
 
@@ -523,11 +525,21 @@ class RPT:
                                          _p(props, _i8p), _p(Ep, _f64p))
         return props, Ep
 
-    def inject(self, mask, props, Ep):
+    def inject(self, mask, props, Ep, lq_cur=None, lq_prop=None):
         mask = np.ascontiguousarray(mask, dtype=np.uint8)
         props = np.ascontiguousarray(props, dtype=np.int8)
         Ep = np.ascontiguousarray(Ep, dtype=np.float64)
         dec = np.zeros(self.R, np.uint8)
+        if lq_cur is not None:
+            a = np.ascontiguousarray(lq_cur, np.float64)
+            b = np.ascontiguousarray(lq_prop, np.float64)
+            lib().oc_rpt_inject_mh(self.R, _p(self.beta, _f64p), self.seed, self.gid, self.Q, _p(mask, _u8p),
+                                   _p(props, _i8p), _p(Ep, _f64p), _p(a, _f64p), _p(b, _f64p), _p(self.spins, _i8p),
+                                   self.g.n, _p(self.E, _f64p), _p(self.prop_att, _u64p), _p(self.prop_acc, _u64p),
+                                   _p(dec, _u8p))
+            self.Q += 1
+            self.best = min(self.best, float(self.E.min()))
+            return dec
         lib().oc_rpt_inject(self.R, _p(self.beta, _f64p), self.seed, self.gid, self.Q, _p(mask, _u8p),
                             _p(props, _i8p), _p(Ep, _f64p), _p(self.spins, _i8p), self.g.n, _p(self.E, _f64p),
                             _p(self.prop_att, _u64p), _p(self.prop_acc, _u64p), _p(dec, _u8p))

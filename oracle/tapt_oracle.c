@@ -436,3 +436,25 @@ void oc_rpt_synthetic_proposals(const oc_rgraph* g, const uint32_t* order, int R
         Eprop[r] = oc_renergy(g, s);
     }
 }
+
+/* MH-corrected variant with FP64 energies: accept iff
+ * uniform < exp(beta[r]*(E[r]-Eprop[r])) * exp(lq_cur[r] - lq_prop[r]). */
+void oc_rpt_inject_mh(int R, const double* beta, uint64_t seed, uint64_t gid, uint64_t round, const uint8_t* mask,
+                      const int8_t* props, const double* Eprop, const double* lq_cur, const double* lq_prop,
+                      int8_t* spins, size_t n, double* E, uint64_t* att, uint64_t* acc, uint8_t* dec) {
+    uint64_t a0 = oc_stream_accept(seed, gid, round);
+    for (int r = 0; r < R; ++r) {
+        if (dec) dec[r] = 0;
+        if (!mask[r]) continue;
+        uint64_t x = oc_draw(a0, (uint64_t)r + 1);
+        double a = exp(beta[r] * (E[r] - Eprop[r])) * exp(lq_cur[r] - lq_prop[r]);
+        int accept = oc_uniform(x) < a;
+        if (att) att[r] += 1;
+        if (accept) {
+            if (acc) acc[r] += 1;
+            memcpy(spins + (size_t)r * n, props + (size_t)r * n, n);
+            E[r] = Eprop[r];
+        }
+        if (dec) dec[r] = (uint8_t)(accept ? 1 : 2);
+    }
+}

@@ -194,3 +194,40 @@ def test_real_lattice_coupling():
     pt = O.RPT(g, betas, 3, 0, g.index_order())
     pt.run(20, 1)
     assert np.array_equal(e.energies()[0], pt.E) and np.array_equal(e.spins()[0], pt.spins)
+
+
+def test_real_host_proposals_and_mh_correction_match_oracle():
+    """Externally supplied proposals on a Gaussian-J graph: plain Eq. 2 and the MH-corrected move
+     with arbitrary log q values, against the FP64 oracle."""
+    fg, gs = graphs()
+    m, g = gs[1]  # clamped Gaussian graph
+    betas = np.linspace(0.3, 2.2, 10)
+    e = T.Ensemble(m, betas, n_instances=2, seed=12, order="reference")
+    e.init_random()
+    pts = [O.RPT(g, betas, 12, k, g.index_order()) for k in range(2)]
+    rs = np.random.default_rng(8)
+    targets = np.array([1, 4, 7, 9], np.uint32)
+    for rnd in range(4):
+        e.run(6, swap_every=1)
+        for pt in pts:
+            pt.run(6, 1)
+        props = np.where(rs.random((2, len(targets), g.n)) < 0.5, 1, -1).astype(np.int8)
+        props[:, :, g.clamp != 0] = g.clamp[g.clamp != 0]
+        lqc, lqp = rs.normal(size=(2, len(targets))), rs.normal(size=(2, len(targets)))
+        mh = rnd % 2 == 1
+        acc = e.inject_proposals(props, targets, lqc if mh else None, lqp if mh else None)
+        for k, pt in enumerate(pts):
+            mask = np.zeros(pt.R, np.uint8)
+            mask[targets] = 1
+            full = np.zeros_like(pt.spins)
+            Ep = np.zeros(pt.R)
+            a, b = np.zeros(pt.R), np.zeros(pt.R)
+            for ti, r in enumerate(targets):
+                full[r] = props[k, ti]
+                Ep[r] = O.lib().oc_renergy(g.roc(), full[r].ctypes.data_as(O._i8p))
+                a[r], b[r] = lqc[k, ti], lqp[k, ti]
+            dec = pt.inject(mask, full, Ep, a if mh else None, b if mh else None)
+            assert np.array_equal(acc[k], (dec[targets] == 1).astype(np.uint8))
+    for k, pt in enumerate(pts):
+        assert np.array_equal(e.energies()[k], pt.E) and np.array_equal(e.spins()[k], pt.spins)
+        assert np.array_equal(e.acceptance()[3][k], pt.prop_acc)
