@@ -472,6 +472,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
+    T.set_device(local)  # the library's own (static) CUDA runtime, explicitly on this rank's GPU
     init_dist(world, local)
     comm = T.NcclComm(share_unique_id(T.NcclComm.unique_id, rank), world, rank) if world > 1 else None
     from paper_2509_23043_b200 import sharding

@@ -31,6 +31,9 @@ struct Shard {
     }
 };
 
+// One process per GPU: make `device` current for the library on this thread before creating handles.
+inline void set_device(int device) { throw_status(tapt_set_device(device)); }
+
 struct ReducedObservables {
     std::vector<std::int64_t> obs;    // [R][5] count, sum E, sum E^2, sum |M|, sum M^2
     std::vector<std::uint64_t> hist;  // [R][nbins] (empty without a histogram)

@@ -78,6 +78,9 @@ const char* tapt_last_error(void);
 const char* tapt_version(void);
 /* Number of CUDA devices visible (0 without a GPU); never fails. */
 int tapt_device_count(void);
+/* Make `device` the current device of this library's CUDA runtime on the calling thread (one process
+ * per GPU: call it once per rank; handles live on the device current at their creation). */
+tapt_status tapt_set_device(int device);
 /* Kernels this library has launched so far (benchmark evidence); never fails. */
 unsigned long long tapt_launch_count(void);
 /* Measured ceiling of the per-update ALU work (one splitmix64 draw + threshold lookup +

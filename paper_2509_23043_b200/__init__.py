@@ -99,6 +99,7 @@ _SIGS = {
     "tapt_last_error": (C.c_char_p, []),
     "tapt_version": (C.c_char_p, []),
     "tapt_device_count": (C.c_int, []),
+    "tapt_set_device": (C.c_int, [C.c_int]),
     "tapt_launch_count": (C.c_ulonglong, []),
     "tapt_probe_decision_rate": (C.c_int, [C.c_int, C.c_int, C.c_uint32, _f64p, _f64p]),
     "tapt_model_create_lattice": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_int, C.POINTER(_vp)]),
@@ -212,6 +213,11 @@ def _p(a, t):
 
 def device_count() -> int:
     return int(lib().tapt_device_count())
+
+
+def set_device(device: int):
+    """Make `device` current for the native library on this thread (one process per GPU)."""
+    _check(lib().tapt_set_device(int(device)))
 
 
 def launch_count() -> int:

@@ -1220,6 +1220,17 @@ tapt_status tapt_probe_decision_rate(int blocks_per_sm, int threads, uint32_t it
         if (decisions_per_s) *decisions_per_s = n / (ms * 1e-3);
     });
 }
+// Make `device` current for this library's CUDA runtime on the calling thread (the library links
+// cudart statically, so a caller's cudaSetDevice through another runtime -- e.g. torch's -- is only
+// seen through the thread's current context; one process per GPU should call this explicitly).
+tapt_status tapt_set_device(int device) {
+    return guard([&] {
+        const int n = tapt_device_count();
+        if (device < 0 || device >= n) throw tapt::ConfigError("device index out of range");
+        CUDA_OK(cudaSetDevice(device));
+    });
+}
+
 int tapt_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) {

@@ -237,3 +237,9 @@ def test_nccl_reductions_one_rank_equal_local_sums():
     with pytest.raises(T.NcclError):
         T.lib().tapt_allreduce_observables  # noqa: B018 (symbol exists)
         T._check(T.lib().tapt_allreduce_observables(e._h, None, None, None, None))
+
+
+def test_set_device_validates_and_selects():
+    T.set_device(0)
+    with pytest.raises(T.ConfigError):
+        T.set_device(T.device_count())

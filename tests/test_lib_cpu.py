@@ -124,6 +124,8 @@ def test_device_calls_fail_loudly_without_gpu():
         T.gibbs_update(m, np.ones(64, np.int8), 3, 0.5, 1)
     with pytest.raises(T.CudaError):
         T.NcclComm(bytes(128), 1, 0)  # no communicator without a device
+    with pytest.raises(T.ConfigError):
+        T.set_device(0)  # no device 0 here
     with pytest.raises(T.ClampedSiteError):  # the reference's error order: dimension, then clamp, then device
         T.gibbs_update(T.Model.graph(2, [0], [1], [1.0], None, [1, 0]), np.ones(2, np.int8), 0, 0.5, 1)
 
