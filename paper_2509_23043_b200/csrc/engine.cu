@@ -2399,9 +2399,10 @@ tapt_status tapt_gibbs_sweep(tapt_model_t m, int8_t* s, size_t len, double beta,
             return;
         }
         std::lock_guard<std::mutex> lock(m->dropin_mu);
-        if (m->real || dE) {
+        if (m->real || (dE && m->free_sites.size() <= 8192)) {
             // K5: the reference's sequential index order in FP64 with every sweep's dE, one launch
-            // (real-valued couplings; integer ones decide by their exact tables)
+            // (real-valued couplings; integer ones decide by their exact tables).  Larger integer
+            // graphs keep K4's parallel dependency levels (one launch and one readback per sweep).
             dropin_real(m, beta).dropin_sweeps(s, beta, *rng_state, n_sweeps, dE, nullptr, 0, 0);
             *rng_state += (uint64_t)n_sweeps * (uint64_t)m->free_sites.size() * tapt_dev::kPhi;
             return;
