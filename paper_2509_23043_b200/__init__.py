@@ -766,6 +766,23 @@ def random_semiprime(seed, gid, bits=16):
     return p.value, q.value
 
 
+def residual_energy(energies, e_gnd, n_spins, best_so_far=False):
+    """residual_energy (SPEC.md:450-456; the C++ tapt::residual_energy): rho(t) = (<E(t)>_runs - E_gnd) / N,
+    energies[run][t] = the coldest replica's energy after global move t of each run (or, with
+    best_so_far, each run's best energy up to t: the non-increasing variant).  e_gnd: scalar, or one
+    reference energy per run (config 3: each instance's best over the whole run)."""
+    E = np.asarray(energies, np.float64)
+    if E.ndim != 2 or E.shape[0] == 0:
+        raise DimensionError("energies must be [runs][moves] with at least one run")
+    if n_spins <= 0:
+        raise ConfigError("n_spins must be > 0")
+    if best_so_far:
+        E = np.minimum.accumulate(E, axis=1)
+    g = np.asarray(e_gnd, np.float64)
+    g = g.reshape(-1, 1) if g.ndim == 1 else g
+    return ((E - g).mean(axis=0)) / float(n_spins)
+
+
 def estimate_ground_energy(model, restarts, sweeps, seed, beta_start=0.1, beta_end=5.0, stages=50,
                            n_instances=1, instance_offset=0, signs=None, disorder_seed=None, clamps=None):
     """estimate_ground_energy: best energy over `restarts` geometric-annealing

@@ -166,3 +166,17 @@ def test_isingmodel_v1_round_trip_and_errors(tmp_path):
         assert O.ref().ref_graph_digest(rg) == m.digest()
         O.ref().ref_graph_free(rg)
         del C
+
+
+def test_residual_energy_spec_examples():
+    """SPEC.md:454-456: ground state -> 0; one excited bond on an N = 10 chain (dE = 2J) -> 0.2;
+    the mean over runs; best-so-far is non-increasing."""
+    eg = -9.0
+    assert np.allclose(T.residual_energy([[eg, eg]], eg, 10), 0.0)
+    assert np.allclose(T.residual_energy([[eg + 2.0, eg + 2.0]], eg, 10), 0.2)
+    assert np.allclose(T.residual_energy([[eg, eg], [eg + 4.0, eg + 4.0]], eg, 10), 0.2)
+    r = T.residual_energy([[eg + 6, eg + 2, eg + 4, eg]], eg, 10, best_so_far=True)
+    assert np.all(np.diff(r) <= 0) and np.allclose(r, [0.6, 0.2, 0.2, 0.0])
+    assert np.allclose(T.residual_energy([[1.0, 0.0], [3.0, 2.0]], [0.0, 2.0], 1), [1.0, 0.0])
+    with pytest.raises(T.DimensionError):
+        T.residual_energy([], eg, 10)

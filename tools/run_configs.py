@@ -89,8 +89,8 @@ def residual(e, n, total, run):
         done = c
         best.append(e.best().astype(np.float64))
     B = np.stack(best)        # [checkpoint][instance]
-    ref = B[-1]               # lowest energy seen over the whole run (all slots)
-    rho = ((B - ref) / n).mean(1)
+    # per instance, its lowest energy over the whole run (all slots) stands in for E_gnd
+    rho = T.residual_energy(B.T, B[-1], n)
     return cps, B, rho
 
 
