@@ -395,7 +395,6 @@ __device__ void rows_attention_fwd(Smem<RB>& s, KVChunk& kv, const FArgs& a, int
             const float p = j <= tr ? __expf(sc - mn) : 0.f;
             lsum[k] = lsum[k] * corr + warp_sum(p);
             float oo = o[k] * corr;
-#pragma unroll 8
             reinterpret_cast<float*>(kv.P[w])[lane] = p;  // broadcast through shared memory, not 32 shuffles
             __syncwarp();
 #pragma unroll
