@@ -68,6 +68,13 @@ class Communicator {
         return r;
     }
 
+    // Per-instance best energies of every rank, in global instance order.
+    std::vector<std::int64_t> allgather_best(tapt_ensemble_t e, std::uint64_t total) const {
+        std::vector<std::int64_t> out(total);
+        throw_status(tapt_allgather_best(e, c_.get(), total, out.data()));
+        return out;
+    }
+
   private:
     std::shared_ptr<void> c_;
 };

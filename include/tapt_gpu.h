@@ -273,6 +273,9 @@ tapt_status tapt_nccl_comm_size(void* comm, int* n_ranks);
  *   best [1]         lowest energy seen by any instance on any rank
  * Integer-coupling ensembles. */
 tapt_status tapt_allreduce_observables(tapt_ensemble_t e, void* comm, int64_t* obs, uint64_t* hist, int64_t* best);
+/* Per-instance best energies of all ranks in global instance order, out[total] (ncclAllGather of each
+ * rank's (instance_offset, count) and of its best energies padded to the largest shard). */
+tapt_status tapt_allgather_best(tapt_ensemble_t e, void* comm, uint64_t total, int64_t* out);
 
 /* ------------------------------------------------------ problem suite -- */
 /* Instance construction for BASELINE config 4 (proj/src/problems.cpp:1 is a

@@ -146,6 +146,7 @@ _SIGS = {
     "tapt_nccl_comm_destroy": (C.c_int, [_vp]),
     "tapt_nccl_comm_size": (C.c_int, [_vp, C.POINTER(C.c_int)]),
     "tapt_allreduce_observables": (C.c_int, [_vp, _vp, _i64p, _u64p, _i64p]),
+    "tapt_allgather_best": (C.c_int, [_vp, _vp, C.c_uint64, _i64p]),
     "tapt_ensemble_set_betas": (C.c_int, [_vp, _f64p, C.c_int]),
     "tapt_ensemble_set_streams": (C.c_int, [_vp, _u64p]),
     "tapt_ensemble_init_from_streams": (C.c_int, [_vp, _u64p]),
@@ -375,6 +376,13 @@ def allreduce_observables(ens, comm: NcclComm):
     hist = np.zeros((ens.R, nb), np.uint64) if nb else None
     _check(lib().tapt_allreduce_observables(ens._h, comm._h, _p(obs, _i64p), _p(hist, _u64p), _p(best, _i64p)))
     return {"obs": obs, "hist": hist, "best": int(best[0])}
+
+
+def allgather_best(ens, comm: NcclComm, total: int):
+    """Every rank's per-instance best energies in global instance order (tapt_allgather_best)."""
+    out = np.zeros(int(total), np.int64)
+    _check(lib().tapt_allgather_best(ens._h, comm._h, int(total), _p(out, _i64p)))
+    return out
 
 
 # ---------------------------------------------------------------- ensembles --

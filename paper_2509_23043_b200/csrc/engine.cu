@@ -2462,6 +2462,7 @@ struct NcclApi {
     ncclResult_t (*all_reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                                cudaStream_t) = nullptr;
     ncclResult_t (*comm_count)(const ncclComm_t, int*) = nullptr;
+    ncclResult_t (*all_gather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
     const char* (*error_string)(ncclResult_t) = nullptr;
 };
 
@@ -2481,8 +2482,10 @@ const NcclApi& nccl() {
         api.comm_destroy = reinterpret_cast<decltype(api.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
         api.all_reduce = reinterpret_cast<decltype(api.all_reduce)>(dlsym(h, "ncclAllReduce"));
         api.comm_count = reinterpret_cast<decltype(api.comm_count)>(dlsym(h, "ncclCommCount"));
+        api.all_gather = reinterpret_cast<decltype(api.all_gather)>(dlsym(h, "ncclAllGather"));
         api.error_string = reinterpret_cast<decltype(api.error_string)>(dlsym(h, "ncclGetErrorString"));
-        if (!api.get_unique_id || !api.comm_init_rank || !api.comm_destroy || !api.all_reduce || !api.comm_count)
+        if (!api.get_unique_id || !api.comm_init_rank || !api.comm_destroy || !api.all_reduce || !api.comm_count ||
+            !api.all_gather)
             err = "NCCL library lacks the expected symbols";
     });
     if (!err.empty()) throw tapt::NcclError(err);
@@ -2583,6 +2586,57 @@ tapt_status tapt_allreduce_observables(tapt_ensemble_t e, void* comm, int64_t* o
             CUDA_OK(cudaMemcpyAsync(hist, h.p, h.n * sizeof(uint64_t), cudaMemcpyDeviceToHost, e->stream));
         if (best) CUDA_OK(cudaMemcpyAsync(best, b.p, sizeof(long long), cudaMemcpyDeviceToHost, e->stream));
         CUDA_OK(cudaStreamSynchronize(e->stream));
+    });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+// Per-instance best energies of every rank's shard in global instance order ("per-
+// instance results come back by ncclAllGather"): each rank contributes (instance_offset, count) and
+// its best energies padded to the largest shard; out[gid] for gid in [0, total).  Shards may be any
+// disjoint blocks that cover [0, total).
+tapt_status tapt_allgather_best(tapt_ensemble_t e, void* comm, uint64_t total, int64_t* out) {
+    return guard([&] {
+        check_ens(e);
+        if (!comm) throw tapt::NcclError("null NCCL communicator");
+        if (!out) throw tapt::ConfigError("null output");
+        if (e->rx) throw tapt::ConfigError("best energies of real-valued models: use tapt_get_best_f64 per rank");
+        e->poll_sched(true);
+        const auto& api = nccl();
+        ncclComm_t c = static_cast<ncclComm_t>(comm);
+        int world = 0;
+        nccl_ok(api.comm_count(c, &world), "ncclCommCount");
+        DevBuf<long long> meta, metas;
+        meta.alloc(2);
+        metas.alloc((size_t)2 * world);
+        const long long mine[2] = {(long long)e->gid0, (long long)e->I};
+        CUDA_OK(cudaMemcpyAsync(meta.p, mine, sizeof(mine), cudaMemcpyHostToDevice, e->stream));
+        nccl_ok(api.all_gather(meta.p, metas.p, 2, ncclInt64, c, e->stream), "ncclAllGather(shards)");
+        std::vector<long long> m((size_t)2 * world);
+        CUDA_OK(cudaMemcpyAsync(m.data(), metas.p, m.size() * sizeof(long long), cudaMemcpyDeviceToHost, e->stream));
+        CUDA_OK(cudaStreamSynchronize(e->stream));
+        long long maxc = 0, sum = 0;
+        for (int r = 0; r < world; ++r) {
+            maxc = std::max(maxc, m[2 * r + 1]);
+            sum += m[2 * r + 1];
+            if (m[2 * r] < 0 || (uint64_t)(m[2 * r] + m[2 * r + 1]) > total)
+                throw tapt::DimensionError("a rank's shard lies outside [0, total)");
+        }
+        if ((uint64_t)sum != total) throw tapt::DimensionError("the ranks' shards do not cover total instances");
+        DevBuf<int> pad;
+        DevBuf<int> all;
+        pad.alloc((size_t)maxc);
+        all.alloc((size_t)maxc * world);
+        pad.zero(e->stream);
+        CUDA_OK(cudaMemcpyAsync(pad.p, e->best.p, (size_t)e->I * sizeof(int), cudaMemcpyDeviceToDevice, e->stream));
+        nccl_ok(api.all_gather(pad.p, all.p, (size_t)maxc, ncclInt32, c, e->stream), "ncclAllGather(best)");
+        std::vector<int> h((size_t)maxc * world);
+        CUDA_OK(cudaMemcpyAsync(h.data(), all.p, h.size() * sizeof(int), cudaMemcpyDeviceToHost, e->stream));
+        CUDA_OK(cudaStreamSynchronize(e->stream));
+        for (int r = 0; r < world; ++r)
+            for (long long k = 0; k < m[2 * r + 1]; ++k) out[m[2 * r] + k] = h[(size_t)r * maxc + k];
     });
 }
 

@@ -233,6 +233,9 @@ def test_nccl_reductions_one_rank_equal_local_sums():
     h = e.histogram()
     assert np.array_equal(r["hist"], h) and h.sum() == 5 * 8 * 10
     assert r["best"] == e.best().min()
+    assert np.array_equal(T.allgather_best(e, comm, 5), e.best())
+    with pytest.raises(T.DimensionError):
+        T.allgather_best(e, comm, 7)  # the ranks' shards must cover the total
     comm.close()
     with pytest.raises(T.NcclError):
         T.lib().tapt_allreduce_observables  # noqa: B018 (symbol exists)
