@@ -214,3 +214,20 @@ def test_tensor_core_forward_equals_cuda_core_forward():
     for b in (0, 4, 8):
         zo = F.forward_logits(p, CFG, tok[b], betas[b])
         assert np.max(np.abs(z_tc[b] - zo)) < LOGIT_TOL * max(1.0, np.max(np.abs(zo)))
+
+
+@pytest.mark.parametrize("Tn", [1, 31, 32, 33, 127, 128, 129, 200])
+def test_tensor_core_forward_ragged_lengths(Tn):
+    """Sequence lengths around the 32-key chunk and 128-query block edges (incl. a single position and
+    one row in the last block), against the fp64 oracle; n_prefix = T gives log q = 0."""
+    f, p = model(seed=7, max_len=256)
+    rs = np.random.default_rng(Tn)
+    B = 3
+    tok = rs.integers(0, 2, (B, Tn)).astype(np.uint8)
+    betas = np.array([0.3, 1.0, 4.0])
+    lq, z = f.log_prob(tok, betas, return_logits=True)
+    for b in range(B):
+        zo = F.forward_logits(p, CFG, tok[b], betas[b])
+        assert np.max(np.abs(z[b] - zo)) < LOGIT_TOL * max(1.0, np.max(np.abs(zo)))
+        assert abs(lq[b] - F.log_prob(p, CFG, tok[b], betas[b])) < 1e-3
+    assert np.all(f.log_prob(tok, betas, n_prefix=Tn) == 0.0)

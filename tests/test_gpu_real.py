@@ -231,3 +231,21 @@ def test_real_host_proposals_and_mh_correction_match_oracle():
     for k, pt in enumerate(pts):
         assert np.array_equal(e.energies()[k], pt.E) and np.array_equal(e.spins()[k], pt.spins)
         assert np.array_equal(e.acceptance()[3][k], pt.prop_acc)
+
+
+def test_real_clamped_colour_order_ragged_groups():
+    """Real couplings with clamps in colour order with R = 40 (a full and a partial 32-lane group) and
+    a swap cadence of 3, against the oracle; per-instance clamps are refused (model clamps only)."""
+    fg, gs = graphs()
+    m, g = gs[1]
+    betas = np.linspace(0.1, 3.0, 40)
+    e = T.Ensemble(m, betas, n_instances=2, seed=21)
+    e.init_random()
+    e.run(25, swap_every=3)
+    order = g.colour_order(m.schedule()[0])
+    for k in range(2):
+        pt = O.RPT(g, betas, 21, k, order)
+        pt.run(25, 3)
+        assert np.array_equal(e.energies()[k], pt.E) and np.array_equal(e.spins()[k], pt.spins)
+    with pytest.raises(T.ConfigError):
+        e.set_clamps(np.zeros((2, g.n), np.int8))
