@@ -50,9 +50,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"],
+    ap.add_argument("--workload", default="cfg5", choices=["cfg1", "cfg2", "cfg3", "cfg4", "cfg5", "real"],
                     help="BASELINE.json config (default cfg5, the headline); cfg1-4 run on one GPU with the "
-                         "reference CPU path timed beside them at SURVEY.md 8(d)'s sub-budgets")
+                         "reference CPU path timed beside them at SURVEY.md 8(d)'s sub-budgets; real: K5 on a "
+                         "Gaussian-coupling 3D lattice (no BASELINE config uses real couplings)")
     ap.add_argument("--instances", type=int, default=4096)
     ap.add_argument("--sweeps-per-step", type=int, default=1000)
     ap.add_argument("--measure-every", type=int, default=10)
@@ -306,6 +307,65 @@ def run_workload(args):
     print(json.dumps(out), flush=True)
 
 
+def run_real(args):
+    """bench.py --workload real: K5 (real-valued couplings) on a 3D lattice L=16 periodic with Gaussian
+    couplings N(0,1) (SPEC.md:511's Gaussian option) and fields N(0, 0.3^2), 64 slots beta linear
+    [0.2, 3.0], 256 instances, the reference's index order (bit-exact with its gibbs_sweep), swap every
+    sweep; one step = 100 sweeps.  The reference CPU path (oracle/_ref: the unmodified gibbs_sweep in the
+    restated PT driver) runs beside it on the same graph."""
+    import ctypes as C
+
+    import torch
+
+    import paper_2509_23043_b200 as T
+    L, R, I, S = 16, 64, 256, 100
+    n = L ** 3
+    ci, cj, _ = T.Model.lattice((L,)).couplings()
+    rs = np.random.default_rng(5)
+    J, h = rs.normal(size=len(ci)), rs.normal(size=n) * 0.3
+    m = T.Model.graph(n, ci, cj, J, h)
+    b = np.linspace(0.2, 3.0, R)
+    torch.cuda.set_device(0)
+    e = T.Ensemble(m, b, n_instances=I, seed=3, order="reference")
+    e.init_random()
+    for _ in range(args.warmup):
+        e.run(S // 10, swap_every=1)
+    e.synchronize()
+    l0 = T.launch_count()
+    with ClockSampler(0) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            e.run(S, swap_every=1)
+        e.synchronize()
+        dt = time.perf_counter() - t0
+    ties, replays = e.near_ties()
+    value = I * R * n * S * args.steps / dt
+    out = {"metric": "spin updates/sec, real-valued couplings (K5)", "value": value, "unit": UNIT, "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+           "higher_is_better": True, "scaling": "replicas only", "vs_baseline": None,
+           "dtype": "f64 local fields / u64 splitmix64", "data": "synthetic",
+           "config": {"workload": "3D lattice L=16, Gaussian J and h, 64 slots, 256 instances, reference index "
+                                  "order, swap every sweep, 100 sweeps per step", "near_ties": ties,
+                      "replays": replays, "kernel": e.launch_log()},
+           "gpu_launches": T.launch_count() - l0, "clocks": clk.summary()}
+    if not args.no_cpu_baseline:
+        from oracle import oracle as O  # the reference CPU path (cpu_baseline leg)
+        k = min(16, os.cpu_count() or 1)
+        g = O.Graph.from_couplings(n, ci, cj, J, h)
+        hs = [O.ref_graph(g) for _ in range(k)]
+        arr = (C.c_void_p * k)(*hs)
+        bb, mb = np.ascontiguousarray(b), np.zeros(R)
+        t0 = time.perf_counter()
+        O.ref().ref_pt_run(arr, k, 0, R, bb.ctypes.data_as(O._f64p), 3, 20, 1, 0, 0, mb.ctypes.data_as(O._f64p), 0,
+                           k, None, None, None, None)
+        dc = time.perf_counter() - t0
+        for hh in hs:
+            O.ref().ref_graph_free(hh)
+        out["cpu_baseline"] = {"value": k * R * n * 20 / dc, "unit": UNIT, "cores": k, "kind": "reference",
+                               "sample": f"{k} instances x 20 sweeps of the same graph ({dc:.1f} s, '{cpu_model()}')"}
+    print(json.dumps(out), flush=True)
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -459,6 +519,9 @@ def main():
     world_checked = check_world(args)
     if args.impl == "reference":
         run_reference(args)
+        return
+    if args.workload == "real":
+        run_real(args)
         return
     if args.workload != "cfg5":
         run_workload(args)

@@ -10,7 +10,6 @@ import torch  # noqa: E402
 
 import paper_2509_23043_b200 as T  # noqa: E402
 from paper_2509_23043_b200 import workloads as WL  # noqa: E402
-from oracle import oracle as O  # noqa: E402  (lattice couplings only)
 
 
 def timed(e, stream, S=500):
@@ -26,7 +25,8 @@ def timed(e, stream, S=500):
 
 stream = torch.cuda.Stream()
 L = 12
-n, ci, cj, w = O.lattice_couplings((L,), 1.0, True)
+ci, cj, w = T.Model.lattice((L,)).couplings()  # the library's LatticeSpec bonds
+n = L ** 3
 cl = np.zeros(n, np.int8)
 cl[: L * L] = 1  # z = 0 plane clamped up
 ml = T.Model.graph(n, ci, cj, w, None, cl)
