@@ -350,19 +350,21 @@ def run_real(args):
            "gpu_launches": T.launch_count() - l0, "clocks": clk.summary()}
     if not args.no_cpu_baseline:
         from oracle import oracle as O  # the reference CPU path (cpu_baseline leg)
+        if not O.have_ref():
+            raise SystemExit("--workload real: oracle/_ref is not built (run __graft_entry__.build())")
         k = min(16, os.cpu_count() or 1)
         g = O.Graph.from_couplings(n, ci, cj, J, h)
         hs = [O.ref_graph(g) for _ in range(k)]
         arr = (C.c_void_p * k)(*hs)
         bb, mb = np.ascontiguousarray(b), np.zeros(R)
         t0 = time.perf_counter()
-        O.ref().ref_pt_run(arr, k, 0, R, bb.ctypes.data_as(O._f64p), 3, 20, 1, 0, 0, mb.ctypes.data_as(O._f64p), 0,
+        O.ref().ref_pt_run(arr, k, 0, R, bb.ctypes.data_as(O._f64p), 3, 2000, 1, 0, 0, mb.ctypes.data_as(O._f64p), 0,
                            k, None, None, None, None)
         dc = time.perf_counter() - t0
         for hh in hs:
             O.ref().ref_graph_free(hh)
-        out["cpu_baseline"] = {"value": k * R * n * 20 / dc, "unit": UNIT, "cores": k, "kind": "reference",
-                               "sample": f"{k} instances x 20 sweeps of the same graph ({dc:.1f} s, '{cpu_model()}')"}
+        out["cpu_baseline"] = {"value": k * R * n * 2000 / dc, "unit": UNIT, "cores": k, "kind": "reference",
+                               "sample": f"{k} instances x 2000 sweeps of the same graph ({dc:.1f} s, '{cpu_model()}')"}
     print(json.dumps(out), flush=True)
 
 
