@@ -49,8 +49,9 @@ struct Csr3 {
 };
 size_t k3_smem_bytes(int R, int nidx, int nadj, int nfree, int n, int ncls, int ipb);
 int k3_row_stride();
-int k3_resident_units(const PTArgs& a, const Csr3& g, int ipb);
-cudaError_t launch_k3(const PTArgs& a, const Csr3& g, int ipb, cudaStream_t st);
+// shape: instance teams per CTA (1..4), or -Q for split sites (Q = 2, 4 lanes per site, one team per CTA)
+int k3_resident_units(const PTArgs& a, const Csr3& g, int shape);
+cudaError_t launch_k3(const PTArgs& a, const Csr3& g, int shape, cudaStream_t st);
 cudaError_t launch_k2(const PTArgs& a, const CsrArgs& g, int threads, bool cluster, cudaStream_t st);
 size_t k4_smem_bytes(int n, int R, int nidx, int nnz, int nfree, int nlev, int ipb);
 int k4_max_ipb();
@@ -750,6 +751,8 @@ struct tapt_ensemble_s {
     // K3 (bit-sliced CSR, k3_bitcsr.cu) for colour-order runs of graphs with small integer
     // couplings and fields; instance teams per CTA (k3_ipb), 0 = not eligible / not decided
     int k3_ipb = -1;
+    int k3_q = 1;  // lanes per site (k3_bitcsr.cu split sites)
+    int k3_shape() const { return k3_q > 1 ? -k3_q : k3_ipb; }
 
     Csr3 k3_args() const {
         Csr3 g{};
@@ -805,6 +808,18 @@ struct tapt_ensemble_s {
         }
         if (const char* e = std::getenv("TAPT_K3_IPB"))
             k3_ipb = std::max(1, std::min(fit, std::atoi(e)));
+        // Split sites (4 lanes per site, one 512-thread team per CTA) when every instance has an SM
+        // to itself: a lone team is bound by its per-site dependency chains, and splitting the
+        // replicas over 4 lanes raises its rate to ~1.9 G updates/s (config 4 at 64 / 148
+        // instances: +11 / +14 %, tools/k3_q_shards.py); with two or more teams per SM one lane per
+        // site wins (no replicated site work).
+        k3_q = 1;
+        if ((int)I <= nsm && I * 1.9 > best) k3_q = 4;
+        if (const char* e = std::getenv("TAPT_K3_Q")) {
+            const int q = std::atoi(e);
+            k3_q = q >= 4 ? 4 : q >= 2 ? 2 : 1;
+        }
+        if (k3_q > 1) k3_ipb = 1;
         return k3_ipb > 0;
     }
 
@@ -973,8 +988,10 @@ struct tapt_ensemble_s {
             log_launch(name, a);
             e = launch_k1(a, m->ld, nt, cluster, stream);
         } else if (!a.energy_only && a.G == 1 && k3_eligible()) {
-            log_launch("k3_bitcsr_pt<" + std::string(a.sched ? "1," : "0,") + std::to_string(k3_ipb) + ">", a);
-            e = launch_k3(a, k3_args(), k3_ipb, stream);
+            log_launch("k3_bitcsr_pt<" + std::string(a.sched ? "1," : "0,") + std::to_string(k3_ipb) + "," +
+                           std::to_string(k3_q) + ">",
+                       a);
+            e = launch_k3(a, k3_args(), k3_shape(), stream);
         } else if (!a.energy_only && a.G == 1 && k4_eligible()) {
             log_launch(std::string("k4_levels_pt<") + (a.sched ? "1>" : "0>"), a);
             e = launch_k4(a, csr_args(true), k4_ipb, stream);
@@ -1039,7 +1056,7 @@ struct tapt_ensemble_s {
         if (const char* e = std::getenv("TAPT_BALANCE"); e && std::atoi(e) == 0) return false;
         if (k1_units < 0)
             k1_units = use_k1           ? k1_resident_units(a, m->ld, k1_threads, cluster)
-                       : k3_eligible() ? k3_resident_units(a, k3_args(), k3_ipb)
+                       : k3_eligible() ? k3_resident_units(a, k3_args(), k3_shape())
                        : k4_eligible() ? k4_resident_units(a, csr_args(true), k4_ipb)
                                        : k2_resident_units(a, csr_args(order == TAPT_ORDER_REFERENCE), k2_nt(), cluster);
         const int M = k1_units;

@@ -18,6 +18,12 @@
 //   * Teams: 4 warps (128 threads) per instance with their own named barrier; up to 4 instances
 //     per CTA share one staged copy of the graph and of the slot threshold table, and progress
 //     independently (no CTA-wide barrier inside the sweep loop).
+//   * Split sites (Q = 2, 4; few instances per GPU): a team of 128 Q threads, Q adjacent lanes per
+//     site.  Every lane of the group forms the site's bit-sliced count (broadcast loads) and decides
+//     the replicas B = Q j + q of its lane q; the group ORs its bits into the word with shuffles.
+//     With 4Q warps per instance instead of 4, the per-site dependency chain (the latency that
+//     bounds an instance when its SM runs nothing else) is ~1/Q as long.  Energies are kept as
+//     integers per owned replica (8 dU per flip, from the same acc the threshold index uses).
 // The draw of replica b at site i in sweep t is the reference's per-site stream position
 // (mcmc.cpp:30-45), so the chain is bit-identical to K2's colour order and to the oracle
 // (oracle/tapt_oracle.c): tests/test_gpu_parity.py.
@@ -183,6 +189,41 @@ struct Csr3 {
     int nidx4;                 // staged slot-table row stride (nidx rounded up to 4)
 };
 
+// Split sites: spread bit j of x to bit Q j.
+template <int Q>
+__device__ __forceinline__ uint32_t spread_q(uint32_t x) {
+    if constexpr (Q == 4) {
+        x &= 0xFFu;
+        x = (x | (x << 12)) & 0x000F000Fu;
+        x = (x | (x << 6)) & 0x03030303u;
+        return (x | (x << 3)) & 0x11111111u;
+    } else {
+        x &= 0xFFFFu;
+        x = (x | (x << 8)) & 0x00FF00FFu;
+        x = (x | (x << 4)) & 0x0F0F0F0Fu;
+        x = (x | (x << 2)) & 0x33333333u;
+        return (x | (x << 1)) & 0x55555555u;
+    }
+}
+
+// Split sites: decision of replica B = Q J + q (N nibble k of N[m] is replica 4k + m, so B sits in
+// Ns[J % (4/Q)] = N[Q (J % (4/Q)) + q] at nibble J / (4/Q)).  Ubq / sbq: this lane's first row / base.
+template <bool HEAVY, int Q, int J>
+__device__ __forceinline__ void k3q_decide_rec(const uint8_t* Ubq, const uint32_t (&Ns)[4 / Q],
+                                               const uint32_t (&Nhs)[4 / Q], const uint64_t* sbq, uint64_t ph,
+                                               const MixConsts& mc, uint32_t& w, uint32_t& tmin,
+                                               uint32_t (&ix8)[32 / Q]) {
+    constexpr int r = J % (4 / Q), sh = 4 * (J / (4 / Q));
+    uint32_t ix = nib8<sh>(Ns[r]);
+    if constexpr (HEAVY) ix += nib128<sh>(Nhs[r]);
+    ix8[J] = ix;
+    const uint32_t thr = *reinterpret_cast<const uint32_t*>(Ubq + ix + Q * J * kRow3 * 4);
+    const uint64_t z = sbq[Q * J] + ph;
+    const uint32_t h = mix_pre_hi<TAPT_K3_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), mc);
+    tmin = min(tmin, decide_acc(h, thr, w) + 1u);
+    if constexpr (J > 0) k3q_decide_rec<HEAVY, Q, J - 1>(Ubq, Ns, Nhs, sbq, ph, mc, w, tmin, ix8);
+}
+
 // Process one class position (site) of this team's instance.
 template <bool HW>
 __device__ __forceinline__ void k3_site(const PTArgs& a, const PTShared& S, const uint4 md, uint8_t* W2,
@@ -248,18 +289,100 @@ __device__ __forceinline__ void k3_site(const PTArgs& a, const PTShared& S, cons
     }
 }
 
+// Split sites: lane q of the site's group of Q lanes decides replicas Q j + q and adds
+// 8 (U(new) - U(old)) of each to dU[j].  Called by the whole warp (full-mask shuffles); lanes past
+// the end of the class (on = false) repeat a valid site and store nothing.
+template <bool HW, int Q>
+__device__ __forceinline__ void k3q_site(const PTArgs& a, const PTShared& S, const uint4 md, uint8_t* W2,
+                                         const uint32_t* adj, const uint8_t* ubq, int n, uint32_t vmask, int nv, int q,
+                                         bool on, int (&dU)[32 / Q]) {
+    const uint32_t i = md.x;
+    const uint64_t ph = (uint64_t)(md.y & 0xFFFFFFu) * kPhi;
+    const int off = (int)(md.w & 0xFFFFu) - 32768;
+    const int nch = (int)((md.w >> 16) & 15u);
+    const int sp = (int)((md.w >> 20) & 127u);
+    const bool heavy = HW && ((md.w >> 27) & 1u);
+    const uint32_t* ap = adj + md.z;
+    uint32_t A[7];
+    if (heavy) {
+        const uint32_t hc = md.y >> 24;
+#pragma unroll
+        for (int p = 0; p < 7; ++p) A[p] = ((hc >> p) & 1u) ? 0xFFFFFFFFu : 0u;
+        for (int ch = 0; ch < nch; ++ch) {
+            uint32_t P[5];
+            chunk_count(W2, ap + 16 * ch, P);
+            uint32_t c;
+            if ((md.w >> (28 + ch)) & 1u) {
+                ha(A[1], P[0], A[1], c);
+#pragma unroll
+                for (int p = 2; p < 6; ++p) fa(A[p], P[p - 1], c, A[p], c);
+                A[6] ^= c;
+            } else {
+                ha(A[0], P[0], A[0], c);
+#pragma unroll
+                for (int p = 1; p < 5; ++p) fa(A[p], P[p], c, A[p], c);
+                ha(A[5], c, A[5], c);
+                A[6] ^= c;
+            }
+        }
+    } else {
+        uint32_t P[5];
+        chunk_count(W2, ap, P);
+#pragma unroll
+        for (int p = 0; p < 5; ++p) A[p] = P[p];
+        A[5] = A[6] = 0;
+    }
+    uint32_t N[4], Nh[4] = {0u, 0u, 0u, 0u};
+    nibbles4(A[0], A[1], A[2], A[3], N);
+    if constexpr (HW) nibbles4(A[4], A[5], A[6], 0u, Nh);
+    uint32_t Ns[4 / Q], Nhs[4 / Q];
+#pragma unroll
+    for (int r = 0; r < 4 / Q; ++r) {
+        const int m = Q * r + q;
+        Ns[r] = m == 0 ? N[0] : m == 1 ? N[1] : m == 2 ? N[2] : N[3];
+        Nhs[r] = m == 0 ? Nh[0] : m == 1 ? Nh[1] : m == 2 ? Nh[2] : Nh[3];
+    }
+    const uint32_t old = *reinterpret_cast<const uint32_t*>(W2 + 4 * i);
+    uint32_t ubr = (uint32_t)__cvta_generic_to_shared(ubq) + (uint32_t)(4 * off);
+    asm("mov.b32 %0, %0;" : "+r"(ubr));
+    const uint8_t* Ub = reinterpret_cast<const uint8_t*>(__cvta_shared_to_generic(ubr));
+    uint32_t w = 0, tmin = 0xFFFFFFFFu, ix8[32 / Q];
+    k3q_decide_rec<HW, Q, 32 / Q - 1>(Ub, Ns, Nhs, &S.sb[q], ph, a.mc, w, tmin, ix8);
+    uint32_t nw = spread_q<Q>(~w) << q;
+#pragma unroll
+    for (int d = 1; d < Q; d <<= 1) nw |= __shfl_xor_sync(0xFFFFFFFFu, nw, d);
+    nw &= vmask;
+    if (__any_sync(0xFFFFFFFFu, tmin <= 2u))
+        nw = k3_decide_exact(a, S, off, A[0], A[1], A[2], A[3], A[4], A[5], A[6], ph, nv);
+    nw |= old & ~vmask;
+    if (on && q == 0) {
+        *reinterpret_cast<uint32_t*>(W2 + 4 * i) = nw;
+        *reinterpret_cast<uint32_t*>(W2 + 4 * (n + i)) = ~nw;
+    }
+    const uint32_t fl = on ? (nw ^ old) >> q : 0u, up = nw >> q;
+    const int s8 = 8 * sp;
+#pragma unroll
+    for (int j = 0; j < 32 / Q; ++j) {
+        const int d = 2 * (int)ix8[j] - s8;  // 8 (U(0) - U(1)) = 8 (2 acc - S')
+        const int sg = -(int)((up >> (Q * j)) & 1u), f = -(int)((fl >> (Q * j)) & 1u);
+        dU[j] += ((d ^ sg) - sg) & f;  // flipped: -d to up, +d to down
+    }
+}
+
 // IPB: instance teams per CTA.  One instantiation per IPB so that each launch shape gets the whole
 // register file for its threads (3 teams: 167 registers, +2 % on config 4 over a 512-thread bound).
-template <bool BAL, int IPB>
-__global__ void __launch_bounds__(kT3 * IPB, 1) k3_bitcsr_pt(const PTArgs a, const Csr3 g) {
+// Q: lanes per site (1: one thread per site word; 2, 4: split sites, IPB = 1).
+template <bool BAL, int IPB, int Q>
+__global__ void __launch_bounds__(kT3 * Q * IPB, 1) k3_bitcsr_pt(const PTArgs a, const Csr3 g) {
+    constexpr int TT = kT3 * Q;  // threads per instance team
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ PTShared SS[kIPB3];
     __shared__ int corr_sh[kIPB3];
     __shared__ uint64_t str_sh[kIPB3][kW];  // the instance's dynamics stream states by slot
     const int n = a.n, nidx = a.nidx, n_free = (int)a.n_free;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
-    const int ipb = nt / kT3, kin = tid / kT3, ti = tid - kin * kT3;
-    const SubTeam tm{ti, kT3, 1 + kin};
+    const int ipb = nt / TT, kin = tid / TT, ti = tid - kin * TT;
+    const SubTeam tm{ti, TT, 1 + kin};
     const int nv = own_count(a, 0);
     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
     // shared memory: Uslot [R][nidx4] | adj [nadj] | meta [n_free] (uint4) | class_ptr [n_classes+1] |
@@ -303,7 +426,7 @@ __global__ void __launch_bounds__(kT3 * IPB, 1) k3_bitcsr_pt(const PTArgs a, con
         const uint64_t t0 = a.t0 + (uint64_t)item.s0;
         {
             const uint32_t* src = a.words + (size_t)inst * n;
-            for (int k = ti; k < n; k += kT3) {
+            for (int k = ti; k < n; k += TT) {
                 const uint32_t v = src[k];
                 W2w[k] = v;
                 W2w[n + k] = ~v;
@@ -314,8 +437,8 @@ __global__ void __launch_bounds__(kT3 * IPB, 1) k3_bitcsr_pt(const PTArgs a, con
             }
         }
         pt_load_perm(a, S, inst, tm);
-        for (int r = ti; r < a.R; r += kT3) str_sh[kin][r] = a.streams[(size_t)inst * a.R + r];
-        for (int b = ti; b < nv; b += kT3) S.Eown[(t0 + 1) & 1][b] = a.E[(size_t)inst * a.B + b];
+        for (int r = ti; r < a.R; r += TT) str_sh[kin][r] = a.streams[(size_t)inst * a.R + r];
+        for (int b = ti; b < nv; b += TT) S.Eown[(t0 + 1) & 1][b] = a.E[(size_t)inst * a.B + b];
         tm.sync();
 
         uint64_t pass = a.p0;
@@ -327,16 +450,52 @@ __global__ void __launch_bounds__(kT3 * IPB, 1) k3_bitcsr_pt(const PTArgs a, con
             par = (int)(t & 1);
             {  // per-buffer stream bases for sweep t (pt_stream_bases with the staged stream states)
                 const uint64_t k0 = a.draw_base + t * (uint64_t)a.n_free + 1ull;
-                for (int b = ti; b < nv; b += kT3) S.sb[b] = str_sh[kin][S.slot_of[b]] + k0 * kPhi;
+                for (int b = ti; b < nv; b += TT) S.sb[b] = str_sh[kin][S.slot_of[b]] + k0 * kPhi;
             }
             // per-buffer threshold rows for the slots the buffers occupy this sweep
-            for (int e = ti; e < kW * (kRow3 / 4); e += kT3) {
+            for (int e = ti; e < kW * (kRow3 / 4); e += TT) {
                 const int b = e / (kRow3 / 4), x4 = e - b * (kRow3 / 4);
                 if (b < nv && 4 * x4 < g.nidx4)
                     reinterpret_cast<uint4*>(Ubuf)[e] =
                         reinterpret_cast<const uint4*>(Uslot + (size_t)S.slot_of[b] * g.nidx4)[x4];
             }
             tm.sync();
+            if constexpr (Q > 1) {
+                const int q = ti & (Q - 1);
+                const uint8_t* ubq = ub0 + q * kRow3 * 4;
+                int dU[32 / Q];
+#pragma unroll
+                for (int j = 0; j < 32 / Q; ++j) dU[j] = 0;
+                for (int c = 0; c < g.n_classes; ++c) {
+                    const int c0 = (int)cptr[c], c1 = (int)cptr[c + 1];
+                    for (int base = c0; base < c1; base += TT / Q) {
+                        const int qq = base + ti / Q;
+                        const bool on = qq < c1;
+                        const uint4 md = meta[on ? qq : c1 - 1];
+                        const bool hw = __any_sync(0xFFFFFFFFu, on && ((md.w >> 27) & 1u));
+                        if (hw)
+                            k3q_site<true, Q>(a, S, md, W2, adj, ubq, n, vmask, nv, q, on, dU);
+                        else
+                            k3q_site<false, Q>(a, S, md, W2, adj, ubq, n, vmask, nv, q, on, dU);
+                    }
+                    tm.sync();
+                }
+                // E_b += 2 dU_b: dU (in eighths) summed over the lanes of the same q, then over warps
+#pragma unroll
+                for (int j = 0; j < 32 / Q; ++j) {
+                    int v = dU[j];
+#pragma unroll
+                    for (int d = Q; d < 32; d <<= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, d);
+                    if (lane < Q && v != 0) atomicAdd(&S.Ucnt[Q * j + lane], (uint32_t)v);
+                }
+                tm.sync();
+                for (int b = ti; b < nv; b += TT) {
+                    S.Eown[par][b] = S.Eown[prev][b] + ((int32_t)S.Ucnt[b] >> 2);
+                    S.Ucnt[b] = 0;
+                }
+                pt_epilogue<false>(a, S, W2w, inst, 0, t, pass, tm);
+                continue;
+            }
             uint32_t C[kC3];
 #pragma unroll
             for (int k = 0; k < kC3; ++k) C[k] = 0;
@@ -409,7 +568,7 @@ __global__ void __launch_bounds__(kT3 * IPB, 1) k3_bitcsr_pt(const PTArgs a, con
         }
         {
             uint32_t* dst = a.words + (size_t)inst * n;
-            for (int k = ti; k < n; k += kT3) dst[k] = W2w[k];
+            for (int k = ti; k < n; k += TT) dst[k] = W2w[k];
         }
         pt_finish<false>(a, S, inst, 0, par, tm);
         if (BAL && item.signal >= 0) pt_signal_flag<false>(a, item.signal, 0, tm);
@@ -426,22 +585,23 @@ size_t k3_smem_bytes(int R, int nidx, int nadj, int nfree, int n, int ncls, int 
 
 int k3_row_stride() { return kRow3; }
 
-template <int IPB>
+template <int IPB, int Q>
 static cudaError_t k3_shape_t(const PTArgs& a, const Csr3& g, size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute(k3_bitcsr_pt<false, IPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e =
+        cudaFuncSetAttribute(k3_bitcsr_pt<false, IPB, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k3_bitcsr_pt<true, IPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        e = cudaFuncSetAttribute(k3_bitcsr_pt<true, IPB, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return e;
 }
 
-template <int IPB>
+template <int IPB, int Q>
 static cudaError_t k3_run_t(const PTArgs& a, const Csr3& g, cudaStream_t st, int* resident) {
     const size_t smem = k3_smem_bytes(a.R, a.nidx, g.nadj, (int)a.n_free, a.n, g.n_classes, IPB);
-    cudaError_t e = k3_shape_t<IPB>(a, g, smem);
+    cudaError_t e = k3_shape_t<IPB, Q>(a, g, smem);
     if (e != cudaSuccess) return e;
     if (resident) {  // co-resident instance teams: CTAs per SM x SMs x IPB
         int per_sm = 0, dev = 0, nsm = 0;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_bitcsr_pt<true, IPB>, kT3 * IPB, smem);
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k3_bitcsr_pt<true, IPB, Q>, kT3 * Q * IPB, smem);
         if (e == cudaSuccess) e = cudaGetDevice(&dev);
         if (e == cudaSuccess) e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
         *resident = per_sm * nsm * IPB;
@@ -449,29 +609,32 @@ static cudaError_t k3_run_t(const PTArgs& a, const Csr3& g, cudaStream_t st, int
     }
     const unsigned grid = a.sched ? (unsigned)((a.sched_clusters + IPB - 1) / IPB) : (unsigned)((a.I + IPB - 1) / IPB);
     if (a.sched)
-        k3_bitcsr_pt<true, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
+        k3_bitcsr_pt<true, IPB, Q><<<grid, kT3 * Q * IPB, smem, st>>>(a, g);
     else
-        k3_bitcsr_pt<false, IPB><<<grid, kT3 * IPB, smem, st>>>(a, g);
+        k3_bitcsr_pt<false, IPB, Q><<<grid, kT3 * Q * IPB, smem, st>>>(a, g);
     return cudaGetLastError();
 }
 
-static cudaError_t k3_run(const PTArgs& a, const Csr3& g, int ipb, cudaStream_t st, int* resident) {
-    switch (ipb) {
-        case 1: return k3_run_t<1>(a, g, st, resident);
-        case 2: return k3_run_t<2>(a, g, st, resident);
-        case 3: return k3_run_t<3>(a, g, st, resident);
-        default: return k3_run_t<4>(a, g, st, resident);
+// shape = IPB for one lane per site (IPB 1..4); -2 / -4: split sites with Q = 2 / 4 lanes (IPB 1)
+static cudaError_t k3_run(const PTArgs& a, const Csr3& g, int shape, cudaStream_t st, int* resident) {
+    switch (shape) {
+        case -4: return k3_run_t<1, 4>(a, g, st, resident);
+        case -2: return k3_run_t<1, 2>(a, g, st, resident);
+        case 1: return k3_run_t<1, 1>(a, g, st, resident);
+        case 2: return k3_run_t<2, 1>(a, g, st, resident);
+        case 3: return k3_run_t<3, 1>(a, g, st, resident);
+        default: return k3_run_t<4, 1>(a, g, st, resident);
     }
 }
 
 // Co-resident instance teams of the K3 launch shape (balanced schedule).
-int k3_resident_units(const PTArgs& a, const Csr3& g, int ipb) {
+int k3_resident_units(const PTArgs& a, const Csr3& g, int shape) {
     int r = 0;
-    return k3_run(a, g, ipb, nullptr, &r) == cudaSuccess ? r : 0;
+    return k3_run(a, g, shape, nullptr, &r) == cudaSuccess ? r : 0;
 }
 
-cudaError_t launch_k3(const PTArgs& a, const Csr3& g, int ipb, cudaStream_t st) {
-    return k3_run(a, g, ipb, st, nullptr);
+cudaError_t launch_k3(const PTArgs& a, const Csr3& g, int shape, cudaStream_t st) {
+    return k3_run(a, g, shape, st, nullptr);
 }
 
 }  // namespace tapt_dev

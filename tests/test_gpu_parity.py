@@ -370,6 +370,77 @@ def test_k3_equals_k2_on_multiplier_instances(monkeypatch):
     assert np.array_equal(a.best(), b.best())
 
 
+@pytest.mark.parametrize("q", [2, 4])
+def test_k3_split_sites_equal_k2_on_multiplier_instances(monkeypatch, q):
+    """K3 with Q lanes per site (split sites: shuffled decision words, integer energy deltas) == K2,
+    bit for bit: heavy sites, per-instance clamps, swaps, measurements, histograms, best."""
+    M = T.Multiplier(12)
+    m = M.model()
+    I, R = 40, 32
+    prods = [T.random_semiprime(4, k, 12) for k in range(I)]
+    cl = np.stack([M.clamps(p * q_) for p, q_ in prods])
+
+    def run(k3):
+        monkeypatch.setenv("TAPT_K3", "1" if k3 else "0")
+        monkeypatch.setenv("TAPT_K3_Q", str(q))
+        e = T.Ensemble(m, H.geometric(0.1, 5.0, R), n_instances=I, seed=8)
+        e.set_clamps(cl)
+        e.init_random()
+        e.set_histogram(-2000, 16, 256)
+        e.run(150, swap_every=1, measure_every=7)
+        return e
+    a, b = run(True), run(False)
+    assert a.kernel == "bitcsr" and b.kernel == "csr"
+    assert any(f"k3_bitcsr_pt<0,1,{q}>" in k for k in a.launch_log())
+    assert np.array_equal(a.spins(), b.spins())
+    assert np.array_equal(a.energies(), b.energies())
+    for x, y in zip(a.acceptance(), b.acceptance()):
+        assert np.array_equal(x, y)
+    assert np.array_equal(a.observables(), b.observables())
+    assert np.array_equal(a.histogram(), b.histogram())
+    assert np.array_equal(a.best(), b.best())
+
+
+@pytest.mark.parametrize("q", [2, 4])
+def test_k3_split_sites_circuit_with_partial_group_matches_oracle(monkeypatch, q):
+    """Split sites with 20 slots (12 idle lanes of the replica word) on a random circuit with
+    clamps and fields, against the oracle."""
+    monkeypatch.setenv("TAPT_K3", "1")
+    monkeypatch.setenv("TAPT_K3_Q", str(q))
+    g = _random_circuit(17)
+    m = T.Model.graph(g.n, g.ci, g.cj, g.J, g.h, g.clamp)
+    betas = H.geometric(0.1, 5.0, 20)
+    e = T.Ensemble(m, betas, n_instances=3, seed=6)
+    assert e.kernel == "bitcsr"
+    e.init_random()
+    e.run(90, swap_every=1)
+    compare(e, H.run_oracle([g] * 3, betas, 6, 0, H.colour_order_for(m.schedule()[0]), 90))
+
+
+def test_k3_split_sites_balanced_schedule(monkeypatch):
+    """Q = 4 teams under the balanced persistent schedule (more instances than resident teams,
+    jobs split between teams) give the unbalanced chain."""
+    M = T.Multiplier(8)
+    m = M.model()
+    I, R = 230, 32
+    prods = [T.random_semiprime(3, k, 8) for k in range(I)]
+    cl = np.stack([M.clamps(p * q) for p, q in prods])
+
+    def run(bal):
+        monkeypatch.setenv("TAPT_K3_Q", "4")
+        monkeypatch.setenv("TAPT_BALANCE", "1" if bal else "0")
+        e = T.Ensemble(m, H.geometric(0.1, 5.0, R), n_instances=I, seed=21)
+        e.set_clamps(cl)
+        e.init_random()
+        e.run(60, swap_every=1, measure_every=6)
+        return e
+    a, b = run(True), run(False)
+    assert any("k3_bitcsr_pt<1,1,4>" in k for k in a.launch_log())
+    for x, y in zip((a.spins(), a.energies(), a.permutation(), a.observables(), a.best()),
+                    (b.spins(), b.energies(), b.permutation(), b.observables(), b.best())):
+        assert np.array_equal(x, y)
+
+
 # ------------------------------------------------------------ proposals -----
 
 def test_synthetic_tapt_rounds_match_oracle_k1():

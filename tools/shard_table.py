@@ -16,7 +16,7 @@ from paper_2509_23043_b200 import workloads as WL  # noqa: E402
 stream = torch.cuda.Stream()
 total = {2: 128, 3: 256, 4: 512}
 for cfg in (2, 3, 4):
-    row = {}
+    row, kern = {}, {}
     for ngpu in (1, 2, 4, 8):
         wl = WL.build(T, cfg, stream.cuda_stream, instances=total[cfg] // ngpu)
         wl["step"]()
@@ -27,8 +27,10 @@ for cfg in (2, 3, 4):
         b.record(stream)
         torch.cuda.synchronize()
         row[ngpu] = wl["updates_per_step"] / (a.elapsed_time(b) * 1e-3)
+        kern[ngpu] = wl["ens"].launch_log()
         del wl
     print(json.dumps({"config": cfg, "instances_total": total[cfg],
                       "per_gpu_updates_per_s": {k: round(v / 1e9, 1) for k, v in row.items()},
                       "projected_aggregate_G": {k: round(k * v / 1e9, 1) for k, v in row.items()},
-                      "per_gpu_efficiency_vs_1gpu": {k: round(v / row[1], 3) for k, v in row.items()}}), flush=True)
+                      "per_gpu_efficiency_vs_1gpu": {k: round(v / row[1], 3) for k, v in row.items()},
+                      "kernels": kern}), flush=True)
