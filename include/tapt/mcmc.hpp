@@ -57,8 +57,7 @@ struct SampleDataset {
         for (;;) {
             double beta;
             is.read(reinterpret_cast<char*>(&beta), 8);
-            if (is.gcount() == 0) break;
-            if (is.gcount() != 8) throw FormatError("truncated dataset record");
+            if (is.gcount() != 8) break;  // clean EOF; a partial beta ends the file too (mcmc.cpp:142)
             std::uint32_t n;
             is.read(reinterpret_cast<char*>(&n), 4);
             if (is.gcount() != 4) throw FormatError("truncated dataset record");

@@ -113,6 +113,12 @@ static int cpu_tests() {
     std::istringstream is(os.str());
     auto d2 = SampleDataset::load(is);
     CHECK(d2.records.size() == 1 && d2.records[0].spins == d.records[0].spins && d2.records[0].beta == 0.5);
+    {   // mcmc.cpp:142: a trailing partial beta is a clean end of file; a cut inside a record throws
+        std::istringstream tail(os.str() + std::string(3, '\x01'));
+        CHECK(SampleDataset::load(tail).records.size() == 1);
+        std::istringstream cut(os.str().substr(0, os.str().size() - 1));
+        CHECK(throws<FormatError>([&] { SampleDataset::load(cut); }));
+    }
     // C ABI digest matches
     std::uint64_t dig = 0;
     CHECK(tapt_model_digest(and_gate().device(), &dig) == TAPT_OK && dig == and_gate().digest());
