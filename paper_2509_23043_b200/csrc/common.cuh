@@ -57,11 +57,12 @@ inline MixConsts make_mix_consts() {
 
 // High word of (z ^ z>>30) * M1 ^ ... * M2, i.e. mix_final(z) BEFORE its last xor-shift.
 // Variant bits (instruction-mix choices, identical results; measured on B200 with
-// tools/probe_variants.sh and tools/k1_variants.sh, default 12 = bits 4|8):
+// tools/probe_variants.sh and tools/k1_variants.sh; default 6 = bits 2|4 since the index scratch
+// (TAPT_K1_IDXS) took the threshold-index shift off the ALU pipe; before that 12 = bits 4|8):
 //   V & 1: high-word right shifts as IMAD.HI by 4 / 32 (FMA pipe) instead of SHF (ALU pipe)  [slower]
-//   V & 2: first 64-bit multiply as an explicit IMAD.WIDE + IMAD + IMAD chain (PTX)           [neutral]
+//   V & 2: first 64-bit multiply as an explicit IMAD.WIDE + IMAD + IMAD chain (PTX)           [+3% with IDXS: 3 ops, not 4]
 //   V & 4: tie band tracked as a running min (k1_lattice.cu)                                   [+4%]
-//   V & 8: threshold-index shift as IMAD.HI on the FMA pipe (k1_lattice.cu)                    [+3%]
+//   V & 8: threshold-index shift as IMAD.HI on the FMA pipe (k1_lattice.cu)                    [+3%; unused with IDXS]
 //   V & 32: first 64-bit multiply as two IMAD + one IMAD.WIDE with a 64-bit addend (3 ops, not 4)
 // The last multiply only needs its high word: IMAD.HI + IMAD + IMAD.
 template <int V>

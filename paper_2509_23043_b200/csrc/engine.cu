@@ -1486,7 +1486,7 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
                 CUDA_OK(cudaGetDevice(&dev));
                 CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
                 nt = (long long)e->I * e->G >= 2ll * nsm ? 256 : TAPT_K1_DEFAULT_THREADS;
-            } else if (k1_smem_bytes(n, true, e->R) <= 100 * 1024) {
+            } else if (k1_smem_bytes(n, true, e->R) <= (100 - (TAPT_K1_IDXS ? 18 : 0)) * 1024) {
                 // mid-size lattices with at least two instance-groups per SM: two independent 256-thread
                 // CTAs per SM (barriers decoupled) instead of one 512-thread CTA (config 3: 803 -> 840
                 // G/s; config 2's 256 groups on 296 slots lose 7 % and keep 512 threads)
@@ -1501,7 +1501,8 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
             // colour-1 sites (2*dim each) and up-spins of its share of all sites
             while (nt < 1024 && ((n / 2 + nt - 1) / nt * 2 * m->dim >= 256 || (n + nt - 1) / nt >= 256)) nt *= 2;
             e->k1_threads = nt;
-            if (k1_smem_bytes(n, true, e->R) > 227 * 1024) throw tapt::SizeError("lattice too large for shared memory");
+            // dynamic part + the kernel's static block (control block ~6 KB, index scratch 32 KB with TAPT_K1_IDXS)
+            if (k1_smem_bytes(n, true, e->R) > (221 - (TAPT_K1_IDXS ? 32 : 0)) * 1024) throw tapt::SizeError("lattice too large for shared memory");
         } else {
             if (m->max_sumabs > 255) throw tapt::SizeError("sum of |J| at a site exceeds 255 (byte-SWAR fields)");
             e->nidx = m->lmax - m->lmin + 1;
@@ -2276,7 +2277,7 @@ static bool refine_proposals(tapt_ensemble_s* e, uint32_t T, uint32_t refine) {
     // but fit two 256-thread CTAs per SM, one wave of those beats two of 512-thread CTAs
     // (config 2: 128 x 2 groups)
     int nt = 0;
-    if (e->use_k1 && e->k1_threads == 512 && k1_smem_bytes(n, true, e->R) <= 100 * 1024) {
+    if (e->use_k1 && e->k1_threads == 512 && k1_smem_bytes(n, true, e->R) <= (100 - (TAPT_K1_IDXS ? 18 : 0)) * 1024) {
         int dev = 0, nsm = 148;
         CUDA_OK(cudaGetDevice(&dev));
         CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));

@@ -160,6 +160,35 @@ __host__ __device__ constexpr size_t k1_stage_offset(int n, bool dis) {
     return (k1_words_offset() + (size_t)n * 4 + (dis ? (size_t)n : 0) + 15) & ~size_t(15);
 }
 
+// TAPT_K1_IDXS: threshold offsets as bytes in shared memory.  Word j of a site's 8 scratch words
+// (thread-interleaved: word (u, j) of thread tid sits at [(u*8 + j)*STRIDE + tid]) takes the even
+// (j < 4) or odd (j >= 4) nibbles of N[j & 3] as bytes 4*q, so replica b = 8y + 4*odd + m reads byte y
+// of word m + 4*odd.
+template <int STRIDE>
+__host__ __device__ constexpr int k1_index_byte(int u, int b) {
+    return ((u * 8 + (b & 3) + 4 * ((b >> 2) & 1)) * STRIDE) * 4 + (b >> 3);
+}
+template <int STRIDE>
+__device__ __forceinline__ void k1_index_bytes(uint32_t* scr_w, int u, const uint32_t (&N)[4]) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        scr_w[(u * 8 + m) * STRIDE] = (N[m] << 2) & 0x1C1C1C1Cu;
+        scr_w[(u * 8 + 4 + m) * STRIDE] = (N[m] >> 2) & 0x1C1C1C1Cu;
+    }
+}
+
+template <int STRIDE>
+__device__ __forceinline__ uint32_t k1_decide_exact_scr(const K1Smem& sm, int W, uint64_t phi_i, const uint8_t* scr,
+                                                        int u) {
+    uint32_t nw = 0;
+    for (int b = 0; b < W; ++b) {
+        const uint32_t idx = scr[k1_index_byte<STRIDE>(u, b)] >> 2;
+        const uint64_t x = mix_final(sm.S.sb[b] + phi_i);
+        if (below(x, sm.T64[b][idx])) nw |= 1u << b;
+    }
+    return nw;
+}
+
 // Heat-bath decisions for one site word over the W replicas of this CTA.
 __device__ __forceinline__ uint32_t k1_decide_exact(const K1Smem& sm, int W, uint64_t phi_i, const uint32_t (&N)[4]) {
     uint32_t nw = 0;
@@ -176,10 +205,13 @@ __device__ __forceinline__ uint32_t k1_decide_exact(const K1Smem& sm, int W, uin
 // loop runs b descending so the carry chain leaves NOT(up_b) at bit b.  NV = 32: full
 // group, fully unrolled; NV = 0: partial group (runtime count nv), rolled loop.
 // V & 4: track the tie band as a running min of (h - U + 1) instead of OR-ing compares.
-template <int NV, int V, int SP>
+// STRIDE > 0 (TAPT_K1_IDXS): the threshold offsets 4*q of the site's 32 replicas were stored as bytes in
+// the thread's shared-memory scratch (k1_index_bytes), so a replica's offset is one LDS.U8 with an
+// immediate address instead of a shift and a mask on the ALU pipe.
+template <int NV, int V, int SP, int STRIDE = 0>
 __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64_t (&ph)[SP],
                                           const uint32_t (&N)[SP][4], const MixConsts& mc, uint32_t (&w)[SP],
-                                          bool& tie) {
+                                          bool& tie, const uint8_t* scr = nullptr) {
     constexpr int U = NV ? NV : 1;
     const int cnt = NV ? NV : nv;
     uint32_t tmin = 0xFFFFFFFFu;
@@ -223,10 +255,16 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
     for (int b = cnt - 1; b >= 0; --b) {
         const uint64_t base = sm.S.sb[b];
         const int m = b & 3, sh = 4 * (b >> 2);
+        uint32_t dmin[SP];
 #pragma unroll
         for (int u = 0; u < SP; ++u) {
             uint32_t thr;
-            if constexpr ((V & 8) != 0) {  // shift on the FMA pipe: (N >> sh) << 2 == hi(N * 2^(34-sh)) & 0x1C
+            if constexpr (STRIDE > 0) {
+                // IDXS = 1: ptxas merges the byte reads into word loads + PRMT; 2: one LDS.U8 per decision
+                const uint32_t ix = TAPT_K1_IDXS == 2 ? *(reinterpret_cast<const volatile uint8_t*>(scr) + k1_index_byte<STRIDE>(u, b))
+                                                      : scr[k1_index_byte<STRIDE>(u, b)];
+                thr = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(&sm.Uhi[b][0]) + ix);
+            } else if constexpr ((V & 8) != 0) {  // shift on the FMA pipe: (N >> sh) << 2 == hi(N * 2^(34-sh)) & 0x1C
                 const uint32_t ix = (sh >= 4 ? __umulhi(N[u][m], mc.nib[sh >> 2]) : (N[u][m] << 2)) & 0x1Cu;
                 thr = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(&sm.Uhi[b][0]) + ix);
             } else {
@@ -235,32 +273,18 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
             const uint64_t z = base + ph[u];
             const uint32_t h = mix_pre_hi<V>((uint32_t)z, (uint32_t)(z >> 32), mc);
             const uint32_t dd = decide_acc(h, thr, w[u]);
-            if constexpr ((V & 4) != 0)
+            dmin[u] = dd;
+            if constexpr (TAPT_K1_UM1 && TAPT_K1_MIN3 && (V & 4) != 0 && SP == 2) {
+            } else if constexpr ((V & 4) != 0)
                 tmin = min(tmin, dd + (TAPT_K1_UM1 ? 0u : 1u));
             else
                 tie |= (dd + (TAPT_K1_UM1 ? 0u : 1u) <= 2u);
         }
+        // tables hold U - 1: the band is d in {0, 1, 2} itself, and one 3-input min covers two sites
+        if constexpr (TAPT_K1_UM1 && TAPT_K1_MIN3 && (V & 4) != 0 && SP == 2) tmin = min(tmin, min(dmin[0], dmin[1]));
     }
     if constexpr ((V & 4) != 0) tie |= tmin <= 2u;
     }
-}
-
-// Kept for the decision-rate probe (two interleaved site words).
-template <int NV, int V>
-__device__ __forceinline__ void k1_decide2(const K1Smem& sm, int nv, uint64_t ph0, uint64_t ph1,
-                                           const uint32_t (&N0)[4], const uint32_t (&N1)[4], const MixConsts& mc,
-                                           uint32_t& w0, uint32_t& w1, bool& tie) {
-    const uint64_t ph[2] = {ph0, ph1};
-    uint32_t N[2][4];
-#pragma unroll
-    for (int m = 0; m < 4; ++m) {
-        N[0][m] = N0[m];
-        N[1][m] = N1[m];
-    }
-    uint32_t w[2] = {w0, w1};
-    k1_decide<NV, V, 2>(sm, nv, ph, N, mc, w, tie);
-    w0 = w[0];
-    w1 = w[1];
 }
 
 // MINB: CTAs per SM the register allocation must allow (2 for the 256-thread small-lattice shape)
@@ -281,6 +305,12 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
     uint64_t* strS = thrS + (size_t)a.R * 8;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     constexpr int KV = DIM == 3 ? TAPT_K1_VARIANT3 : TAPT_K1_VARIANT;  // decision instruction mix
+    // threshold offsets of the thread's SP site words as bytes (static: addresses fold into immediates)
+    constexpr int XS = (TAPT_K1_IDXS && SP * MAXT <= 1024) ? MAXT : 0;
+    static_assert(!(TAPT_K1_IDXS && TAPT_K1_PIPE), "the index scratch holds one site pair at a time");
+    __shared__ uint32_t idx_scr[XS ? SP * 8 * XS : 1];
+    uint32_t* const scr_w = idx_scr + tid;
+    const uint8_t* const scr_b = reinterpret_cast<const uint8_t*>(scr_w);
     const int cl = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
     const int half = n >> 1, nsub = half / SP;
@@ -382,6 +412,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
                     is_[u] = colour_site<DIM>(jj + u * nsub, c, d, x, y, z);
                     k1_stencil<DIM, DIS>(words, bonds, is_[u], x, y, z, d, q_[u][0], q_[u][1], q_[u][2]);
                     nibbles(q_[u][0], q_[u][1], q_[u][2], N_[u]);
+                    if constexpr (XS > 0) k1_index_bytes<XS>(scr_w, u, N_[u]);
                 }
             };
             if (tid < nsub) stencil(tid, is, q, N);
@@ -404,19 +435,21 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
                     // full 32-, 16- and 8-replica groups unrolled (narrow groups spread an instance over
                     // more CTAs when instances are few); partial groups take the rolled loop
                     if (nv == kW)
-                        k1_decide<kW, KV, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                        k1_decide<kW, KV, SP, XS>(sm, nv, ph, N, a.mc, nw, tie, scr_b);
                     else if (NAR && nv == 16)
-                        k1_decide<16, KV, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                        k1_decide<16, KV, SP, XS>(sm, nv, ph, N, a.mc, nw, tie, scr_b);
                     else if (NAR && nv == 8)
-                        k1_decide<8, KV, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                        k1_decide<8, KV, SP, XS>(sm, nv, ph, N, a.mc, nw, tie, scr_b);
                     else
-                        k1_decide<0, KV, SP>(sm, nv, ph, N, a.mc, nw, tie);
+                        k1_decide<0, KV, SP, XS>(sm, nv, ph, N, a.mc, nw, tie, scr_b);
                     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
 #pragma unroll
                     for (int u = 0; u < SP; ++u) nw[u] = ~nw[u] & vmask;
                     if (tie) {  // probability ~ 2^-31 per decision: redo the words exactly
 #pragma unroll
-                        for (int u = 0; u < SP; ++u) nw[u] = k1_decide_exact(sm, nv, ph[u], N[u]);
+                        for (int u = 0; u < SP; ++u)
+                            nw[u] = XS > 0 ? k1_decide_exact_scr<(XS > 0 ? XS : 1)>(sm, nv, ph[u], scr_b, u)
+                                           : k1_decide_exact(sm, nv, ph[u], N[u]);
                     }
 #pragma unroll
                     for (int u = 0; u < SP; ++u) words[is[u]] = nw[u];
@@ -588,26 +621,36 @@ namespace tapt_dev {
 template <int V>
 __global__ void __launch_bounds__(512) k_decision_probe(uint32_t iters, uint32_t* sink, MixConsts mc) {
     __shared__ K1Smem sm;
+    constexpr int XS = TAPT_K1_IDXS ? 512 : 0;  // the sweep kernel's scratch-indexed thresholds
+    __shared__ uint32_t idx_scr[XS ? 2 * 8 * XS : 1];
     const int tid = threadIdx.x;
     for (int e = tid; e < kW * 8; e += blockDim.x) sm.Uhi[e >> 3][e & 7] = 0x80000000u + (uint32_t)e * 977u;
     for (int e = tid; e < kW; e += blockDim.x) sm.S.sb[e] = 0x1234567ull * (e + 1);
     __syncthreads();
     const uint32_t gid = blockIdx.x * blockDim.x + tid;
-    uint32_t N0[4], N1[4];
+    uint32_t N[2][4];
     for (int m = 0; m < 4; ++m) {
-        N0[m] = gid * 0x9E3779B9u + m;
-        N1[m] = gid * 0x85EBCA6Bu + m;
+        N[0][m] = gid * 0x9E3779B9u + m;
+        N[1][m] = gid * 0x85EBCA6Bu + m;
+    }
+    uint32_t* const scr_w = idx_scr + (XS ? tid : 0);
+    if constexpr (XS > 0) {
+        k1_index_bytes<(XS > 0 ? XS : 1)>(scr_w, 0, N[0]);
+        k1_index_bytes<(XS > 0 ? XS : 1)>(scr_w, 1, N[1]);
     }
     uint32_t acc = 0;
     bool tie = false;
     for (uint32_t it = 0; it < iters; ++it) {
-        const uint64_t ph0 = (uint64_t)(2 * gid + it * 7919u) * kPhi;
-        const uint64_t ph1 = ph0 + kPhi;
-        uint32_t w0 = 0, w1 = 0;
-        k1_decide2<kW, V>(sm, kW, ph0, ph1, N0, N1, mc, w0, w1, tie);
-        N0[it & 3] ^= w0 >> 3;
-        N1[it & 3] ^= w1 << 1;
-        acc += w0 ^ w1;
+        const uint64_t ph[2] = {(uint64_t)(2 * gid + it * 7919u) * kPhi, (uint64_t)(2 * gid + it * 7919u) * kPhi + kPhi};
+        uint32_t w[2] = {0, 0};
+        k1_decide<kW, V, 2, XS>(sm, kW, ph, N, mc, w, tie, reinterpret_cast<const uint8_t*>(scr_w));
+        if constexpr (XS > 0) {  // keep the offsets changing (one word of the scratch per iteration)
+            scr_w[(it & 15) * XS] = (scr_w[(it & 15) * XS] ^ (w[0] >> 3) ^ (w[1] << 1)) & 0x1C1C1C1Cu;
+        } else {
+            N[0][it & 3] ^= w[0] >> 3;
+            N[1][it & 3] ^= w[1] << 1;
+        }
+        acc += w[0] ^ w[1];
     }
     sink[gid] = acc + (tie ? 1u : 0u);
 }
@@ -622,7 +665,7 @@ cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint3
         TAPT_PROBE_CASE(4) TAPT_PROBE_CASE(5) TAPT_PROBE_CASE(6) TAPT_PROBE_CASE(7)
         TAPT_PROBE_CASE(8) TAPT_PROBE_CASE(9) TAPT_PROBE_CASE(10) TAPT_PROBE_CASE(11)
         TAPT_PROBE_CASE(12) TAPT_PROBE_CASE(13) TAPT_PROBE_CASE(14) TAPT_PROBE_CASE(15)
-        TAPT_PROBE_CASE(28)
+        TAPT_PROBE_CASE(28) TAPT_PROBE_CASE(36) TAPT_PROBE_CASE(38) TAPT_PROBE_CASE(44)
 #undef TAPT_PROBE_CASE
         default: return cudaErrorInvalidValue;
     }

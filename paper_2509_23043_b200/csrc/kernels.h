@@ -25,7 +25,16 @@ constexpr int kCnt = 8;      // planes of the sliced per-thread counters
 #define TAPT_K1_IDX2 1       // 1: masked-add periodic neighbour indices
 #endif
 #ifndef TAPT_K1_UM1
-#define TAPT_K1_UM1 0        // 1: tables hold U - 1, tie band without the +1 (measured 0.8% slower on K1)
+#define TAPT_K1_UM1 1        // 1: tables hold U - 1, so the tie band is d in {0, 1, 2} itself (needed by MIN3)
+#endif
+#ifndef TAPT_K1_MIN3
+#define TAPT_K1_MIN3 1       // 1 (needs UM1): tie band of two sites folded by one 3-input min (VIMNMX3): +0.6..2 %
+#endif
+#ifndef TAPT_K1_IDXS
+// Threshold offsets 4*q of a site's 32 replicas as bytes in a per-thread shared-memory scratch: one LDS.U8
+// per decision replaces a shift and a mask on the ALU pipe (the binding pipe).  1: plain reads (ptxas may
+// merge them into word loads + PRMT), 2: one LDS.U8 each.  Config-5 slice 900 -> 950 G/s.
+#define TAPT_K1_IDXS 2
 #endif
 #ifndef TAPT_K2_MIXV
 #define TAPT_K2_MIXV TAPT_K1_VARIANT  // mix_pre_hi variant of the K2 decisions
@@ -46,10 +55,10 @@ constexpr int kCnt = 8;      // planes of the sliced per-thread counters
 #define TAPT_K1_EPOST 0      // 1: energies in a separate pass after the two colour halves
 #endif
 #ifndef TAPT_K1_VARIANT
-#define TAPT_K1_VARIANT 12   // instruction-mix variant of the decision loop (common.cuh): 2D lattices
+#define TAPT_K1_VARIANT 6    // instruction-mix variant of the decision loop (common.cuh): 2D lattices
 #endif
 #ifndef TAPT_K1_VARIANT3
-#define TAPT_K1_VARIANT3 4   // the same for 3D lattices (measured: config 5 +1.9 %, config 3 +1.3 % over 12)
+#define TAPT_K1_VARIANT3 6   // the same for 3D lattices (with IDXS the explicit 3-op first multiply, V & 2, adds 3 %)
 #endif
 
 struct LatDims {
