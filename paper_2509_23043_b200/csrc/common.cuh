@@ -63,6 +63,7 @@ inline MixConsts make_mix_consts() {
 //   V & 2: first 64-bit multiply as an explicit IMAD.WIDE + IMAD + IMAD chain (PTX)           [+3% with IDXS: 3 ops, not 4]
 //   V & 4: tie band tracked as a running min (k1_lattice.cu)                                   [+4%]
 //   V & 8: threshold-index shift as IMAD.HI on the FMA pipe (k1_lattice.cu)                    [+3%; unused with IDXS]
+//   V & 64 / V & 128: the first / second high-word right shift as an immediate-form IMAD.HI (inline PTX)
 //   V & 32: first 64-bit multiply as two IMAD + one IMAD.WIDE with a 64-bit addend (3 ops, not 4)
 // The last multiply only needs its high word: IMAD.HI + IMAD + IMAD.
 template <int V>
@@ -72,7 +73,13 @@ __device__ __forceinline__ uint32_t mix_pre_hi(uint32_t zl, uint32_t zh, const M
     uint32_t t;
     asm("shf.r.clamp.b32 %0, %1, %2, 30;" : "=r"(t) : "r"(zl), "r"(zh));
     zl ^= t;
-    zh ^= (V & 1) ? __umulhi(zh, c.k4) : (zh >> 30);
+    if constexpr ((V & 64) != 0) {  // immediate-form IMAD.HI (ptxas keeps an inline mul.hi by 4)
+        uint32_t s;
+        asm("mul.hi.u32 %0, %1, 4;" : "=r"(s) : "r"(zh));
+        zh ^= s;
+    } else {
+        zh ^= (V & 1) ? __umulhi(zh, c.k4) : (zh >> 30);
+    }
     if constexpr ((V & 32) != 0) {
         asm("{\n\t.reg .u32 x;\n\t.reg .u64 c, w;\n\t"
             "mul.lo.u32 x, %2, %5;\n\t"
@@ -99,7 +106,13 @@ __device__ __forceinline__ uint32_t mix_pre_hi(uint32_t zl, uint32_t zh, const M
     }
     asm("shf.r.clamp.b32 %0, %1, %2, 27;" : "=r"(t) : "r"(zl), "r"(zh));
     zl ^= t;
-    zh ^= (V & 1) ? __umulhi(zh, c.k32) : (zh >> 27);
+    if constexpr ((V & 128) != 0) {
+        uint32_t s;
+        asm("mul.hi.u32 %0, %1, 32;" : "=r"(s) : "r"(zh));
+        zh ^= s;
+    } else {
+        zh ^= (V & 1) ? __umulhi(zh, c.k32) : (zh >> 27);
+    }
     return __umulhi(zl, B_LO) + zh * B_LO + zl * B_HI;
 }
 

@@ -1495,6 +1495,12 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
                 CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
                 if ((long long)e->I * e->G >= 2ll * nsm) nt = 256;
             }
+            // large lattices (config 5): 640 threads (5 warps per scheduler at <= 102 registers, now that the
+            // threshold offsets live in the shared-memory scratch) when the site pairs still divide evenly enough
+            if (nt == 512 && TAPT_K1_IDXS && n / 4 >= 8 * 640 &&
+                (double)(n / 4) / (double)(((n / 4 + 639) / 640) * 640) >= 0.97 &&
+                k1_smem_bytes(n, true, e->R) + 640 * 64 + 11 * 1024 <= 227 * 1024)
+                nt = 640;
             if (const char* env = std::getenv("TAPT_K1_THREADS")) nt = std::max(32, std::min(1024, std::atoi(env)));
             nt = (nt / 32) * 32;
             // the per-thread bit-sliced counters hold < 256: unsatisfied bonds of this thread's

@@ -156,6 +156,10 @@ struct K1Smem {
 
 // Dynamic shared memory holds the spin words (and bond bytes); the control block is static.
 __host__ __device__ constexpr size_t k1_words_offset() { return 0; }
+// Stride (threads) of the per-thread threshold-offset scratch of a launch shape; 0: no scratch.
+__host__ __device__ constexpr int k1_scratch_stride(int sp, int maxt) {
+    return (TAPT_K1_IDXS && sp * maxt <= 1536) ? maxt : 0;
+}
 __host__ __device__ constexpr size_t k1_stage_offset(int n, bool dis) {
     return (k1_words_offset() + (size_t)n * 4 + (dis ? (size_t)n : 0) + 15) & ~size_t(15);
 }
@@ -270,8 +274,16 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
             } else {
                 thr = sm.Uhi[b][(N[u][m] >> sh) & 7u];
             }
+#if TAPT_K1_PHOPQ
+            uint32_t zl_, zh_;  // explicit carry-chain add: IADD3 + IADD3.X / IMAD.X instead of IMAD.WIDE + IMAD.IADD
+            asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
+                : "=r"(zl_), "=r"(zh_)
+                : "r"((uint32_t)base), "r"((uint32_t)(base >> 32)), "r"((uint32_t)ph[u]), "r"((uint32_t)(ph[u] >> 32)));
+            const uint32_t h = mix_pre_hi<V>(zl_, zh_, mc);
+#else
             const uint64_t z = base + ph[u];
             const uint32_t h = mix_pre_hi<V>((uint32_t)z, (uint32_t)(z >> 32), mc);
+#endif
             const uint32_t dd = decide_acc(h, thr, w[u]);
             dmin[u] = dd;
             if constexpr (TAPT_K1_UM1 && TAPT_K1_MIN3 && (V & 4) != 0 && SP == 2) {
@@ -297,19 +309,21 @@ template <int DIM, bool DIS, bool CLU, int SP, int MAXT, int MINB = 1, bool BULK
 __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, const LatDims d) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ K1Smem sm;  // static: table addresses fold into LDS immediates
-    uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw);
+    constexpr size_t kScr0 = (size_t)k1_scratch_stride(SP, MAXT) * SP * 8 * 4;
+    uint32_t* words = reinterpret_cast<uint32_t*>(smem_raw + kScr0);
     uint8_t* bonds = reinterpret_cast<uint8_t*>(words + a.n);
     // staged once per launch / item: heat-bath thresholds of every slot and the instance's stream
     // states, so that the per-sweep table and stream-base refresh reads no global memory
-    uint64_t* thrS = reinterpret_cast<uint64_t*>(smem_raw + k1_stage_offset(a.n, a.bonds != nullptr));
+    uint64_t* thrS = reinterpret_cast<uint64_t*>(smem_raw + kScr0 + k1_stage_offset(a.n, a.bonds != nullptr));
     uint64_t* strS = thrS + (size_t)a.R * 8;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     constexpr int KV = DIM == 3 ? TAPT_K1_VARIANT3 : TAPT_K1_VARIANT;  // decision instruction mix
     // threshold offsets of the thread's SP site words as bytes (static: addresses fold into immediates)
-    constexpr int XS = (TAPT_K1_IDXS && SP * MAXT <= 1024) ? MAXT : 0;
+    // (at the front of the dynamic block, so its addresses are the thread's offset + an immediate)
+    constexpr int XS = k1_scratch_stride(SP, MAXT);
     static_assert(!(TAPT_K1_IDXS && TAPT_K1_PIPE), "the index scratch holds one site pair at a time");
-    __shared__ uint32_t idx_scr[XS ? SP * 8 * XS : 1];
-    uint32_t* const scr_w = idx_scr + tid;
+    constexpr size_t kScr = (size_t)XS * SP * 8 * 4;
+    uint32_t* const scr_w = reinterpret_cast<uint32_t*>(smem_raw) + tid;
     const uint8_t* const scr_b = reinterpret_cast<const uint8_t*>(scr_w);
     const int cl = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
@@ -429,6 +443,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
 #pragma unroll
                     for (int u = 0; u < SP; ++u) {
                         ph[u] = (uint64_t)(uint32_t)is[u] * kPhi;
+#if TAPT_K1_PHOPQ
+                        asm volatile("" : "+l"(ph[u]));  // keep base + ph a 64-bit add (no IMAD.WIDE re-multiply)
+#endif
                         nw[u] = 0;  // NOT(up) bits, replica b at bit b
                     }
                     bool tie = false;
@@ -517,7 +534,6 @@ size_t k1_smem_bytes(int n, bool dis, int R) {
 template <int DIM, bool DIS, bool CLU>
 static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st, int* resident,
                                char* name) {
-    const size_t smem = k1_smem_bytes(a.n, DIS, a.R);
     // SP = 1 site word per thread-iteration at 1024 threads, else 2 interleaved at <= 512
     // launch shapes: 2 interleaved site words per thread-iteration at <= 512 threads (default),
     // 2 at 513..768 (<= 85 registers), 1 at > 768, 4 at <= 256
@@ -526,21 +542,27 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
     const bool narrow = a.W < kW;
     // (SP, MAXT, MINB, BULK, NAR) of the instantiation this launch shape selects
     const int pick = threads > 768                ? 0
-                     : threads > 512              ? 1
+                     : threads > 640              ? 1
+                     : threads > 512 && bulk && !narrow ? 9
+                     : threads > 512              ? 8
                      : threads > 256 && narrow    ? 2
                      : threads > 256 && bulk      ? 3
                      : threads > 256              ? 4
                      : threads == 256 && narrow   ? 5
                      : threads == 256             ? 6
                                                   : 7;
-    static const int shape[8][5] = {{1, 1024, 1, 0, 1}, {2, 768, 1, 0, 1},   {2, 512, 1, 0, 1}, {2, 512, 1, 1, NAR3},
-                                    {2, 512, 1, 0, NAR3}, {2, 256, 2, 0, 1}, {2, 256, 2, 0, NAR3}, {4, 256, 1, 0, 1}};
-    static void (*const table[8])(const PTArgs, const LatDims) = {
+    static const int shape[10][5] = {{1, 1024, 1, 0, 1}, {2, 768, 1, 0, 1},   {2, 512, 1, 0, 1}, {2, 512, 1, 1, NAR3},
+                                    {2, 512, 1, 0, NAR3}, {2, 256, TAPT_K1_MINB256, 0, 1}, {2, 256, TAPT_K1_MINB256, 0, NAR3}, {4, 256, 1, 0, 1},
+                                    {2, 640, 1, 0, 1}, {2, 640, 1, 1, NAR3}};
+    static void (*const table[10])(const PTArgs, const LatDims) = {
         k1_lattice_pt<DIM, DIS, CLU, 1, 1024>,          k1_lattice_pt<DIM, DIS, CLU, 2, 768>,
         k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, true>, k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, true, NAR3>,
-        k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, NAR3>, k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2, false, true>,
-        k1_lattice_pt<DIM, DIS, CLU, 2, 256, 2, false, NAR3>, k1_lattice_pt<DIM, DIS, CLU, 4, 256>};
+        k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, NAR3>, k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, true>,
+        k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, NAR3>, k1_lattice_pt<DIM, DIS, CLU, 4, 256>,
+        k1_lattice_pt<DIM, DIS, CLU, 2, 640>, k1_lattice_pt<DIM, DIS, CLU, 2, 640, 1, true, NAR3>};
     auto fn = table[pick];
+    const size_t smem = k1_smem_bytes(a.n, DIS, a.R) +
+                        (size_t)k1_scratch_stride(shape[pick][0], shape[pick][1]) * shape[pick][0] * 32;
     if (name) {
         const int* v = shape[pick];
         snprintf(name, 96, "k1_lattice_pt<%d,%d,%d,%d,%d,%d,%d,%d>", DIM, (int)DIS, (int)CLU, v[0], v[1], v[2], v[3],
@@ -665,7 +687,7 @@ cudaError_t launch_decision_probe(int blocks, int threads, uint32_t iters, uint3
         TAPT_PROBE_CASE(4) TAPT_PROBE_CASE(5) TAPT_PROBE_CASE(6) TAPT_PROBE_CASE(7)
         TAPT_PROBE_CASE(8) TAPT_PROBE_CASE(9) TAPT_PROBE_CASE(10) TAPT_PROBE_CASE(11)
         TAPT_PROBE_CASE(12) TAPT_PROBE_CASE(13) TAPT_PROBE_CASE(14) TAPT_PROBE_CASE(15)
-        TAPT_PROBE_CASE(28) TAPT_PROBE_CASE(36) TAPT_PROBE_CASE(38) TAPT_PROBE_CASE(44)
+        TAPT_PROBE_CASE(22) TAPT_PROBE_CASE(70) TAPT_PROBE_CASE(134) TAPT_PROBE_CASE(198) TAPT_PROBE_CASE(28) TAPT_PROBE_CASE(36) TAPT_PROBE_CASE(38) TAPT_PROBE_CASE(44)
 #undef TAPT_PROBE_CASE
         default: return cudaErrorInvalidValue;
     }

@@ -36,6 +36,13 @@ constexpr int kCnt = 8;      // planes of the sliced per-thread counters
 // merge them into word loads + PRMT), 2: one LDS.U8 each.  Config-5 slice 900 -> 950 G/s.
 #define TAPT_K1_IDXS 2
 #endif
+#ifndef TAPT_K1_PHOPQ
+#define TAPT_K1_PHOPQ 1       // 1: stream base + counter as an explicit carry-chain add (IADD3 + IMAD.X, 4 pipe cycles) instead of
+                             // ptxas's IMAD.WIDE + IMAD.IADD (6): config-5 slice +1 %, configs 1/2/3 +3.1 / +4.5 / +0.8 %
+#endif
+#ifndef TAPT_K1_MINB256
+#define TAPT_K1_MINB256 2    // CTAs per SM the 256-thread K1 shapes are compiled for (register cap 128 / 85)
+#endif
 #ifndef TAPT_K2_MIXV
 #define TAPT_K2_MIXV TAPT_K1_VARIANT  // mix_pre_hi variant of the K2 decisions
 #endif

@@ -951,9 +951,9 @@ def test_cfg5_headline_kernel_bit_exact_with_oracle():
     e.generate_proposals(np.arange(56, dtype=np.uint32), None, refine=5, return_accepted=False)
     e.run(S2, swap_every=1)
     log = e.launch_log()
-    head = [x for x in log if x.startswith("k1_lattice_pt<3,1,1,2,512,1,1,0> balanced M=")]
+    head = [x for x in log if x.startswith("k1_lattice_pt<3,1,1,2,640,1,1,0> balanced M=")]
     assert head, log  # the bench's instantiation (3D, disorder, cluster, bulk) on the balanced grid
-    assert any(x.startswith("k1_lattice_pt<3,1,0,2,512,1,1,0>") for x in log), log  # bulk refinement sweeps
+    assert any(x.startswith("k1_lattice_pt<3,1,0,2,640,1,1,0>") for x in log), log  # bulk refinement sweeps
     M = int(head[0].split("M=")[1])
     split = mcnaughton_split(I, S1, M)
     assert split, (I, S1, M)
@@ -968,10 +968,16 @@ def test_cfg5_headline_kernel_bit_exact_with_oracle():
         assert np.array_equal(pc[gid], pt.prop_acc), gid
 
 
-def test_cfg5_bulk_kernel_with_forced_full_groups(monkeypatch):
+@pytest.mark.parametrize("threads,name", [(None, "k1_lattice_pt<3,1,1,2,640,1,1,0>"),
+                                          (512, "k1_lattice_pt<3,1,1,2,512,1,1,0>"),
+                                          (768, "k1_lattice_pt<3,1,1,2,768,1,0,1>")])
+def test_cfg5_bulk_kernel_with_forced_full_groups(monkeypatch, threads, name):
     """Few instances: the group-width model would narrow the replica groups; TAPT_K1_W=32 forces
-    the 32-replica bulk instantiation (plain grid, no balancing) and it must match the oracle."""
+    the 32-replica bulk instantiation (plain grid, no balancing) and it must match the oracle.  The
+    default launch shape (640 threads), the 512-thread bulk shape and the 768-thread shape all do."""
     monkeypatch.setenv("TAPT_K1_W", "32")
+    if threads:
+        monkeypatch.setenv("TAPT_K1_THREADS", str(threads))
     L, R, I = 32, 64, 2
     e = T.Ensemble(T.Model.lattice((L,)), H.linear(0.2, 3.0, R), n_instances=I, seed=20250923, instance_offset=7)
     e.generate_ea_disorder(43)
@@ -979,7 +985,7 @@ def test_cfg5_bulk_kernel_with_forced_full_groups(monkeypatch):
     e.run(12, swap_every=1)
     e.generate_proposals(np.arange(56, dtype=np.uint32), None, refine=5, return_accepted=False)
     e.run(12, swap_every=1)
-    assert "k1_lattice_pt<3,1,1,2,512,1,1,0>" in e.launch_log(), e.launch_log()
+    assert name in e.launch_log(), e.launch_log()
     pts = _cfg5_oracle([7, 8], 12, 12)
     compare(e, pts)
 
