@@ -38,6 +38,15 @@ constexpr int kIPB3 = 4;     // max instance teams per CTA
 constexpr int kRow3 = 132;   // threshold row stride (entries) of the per-buffer table
 constexpr int kC3 = 12;      // sliced energy-counter planes (per-thread weight per sweep < 4096)
 #ifndef TAPT_K3_VARIANT
+#ifndef TAPT_K3_IDXS
+#define TAPT_K3_IDXS 0   // (measured -1 % on config 4: the gathers already load the LSU) light rows: threshold offsets 8*acc as bytes in a per-thread shared-memory scratch
+#endif
+#ifndef TAPT_K3_UM1
+#define TAPT_K3_UM1 1    // threshold rows hold U - 1: the tie band is d in {0, 1, 2}; two decisions share a 3-input min
+#endif
+#ifndef TAPT_K3_CADD
+#define TAPT_K3_CADD 1   // stream base + counter as an explicit carry-chain add
+#endif
 #define TAPT_K3_VARIANT TAPT_K1_VARIANT  // mix_pre_hi instruction mix (common.cuh; V & 32 measured: no gain)
 #endif
 
@@ -114,25 +123,63 @@ __device__ __forceinline__ uint32_t nib128(uint32_t N) {
 
 // Decisions of the 32 replicas of one site word, descending b so that the carry chain leaves
 // NOT(up_b) in bit b.  Ub: byte address of this site's threshold base (per-buffer rows).
-template <bool HEAVY, int B>
-__device__ __forceinline__ void k3_decide_one(const uint8_t* Ub, const uint32_t (&N)[4], const uint32_t (&Nh)[4],
-                                              const PTShared& S, uint64_t ph, const MixConsts& mc, uint32_t& w,
-                                              uint32_t& tmin) {
-    constexpr int m = B & 3, sh = 4 * (B >> 2);
-    uint32_t ix = nib8<sh>(N[m]);
-    if constexpr (HEAVY) ix += nib128<sh>(Nh[m]);
-    const uint32_t thr = *reinterpret_cast<const uint32_t*>(Ub + ix + B * kRow3 * 4);
-    const uint64_t z = S.sb[B] + ph;
-    const uint32_t h = mix_pre_hi<TAPT_K3_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), mc);
-    tmin = min(tmin, decide_acc(h, thr, w) + 1u);
+// z = stream base + counter, high word of the mix before its last xor-shift
+__device__ __forceinline__ uint32_t k3_mix(uint64_t base, uint64_t ph, const MixConsts& mc) {
+#if TAPT_K3_CADD
+    uint32_t zl, zh;
+    asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
+        : "=r"(zl), "=r"(zh)
+        : "r"((uint32_t)base), "r"((uint32_t)(base >> 32)), "r"((uint32_t)ph), "r"((uint32_t)(ph >> 32)));
+    return mix_pre_hi<TAPT_K3_VARIANT>(zl, zh, mc);
+#else
+    const uint64_t z = base + ph;
+    return mix_pre_hi<TAPT_K3_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), mc);
+#endif
 }
 
-template <bool HEAVY, int B>
+// Light rows with TAPT_K3_IDXS: byte y of scratch word m + 4*odd of the thread (words STRIDE apart) holds
+// 8*acc of replica 8y + 4*odd + m (even / odd nibbles of N[m]).
+template <int STRIDE>
+__host__ __device__ constexpr int k3_index_byte(int b) {
+    return (((b & 3) + 4 * ((b >> 2) & 1)) * STRIDE) * 4 + (b >> 3);
+}
+template <int STRIDE>
+__device__ __forceinline__ void k3_index_bytes(uint32_t* scr_w, const uint32_t (&N)[4]) {
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        scr_w[m * STRIDE] = (N[m] << 3) & 0x78787878u;
+        scr_w[(4 + m) * STRIDE] = (N[m] >> 1) & 0x78787878u;
+    }
+}
+
+template <bool HEAVY, int B, int STRIDE>
+__device__ __forceinline__ uint32_t k3_decide_one(const uint8_t* Ub, const uint32_t (&N)[4], const uint32_t (&Nh)[4],
+                                                  const PTShared& S, uint64_t ph, const MixConsts& mc, uint32_t& w,
+                                                  const uint8_t* scr) {
+    constexpr int m = B & 3, sh = 4 * (B >> 2);
+    uint32_t ix;
+    if constexpr (!HEAVY && STRIDE > 0) {
+        ix = *(reinterpret_cast<const volatile uint8_t*>(scr) + k3_index_byte<(STRIDE > 0 ? STRIDE : 1)>(B));
+    } else {
+        ix = nib8<sh>(N[m]);
+        if constexpr (HEAVY) ix += nib128<sh>(Nh[m]);
+    }
+    const uint32_t thr = *reinterpret_cast<const uint32_t*>(Ub + ix + B * kRow3 * 4);
+    return decide_acc(k3_mix(S.sb[B], ph, mc), thr, w);
+}
+
+template <bool HEAVY, int B, int STRIDE>
 __device__ __forceinline__ void k3_decide_rec(const uint8_t* Ub, const uint32_t (&N)[4], const uint32_t (&Nh)[4],
                                               const PTShared& S, uint64_t ph, const MixConsts& mc, uint32_t& w,
-                                              uint32_t& tmin) {
-    k3_decide_one<HEAVY, B>(Ub, N, Nh, S, ph, mc, w, tmin);
-    if constexpr (B > 0) k3_decide_rec<HEAVY, B - 1>(Ub, N, Nh, S, ph, mc, w, tmin);
+                                              uint32_t& tmin, const uint8_t* scr) {
+    static_assert(B & 1, "pairs (B, B - 1)");
+    const uint32_t d1 = k3_decide_one<HEAVY, B, STRIDE>(Ub, N, Nh, S, ph, mc, w, scr);
+    const uint32_t d0 = k3_decide_one<HEAVY, B - 1, STRIDE>(Ub, N, Nh, S, ph, mc, w, scr);
+    if constexpr (TAPT_K3_UM1)
+        tmin = min(tmin, min(d1, d0));
+    else
+        tmin = min(min(tmin, d1 + 1u), d0 + 1u);
+    if constexpr (B > 1) k3_decide_rec<HEAVY, B - 2, STRIDE>(Ub, N, Nh, S, ph, mc, w, tmin, scr);
 }
 
 // Exact 64-bit decisions (tie band, p ~ 2^-31 per site word).
@@ -218,17 +265,15 @@ __device__ __forceinline__ void k3q_decide_rec(const uint8_t* Ubq, const uint32_
     if constexpr (HEAVY) ix += nib128<sh>(Nhs[r]);
     ix8[J] = ix;
     const uint32_t thr = *reinterpret_cast<const uint32_t*>(Ubq + ix + Q * J * kRow3 * 4);
-    const uint64_t z = sbq[Q * J] + ph;
-    const uint32_t h = mix_pre_hi<TAPT_K3_VARIANT>((uint32_t)z, (uint32_t)(z >> 32), mc);
-    tmin = min(tmin, decide_acc(h, thr, w) + 1u);
+    tmin = min(tmin, decide_acc(k3_mix(sbq[Q * J], ph, mc), thr, w) + (TAPT_K3_UM1 ? 0u : 1u));
     if constexpr (J > 0) k3q_decide_rec<HEAVY, Q, J - 1>(Ubq, Ns, Nhs, sbq, ph, mc, w, tmin, ix8);
 }
 
 // Process one class position (site) of this team's instance.
-template <bool HW>
+template <bool HW, int STRIDE>
 __device__ __forceinline__ void k3_site(const PTArgs& a, const PTShared& S, const uint4 md, uint8_t* W2,
                                         const uint32_t* adj, const uint8_t* ub0, int n, uint32_t vmask, int nv,
-                                        uint32_t (&C)[kC3], int& corr) {
+                                        uint32_t (&C)[kC3], int& corr, uint32_t* scr_w) {
     const uint32_t i = md.x;
     const uint64_t ph = (uint64_t)(md.y & 0xFFFFFFu) * kPhi;
     const int off = (int)(md.w & 0xFFFFu) - 32768;
@@ -274,7 +319,8 @@ __device__ __forceinline__ void k3_site(const PTArgs& a, const PTShared& S, cons
     asm("mov.b32 %0, %0;" : "+r"(ubr));
     const uint8_t* Ub = reinterpret_cast<const uint8_t*>(__cvta_shared_to_generic(ubr));
     uint32_t w = 0, tmin = 0xFFFFFFFFu;
-    k3_decide_rec<HW, kW - 1>(Ub, N, Nh, S, ph, a.mc, w, tmin);
+    if constexpr (!HW && STRIDE > 0) k3_index_bytes<(STRIDE > 0 ? STRIDE : 1)>(scr_w, N);
+    k3_decide_rec<HW, kW - 1, STRIDE>(Ub, N, Nh, S, ph, a.mc, w, tmin, reinterpret_cast<const uint8_t*>(scr_w));
     uint32_t nw = ~w & vmask;
     if (tmin <= 2u) nw = k3_decide_exact(a, S, off, A[0], A[1], A[2], A[3], A[4], A[5], A[6], ph, nv);
     nw |= old & ~vmask;
@@ -387,7 +433,9 @@ __global__ void __launch_bounds__(kT3 * Q * IPB, 1) k3_bitcsr_pt(const PTArgs a,
     const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
     // shared memory: Uslot [R][nidx4] | adj [nadj] | meta [n_free] (uint4) | class_ptr [n_classes+1] |
     // per team: Ub [32][kRow3] | W2 [n2]
-    uint32_t* Uslot = reinterpret_cast<uint32_t*>(smem_raw);
+    constexpr int XS = (TAPT_K3_IDXS && Q == 1) ? kT3 * IPB : 0;  // scratch stride (threads); 8 words per thread
+    uint32_t* const scr_w = reinterpret_cast<uint32_t*>(smem_raw) + tid;
+    uint32_t* Uslot = reinterpret_cast<uint32_t*>(smem_raw) + 8 * XS;
     uint32_t* adj = Uslot + (size_t)a.R * g.nidx4;
     uint4* meta = reinterpret_cast<uint4*>(adj + ((g.nadj + 3) & ~3));
     uint32_t* cptr = reinterpret_cast<uint32_t*>(meta + n_free);
@@ -399,7 +447,8 @@ __global__ void __launch_bounds__(kT3 * Q * IPB, 1) k3_bitcsr_pt(const PTArgs a,
     PTShared& S = SS[kin];
     for (int k = tid; k < a.R * g.nidx4; k += nt) {
         const int r = k / g.nidx4, x = k - r * g.nidx4;
-        Uslot[k] = x < nidx ? thr_hi(a.thr[(size_t)r * nidx + x]) : 0u;
+        const uint32_t U = x < nidx ? thr_hi(a.thr[(size_t)r * nidx + x]) : 0u;
+        Uslot[k] = TAPT_K3_UM1 ? max(U, 1u) - 1u : U;  // U - 1: h - (U - 1) in {0, 1, 2} is the tie band
     }
     for (int k = tid; k < g.nadj; k += nt) adj[k] = g.adj[k];
     for (int k = tid; k < n_free; k += nt) meta[k] = g.meta[k];
@@ -509,9 +558,9 @@ __global__ void __launch_bounds__(kT3 * Q * IPB, 1) k3_bitcsr_pt(const PTArgs a,
                     const bool hw = __any_sync(0xFFFFFFFFu, on && ((md.w >> 27) & 1u));
                     if (on) {
                         if (hw)
-                            k3_site<true>(a, S, md, W2, adj, ub0, n, vmask, nv, C, corr);
+                            k3_site<true, XS>(a, S, md, W2, adj, ub0, n, vmask, nv, C, corr, scr_w);
                         else
-                            k3_site<false>(a, S, md, W2, adj, ub0, n, vmask, nv, C, corr);
+                            k3_site<false, XS>(a, S, md, W2, adj, ub0, n, vmask, nv, C, corr, scr_w);
                     }
                 }
                 tm.sync();
@@ -578,7 +627,8 @@ __global__ void __launch_bounds__(kT3 * Q * IPB, 1) k3_bitcsr_pt(const PTArgs a,
 
 size_t k3_smem_bytes(int R, int nidx, int nadj, int nfree, int n, int ncls, int ipb) {
     const size_t nidx4 = ((size_t)nidx + 3) & ~size_t(3), n2 = ((size_t)2 * n + 2 + 3) & ~size_t(3);
-    return ((size_t)R * nidx4 + (((size_t)nadj + 3) & ~size_t(3)) + 4 * (size_t)nfree +
+    // (the index scratch of the one-lane-per-site shapes is counted for every shape: 8 words per thread)
+    return ((TAPT_K3_IDXS ? (size_t)8 * kT3 * ipb : 0) + (size_t)R * nidx4 + (((size_t)nadj + 3) & ~size_t(3)) + 4 * (size_t)nfree +
             (((size_t)ncls + 1 + 3) & ~size_t(3)) +
             (size_t)ipb * ((size_t)kW * kRow3 + n2)) * 4;
 }
