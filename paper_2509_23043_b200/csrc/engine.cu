@@ -73,6 +73,8 @@ __global__ void k_swap_pass(const int32_t*, uint8_t*, uint8_t*, int, const uint6
                             uint64_t*, uint64_t*);
 __global__ void k_accept_proposals(int32_t*, const uint8_t*, int, const int32_t*, int, const uint32_t*,
                                    const uint64_t*, MetroTable, const uint8_t*, uint8_t*, uint64_t*, uint64_t*);
+__global__ void k_decide_mh(const int32_t*, const uint8_t*, int, const int32_t*, int, const uint32_t*, const uint64_t*,
+                            const double*, const double*, const double*, uint8_t*, uint32_t*);
 __global__ void k_apply_proposals(uint32_t*, int, int, int, const uint8_t*, int, const uint32_t*, int, int,
                                   const uint32_t*, int, const uint8_t*);
 __global__ void k_gen_proposals(uint32_t*, int, int, int, int, const uint64_t*, const uint64_t*, const int8_t*, int);
@@ -901,6 +903,10 @@ struct tapt_ensemble_s {
     DevBuf<uint32_t> pwords;
     DevBuf<int32_t> pE;
     DevBuf<uint8_t> pslot, pacc, pforced, pbytes;
+    DevBuf<double> plq, dbetas;      // MH correction: log q (cur | prop) of the round, the ladder
+    std::vector<double> dbetas_host;  // the ladder dbetas holds
+    DevBuf<uint32_t> pties;
+    uint64_t mh_tie_rounds = 0;       // MH rounds that fell back to the host decisions
     DevBuf<int8_t> pint8;
     DevBuf<uint64_t> pstreams, paccs, ptup, pfull;
     std::vector<uint32_t> last_targets;  // prepare_targets: device copies are current for these
@@ -2158,26 +2164,50 @@ void finish_proposals(tapt_ensemble_s* e, const uint32_t* targets, uint32_t T, b
     CUDA_OK(cudaGetLastError());
     e->pacc.alloc((size_t)e->I * T);
     const uint8_t* forced = nullptr;
-    if (lqc) {  // MH correction: decide on the host with libm exp (bit-exact with the oracle)
-        std::vector<uint64_t> as(e->I);
-        for (uint32_t i = 0; i < e->I; ++i)
-            as[i] = tapt::RngStream::derive(e->seed, {tapt::stream::kCoordinator, e->gid0 + i, e->Q + 1}).state();
-        std::vector<int32_t> Ep = e->pE.download(e->stream);
-        std::vector<int32_t> Eb = e->E.download(e->stream);
-        std::vector<uint8_t> bo = e->buf_of.download(e->stream);
-        std::vector<uint8_t> f((size_t)e->I * T);
-        for (uint32_t i = 0; i < e->I; ++i)
-            for (uint32_t t = 0; t < T; ++t) {
-                const uint32_t r = targets[t];
-                const double ec = Eb[(size_t)i * e->R + bo[(size_t)i * e->R + r]];
-                const double ep = Ep[(size_t)i * T + t];
-                const double a = std::exp(e->betas[r] * (ec - ep)) *
-                                 std::exp(lqc[(size_t)i * T + t] - lqp[(size_t)i * T + t]);
-                const uint64_t x = tapt::RngStream::from_state(as[i]).at(r + 1);
-                const double u = (double)(x >> 11) * 0x1.0p-53;
-                f[(size_t)i * T + t] = u < a ? 1 : 0;
-            }
-        e->pforced.upload(f, e->stream);
+    if (lqc) {
+        // MH correction: decided on the device (k_decide_mh); only a draw within 1e-12 (relative) of the
+        // acceptance probability -- where the device exp could disagree with glibc -- sends the round to
+        // the host path below, so the usual round reads back four bytes instead of three arrays.
+        const size_t IT = (size_t)e->I * T;
+        e->plq.alloc(2 * IT);
+        CUDA_OK(cudaMemcpyAsync(e->plq.p, lqc, IT * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+        CUDA_OK(cudaMemcpyAsync(e->plq.p + IT, lqp, IT * sizeof(double), cudaMemcpyHostToDevice, e->stream));
+        if (e->dbetas.n != (size_t)e->R || e->dbetas_host != e->betas) {
+            e->dbetas.upload(e->betas, e->stream);
+            e->dbetas_host = e->betas;
+        }
+        e->pforced.alloc(IT);
+        e->pties.alloc(1);
+        e->pties.zero(e->stream);
+        ++g_launches;
+        k_decide_mh<<<e->I, std::max(32, ((int)T + 31) / 32 * 32), 0, e->stream>>>(
+            e->E.p, e->buf_of.p, e->R, e->pE.p, (int)T, e->ptargets.p, e->paccs.p, e->dbetas.p, e->plq.p,
+            e->plq.p + IT, e->pforced.p, e->pties.p);
+        CUDA_OK(cudaGetLastError());
+        uint32_t ties = e->pties.download(e->stream)[0];
+        if (std::getenv("TAPT_MH_HOST")) ties = 1;  // tests: force the glibc path
+        e->mh_tie_rounds += ties ? 1 : 0;
+        if (ties) {  // decide the whole round on the host with glibc exp (bit-exact with the oracle)
+            std::vector<uint64_t> as(e->I);
+            for (uint32_t i = 0; i < e->I; ++i)
+                as[i] = tapt::RngStream::derive(e->seed, {tapt::stream::kCoordinator, e->gid0 + i, e->Q + 1}).state();
+            std::vector<int32_t> Ep = e->pE.download(e->stream);
+            std::vector<int32_t> Eb = e->E.download(e->stream);
+            std::vector<uint8_t> bo = e->buf_of.download(e->stream);
+            std::vector<uint8_t> f(IT);
+            for (uint32_t i = 0; i < e->I; ++i)
+                for (uint32_t t = 0; t < T; ++t) {
+                    const uint32_t r = targets[t];
+                    const double ec = Eb[(size_t)i * e->R + bo[(size_t)i * e->R + r]];
+                    const double ep = Ep[(size_t)i * T + t];
+                    const double a = std::exp(e->betas[r] * (ec - ep)) *
+                                     std::exp(lqc[(size_t)i * T + t] - lqp[(size_t)i * T + t]);
+                    const uint64_t x = tapt::RngStream::from_state(as[i]).at(r + 1);
+                    const double u = (double)(x >> 11) * 0x1.0p-53;
+                    f[(size_t)i * T + t] = u < a ? 1 : 0;
+                }
+            e->pforced.upload(f, e->stream);
+        }
         forced = e->pforced.p;
     }
     ++g_launches;

@@ -195,6 +195,29 @@ __global__ void k_accept_proposals(int32_t* E, const uint8_t* buf_of, int R, con
     accepted[(size_t)inst * T + t] = a ? 1 : 0;
 }
 
+// MH-corrected acceptance decided on the device:
+//   a = exp(beta_r (E_r - E^T_r)) * exp(log q(cur) - log q(prop)),  accept iff uniform < a,
+// with the device exp.  Device and glibc exp differ by a few ulp (~1e-16 relative), so a decision whose
+// draw lies outside a relative band of 1e-12 around a is glibc's decision too; a draw inside the band
+// (or a NaN) is counted in *n_ties and the host redoes the round's decisions with glibc (engine.cu).
+// forced[i*T + t] receives the decision for k_accept_proposals.  grid: I, block >= n_targets
+__global__ void k_decide_mh(const int32_t* E, const uint8_t* buf_of, int R, const int32_t* Eprop, int T,
+                            const uint32_t* targets, const uint64_t* accept_streams, const double* betas,
+                            const double* lq_cur, const double* lq_prop, uint8_t* forced, uint32_t* n_ties) {
+    const int inst = blockIdx.x, t = threadIdx.x;
+    if (t >= T) return;
+    const int slot = (int)targets[t];
+    const int b = buf_of[(size_t)inst * R + slot];
+    const double ec = (double)E[(size_t)inst * R + b], ep = (double)Eprop[(size_t)inst * T + t];
+    const size_t k = (size_t)inst * T + t;
+    const double a = __dmul_rn(exp(__dmul_rn(betas[slot], ec - ep)), exp(lq_cur[k] - lq_prop[k]));
+    const uint64_t x = draw(accept_streams[inst], (uint64_t)slot + 1ull);
+    const double u = (double)(x >> 11) * 0x1.0p-53;
+    const bool lo = u < a * (1.0 - 1e-12), hi = u > a * (1.0 + 1e-12);
+    if (!lo && !hi) atomicAdd(n_ties, 1u);
+    forced[k] = u < a ? 1 : 0;
+}
+
 // Copy accepted proposals into the ensemble: for every (instance, group, site), bit
 // (b % W) of the group word takes bit t of the proposal word when proposal t (slot
 // targets[t], buffer b) was accepted.  grid: (ceil(n/256), G, I)

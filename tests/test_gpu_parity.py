@@ -538,7 +538,12 @@ def test_inject_host_proposals_int8_and_packed():
     compare(e, pts)
 
 
-def test_inject_mh_corrected():
+@pytest.mark.parametrize("host_path", [False, True])
+def test_inject_mh_corrected(monkeypatch, host_path):
+    """mh_corrected_move: the device decisions (device exp with a 1e-12 tie band) and
+    the glibc host decisions (TAPT_MH_HOST forces the tie fallback) both equal the oracle's."""
+    if host_path:
+        monkeypatch.setenv("TAPT_MH_HOST", "1")
     R = 6
     betas = H.linear(0.5, 2.0, R)
     g = O.lattice_graph((8, 8))
