@@ -628,11 +628,12 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         n_inst = max(args.cpu_sample_instances, threads)
-        rate, dt, kind, cores, _ = cpu_reference_rate(n_inst, args.cpu_sample_sweeps, threads,
-                                                      args.cpu_sample_sweeps // 2)
+        # about 10-30 s of CPU work: three times the reference arm's per-step sample
+        cs = 3 * args.cpu_sample_sweeps
+        rate, dt, kind, cores, _ = cpu_reference_rate(n_inst, cs, threads, cs // 2)
         out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
-                               "sample": f"{n_inst} instances x {args.cpu_sample_sweeps} sweeps of the config-5 "
-                                         f"geometry with a TAPT round every {args.cpu_sample_sweeps // 2} sweeps "
+                               "sample": f"{n_inst} instances x {cs} sweeps of the config-5 "
+                                         f"geometry with a TAPT round every {cs // 2} sweeps "
                                          f"({dt:.1f} s, '{cpu_model()}')"}
     if rank == 0:
         print(json.dumps(out), flush=True)
