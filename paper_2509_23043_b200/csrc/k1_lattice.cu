@@ -154,7 +154,8 @@ struct K1Smem {
     uint64_t T64[kW][8];   // per own buffer: exact thresholds (tie path)
 };
 
-// Dynamic shared memory holds the spin words (and bond bytes); the control block is static.
+// Dynamic shared memory: [threshold-offset scratch of the launch shape |] spin words | bond bytes |
+// staged slot thresholds and stream states; the control block is static.
 __host__ __device__ constexpr size_t k1_words_offset() { return 0; }
 // Stride (threads) of the per-thread threshold-offset scratch of a launch shape; 0: no scratch.
 __host__ __device__ constexpr int k1_scratch_stride(int sp, int maxt) {
@@ -318,11 +319,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
     uint64_t* strS = thrS + (size_t)a.R * 8;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     constexpr int KV = DIM == 3 ? TAPT_K1_VARIANT3 : TAPT_K1_VARIANT;  // decision instruction mix
-    // threshold offsets of the thread's SP site words as bytes (static: addresses fold into immediates)
-    // (at the front of the dynamic block, so its addresses are the thread's offset + an immediate)
+    // threshold offsets of the thread's SP site words as bytes, at the front of the dynamic block so that
+    // their addresses are the thread's offset + an immediate
     constexpr int XS = k1_scratch_stride(SP, MAXT);
     static_assert(!(TAPT_K1_IDXS && TAPT_K1_PIPE), "the index scratch holds one site pair at a time");
-    constexpr size_t kScr = (size_t)XS * SP * 8 * 4;
     uint32_t* const scr_w = reinterpret_cast<uint32_t*>(smem_raw) + tid;
     const uint8_t* const scr_b = reinterpret_cast<const uint8_t*>(scr_w);
     const int cl = blockIdx.x / a.G, grp = blockIdx.x % a.G;
@@ -524,8 +524,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
 }
 
 size_t k1_smem_bytes(int n, bool dis, int R) {
-    // dynamic part only (the static K1Smem block is accounted by the compiler): words, bond bytes,
-    // then the staged slot thresholds [R][8] and stream states [R]
+    // dynamic part without the launch shape's threshold-offset scratch, which launch_k1_t adds (the static
+    // K1Smem block is accounted by the compiler): words, bond bytes, then the staged slot thresholds
+    // [R][8] and stream states [R]
     return k1_stage_offset(n, dis) + (size_t)R * 9 * 8;
 }
 
@@ -534,9 +535,8 @@ size_t k1_smem_bytes(int n, bool dis, int R) {
 template <int DIM, bool DIS, bool CLU>
 static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, cudaStream_t st, int* resident,
                                char* name) {
-    // SP = 1 site word per thread-iteration at 1024 threads, else 2 interleaved at <= 512
-    // launch shapes: 2 interleaved site words per thread-iteration at <= 512 threads (default),
-    // 2 at 513..768 (<= 85 registers), 1 at > 768, 4 at <= 256
+    // launch shapes: 2 interleaved site words per thread-iteration at 257..768 threads (640 is the
+    // config-5 default: <= 102 registers, 5 warps per scheduler), 1 at > 768, 4 at < 256
     const bool bulk = (a.n & 15) == 0 && a.n >= 16384;
     constexpr bool NAR3 = DIM == 2;  // 3D: narrow decision paths only in the narrow-group instantiations
     const bool narrow = a.W < kW;
