@@ -43,13 +43,23 @@ __device__ __forceinline__ int colour_site(int j, int c, const LatDims& d, int& 
 template <int DIM, bool DIS>
 __device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const uint8_t* __restrict__ bonds, int i,
                                            int x, int y, int z, const LatDims& d, uint32_t& q0, uint32_t& q1,
-                                           uint32_t& q2) {
+                                           uint32_t& q2, const uint32_t* bm = nullptr) {
     const int Lx = 1 << d.log2Lx, Ly = 1 << d.log2Ly;
 #if TAPT_K1_IDX2
     // periodic neighbours by masked add on the packed index (power-of-two extents)
     const int mx = Lx - 1, my = (Ly - 1) << d.log2Lx;
+#if TAPT_K1_XSEL
+    // bit-field select (mask ? stepped : i) as one LOP3 each (the compiler's form shares i & ~mx and
+    // spends an AND and an OR per neighbour)
+    uint32_t ixp, ixm;
+    asm("lop3.b32 %0, %1, %2, %3, 0xB8;" : "=r"(ixp) : "r"(i), "r"(mx), "r"(i + 1));
+    asm("lop3.b32 %0, %1, %2, %3, 0xB8;" : "=r"(ixm) : "r"(i), "r"(mx), "r"(i - 1));
+    uint32_t p0 = w[ixp];
+    uint32_t p1 = w[ixm];
+#else
     uint32_t p0 = w[(i & ~mx) | ((i + 1) & mx)];
     uint32_t p1 = w[(i & ~mx) | ((i - 1) & mx)];
+#endif
     uint32_t p2 = w[(i & ~my) | ((i + Lx) & my)];
     uint32_t p3 = w[(i & ~my) | ((i - Lx) & my)];
     uint32_t p4 = 0, p5 = 0;
@@ -80,6 +90,21 @@ __device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const
 #endif
     if constexpr (DIS) {
         const uint32_t bb = bonds[i];  // bit d set: bond in direction d has J = -J0
+#if TAPT_K1_BLUT
+        if (bm) {  // the six sign masks of this byte from a 64-row shared-memory table (2 loads, no shifts)
+            const uint4 m0 = *reinterpret_cast<const uint4*>(bm + 8 * bb);
+            const uint2 m1 = *reinterpret_cast<const uint2*>(bm + 8 * bb + 4);
+            p0 ^= m0.x;
+            p1 ^= m0.y;
+            p2 ^= m0.z;
+            p3 ^= m0.w;
+            if constexpr (DIM == 3) {
+                p4 ^= m1.x;
+                p5 ^= m1.y;
+            }
+        } else
+#endif
+        {
         p0 ^= 0u - (bb & 1u);
         p1 ^= 0u - ((bb >> 1) & 1u);
         p2 ^= 0u - ((bb >> 2) & 1u);
@@ -87,6 +112,7 @@ __device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const
         if constexpr (DIM == 3) {
             p4 ^= 0u - ((bb >> 4) & 1u);
             p5 ^= 0u - ((bb >> 5) & 1u);
+        }
         }
     }
     if constexpr (DIM == 3) {
@@ -337,6 +363,12 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
     // BULK (tiles of >= 16384 sites, config 5: +0.5 %): spin words and bond bytes of each item come
     // in as bulk copies (copy engine, mbarrier).  Smaller tiles use uint4 loads, in an instantiation
     // without this code (with it, config 2 measured 4.5 % slower even when the path was unused).
+    // sign masks of the 64 bond bytes: row bb = {-(bb & 1), -(bb >> 1 & 1), ...} (TAPT_K1_BLUT; the
+    // config-5 shape only: +0.4 % there on top of XSEL, -1.6 % on config 3)
+    __shared__ __align__(16) uint32_t bmask[(DIS && BULK && TAPT_K1_BLUT) ? 64 : 1][8];
+    if constexpr (DIS && BULK && TAPT_K1_BLUT) {
+        for (int e = tid; e < 64 * 8; e += nt) bmask[e >> 3][e & 7] = 0u - (((uint32_t)(e >> 3) >> (e & 7)) & 1u);
+    }
     __shared__ uint64_t tile_bar;
     constexpr bool bulk = BULK;
     uint32_t tile_phase = 0;
@@ -424,7 +456,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
                 for (int u = 0; u < SP; ++u) {
                     int x, y, z;
                     is_[u] = colour_site<DIM>(jj + u * nsub, c, d, x, y, z);
-                    k1_stencil<DIM, DIS>(words, bonds, is_[u], x, y, z, d, q_[u][0], q_[u][1], q_[u][2]);
+                    k1_stencil<DIM, DIS>(words, bonds, is_[u], x, y, z, d, q_[u][0], q_[u][1], q_[u][2],
+                                         (DIS && BULK && TAPT_K1_BLUT) ? &bmask[0][0] : nullptr);
                     nibbles(q_[u][0], q_[u][1], q_[u][2], N_[u]);
                     if constexpr (XS > 0) k1_index_bytes<XS>(scr_w, u, N_[u]);
                 }

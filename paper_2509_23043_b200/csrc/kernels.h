@@ -40,6 +40,12 @@ constexpr int kCnt = 8;      // planes of the sliced per-thread counters
 #define TAPT_K1_PHOPQ 1       // 1: stream base + counter as an explicit carry-chain add (IADD3 + IMAD.X, 4 pipe cycles) instead of
                              // ptxas's IMAD.WIDE + IMAD.IADD (6): config-5 slice +1 %, configs 1/2/3 +3.1 / +4.5 / +0.8 %
 #endif
+#ifndef TAPT_K1_XSEL
+#define TAPT_K1_XSEL 1       // x-neighbour indices as one LOP3 bit-field select each (config-5 slice +2.0 %, config 3 +1.6 %)
+#endif
+#ifndef TAPT_K1_BLUT
+#define TAPT_K1_BLUT 1       // bond sign masks from a 64-row shared-memory table (bulk shape only)
+#endif
 #ifndef TAPT_K1_MINB256
 #define TAPT_K1_MINB256 2    // CTAs per SM the 256-thread K1 shapes are compiled for (register cap 128 / 85)
 #endif
