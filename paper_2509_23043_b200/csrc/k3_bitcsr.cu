@@ -37,7 +37,6 @@ constexpr int kT3 = 128;     // threads per instance team
 constexpr int kIPB3 = 4;     // max instance teams per CTA
 constexpr int kRow3 = 132;   // threshold row stride (entries) of the per-buffer table
 constexpr int kC3 = 12;      // sliced energy-counter planes (per-thread weight per sweep < 4096)
-#ifndef TAPT_K3_VARIANT
 #ifndef TAPT_K3_IDXS
 #define TAPT_K3_IDXS 0   // (measured -1 % on config 4: the gathers already load the LSU) light rows: threshold offsets 8*acc as bytes in a per-thread shared-memory scratch
 #endif
@@ -47,6 +46,7 @@ constexpr int kC3 = 12;      // sliced energy-counter planes (per-thread weight 
 #ifndef TAPT_K3_CADD
 #define TAPT_K3_CADD 1   // stream base + counter as an explicit carry-chain add
 #endif
+#ifndef TAPT_K3_VARIANT
 #define TAPT_K3_VARIANT TAPT_K1_VARIANT  // mix_pre_hi instruction mix (common.cuh; V & 32 measured: no gain)
 #endif
 
