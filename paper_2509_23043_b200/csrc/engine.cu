@@ -1460,12 +1460,12 @@ tapt_status tapt_ensemble_create(tapt_model_t m, const tapt_ensemble_desc* d, ta
             CUDA_OK(cudaGetDevice(&dev));
             CUDA_OK(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
             // Model: throughput ~ eff(W) x min(1, CTAs / SMs) with one 512-thread CTA per SM; eff measured
-            // on config 3 (tools/narrow_groups.py: 32 / 16 / 8 replicas -> 782 / 550 / 355 G/s at 256
-            // instances).  Small lattices (several 128-thread CTAs per SM) keep 32-replica groups.
+            // on config 3 (tools/narrow_groups.py: 32 / 16 / 8 replicas -> 975 / 727 / 600 G/s at 256
+            // instances, with the narrow groups' lattice folded so that a word holds 2 / 4 sites).  Small lattices (several 128-thread CTAs per SM) keep 32-replica groups.
             int w = e->W;
             if (n / 4 >= TAPT_K1_DEFAULT_THREADS) {
                 auto score = [&](int cand) {
-                    const double eff = cand >= 32 ? 1.0 : (cand >= 16 ? 0.70 : 0.455);
+                    const double eff = cand >= 32 ? 1.0 : (cand >= 16 ? 0.745 : 0.615);
                     const double ctas = (double)e->I * ((e->R + cand - 1) / cand);
                     return eff * std::min(1.0, ctas / nsm);
                 };

@@ -40,14 +40,16 @@ __device__ __forceinline__ int colour_site(int j, int c, const LatDims& d, int& 
 }
 
 // Bit-sliced count of neighbours with J*s_j = +1: returns planes q0 (1), q1 (2), q2 (4).
-template <int DIM, bool DIS>
+template <int DIM, bool DIS, int PACK = 1>
 __device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const uint8_t* __restrict__ bonds, int i,
                                            int x, int y, int z, const LatDims& d, uint32_t& q0, uint32_t& q1,
-                                           uint32_t& q2, const uint32_t* bm = nullptr) {
+                                           uint32_t& q2, const uint32_t* bm = nullptr, int nfold = 0) {
     const int Lx = 1 << d.log2Lx, Ly = 1 << d.log2Ly;
 #if TAPT_K1_IDX2
     // periodic neighbours by masked add on the packed index (power-of-two extents)
-    const int mx = Lx - 1, my = (Ly - 1) << d.log2Lx;
+    // (PACK > 1: the slowest dimension is folded to nfold = n/PACK sites, so its mask shrinks)
+    const int mx = Lx - 1;
+    const int my = (PACK > 1 && DIM == 2) ? ((nfold - 1) & ~(Lx - 1)) : ((Ly - 1) << d.log2Lx);
 #if TAPT_K1_XSEL
     // bit-field select (mask ? stepped : i) as one LOP3 each (the compiler's form shares i & ~mx and
     // spends an AND and an OR per neighbour)
@@ -64,7 +66,8 @@ __device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const
     uint32_t p3 = w[(i & ~my) | ((i - Lx) & my)];
     uint32_t p4 = 0, p5 = 0;
     if constexpr (DIM == 3) {
-        const int P = Lx * Ly, mz = (Ly - 1) << (d.log2Lx + d.log2Ly);
+        const int P = Lx * Ly;
+        const int mz = PACK > 1 ? ((nfold - 1) & ~(P - 1)) : ((Ly - 1) << (d.log2Lx + d.log2Ly));
         p4 = w[(i & ~mz) | ((i + P) & mz)];
         p5 = w[(i & ~mz) | ((i - P) & mz)];
     }
@@ -72,6 +75,7 @@ __device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const
     (void)y;
     (void)z;
 #else
+    static_assert(PACK == 1, "packed narrow groups use the masked-add neighbour indices");
     const int rowb = i - x;
     uint32_t p0 = w[rowb + ((x + 1) & (Lx - 1))];
     uint32_t p1 = w[rowb + ((x - 1) & (Lx - 1))];
@@ -88,7 +92,39 @@ __device__ __forceinline__ void k1_stencil(const uint32_t* __restrict__ w, const
         p5 = w[km];
     }
 #endif
-    if constexpr (DIS) {
+    if constexpr (PACK > 1) {
+        // Packed narrow groups: the word holds PACK sites i + k*n/PACK (k-th field of 32/PACK replica
+        // bits), i.e. the lattice is folded PACK times along its slowest dimension.  The masked adds
+        // above wrapped inside the folded lattice; a neighbour across the fold seam is the next /
+        // previous field of the wrapped word, i.e. the word rotated by one field.
+        constexpr int FW = 32 / PACK;
+        const int S = DIM == 3 ? (Lx * Ly) : Lx;  // stride of the folded dimension
+        const bool seam_p = (i + S) >= nfold, seam_m = i < S;
+        uint32_t& pp = DIM == 3 ? p4 : p2;
+        uint32_t& pm = DIM == 3 ? p5 : p3;
+        if (seam_p) pp = __funnelshift_r(pp, pp, FW);  // field k takes field k+1 of the wrapped word
+        if (seam_m) pm = __funnelshift_l(pm, pm, FW);  // field k takes field k-1
+    }
+    if constexpr (DIS && PACK > 1) {
+        // one bond byte per folded site: direction d's sign mask is field k all-ones iff byte k has bit d
+        constexpr int FW = 32 / PACK;
+        constexpr uint32_t F1 = FW == 16 ? 0xFFFFu : 0xFFu;
+        uint32_t m[6] = {0, 0, 0, 0, 0, 0};
+#pragma unroll
+        for (int k = 0; k < PACK; ++k) {
+            const uint32_t bb = bonds[i + k * nfold];
+#pragma unroll
+            for (int dd = 0; dd < 2 * DIM; ++dd) m[dd] |= ((bb >> dd) & 1u) * (F1 << (k * FW));
+        }
+        p0 ^= m[0];
+        p1 ^= m[1];
+        p2 ^= m[2];
+        p3 ^= m[3];
+        if constexpr (DIM == 3) {
+            p4 ^= m[4];
+            p5 ^= m[5];
+        }
+    } else if constexpr (DIS) {
         const uint32_t bb = bonds[i];  // bit d set: bond in direction d has J = -J0
 #if TAPT_K1_BLUT
         if (bm) {  // the six sign masks of this byte from a 64-row shared-memory table (2 loads, no shifts)
@@ -208,14 +244,18 @@ __device__ __forceinline__ void k1_index_bytes(uint32_t* scr_w, int u, const uin
     }
 }
 
-template <int STRIDE>
+// PACK > 1: lane b is replica b % (32/PACK) of the word's field b / (32/PACK), whose site counter is dph
+// per field further on.
+template <int STRIDE, int PACK = 1>
 __device__ __forceinline__ uint32_t k1_decide_exact_scr(const K1Smem& sm, int W, uint64_t phi_i, const uint8_t* scr,
-                                                        int u) {
+                                                        int u, uint64_t dph = 0) {
+    constexpr int FW = kW / PACK;
     uint32_t nw = 0;
     for (int b = 0; b < W; ++b) {
         const uint32_t idx = scr[k1_index_byte<STRIDE>(u, b)] >> 2;
-        const uint64_t x = mix_final(sm.S.sb[b] + phi_i);
-        if (below(x, sm.T64[b][idx])) nw |= 1u << b;
+        const int rb = b & (FW - 1);
+        const uint64_t x = mix_final(sm.S.sb[rb] + phi_i + (uint64_t)(b / FW) * dph);
+        if (below(x, sm.T64[rb][idx])) nw |= 1u << b;
     }
     return nw;
 }
@@ -239,10 +279,17 @@ __device__ __forceinline__ uint32_t k1_decide_exact(const K1Smem& sm, int W, uin
 // STRIDE > 0 (TAPT_K1_IDXS): the threshold offsets 4*q of the site's 32 replicas were stored as bytes in
 // the thread's shared-memory scratch (k1_index_bytes), so a replica's offset is one LDS.U8 with an
 // immediate address instead of a shift and a mask on the ALU pipe.
-template <int NV, int V, int SP, int STRIDE = 0>
+template <int NV, int V, int SP, int STRIDE = 0, int PACK = 1>
 __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64_t (&ph)[SP],
                                           const uint32_t (&N)[SP][4], const MixConsts& mc, uint32_t (&w)[SP],
-                                          bool& tie, const uint8_t* scr = nullptr) {
+                                          bool& tie, const uint8_t* scr = nullptr, uint64_t dph = 0) {
+    static_assert(PACK == 1 || (NV == kW && STRIDE > 0 && (V & 16) == 0), "packed groups: all 32 lanes, index scratch");
+    constexpr int FW = kW / PACK;  // lanes per field (= replicas of the group)
+    uint64_t phf[SP][PACK];        // site counter of each field of each word
+#pragma unroll
+    for (int u = 0; u < SP; ++u)
+#pragma unroll
+        for (int k = 0; k < PACK; ++k) phf[u][k] = ph[u] + (uint64_t)k * dph;
     constexpr int U = NV ? NV : 1;
     const int cnt = NV ? NV : nv;
     uint32_t tmin = 0xFFFFFFFFu;
@@ -284,7 +331,8 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
     } else {
 #pragma unroll U
     for (int b = cnt - 1; b >= 0; --b) {
-        const uint64_t base = sm.S.sb[b];
+        const int rb = b & (FW - 1), fk = b / FW;  // replica of the group, field of the word
+        const uint64_t base = sm.S.sb[rb];
         const int m = b & 3, sh = 4 * (b >> 2);
         uint32_t dmin[SP];
 #pragma unroll
@@ -294,7 +342,7 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
                 // IDXS = 1: ptxas merges the byte reads into word loads + PRMT; 2: one LDS.U8 per decision
                 const uint32_t ix = TAPT_K1_IDXS == 2 ? *(reinterpret_cast<const volatile uint8_t*>(scr) + k1_index_byte<STRIDE>(u, b))
                                                       : scr[k1_index_byte<STRIDE>(u, b)];
-                thr = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(&sm.Uhi[b][0]) + ix);
+                thr = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(&sm.Uhi[rb][0]) + ix);
             } else if constexpr ((V & 8) != 0) {  // shift on the FMA pipe: (N >> sh) << 2 == hi(N * 2^(34-sh)) & 0x1C
                 const uint32_t ix = (sh >= 4 ? __umulhi(N[u][m], mc.nib[sh >> 2]) : (N[u][m] << 2)) & 0x1Cu;
                 thr = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(&sm.Uhi[b][0]) + ix);
@@ -305,10 +353,10 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
             uint32_t zl_, zh_;  // explicit carry-chain add: IADD3 + IADD3.X / IMAD.X instead of IMAD.WIDE + IMAD.IADD
             asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
                 : "=r"(zl_), "=r"(zh_)
-                : "r"((uint32_t)base), "r"((uint32_t)(base >> 32)), "r"((uint32_t)ph[u]), "r"((uint32_t)(ph[u] >> 32)));
+                : "r"((uint32_t)base), "r"((uint32_t)(base >> 32)), "r"((uint32_t)phf[u][fk]), "r"((uint32_t)(phf[u][fk] >> 32)));
             const uint32_t h = mix_pre_hi<V>(zl_, zh_, mc);
 #else
-            const uint64_t z = base + ph[u];
+            const uint64_t z = base + phf[u][fk];
             const uint32_t h = mix_pre_hi<V>((uint32_t)z, (uint32_t)(z >> 32), mc);
 #endif
             const uint32_t dd = decide_acc(h, thr, w[u]);
@@ -332,8 +380,13 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
 // are separate instantiations because the extra code shifts the hot loop's code generation: with the
 // narrow paths compiled in, 2D shapes measured up to 4 % faster and 3D shapes up to 1.2 % slower, so
 // 3D shapes carry them only when the launch uses narrow groups (tools/cfg_ab.sh, tools/k1_ab.sh).
-template <int DIM, bool DIS, bool CLU, int SP, int MAXT, int MINB = 1, bool BULK = false, bool NAR = true>
+// PACK: sites per word of a narrow group (2: 16 replicas, 4: 8 replicas): the lattice is folded PACK times
+// along its slowest dimension and a word holds the PACK folded sites, so the per-site work (stencil, nibble
+// spread, offset bytes, energy planes) is amortised over 32 decisions again.  Needs full groups and an even
+// number of planes per fold (both colours stay aligned); launch_k1_t checks.
+template <int DIM, bool DIS, bool CLU, int SP, int MAXT, int MINB = 1, bool BULK = false, bool NAR = true, int PACK = 1>
 __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, const LatDims d) {
+    static_assert(PACK == 1 || (!BULK && TAPT_K1_IDXS), "packed groups: small lattices with the index scratch");
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ K1Smem sm;  // static: table addresses fold into LDS immediates
     constexpr size_t kScr0 = (size_t)k1_scratch_stride(SP, MAXT) * SP * 8 * 4;
@@ -353,7 +406,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
     const uint8_t* const scr_b = reinterpret_cast<const uint8_t*>(scr_w);
     const int cl = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
-    const int half = n >> 1, nsub = half / SP;
+    const int nfold = n / PACK;  // words of the (folded) lattice
+    const int half = nfold >> 1, nsub = half / SP;
+    const uint64_t dph = (uint64_t)nfold * kPhi;  // site-counter step from one field of a word to the next
     const int tl = a.sched ? pt_timeline(cl, a.sched_clusters) : 0;
     const int it0 = a.sched ? a.sched_ptr[tl] : 0, it1 = a.sched ? a.sched_ptr[tl + 1] : 1;
     for (int e = tid; e < a.R * 8; e += nt) {
@@ -394,9 +449,19 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
             if constexpr (DIS) bulk_g2s(bonds, a.bonds + (size_t)inst * n, bb, &tile_bar);
         }
     } else {
+        if constexpr (PACK > 1) {
+            const uint32_t* src = a.words + ((size_t)inst * a.G + grp) * n;
+            for (int k = tid; k < nfold; k += nt) {
+                uint32_t v = 0;
+#pragma unroll
+                for (int f = 0; f < PACK; ++f) v |= (src[k + f * nfold] & ((1u << (kW / PACK)) - 1u)) << (f * (kW / PACK));
+                words[k] = v;
+            }
+        } else {
         const uint4* src = reinterpret_cast<const uint4*>(a.words + ((size_t)inst * a.G + grp) * n);
         uint4* dst = reinterpret_cast<uint4*>(words);
         for (int k = tid; k < (n >> 2); k += nt) dst[k] = src[k];
+        }
         if constexpr (DIS) {
             const uint4* bs = reinterpret_cast<const uint4*>(a.bonds + (size_t)inst * n);
             uint4* bd = reinterpret_cast<uint4*>(bonds);
@@ -456,8 +521,8 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
                 for (int u = 0; u < SP; ++u) {
                     int x, y, z;
                     is_[u] = colour_site<DIM>(jj + u * nsub, c, d, x, y, z);
-                    k1_stencil<DIM, DIS>(words, bonds, is_[u], x, y, z, d, q_[u][0], q_[u][1], q_[u][2],
-                                         (DIS && BULK && TAPT_K1_BLUT) ? &bmask[0][0] : nullptr);
+                    k1_stencil<DIM, DIS, PACK>(words, bonds, is_[u], x, y, z, d, q_[u][0], q_[u][1], q_[u][2],
+                                               (DIS && BULK && TAPT_K1_BLUT) ? &bmask[0][0] : nullptr, nfold);
                     nibbles(q_[u][0], q_[u][1], q_[u][2], N_[u]);
                     if constexpr (XS > 0) k1_index_bytes<XS>(scr_w, u, N_[u]);
                 }
@@ -484,7 +549,9 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
                     bool tie = false;
                     // full 32-, 16- and 8-replica groups unrolled (narrow groups spread an instance over
                     // more CTAs when instances are few); partial groups take the rolled loop
-                    if (nv == kW)
+                    if constexpr (PACK > 1)
+                        k1_decide<kW, KV, SP, XS, PACK>(sm, kW, ph, N, a.mc, nw, tie, scr_b, dph);
+                    else if (nv == kW)
                         k1_decide<kW, KV, SP, XS>(sm, nv, ph, N, a.mc, nw, tie, scr_b);
                     else if (NAR && nv == 16)
                         k1_decide<16, KV, SP, XS>(sm, nv, ph, N, a.mc, nw, tie, scr_b);
@@ -492,13 +559,14 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
                         k1_decide<8, KV, SP, XS>(sm, nv, ph, N, a.mc, nw, tie, scr_b);
                     else
                         k1_decide<0, KV, SP, XS>(sm, nv, ph, N, a.mc, nw, tie, scr_b);
-                    const uint32_t vmask = nv >= 32 ? 0xFFFFFFFFu : ((1u << nv) - 1u);
+                    const uint32_t vmask = (PACK > 1 || nv >= 32) ? 0xFFFFFFFFu : ((1u << nv) - 1u);
 #pragma unroll
                     for (int u = 0; u < SP; ++u) nw[u] = ~nw[u] & vmask;
                     if (tie) {  // probability ~ 2^-31 per decision: redo the words exactly
 #pragma unroll
                         for (int u = 0; u < SP; ++u)
-                            nw[u] = XS > 0 ? k1_decide_exact_scr<(XS > 0 ? XS : 1)>(sm, nv, ph[u], scr_b, u)
+                            nw[u] = XS > 0 ? k1_decide_exact_scr<(XS > 0 ? XS : 1), PACK>(sm, PACK > 1 ? kW : nv, ph[u],
+                                                                                          scr_b, u, dph)
                                            : k1_decide_exact(sm, nv, ph[u], N[u]);
                     }
 #pragma unroll
@@ -529,7 +597,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
         // exact energies: E = J0 * (2*U - n*dim)
         {
             const uint32_t tot = warp_sliced_total<kCnt>(C);
-            if (lane < nv) atomicAdd(&sm.S.Ucnt[lane], tot);
+            if constexpr (PACK > 1)
+                atomicAdd(&sm.S.Ucnt[lane & (kW / PACK - 1)], tot);  // the fields of a word are the same replicas
+            else if (lane < nv)
+                atomicAdd(&sm.S.Ucnt[lane], tot);
             __syncthreads();
             if (tid < nv) {
                 sm.S.Eown[par][tid] = d.J0 * (2 * (int)sm.S.Ucnt[tid] - n * DIM);
@@ -537,7 +608,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
             }
         }
         if (a.energy_only) break;
-        pt_epilogue<CLU>(a, sm.S, words, inst, grp, t, pass);
+        pt_epilogue<CLU>(a, sm.S, words, inst, grp, t, pass, CtaTeam{}, PACK);
     }
     if (a.energy_only) {
         __syncthreads();
@@ -546,9 +617,19 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
     }
     // ---- write back
     {
+        if constexpr (PACK > 1) {
+            uint32_t* dst = a.words + ((size_t)inst * a.G + grp) * n;
+            constexpr uint32_t F1 = (1u << (kW / PACK)) - 1u;
+            for (int k = tid; k < nfold; k += nt) {
+                const uint32_t v = words[k];
+#pragma unroll
+                for (int f = 0; f < PACK; ++f) dst[k + f * nfold] = (v >> (f * (kW / PACK))) & F1;
+            }
+        } else {
         uint4* dst = reinterpret_cast<uint4*>(a.words + ((size_t)inst * a.G + grp) * n);
         const uint4* src = reinterpret_cast<const uint4*>(words);
         for (int k = tid; k < (n >> 2); k += nt) dst[k] = src[k];
+        }
     }
     pt_finish<CLU>(a, sm.S, inst, grp, par);
     if (item.signal >= 0) pt_signal_flag<CLU>(a, item.signal, grp);
@@ -584,6 +665,19 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
                      : threads == 256 && narrow   ? 5
                      : threads == 256             ? 6
                                                   : 7;
+    // packed narrow groups (PACK template parameter): full 16- or 8-replica groups on a lattice whose
+    // slowest dimension folds into 32/W parts of an even number of planes
+    int pack = 1;
+    if (narrow && TAPT_K1_IDXS && TAPT_K1_PACK && (a.W == 16 || a.W == 8) && a.B % a.W == 0 && threads > 128 &&
+        threads <= 512) {
+        const int pk = kW / a.W, Ls = 1 << d.log2Ly;  // extent of the slowest dimension (3D lattices are cubic)
+        if (Ls >= 2 * pk && (a.n / pk / 2) % 2 == 0) pack = pk;
+    }
+    const int ppick = pack == 1 ? -1 : (threads > 256 ? 0 : 2) + (pack == 4 ? 1 : 0);
+    static void (*const ptable[4])(const PTArgs, const LatDims) = {
+        k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, true, 2>, k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, true, 4>,
+        k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, true, 2>,
+        k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, true, 4>};
     static const int shape[10][5] = {{1, 1024, 1, 0, 1}, {2, 768, 1, 0, 1},   {2, 512, 1, 0, 1}, {2, 512, 1, 1, NAR3},
                                     {2, 512, 1, 0, NAR3}, {2, 256, TAPT_K1_MINB256, 0, 1}, {2, 256, TAPT_K1_MINB256, 0, NAR3}, {4, 256, 1, 0, 1},
                                     {2, 640, 1, 0, 1}, {2, 640, 1, 1, NAR3}};
@@ -593,11 +687,15 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
         k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, NAR3>, k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, true>,
         k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, NAR3>, k1_lattice_pt<DIM, DIS, CLU, 4, 256>,
         k1_lattice_pt<DIM, DIS, CLU, 2, 640>, k1_lattice_pt<DIM, DIS, CLU, 2, 640, 1, true, NAR3>};
-    auto fn = table[pick];
+    auto fn = ppick >= 0 ? ptable[ppick] : table[pick];
     const size_t smem = k1_smem_bytes(a.n, DIS, a.R) +
                         (size_t)k1_scratch_stride(shape[pick][0], shape[pick][1]) * shape[pick][0] * 32;
     if (name) {
         const int* v = shape[pick];
+        if (pack > 1)
+            snprintf(name, 96, "k1_lattice_pt<%d,%d,%d,%d,%d,%d,%d,%d,%d>", DIM, (int)DIS, (int)CLU, v[0], v[1], v[2],
+                     v[3], v[4], pack);
+        else
         snprintf(name, 96, "k1_lattice_pt<%d,%d,%d,%d,%d,%d,%d,%d>", DIM, (int)DIS, (int)CLU, v[0], v[1], v[2], v[3],
                  v[4]);
         return cudaSuccess;

@@ -118,9 +118,10 @@ __device__ __forceinline__ void pt_stream_bases(const PTArgs& a, PTShared& S, in
 
 // After Eown[par] is final for this CTA: gather, best, swap, measure.
 // `words` = this CTA's group spins in shared memory (n words).
+// pack > 1 (K1's packed narrow groups): a word holds `pack` sites of 32/pack replicas each.
 template <bool CLU, class TM = CtaTeam>
 __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words, int inst, int grp, uint64_t t,
-                            uint64_t& pass, const TM& tm = TM{}) {
+                            uint64_t& pass, const TM& tm = TM{}, int pack = 1) {
     const int tid = tm.tid(), nt = tm.nt(), lane = tid & 31;
     const int par = (int)(t & 1);
     if constexpr (CLU) {
@@ -170,9 +171,12 @@ __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words,
         uint32_t C[kCnt];
 #pragma unroll
         for (int k = 0; k < kCnt; ++k) C[k] = 0;
-        for (int i = tid; i < a.n; i += nt) sliced_add1<kCnt>(C, words[i]);
+        for (int i = tid; i < a.n / pack; i += nt) sliced_add1<kCnt>(C, words[i]);
         const uint32_t tot = warp_sliced_total<kCnt>(C);
-        if (lane < own_count(a, grp)) atomicAdd(&S.Mcnt[lane], tot);
+        if (pack > 1)
+            atomicAdd(&S.Mcnt[lane & (kW / pack - 1)], tot);  // every field of the word is one of the group's replicas
+        else if (lane < own_count(a, grp))
+            atomicAdd(&S.Mcnt[lane], tot);
         tm.sync();
         if (tid < own_count(a, grp)) {
             const int gb = grp * a.W + tid;

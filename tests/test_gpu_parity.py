@@ -286,6 +286,39 @@ def test_k1_group_width_does_not_change_the_chain(monkeypatch, dims, R):
     monkeypatch.delenv("TAPT_K1_W")
 
 
+@pytest.mark.parametrize("dims,R,w,packed", [((16,), 64, 16, 2), ((16,), 64, 8, 4), ((4,), 32, 16, 2), ((8,), 16, 8, 4),
+                                              ((8, 8), 32, 8, 4), ((64, 4), 32, 16, 2), ((4,), 16, 8, 0),
+                                              ((16, 16), 40, 16, 0)])
+def test_k1_packed_narrow_groups_match_the_oracle(monkeypatch, dims, R, w, packed):
+    """Narrow groups fold the lattice along its slowest dimension and keep 32/W sites per word (the
+    launch log's last template argument); seam neighbours, per-field draw counters, bond bytes, energies
+    and magnetisations must give the oracle's chain.  Lattices whose fold would hold an odd number of
+    planes, and ladders with a partial last group, keep one site per word."""
+    monkeypatch.setenv("TAPT_K1_W", str(w))
+    betas = H.linear(0.2, 2.5, R)
+    I = 2
+    e = T.Ensemble(T.Model.lattice(dims), betas, n_instances=I, seed=91, instance_offset=3)
+    three_d = len(dims) == 1
+    if three_d:
+        e.generate_ea_disorder(7)
+        graphs = [O.ea_graph(dims, 7, 3 + k) for k in range(I)]
+    else:
+        graphs = [O.lattice_graph(dims)] * I
+    e.init_random()
+    e.run(25, swap_every=1, measure_every=5)
+    names = [x.split(" ")[0] for x in e.launch_log() if x.startswith("k1_lattice_pt<")]
+    if packed:
+        assert any(x.count(",") == 8 and x.endswith(f",{packed}>") for x in names), names
+    else:
+        assert all(x.count(",") == 7 for x in names), names
+    pts = H.run_oracle(graphs, betas, 91, 3, H.checkerboard_order(dims), 25, measure_every=5)
+    compare(e, pts)
+    for k in range(I):
+        obs = e.observables()[k]
+        for j, key in enumerate(("cnt", "sumE", "sumE2", "sumAbsM", "sumM2")):
+            assert np.array_equal(obs[:, j], pts[k].meas[key]), (k, key)
+
+
 def test_k1_automatic_group_width_for_few_instances(monkeypatch):
     """Few instances (4 x 64 slots on a 16^3 lattice: 8 groups of 32 < SMs) take narrower groups
     automatically; the chain equals the 32-replica one."""
