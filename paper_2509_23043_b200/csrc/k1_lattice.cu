@@ -253,9 +253,14 @@ __device__ __forceinline__ uint32_t k1_decide_exact_scr(const K1Smem& sm, int W,
     uint32_t nw = 0;
     for (int b = 0; b < W; ++b) {
         const uint32_t idx = scr[k1_index_byte<STRIDE>(u, b)] >> 2;
-        const int rb = b & (FW - 1);
-        const uint64_t x = mix_final(sm.S.sb[rb] + phi_i + (uint64_t)(b / FW) * dph);
-        if (below(x, sm.T64[rb][idx])) nw |= 1u << b;
+        if constexpr (PACK > 1) {
+            const int rb = b & (FW - 1);
+            const uint64_t x = mix_final(sm.S.sb[rb] + phi_i + (uint64_t)(b / FW) * dph);
+            if (below(x, sm.T64[rb][idx])) nw |= 1u << b;
+        } else {
+            const uint64_t x = mix_final(sm.S.sb[b] + phi_i);
+            if (below(x, sm.T64[b][idx])) nw |= 1u << b;
+        }
     }
     return nw;
 }
@@ -285,11 +290,13 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
                                           bool& tie, const uint8_t* scr = nullptr, uint64_t dph = 0) {
     static_assert(PACK == 1 || (NV == kW && STRIDE > 0 && (V & 16) == 0), "packed groups: all 32 lanes, index scratch");
     constexpr int FW = kW / PACK;  // lanes per field (= replicas of the group)
-    uint64_t phf[SP][PACK];        // site counter of each field of each word
+    [[maybe_unused]] uint64_t phf[SP][PACK];  // PACK > 1: site counter of each field of each word
+    if constexpr (PACK > 1) {
 #pragma unroll
-    for (int u = 0; u < SP; ++u)
+        for (int u = 0; u < SP; ++u)
 #pragma unroll
-        for (int k = 0; k < PACK; ++k) phf[u][k] = ph[u] + (uint64_t)k * dph;
+            for (int k = 0; k < PACK; ++k) phf[u][k] = ph[u] + (uint64_t)k * dph;
+    }
     constexpr int U = NV ? NV : 1;
     const int cnt = NV ? NV : nv;
     uint32_t tmin = 0xFFFFFFFFu;
@@ -331,7 +338,11 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
     } else {
 #pragma unroll U
     for (int b = cnt - 1; b >= 0; --b) {
-        const int rb = b & (FW - 1), fk = b / FW;  // replica of the group, field of the word
+        int rb = b, fk = 0;  // replica of the group, field of the word
+        if constexpr (PACK > 1) {
+            rb = b & (FW - 1);
+            fk = b / FW;
+        }
         const uint64_t base = sm.S.sb[rb];
         const int m = b & 3, sh = 4 * (b >> 2);
         uint32_t dmin[SP];
@@ -349,14 +360,16 @@ __device__ __forceinline__ void k1_decide(const K1Smem& sm, int nv, const uint64
             } else {
                 thr = sm.Uhi[b][(N[u][m] >> sh) & 7u];
             }
+            uint64_t phv = ph[u];
+            if constexpr (PACK > 1) phv = phf[u][fk];
 #if TAPT_K1_PHOPQ
             uint32_t zl_, zh_;  // explicit carry-chain add: IADD3 + IADD3.X / IMAD.X instead of IMAD.WIDE + IMAD.IADD
             asm("add.cc.u32 %0, %2, %4;\n\taddc.u32 %1, %3, %5;"
                 : "=r"(zl_), "=r"(zh_)
-                : "r"((uint32_t)base), "r"((uint32_t)(base >> 32)), "r"((uint32_t)phf[u][fk]), "r"((uint32_t)(phf[u][fk] >> 32)));
+                : "r"((uint32_t)base), "r"((uint32_t)(base >> 32)), "r"((uint32_t)phv), "r"((uint32_t)(phv >> 32)));
             const uint32_t h = mix_pre_hi<V>(zl_, zh_, mc);
 #else
-            const uint64_t z = base + phf[u][fk];
+            const uint64_t z = base + phv;
             const uint32_t h = mix_pre_hi<V>((uint32_t)z, (uint32_t)(z >> 32), mc);
 #endif
             const uint32_t dd = decide_acc(h, thr, w[u]);
@@ -406,9 +419,10 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
     const uint8_t* const scr_b = reinterpret_cast<const uint8_t*>(scr_w);
     const int cl = blockIdx.x / a.G, grp = blockIdx.x % a.G;
     const int n = a.n, W = a.W, nv = own_count(a, grp);
-    const int nfold = n / PACK;  // words of the (folded) lattice
-    const int half = nfold >> 1, nsub = half / SP;
-    const uint64_t dph = (uint64_t)nfold * kPhi;  // site-counter step from one field of a word to the next
+    const int nfold = PACK > 1 ? n / PACK : n;  // words of the (folded) lattice
+    const int half = (PACK > 1 ? nfold : n) >> 1, nsub = half / SP;
+    // site-counter step from one field of a word to the next
+    [[maybe_unused]] const uint64_t dph = PACK > 1 ? (uint64_t)nfold * kPhi : 0ull;
     const int tl = a.sched ? pt_timeline(cl, a.sched_clusters) : 0;
     const int it0 = a.sched ? a.sched_ptr[tl] : 0, it1 = a.sched ? a.sched_ptr[tl + 1] : 1;
     for (int e = tid; e < a.R * 8; e += nt) {
@@ -608,7 +622,7 @@ __global__ void __launch_bounds__(MAXT, MINB) k1_lattice_pt(const PTArgs a, cons
             }
         }
         if (a.energy_only) break;
-        pt_epilogue<CLU>(a, sm.S, words, inst, grp, t, pass, CtaTeam{}, PACK);
+        pt_epilogue<CLU, CtaTeam, PACK>(a, sm.S, words, inst, grp, t, pass);
     }
     if (a.energy_only) {
         __syncthreads();

@@ -119,9 +119,10 @@ __device__ __forceinline__ void pt_stream_bases(const PTArgs& a, PTShared& S, in
 // After Eown[par] is final for this CTA: gather, best, swap, measure.
 // `words` = this CTA's group spins in shared memory (n words).
 // pack > 1 (K1's packed narrow groups): a word holds `pack` sites of 32/pack replicas each.
-template <bool CLU, class TM = CtaTeam>
+template <bool CLU, class TM = CtaTeam, int PACK = 1>
 __device__ void pt_epilogue(const PTArgs& a, PTShared& S, const uint32_t* words, int inst, int grp, uint64_t t,
-                            uint64_t& pass, const TM& tm = TM{}, int pack = 1) {
+                            uint64_t& pass, const TM& tm = TM{}) {
+    constexpr int pack = PACK;
     const int tid = tm.tid(), nt = tm.nt(), lane = tid & 31;
     const int par = (int)(t & 1);
     if constexpr (CLU) {
