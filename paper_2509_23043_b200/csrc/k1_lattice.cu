@@ -687,11 +687,16 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
         const int pk = kW / a.W, Ls = 1 << d.log2Ly;  // extent of the slowest dimension (3D lattices are cubic)
         if (Ls >= 2 * pk && (a.n / pk / 2) % 2 == 0) pack = pk;
     }
-    const int ppick = pack == 1 ? -1 : (threads > 256 ? 0 : 2) + (pack == 4 ? 1 : 0);
-    static void (*const ptable[4])(const PTArgs, const LatDims) = {
+    // one word per thread-iteration (SP = 1) when two would leave threads of a 512-thread CTA without work
+    const bool sp1 = pack > 1 && threads > 256 && TAPT_K1_PACK_SP1 && a.n / pack / 4 < threads;
+    const int ppick = pack == 1 ? -1 : (sp1 ? 4 : threads > 256 ? 0 : 2) + (pack == 4 ? 1 : 0);
+    static void (*const ptable[6])(const PTArgs, const LatDims) = {
         k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, true, 2>, k1_lattice_pt<DIM, DIS, CLU, 2, 512, 1, false, true, 4>,
         k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, true, 2>,
-        k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, true, 4>};
+        k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, true, 4>,
+        k1_lattice_pt<DIM, DIS, CLU, 1, 512, 1, false, true, 2>, k1_lattice_pt<DIM, DIS, CLU, 1, 512, 1, false, true, 4>};
+    static const int pshape[6][5] = {{2, 512, 1, 0, 1}, {2, 512, 1, 0, 1}, {2, 256, TAPT_K1_MINB256, 0, 1},
+                                     {2, 256, TAPT_K1_MINB256, 0, 1}, {1, 512, 1, 0, 1}, {1, 512, 1, 0, 1}};
     static const int shape[10][5] = {{1, 1024, 1, 0, 1}, {2, 768, 1, 0, 1},   {2, 512, 1, 0, 1}, {2, 512, 1, 1, NAR3},
                                     {2, 512, 1, 0, NAR3}, {2, 256, TAPT_K1_MINB256, 0, 1}, {2, 256, TAPT_K1_MINB256, 0, NAR3}, {4, 256, 1, 0, 1},
                                     {2, 640, 1, 0, 1}, {2, 640, 1, 1, NAR3}};
@@ -702,10 +707,9 @@ static cudaError_t launch_k1_t(const PTArgs& a, const LatDims& d, int threads, c
         k1_lattice_pt<DIM, DIS, CLU, 2, 256, TAPT_K1_MINB256, false, NAR3>, k1_lattice_pt<DIM, DIS, CLU, 4, 256>,
         k1_lattice_pt<DIM, DIS, CLU, 2, 640>, k1_lattice_pt<DIM, DIS, CLU, 2, 640, 1, true, NAR3>};
     auto fn = ppick >= 0 ? ptable[ppick] : table[pick];
-    const size_t smem = k1_smem_bytes(a.n, DIS, a.R) +
-                        (size_t)k1_scratch_stride(shape[pick][0], shape[pick][1]) * shape[pick][0] * 32;
+    const int* v = ppick >= 0 ? pshape[ppick] : shape[pick];
+    const size_t smem = k1_smem_bytes(a.n, DIS, a.R) + (size_t)k1_scratch_stride(v[0], v[1]) * v[0] * 32;
     if (name) {
-        const int* v = shape[pick];
         if (pack > 1)
             snprintf(name, 96, "k1_lattice_pt<%d,%d,%d,%d,%d,%d,%d,%d,%d>", DIM, (int)DIS, (int)CLU, v[0], v[1], v[2],
                      v[3], v[4], pack);

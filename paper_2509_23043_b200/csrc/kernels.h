@@ -49,6 +49,9 @@ constexpr int kCnt = 8;      // planes of the sliced per-thread counters
 #ifndef TAPT_K1_PACK
 #define TAPT_K1_PACK 1       // 1: narrow replica groups fold the lattice and pack 2 / 4 sites per word (k1_lattice.cu)
 #endif
+#ifndef TAPT_K1_PACK_SP1
+#define TAPT_K1_PACK_SP1 1
+#endif
 #ifndef TAPT_K1_MINB256
 #define TAPT_K1_MINB256 2    // CTAs per SM the 256-thread K1 shapes are compiled for (register cap 128 / 85)
 #endif
