@@ -494,6 +494,31 @@ def test_synthetic_tapt_rounds_match_oracle_k1():
     assert e.acceptance()[3].sum() > 0
 
 
+@pytest.mark.parametrize("dims,nt", [((16, 16), 16), ((16, 16), 8), ((8,), 16), ((8,), 8)])
+def test_tapt_rounds_with_packed_proposal_groups(dims, nt):
+    """16 or 8 targets: the proposal group is a full narrow group, so its energy evaluation and refinement
+    sweeps run on the folded lattice (2 / 4 sites per word); the R = 16 main group is packed too."""
+    R = 16
+    betas = H.geometric(0.3, 0.9, R)
+    mb = np.array([O.yang_m(b) for b in betas])
+    e = T.Ensemble(T.Model.lattice(dims), betas, n_instances=2, seed=78, instance_offset=2)
+    if len(dims) == 1:
+        e.generate_ea_disorder(9)
+        graphs = [O.ea_graph(dims, 9, 2 + k) for k in range(2)]
+    else:
+        graphs = [O.lattice_graph(dims)] * 2
+    e.init_random()
+    for _ in range(4):
+        e.run(10, swap_every=1)
+        e.generate_proposals(np.arange(nt), mb[:nt], refine=3)
+    names = [x.split(" ")[0] for x in e.launch_log() if x.startswith("k1_lattice_pt<")]
+    assert any(x.count(",") == 8 and x.endswith(f",{32 // nt}>") for x in names), names  # the proposal groups
+    assert any(x.count(",") == 8 and x.endswith(",2>") for x in names), names             # the 16-slot ladder
+    pts = H.run_oracle(graphs, betas, 78, 2, H.checkerboard_order(dims), 40,
+                       props=dict(every=10, targets=nt, m_bias=mb, refine=3))
+    compare(e, pts)
+
+
 def test_synthetic_tapt_reference_order_matches_reference_golden():
     f = np.load(os.path.join(GOLD, "pt_tapt2d16.npz"))
     I, R, n = (int(x) for x in f["shape"])
