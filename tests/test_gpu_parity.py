@@ -319,6 +319,52 @@ def test_k1_packed_narrow_groups_match_the_oracle(monkeypatch, dims, R, w, packe
             assert np.array_equal(obs[:, j], pts[k].meas[key]), (k, key)
 
 
+@pytest.mark.parametrize("fuzz_seed", [20251021, 7, 99] + [1000 + k for k in range(int(os.environ.get("TAPT_FUZZ_EXTRA", "0")))])
+def test_k1_random_shapes_widths_and_threads_match_the_oracle(monkeypatch, fuzz_seed):
+    """Seeded sweep over lattice shapes, ladder lengths, group widths and thread counts (packed and
+    unpacked narrow groups, partial groups, clusters, proposal rounds): every run equals the oracle."""
+    rs = np.random.default_rng(fuzz_seed)
+    shapes = [(4,), (8,), (16,), (4, 4), (8, 8), (16, 8), (8, 32), (32, 32), (64, 16)]
+    for case in range(24):
+        dims = shapes[rs.integers(len(shapes))]
+        R = int(rs.choice([5, 8, 16, 24, 32, 40, 48, 64]))
+        w = int(rs.choice([8, 16, 32]))
+        if (R + w - 1) // w > 8:
+            w = 32
+        threads = rs.choice(["", "128", "256", "512"])
+        monkeypatch.setenv("TAPT_K1_W", str(w))
+        if threads:
+            monkeypatch.setenv("TAPT_K1_THREADS", threads)
+        else:
+            monkeypatch.delenv("TAPT_K1_THREADS", raising=False)
+        I, seed, off = int(rs.integers(1, 4)), int(rs.integers(1, 1000)), int(rs.integers(0, 50))
+        betas = H.linear(0.15, 2.0, R)
+        e = T.Ensemble(T.Model.lattice(dims), betas, n_instances=I, seed=seed, instance_offset=off)
+        if len(dims) == 1:
+            e.generate_ea_disorder(seed + 1)
+            graphs = [O.ea_graph(dims, seed + 1, off + k) for k in range(I)]
+        else:
+            graphs = [O.lattice_graph(dims)] * I
+        e.init_random()
+        nt = int(min(R, rs.choice([3, 8, 16, 20])))
+        mb = np.full(R, 0.3)
+        for _ in range(2):
+            e.run(7, swap_every=1, measure_every=2)
+            e.generate_proposals(np.arange(nt), mb[:nt], refine=2)
+        pts = H.run_oracle(graphs, betas, seed, off, H.checkerboard_order(dims), 14, measure_every=2,
+                           props=dict(every=7, targets=nt, m_bias=mb, refine=2))
+        try:
+            compare(e, pts)
+            for k in range(I):
+                obs = e.observables()[k]
+                for j, key in enumerate(("cnt", "sumE", "sumE2", "sumAbsM", "sumM2")):
+                    assert np.array_equal(obs[:, j], pts[k].meas[key]), key
+        except AssertionError as err:
+            raise AssertionError(f"case {case}: dims={dims} R={R} W={w} threads={threads!r} I={I} nt={nt}: {err}\n"
+                                 f"{e.launch_log()}") from err
+    monkeypatch.delenv("TAPT_K1_W")
+
+
 def test_k1_automatic_group_width_for_few_instances(monkeypatch):
     """Few instances (4 x 64 slots on a 16^3 lattice: 8 groups of 32 < SMs) take narrower groups
     automatically; the chain equals the 32-replica one."""
