@@ -47,6 +47,48 @@ def run_both(g, betas, seed, order, n_sweeps=60, n_inst=2, swap_every=1, props=N
     return e, pts
 
 
+@pytest.mark.parametrize("fuzz_seed", [11, 12] + [2000 + k for k in range(int(__import__("os").environ.get("TAPT_FUZZ_EXTRA", "0")))])
+def test_random_integer_graphs_all_csr_kernels_match_the_oracle(fuzz_seed, monkeypatch):
+    """Seeded sweep over random integer graphs (sizes, degrees, |J| <= 3, fields, clamps), ladder lengths,
+    sweep orders, K3 team / lane shapes and proposal rounds: K3 (colour order, <= 32 slots), K2 (more slots or
+    TAPT_K3=0) and K4 / K2 (the reference's index order) all equal the oracle."""
+    rs = np.random.default_rng(fuzz_seed)
+    for case in range(16):
+        n = int(rs.integers(6, 90))
+        ne = int(rs.integers(n, 4 * n))
+        ci, cj = rs.integers(0, n, ne), rs.integers(0, n, ne)
+        keep = ci != cj
+        J = rs.choice([-3.0, -2.0, -1.0, 1.0, 2.0, 3.0], ne)[keep]
+        h = rs.integers(-3, 4, n).astype(float) if rs.random() < 0.7 else np.zeros(n)
+        cl = np.where(rs.random(n) < rs.choice([0.0, 0.1, 0.3]), rs.choice([-1, 1], n), 0).astype(np.int8)
+        g = O.Graph.from_couplings(n, ci[keep], cj[keep], J, h, cl)
+        R = int(rs.choice([3, 8, 17, 32, 40]))
+        order = str(rs.choice(["colour", "colour", "reference"]))
+        for var in ("TAPT_K3", "TAPT_K3_IPB", "TAPT_K3_Q", "TAPT_K4"):
+            monkeypatch.delenv(var, raising=False)
+        knobs = {}
+        if rs.random() < 0.25:
+            knobs["TAPT_K3"] = "0"
+        if rs.random() < 0.4:
+            knobs["TAPT_K3_IPB"] = str(rs.integers(1, 5))
+        if rs.random() < 0.3:
+            knobs["TAPT_K3_Q"] = str(rs.choice([2, 4]))
+        if rs.random() < 0.3:
+            knobs["TAPT_K4"] = "0"
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        betas = H.geometric(0.1, 2.0, R)
+        nt = int(min(R, rs.choice([2, 7, 16])))
+        props = dict(every=6, targets=nt, m_bias=np.full(R, 0.2), refine=2) if rs.random() < 0.5 else None
+        n_inst = int(rs.integers(1, 5))
+        try:
+            e, pts = run_both(g, betas, int(rs.integers(1, 999)), order, n_sweeps=18, n_inst=n_inst, props=props)
+            compare(e, pts)
+        except AssertionError as err:
+            raise AssertionError(f"case {case}: n={n} R={R} order={order} knobs={knobs} props={props is not None} "
+                                 f"I={n_inst}: {err}") from err
+
+
 @pytest.mark.parametrize("order", ["colour", "reference"])
 def test_fields_only_no_couplings(order):
     rs = np.random.default_rng(1)
